@@ -1,0 +1,165 @@
+/*
+ * bdm.h -- C ABI of the B200-native BioDynaMo mechanical-interaction step (libbdm.so).
+ *
+ * One mechanical step over N spherical agents (BASELINE.json north_star):
+ *   (a) uniform-grid rebuild, box edge = largest diameter      PAPER.md:313-322 (§2.1, Environment)
+ *   (b) 27-box neighbour search                                  PAPER.md:318-320 (§2.1)
+ *   (c) sphere-sphere force  f = k*delta - gamma*sqrt(r*delta)   north_star
+ *   (d) displacement with adherence threshold and max-displacement clamp, then position update
+ *                                                                north_star
+ * The arithmetic reading (O1-O8, every ambiguity) is DESIGN.md §3.
+ *
+ * Conventions (all functions):
+ *   - Return int status: BDM_OK (0) or a negative BDM_E* code.  Functions never abort or throw.
+ *     The message for the last failure is returned by bdm_last_error(h) (thread-local when h is NULL
+ *     or the handle could not be created).
+ *   - Positions are n x 3 row-major fp64 (x0,y0,z0,x1,...) in micrometres; diameters n fp64.
+ *   - Agent id = input index (0..n-1).  Every per-agent output is in id order.
+ *   - Pointers are HOST pointers unless params.flags has BDM_DEVICE_PTRS, in which case every
+ *     array argument of bdm_init and of the bdm_get_* array getters is a CUDA device pointer on the
+ *     handle's device, used on the handle's stream (bdm_set_stream).
+ *   - Input arrays are caller-owned and only read during the call (the library copies them).
+ *     Outputs go to caller-allocated buffers of the documented size.  The handle owns all device
+ *     state until bdm_destroy.  A handle is not thread-safe: one controlling caller.
+ *   - All work is issued on the handle's stream.  Host-pointer getters synchronise that stream;
+ *     device-pointer getters and bdm_mech_step return once the work is enqueued (call bdm_sync to
+ *     wait and to collect asynchronous errors such as BDM_ENONFINITE / BDM_ERANGE).
+ */
+#ifndef BDM_H
+#define BDM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BDM_ABI_VERSION 1
+
+/* status codes */
+#define BDM_OK 0
+#define BDM_EINVAL (-1)     /* bad argument: n<0, NULL with n>0, D<=0 or non-finite, non-finite
+                               position, bad params (eta<=0, max_disp<=0, negative or
+                               non-finite k/gamma/adherence/dt/box_edge_min) */
+#define BDM_ESTATE (-2)     /* call out of order (e.g. displacements before any step, handle poisoned
+                               by an earlier asynchronous error) */
+#define BDM_ENOMEM (-3)     /* device or host allocation failed */
+#define BDM_ECUDA (-4)      /* CUDA runtime error (no device, launch failure, ...) */
+#define BDM_ENONFINITE (-6) /* a summed force or displacement was not finite */
+#define BDM_ERANGE (-7)     /* n >= 2^32, n_boxes >= 2^32, or |p * inv| >= 2^20 boxes (R9) */
+#define BDM_ETRUNC (-8)     /* output buffer too small; the required size was written back */
+
+/* params.flags */
+#define BDM_DEVICE_PTRS 0x1u /* array arguments are CUDA device pointers */
+#define BDM_RECORD 0x2u      /* force kernel also records per-agent neighbour / contact statistics */
+
+/* bdm_get_pairs kind */
+#define BDM_NEIGHBOR 0 /* unordered pairs with d2 <= L2 (O3) */
+#define BDM_CONTACT 1  /* unordered pairs with delta > 0  (O4) */
+
+typedef struct bdm_ctx* bdm_handle;
+
+typedef struct {
+  double k_rep;        /* repulsion coefficient k          default 10.0          */
+  double gamma_att;    /* attraction coefficient gamma     default 4.0   (R3)          */
+  double adherence;    /* |F| threshold; |F| <= it -> no motion, default 0.1 (R4)      */
+  double dt;           /* time step                        default 1.0          */
+  double eta;          /* viscosity                        default 1.0          */
+  double max_disp;     /* clamp on |Delta p| per step, um  default 3.0          */
+  double box_edge_min; /* box edge = max(max D, this), um  default 0.0          */
+  uint32_t flags;      /* BDM_DEVICE_PTRS | BDM_RECORD                                          */
+  int32_t device;      /* CUDA device ordinal; -1 = current device                              */
+} bdm_params;
+
+typedef struct {
+  double L;         /* box edge (O1) */
+  double L2;        /* L*L, the neighbour threshold on d2 (O3) */
+  double inv;       /* 1/(L*(1+2^-30)), binning factor (O1, R9) */
+  int32_t lo[3];    /* min integer box coordinate per axis (O2) */
+  int32_t hi[3];    /* max integer box coordinate per axis */
+  int64_t n_boxes;  /* (hi-lo+1) product */
+  int64_t n_agents; /* N */
+} bdm_grid_info;
+
+/* Per-agent statistics (only with BDM_RECORD; arrays of n, id order; any pointer may be NULL). */
+typedef struct {
+  int32_t* n_cand;   /* candidates visited in the 27 boxes, self excluded */
+  int32_t* n_nb;     /* neighbours, d2 <= L2 */
+  int32_t* n_ct;     /* contacts, delta > 0 */
+  int8_t* branch;    /* 0 = below adherence, 1 = clamped, 2 = free (O6) */
+  uint64_t* nb_hash; /* sum over neighbours j of mix64(j) mod 2^64 (order-free digest) */
+  uint64_t* ct_hash; /* sum over contacts j of mix64(j) mod 2^64 */
+} bdm_agent_stats;
+
+/* Fill *p with the defaults listed above.  EINVAL if p is NULL. */
+int bdm_params_default(bdm_params* p);
+
+/* Create a handle holding n agents.  pos: n x 3 fp64, diam: n fp64 (host, or device with
+ * BDM_DEVICE_PTRS).  Validates every input (EINVAL, message names the first bad index).  n = 0 is
+ * valid: steps are no-ops.  The state is "no grid" until bdm_grid_build or the
+ * first step.  On failure *h is set to NULL. */
+int bdm_init(bdm_handle* h, int64_t n, const double* pos, const double* diam, const bdm_params* p);
+
+/* Rebuild the uniform grid from the current positions (O1-O2 + counting sort, ascending id inside
+ * each box, box start table).  Marks the grid fresh so the next step does not rebuild again. */
+int bdm_grid_build(bdm_handle h);
+
+/* Run n_steps mechanical steps (n_steps >= 0; 0 is a no-op).  Each step: rebuild the
+ * grid unless fresh, compute every force from the step-start snapshot, displacements (O6), then
+ * update all positions (O7, Jacobi).  Asynchronous; errors detected on the device are reported by
+ * the next synchronising call. */
+int bdm_mech_step(bdm_handle h, int32_t n_steps);
+
+/* Displacements Delta p of the last step, n x 3 fp64, id order.  ESTATE before the first step. */
+int bdm_get_displacements(bdm_handle h, double* out);
+
+/* Current positions, n x 3 fp64, id order. */
+int bdm_get_positions(bdm_handle h, double* out);
+
+/* Integer box coordinates floor(p * inv) of the current positions under the current grid,
+ * n x 3 int32, id order.  Builds the grid if it is not fresh. */
+int bdm_get_box_coords(bdm_handle h, int32_t* out);
+
+/* Grid of the last build (host struct).  ESTATE if no grid was built yet. */
+int bdm_get_grid_info(bdm_handle h, bdm_grid_info* out);
+
+/* Per-agent statistics of the last step (requires BDM_RECORD at init; ESTATE otherwise).  Output
+ * arrays are host or device according to BDM_DEVICE_PTRS. */
+int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out);
+
+/* Unordered pair set of the current positions (kind BDM_NEIGHBOR or BDM_CONTACT): pairs (min id,
+ * max id) sorted lexicographically into out[2*cap] (HOST memory always).  *n_pairs receives the
+ * count; ETRUNC (and nothing written) if it exceeds cap.  Builds the grid if not fresh. */
+int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_t cap);
+
+/* Issue all later work on this CUDA stream (cudaStream_t; NULL = legacy default stream). */
+int bdm_set_stream(bdm_handle h, void* cuda_stream);
+
+/* Wait for the handle's stream; returns any pending asynchronous error. */
+int bdm_sync(bdm_handle h);
+
+/* Device time of the kernels of the last bdm_mech_step call, per kernel family, in ms (filled
+ * only when timing was enabled with bdm_set_timing(h, 1)).  out[0] grid build, out[1] force. */
+int bdm_set_timing(bdm_handle h, int enabled);
+int bdm_get_timing(bdm_handle h, double* out2);
+
+/* Counter-based uniform population on the device (kernel K0; bdm_inputs/__init__.py holds the
+ * NumPy twin): for ids [id0, id0+n): pos[i][a] = lo[a] + (hi[a]-lo[a])*u(seed, id, a),
+ * diam[i] = dlo + (dhi-dlo)*u(seed, id, 3), u = (splitmix64(seed*0x9E3779B97F4A7C15 + 4*id + s) >> 11)
+ * * 2^-53.  pos (n x 3) and diam (n) are DEVICE pointers; issued on the given stream. */
+int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo3, const double* hi3, double dlo,
+                         double dhi, double* pos, double* diam, void* cuda_stream);
+
+/* Human-readable message of the last failure on h (or of the calling thread when h is NULL). */
+const char* bdm_last_error(bdm_handle h);
+
+/* Release every resource of h.  NULL is a no-op. */
+void bdm_destroy(bdm_handle h);
+
+/* ABI version (BDM_ABI_VERSION). */
+int bdm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BDM_H */

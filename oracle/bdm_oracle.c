@@ -1,0 +1,451 @@
+/*
+ * bdm_oracle.c -- plain, slow CPU oracle for one BioDynaMo mechanical-interaction step.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant generator with the CUDA path in paper_2006_06775_b200/.
+ *
+ * It follows, step by step, the reading recorded in DESIGN.md §3:
+ *
+ *   O1  box edge   L = max(max_i D_i, box_edge_min); L2 = L*L; inv = 1/(L*(1+2^-30))
+ *                  PAPER.md:321-322 (§2.1 "box size is chosen based on the largest agent")
+ *   O2  boxes      b_i = (floor(x_i*inv), floor(y_i*inv), floor(z_i*inv))
+ *                  PAPER.md:315-317 (§2.1 "assigns agents to boxes based on the center of mass")
+ *   O3  neighbours j != i in the 27 boxes b_i + {-1,0,1}^3 with d2 <= L2,
+ *                  d2 = (dx*dx + dy*dy) + dz*dz, dx = x_i - x_j
+ *                  PAPER.md:318-320 (§2.1 "iterating over the assigned box and all its
+ *                  surrounding boxes (27 boxes in total)")
+ *   O4  pair force d = sqrt(d2); r_i = 0.5*D_i; s = r_i + r_j; delta = s - d; contact iff delta > 0;
+ *                  r = (r_i*r_j)/s; f = k*delta - gamma*sqrt(r*delta); m = f/d; F_ij = m*(dx,dy,dz)
+ *                  (BASELINE.json north_star: "overlap delta=r1+r2-d gives a repulsion term minus
+ *                  a sqrt(r*delta) attraction term"; PAPER.md:109, 724-725 defer to Zubler-Douglas)
+ *                  d2 == 0 exactly: delta = s, force +f*x_hat on the higher id (R8)
+ *   O5  sum        F_i = sum of F_ij over contacts, boxes in (dx,dy,dz) lexicographic order from
+ *                  (-1,-1,-1), within a box by ascending id (R13/R14)
+ *   O6  displacement |F| = sqrt((Fx*Fx + Fy*Fy) + Fz*Fz); |F| <= adherence -> 0;
+ *                  c = dt/eta; |F|*c > max_disp -> F*(max_disp/|F|); else F*c
+ *                  (north_star "displacement rule with its adherence threshold and
+ *                  max-displacement clamp"; "Delta p = F/eta*Delta t, clamps")
+ *   O7  update     p_i' = p_i + Delta p_i after all forces (Jacobi)
+ *
+ * Every +, -, * is a separately rounded IEEE binary64 operation: build with
+ * -ffp-contract=off (no FMA).  sqrt and / are correctly rounded (libm sqrt).
+ *
+ * Implementation is deliberately plain: agents are sorted by (box key, id) with qsort and each
+ * of the 27 boxes is found by binary search.  No blocking, no fusion.  Optional OpenMP over
+ * agents (each agent's sum is independent and computed in the same order).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define ORC_OK 0
+#define ORC_EINVAL (-1)
+#define ORC_ENOMEM (-3)
+#define ORC_ENONFINITE (-6)
+#define ORC_ERANGE (-7)
+#define ORC_ETRUNC (-8)
+
+typedef struct {
+  double k_rep, gamma_att, adherence, dt, eta, max_disp, box_edge_min;
+} orc_params;
+
+typedef struct {
+  double L, L2, inv;
+  int64_t lo[3], hi[3];
+} orc_grid;
+
+/* per-agent record; any pointer may be NULL */
+typedef struct {
+  int32_t* n_cand;   /* candidates visited in the 27 boxes (self excluded) */
+  int32_t* n_nb;     /* |{j : d2 <= L2}| */
+  int32_t* n_ct;     /* |{j : delta > 0}| */
+  double* s_abs;     /* sum |f_ij| over contacts */
+  int8_t* branch;    /* 0 = below adherence, 1 = clamped, 2 = free */
+  uint64_t* nb_hash; /* sum mix64(j) over neighbours (mod 2^64) */
+  uint64_t* ct_hash; /* sum mix64(j) over contacts   (mod 2^64) */
+  double* force;     /* 3n summed force F_i */
+} orc_record;
+
+int orc_version(void) { return 1; }
+
+void orc_params_default(orc_params* p) {
+  p->k_rep = 10.0;       /* SPEC.md:248 k=10 */
+  p->gamma_att = 4.0;    /* SPEC.md:248 k_adh = 0.4 k, re-read as gamma (R3) */
+  p->adherence = 0.1;    /* DESIGN.md R4 */
+  p->dt = 1.0;
+  p->eta = 1.0;
+  p->max_disp = 3.0;
+  p->box_edge_min = 0.0;
+}
+
+uint64_t orc_mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+/* O1 + the box extents used by O2's key. */
+int orc_grid_params(int64_t n, const double* pos, const double* diam, double box_edge_min, orc_grid* g) {
+  double maxd = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    if (diam[i] > maxd) maxd = diam[i];
+  double L = maxd > box_edge_min ? maxd : box_edge_min;
+  g->L = L;
+  g->L2 = L * L;
+  g->inv = 1.0 / (L * (1.0 + 0x1p-30));
+  for (int a = 0; a < 3; ++a) {
+    g->lo[a] = 0;
+    g->hi[a] = 0;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    for (int a = 0; a < 3; ++a) {
+      double q = pos[3 * i + a] * g->inv;
+      if (!(fabs(q) < 1048576.0)) return ORC_ERANGE; /* |p*inv| < 2^20 keeps the 2^-30 margin valid */
+      int64_t b = (int64_t)floor(q);
+      if (i == 0 || b < g->lo[a]) g->lo[a] = b;
+      if (i == 0 || b > g->hi[a]) g->hi[a] = b;
+    }
+  }
+  return ORC_OK;
+}
+
+void orc_box_coords(int64_t n, const double* pos, const orc_grid* g, int64_t* b) {
+  for (int64_t i = 0; i < 3 * n; ++i) b[i] = (int64_t)floor(pos[i] * g->inv);
+}
+
+/* ---- the grid: agents sorted by (key, id) ---- */
+typedef struct {
+  uint64_t key;
+  int64_t id;
+} orc_entry;
+
+static int cmp_entry(const void* a, const void* b) {
+  const orc_entry* x = (const orc_entry*)a;
+  const orc_entry* y = (const orc_entry*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  if (x->id != y->id) return x->id < y->id ? -1 : 1;
+  return 0;
+}
+
+typedef struct {
+  orc_grid g;
+  int64_t n;
+  int64_t ny, nz;
+  int64_t* b;        /* 3n box coordinates */
+  orc_entry* sorted; /* n entries sorted by (key, id) */
+} orc_index;
+
+static uint64_t key_of(const orc_index* ix, int64_t bx, int64_t by, int64_t bz) {
+  return (uint64_t)(((bx - ix->g.lo[0]) * ix->ny + (by - ix->g.lo[1])) * ix->nz + (bz - ix->g.lo[2]));
+}
+
+static void free_index(orc_index* ix) {
+  free(ix->b);
+  free(ix->sorted);
+}
+
+static int build_index(orc_index* ix, int64_t n, const double* pos, const double* diam, double box_edge_min) {
+  memset(ix, 0, sizeof(*ix));
+  ix->n = n;
+  int rc = orc_grid_params(n, pos, diam, box_edge_min, &ix->g);
+  if (rc) return rc;
+  ix->ny = ix->g.hi[1] - ix->g.lo[1] + 1;
+  ix->nz = ix->g.hi[2] - ix->g.lo[2] + 1;
+  ix->b = (int64_t*)malloc(sizeof(int64_t) * 3 * (n > 0 ? n : 1));
+  ix->sorted = (orc_entry*)malloc(sizeof(orc_entry) * (n > 0 ? n : 1));
+  if (!ix->b || !ix->sorted) {
+    free_index(ix);
+    return ORC_ENOMEM;
+  }
+  orc_box_coords(n, pos, &ix->g, ix->b);
+  for (int64_t i = 0; i < n; ++i) {
+    ix->sorted[i].key = key_of(ix, ix->b[3 * i], ix->b[3 * i + 1], ix->b[3 * i + 2]);
+    ix->sorted[i].id = i;
+  }
+  qsort(ix->sorted, (size_t)n, sizeof(orc_entry), cmp_entry);
+  return ORC_OK;
+}
+
+/* first position in sorted[] whose key >= k */
+static int64_t lower_bound(const orc_index* ix, uint64_t k) {
+  int64_t lo = 0, hi = ix->n;
+  while (lo < hi) {
+    int64_t mid = lo + (hi - lo) / 2;
+    if (ix->sorted[mid].key < k)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+/* O4 for one pair (i, j) with d2 already known to be a neighbour.  Returns 1 on contact and
+ * writes the force on i into t[3] and f into *fout. */
+static int pair_force(const double* pi, const double* pj, double Di, double Dj, int64_t idi, int64_t idj,
+                      double dx, double dy, double dz, double d2, const orc_params* p, double* t, double* fout) {
+  double d = sqrt(d2);
+  double ri = 0.5 * Di;
+  double rj = 0.5 * Dj;
+  double s = ri + rj;
+  double delta = s - d;
+  (void)pi;
+  (void)pj;
+  if (!(delta > 0.0)) return 0;
+  double r = (ri * rj) / s;
+  double f = p->k_rep * delta - p->gamma_att * sqrt(r * delta);
+  *fout = f;
+  if (d2 == 0.0) { /* coincident centres, R8 */
+    double sign = idi > idj ? 1.0 : -1.0;
+    t[0] = sign * f;
+    t[1] = 0.0;
+    t[2] = 0.0;
+    return 1;
+  }
+  double m = f / d;
+  t[0] = m * dx;
+  t[1] = m * dy;
+  t[2] = m * dz;
+  return 1;
+}
+
+/* O6 */
+static int displacement(const double F[3], const orc_params* p, double dp[3]) {
+  double fn = sqrt((F[0] * F[0] + F[1] * F[1]) + F[2] * F[2]);
+  if (fn <= p->adherence) {
+    dp[0] = 0.0;
+    dp[1] = 0.0;
+    dp[2] = 0.0;
+    return 0;
+  }
+  double c = p->dt / p->eta;
+  if (fn * c > p->max_disp) {
+    double scale = p->max_disp / fn;
+    dp[0] = F[0] * scale;
+    dp[1] = F[1] * scale;
+    dp[2] = F[2] * scale;
+    return 1;
+  }
+  dp[0] = F[0] * c;
+  dp[1] = F[1] * c;
+  dp[2] = F[2] * c;
+  return 2;
+}
+
+/* O3-O6 for agent i using the index. */
+static int agent_update(const orc_index* ix, int64_t i, const double* pos, const double* diam, const orc_params* p,
+                        double* dp_out, const orc_record* rec) {
+  const double* pi = pos + 3 * i;
+  double F[3] = {0.0, 0.0, 0.0};
+  int32_t n_cand = 0, n_nb = 0, n_ct = 0;
+  double s_abs = 0.0;
+  uint64_t nb_hash = 0, ct_hash = 0;
+  for (int ddx = -1; ddx <= 1; ++ddx)
+    for (int ddy = -1; ddy <= 1; ++ddy)
+      for (int ddz = -1; ddz <= 1; ++ddz) {
+        int64_t cx = ix->b[3 * i] + ddx, cy = ix->b[3 * i + 1] + ddy, cz = ix->b[3 * i + 2] + ddz;
+        if (cx < ix->g.lo[0] || cx > ix->g.hi[0] || cy < ix->g.lo[1] || cy > ix->g.hi[1] || cz < ix->g.lo[2] ||
+            cz > ix->g.hi[2])
+          continue;
+        uint64_t k = key_of(ix, cx, cy, cz);
+        for (int64_t q = lower_bound(ix, k); q < ix->n && ix->sorted[q].key == k; ++q) {
+          int64_t j = ix->sorted[q].id;
+          if (j == i) continue;
+          ++n_cand;
+          const double* pj = pos + 3 * j;
+          double dx = pi[0] - pj[0];
+          double dy = pi[1] - pj[1];
+          double dz = pi[2] - pj[2];
+          double d2 = (dx * dx + dy * dy) + dz * dz;
+          if (!(d2 <= ix->g.L2)) continue;
+          ++n_nb;
+          nb_hash += orc_mix64((uint64_t)j);
+          double t[3], f;
+          if (pair_force(pi, pj, diam[i], diam[j], i, j, dx, dy, dz, d2, p, t, &f)) {
+            ++n_ct;
+            ct_hash += orc_mix64((uint64_t)j);
+            s_abs += fabs(f);
+            F[0] = F[0] + t[0];
+            F[1] = F[1] + t[1];
+            F[2] = F[2] + t[2];
+          }
+        }
+      }
+  int br = displacement(F, p, dp_out);
+  if (rec) {
+    if (rec->n_cand) rec->n_cand[i] = n_cand;
+    if (rec->n_nb) rec->n_nb[i] = n_nb;
+    if (rec->n_ct) rec->n_ct[i] = n_ct;
+    if (rec->s_abs) rec->s_abs[i] = s_abs;
+    if (rec->branch) rec->branch[i] = (int8_t)br;
+    if (rec->nb_hash) rec->nb_hash[i] = nb_hash;
+    if (rec->ct_hash) rec->ct_hash[i] = ct_hash;
+    if (rec->force) {
+      rec->force[3 * i] = F[0];
+      rec->force[3 * i + 1] = F[1];
+      rec->force[3 * i + 2] = F[2];
+    }
+  }
+  if (!isfinite(F[0]) || !isfinite(F[1]) || !isfinite(F[2])) return ORC_ENONFINITE;
+  return ORC_OK;
+}
+
+static int check_inputs(int64_t n, const double* pos, const double* diam, const orc_params* p) {
+  if (n < 0 || (n > 0 && (!pos || !diam)) || !p) return ORC_EINVAL;
+  if (!(p->eta > 0.0) || !(p->max_disp > 0.0) || !isfinite(p->eta) || !isfinite(p->max_disp)) return ORC_EINVAL;
+  if (!(p->k_rep >= 0.0) || !(p->gamma_att >= 0.0) || !(p->adherence >= 0.0) || !(p->dt >= 0.0) ||
+      !(p->box_edge_min >= 0.0) || !isfinite(p->k_rep) || !isfinite(p->gamma_att) || !isfinite(p->adherence) ||
+      !isfinite(p->dt) || !isfinite(p->box_edge_min))
+    return ORC_EINVAL;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(diam[i] > 0.0) || !isfinite(diam[i])) return ORC_EINVAL;
+    for (int a = 0; a < 3; ++a)
+      if (!isfinite(pos[3 * i + a])) return ORC_EINVAL;
+  }
+  return ORC_OK;
+}
+
+/*
+ * One step (O1-O7) for the agents listed in sample[0..n_sample) (all agents if sample == NULL).
+ * dp: 3*n_out displacements (n_out = n_sample or n); pos_new: 3*n_out or NULL;
+ * rec arrays are indexed by agent id (length n).  nthreads <= 0: OpenMP default.
+ */
+int orc_step_sample(int64_t n, const double* pos, const double* diam, const orc_params* p, int64_t n_sample,
+                    const int64_t* sample, double* dp, double* pos_new, const orc_record* rec, int nthreads) {
+  int rc = check_inputs(n, pos, diam, p);
+  if (rc) return rc;
+  if (n == 0) return ORC_OK;
+  orc_index ix;
+  rc = build_index(&ix, n, pos, diam, p->box_edge_min);
+  if (rc) return rc;
+  int64_t m = sample ? n_sample : n;
+  int bad = 0;
+#ifdef _OPENMP
+  if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1024) reduction(| : bad)
+#endif
+  for (int64_t q = 0; q < m; ++q) {
+    int64_t i = sample ? sample[q] : q;
+    if (i < 0 || i >= n) {
+      bad |= 1;
+      continue;
+    }
+    if (agent_update(&ix, i, pos, diam, p, dp + 3 * q, rec)) bad |= 2;
+    if (pos_new)
+      for (int a = 0; a < 3; ++a) pos_new[3 * q + a] = pos[3 * i + a] + dp[3 * q + a];
+  }
+  (void)nthreads;
+  free_index(&ix);
+  if (bad & 1) return ORC_EINVAL;
+  if (bad & 2) return ORC_ENONFINITE;
+  return ORC_OK;
+}
+
+int orc_step(int64_t n, const double* pos, const double* diam, const orc_params* p, double* dp, double* pos_new,
+             const orc_record* rec, int nthreads) {
+  return orc_step_sample(n, pos, diam, p, n, NULL, dp, pos_new, rec, nthreads);
+}
+
+/* O8: n_steps repetitions of O1-O7 in place on pos; dp receives the last step's displacement. */
+int orc_run(int64_t n, double* pos, const double* diam, const orc_params* p, int32_t n_steps, double* dp,
+            int nthreads) {
+  if (n_steps < 0) return ORC_EINVAL;
+  double* tmp = (double*)malloc(sizeof(double) * 3 * (n > 0 ? n : 1));
+  if (!tmp) return ORC_ENOMEM;
+  for (int32_t s = 0; s < n_steps; ++s) {
+    int rc = orc_step(n, pos, diam, p, dp, tmp, NULL, nthreads);
+    if (rc) {
+      free(tmp);
+      return rc;
+    }
+    memcpy(pos, tmp, sizeof(double) * 3 * n);
+  }
+  free(tmp);
+  return ORC_OK;
+}
+
+/*
+ * Unordered pair sets.  kind 0 = neighbour set N (d2 <= L2), kind 1 = contact set C (delta > 0).
+ * Writes (min id, max id) pairs, sorted lexicographically, into out[2*cap]; returns the number of
+ * pairs (>= 0) or an error code.  If the count exceeds cap, nothing beyond cap is written and the
+ * caller learns the size from the return value.
+ */
+static int cmp_pair(const void* a, const void* b) {
+  const int64_t* x = (const int64_t*)a;
+  const int64_t* y = (const int64_t*)b;
+  if (x[0] != y[0]) return x[0] < y[0] ? -1 : 1;
+  if (x[1] != y[1]) return x[1] < y[1] ? -1 : 1;
+  return 0;
+}
+
+int64_t orc_pairs(int64_t n, const double* pos, const double* diam, const orc_params* p, int kind, int64_t* out,
+                  int64_t cap) {
+  int rc = check_inputs(n, pos, diam, p);
+  if (rc) return rc;
+  if (n == 0) return 0;
+  orc_index ix;
+  rc = build_index(&ix, n, pos, diam, p->box_edge_min);
+  if (rc) return rc;
+  int64_t cnt = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const double* pi = pos + 3 * i;
+    for (int ddx = -1; ddx <= 1; ++ddx)
+      for (int ddy = -1; ddy <= 1; ++ddy)
+        for (int ddz = -1; ddz <= 1; ++ddz) {
+          int64_t cx = ix.b[3 * i] + ddx, cy = ix.b[3 * i + 1] + ddy, cz = ix.b[3 * i + 2] + ddz;
+          if (cx < ix.g.lo[0] || cx > ix.g.hi[0] || cy < ix.g.lo[1] || cy > ix.g.hi[1] || cz < ix.g.lo[2] ||
+              cz > ix.g.hi[2])
+            continue;
+          uint64_t k = key_of(&ix, cx, cy, cz);
+          for (int64_t q = lower_bound(&ix, k); q < n && ix.sorted[q].key == k; ++q) {
+            int64_t j = ix.sorted[q].id;
+            if (j <= i) continue; /* each unordered pair once */
+            const double* pj = pos + 3 * j;
+            double dx = pi[0] - pj[0];
+            double dy = pi[1] - pj[1];
+            double dz = pi[2] - pj[2];
+            double d2 = (dx * dx + dy * dy) + dz * dz;
+            if (!(d2 <= ix.g.L2)) continue;
+            if (kind == 1) {
+              double t[3], f;
+              if (!pair_force(pi, pj, diam[i], diam[j], i, j, dx, dy, dz, d2, p, t, &f)) continue;
+            }
+            if (cnt < cap) {
+              out[2 * cnt] = i;
+              out[2 * cnt + 1] = j;
+            }
+            ++cnt;
+          }
+        }
+  }
+  free_index(&ix);
+  if (cnt <= cap) qsort(out, (size_t)cnt, 2 * sizeof(int64_t), cmp_pair);
+  return cnt;
+}
+
+/* Force on agent i from agent j alone (O4), for closed-form pins.  Returns 1 on contact. */
+int orc_pair_force(const double* pi, const double* pj, double Di, double Dj, int64_t idi, int64_t idj,
+                   const orc_params* p, double* t) {
+  double dx = pi[0] - pj[0];
+  double dy = pi[1] - pj[1];
+  double dz = pi[2] - pj[2];
+  double d2 = (dx * dx + dy * dy) + dz * dz;
+  double f;
+  t[0] = t[1] = t[2] = 0.0;
+  return pair_force(pi, pj, Di, Dj, idi, idj, dx, dy, dz, d2, p, t, &f);
+}
+
+/* O6 alone, for pins.  Returns the branch (0 adherence, 1 clamp, 2 free). */
+int orc_displacement(const double* F, const orc_params* p, double* dp) { return displacement(F, p, dp); }
+
+int orc_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
