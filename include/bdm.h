@@ -138,10 +138,17 @@ int bdm_set_stream(bdm_handle h, void* cuda_stream);
 /* Wait for the handle's stream; returns any pending asynchronous error. */
 int bdm_sync(bdm_handle h);
 
-/* Device time of the kernels of the last bdm_mech_step call, per kernel family, in ms (filled
- * only when timing was enabled with bdm_set_timing(h, 1)).  out[0] grid build, out[1] force. */
+/* Replace the population of h (same n) with new positions / diameters (host or device per
+ * BDM_DEVICE_PTRS), re-validated as in bdm_init; ids stay 0..n-1.  Reuses every device buffer, so
+ * repeated batches pay only the copy.  Clears an earlier asynchronous data error. */
+int bdm_set_agents(bdm_handle h, const double* pos, const double* diam);
+
+/* Per-step device timing with CUDA events on the handle's stream (bdm_set_timing(h, 1) enables
+ * it).  bdm_get_timing synchronises and writes, summed over the steps since the previous call:
+ * out4[0] grid-build ms, out4[1] force-kernel ms, out4[2] steps, out4[3] kernels of this library
+ * launched (counted whether or not timing is enabled); then resets the sums. */
 int bdm_set_timing(bdm_handle h, int enabled);
-int bdm_get_timing(bdm_handle h, double* out2);
+int bdm_get_timing(bdm_handle h, double* out4);
 
 /* Counter-based uniform population on the device (kernel K0; bdm_inputs/__init__.py holds the
  * NumPy twin): for ids [id0, id0+n): pos[i][a] = lo[a] + (hi[a]-lo[a])*u(seed, id, a),

@@ -71,6 +71,7 @@ def lib():
         L.orc_pair_force.argtypes = [_f64p, _f64p, ctypes.c_double, ctypes.c_double, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.POINTER(Params), _f64p]
         L.orc_displacement.argtypes = [_f64p, ctypes.POINTER(Params), _f64p]
+        L.orc_box_coords.argtypes = [ctypes.c_int64, _f64p, ctypes.POINTER(Grid), _i64p]
         L.orc_mix64.argtypes = [ctypes.c_uint64]
         L.orc_mix64.restype = ctypes.c_uint64
         _lib = L
@@ -101,6 +102,18 @@ def grid_params(pos, diam, box_edge_min=0.0):
     if rc:
         raise OracleError(rc)
     return dict(L=g.L, L2=g.L2, inv=g.inv, lo=tuple(g.lo), hi=tuple(g.hi))
+
+
+def box_coords(pos, diam, box_edge_min=0.0):
+    """O2: integer box coordinates of every agent under the grid of O1."""
+    pos, diam = _c(pos), _c(diam)
+    g = Grid()
+    rc = lib().orc_grid_params(len(diam), _ptr(pos), _ptr(diam), box_edge_min, ctypes.byref(g))
+    if rc:
+        raise OracleError(rc)
+    b = np.zeros((len(diam), 3), np.int64)
+    lib().orc_box_coords(len(diam), _ptr(pos), ctypes.byref(g), _ptr(b, _i64p))
+    return b
 
 
 class OracleError(RuntimeError):

@@ -1,0 +1,292 @@
+"""Thin Python binding of libbdm.so (include/bdm.h) -- argument marshalling only.
+
+Every step of the mechanical-interaction path runs in the CUDA kernels of libbdm.so; this module
+never computes any part of it and has no fallback: if the library is missing or no CUDA device
+is present, the calls raise.
+
+Functions carry the C names (bdm_init, bdm_grid_build, bdm_mech_step, bdm_get_displacements, ...).
+Arrays may be NumPy arrays (host; copied by the library) or CUDA torch tensors (passed as device
+pointers with BDM_DEVICE_PTRS on the handle's stream).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libbdm.so")
+HEADER = os.path.join(ROOT, "include", "bdm.h")
+
+BDM_OK = 0
+BDM_EINVAL = -1
+BDM_ESTATE = -2
+BDM_ENOMEM = -3
+BDM_ECUDA = -4
+BDM_ENONFINITE = -6
+BDM_ERANGE = -7
+BDM_ETRUNC = -8
+BDM_DEVICE_PTRS = 0x1
+BDM_RECORD = 0x2
+BDM_NEIGHBOR = 0
+BDM_CONTACT = 1
+
+ERRNAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -6: "ENONFINITE", -7: "ERANGE", -8: "ETRUNC"}
+
+
+class BdmError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"BDM_{ERRNAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class bdm_params(ctypes.Structure):
+    _fields_ = [("k_rep", ctypes.c_double), ("gamma_att", ctypes.c_double), ("adherence", ctypes.c_double),
+                ("dt", ctypes.c_double), ("eta", ctypes.c_double), ("max_disp", ctypes.c_double),
+                ("box_edge_min", ctypes.c_double), ("flags", ctypes.c_uint32), ("device", ctypes.c_int32)]
+
+
+class bdm_grid_info(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double), ("L2", ctypes.c_double), ("inv", ctypes.c_double),
+                ("lo", ctypes.c_int32 * 3), ("hi", ctypes.c_int32 * 3), ("n_boxes", ctypes.c_int64),
+                ("n_agents", ctypes.c_int64)]
+
+
+class bdm_agent_stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("n_cand", "n_nb", "n_ct", "branch", "nb_hash", "ct_hash")]
+
+
+_vp = ctypes.c_void_p
+_SIGS = {
+    "bdm_abi_version": ([], ctypes.c_int),
+    "bdm_params_default": ([ctypes.POINTER(bdm_params)], ctypes.c_int),
+    "bdm_init": ([ctypes.POINTER(_vp), ctypes.c_int64, _vp, _vp, ctypes.POINTER(bdm_params)], ctypes.c_int),
+    "bdm_grid_build": ([_vp], ctypes.c_int),
+    "bdm_mech_step": ([_vp, ctypes.c_int32], ctypes.c_int),
+    "bdm_get_displacements": ([_vp, _vp], ctypes.c_int),
+    "bdm_get_positions": ([_vp, _vp], ctypes.c_int),
+    "bdm_get_box_coords": ([_vp, _vp], ctypes.c_int),
+    "bdm_get_grid_info": ([_vp, ctypes.POINTER(bdm_grid_info)], ctypes.c_int),
+    "bdm_get_agent_stats": ([_vp, ctypes.POINTER(bdm_agent_stats)], ctypes.c_int),
+    "bdm_get_pairs": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, ctypes.c_int64], ctypes.c_int),
+    "bdm_set_agents": ([_vp, _vp, _vp], ctypes.c_int),
+    "bdm_set_stream": ([_vp, _vp], ctypes.c_int),
+    "bdm_sync": ([_vp], ctypes.c_int),
+    "bdm_set_timing": ([_vp, ctypes.c_int], ctypes.c_int),
+    "bdm_get_timing": ([_vp, _vp], ctypes.c_int),
+    "bdm_generate_uniform": ([ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, ctypes.c_double,
+                              ctypes.c_double, _vp, _vp, _vp], ctypes.c_int),
+    "bdm_last_error": ([_vp], ctypes.c_char_p),
+    "bdm_destroy": ([_vp], None),
+}
+
+_lib = None
+
+
+def load_library():
+    """Load libbdm.so (raises if it has not been built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `make` or __graft_entry__.build() first")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    return _lib
+
+
+def header_symbols(path: str = HEADER) -> list[str]:
+    """Function names declared in include/bdm.h."""
+    txt = open(path).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(bdm_\w+)\s*\(", txt, flags=re.M)))
+
+
+def _check(rc: int, h=None):
+    if rc != BDM_OK:
+        msg = load_library().bdm_last_error(h)
+        raise BdmError(rc, msg.decode() if msg else "")
+
+
+def bdm_params_default(**overrides) -> bdm_params:
+    p = bdm_params()
+    _check(load_library().bdm_params_default(ctypes.byref(p)))
+    for k, v in overrides.items():
+        setattr(p, k, v)
+    return p
+
+
+def _is_torch(a) -> bool:
+    return type(a).__module__.startswith("torch")
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if _is_torch(a):
+        return ctypes.c_void_p(a.data_ptr())
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class Handle:
+    """Owns a bdm_handle; destroyed with the object."""
+
+    def __init__(self, raw: ctypes.c_void_p, n: int, device_ptrs: bool):
+        self.raw = raw
+        self.n = n
+        self.device_ptrs = device_ptrs
+
+    def __del__(self):
+        if getattr(self, "raw", None) and _lib is not None:
+            _lib.bdm_destroy(self.raw)
+            self.raw = None
+
+    def close(self):
+        self.__del__()
+
+
+def bdm_init(pos, diam, params: bdm_params | None = None, stream=None) -> Handle:
+    """pos [n,3] fp64 and diam [n] fp64, NumPy (host) or CUDA torch tensors (device pointers)."""
+    lib = load_library()
+    p = params if params is not None else bdm_params_default()
+    dev = _is_torch(pos) and pos.is_cuda
+    if dev:
+        import torch
+
+        assert pos.dtype == torch.float64 and diam.dtype == torch.float64 and pos.is_contiguous()
+        p.flags |= BDM_DEVICE_PTRS
+        if p.device < 0:
+            p.device = pos.device.index
+        n = pos.shape[0]
+    else:
+        p.flags &= ~BDM_DEVICE_PTRS
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        diam = np.ascontiguousarray(diam, dtype=np.float64).reshape(-1)
+        n = pos.shape[0]
+        if diam.shape[0] != n:
+            raise ValueError("pos and diam lengths differ")
+    raw = ctypes.c_void_p()
+    if dev and stream is not None:
+        # the copy kernel of bdm_init runs on the default stream; order it after the producer
+        stream.synchronize()
+    _check(lib.bdm_init(ctypes.byref(raw), n, _ptr(pos), _ptr(diam), ctypes.byref(p)))
+    h = Handle(raw, n, dev)
+    if stream is not None:
+        bdm_set_stream(h, stream)
+    return h
+
+
+def bdm_set_agents(h: Handle, pos, diam) -> None:
+    """Replace the population (same n); host arrays or CUDA tensors matching the handle's mode."""
+    if not h.device_ptrs:
+        pos = np.ascontiguousarray(pos, dtype=np.float64)
+        diam = np.ascontiguousarray(diam, dtype=np.float64)
+    _check(load_library().bdm_set_agents(h.raw, _ptr(pos), _ptr(diam)), h.raw)
+
+
+def bdm_set_stream(h: Handle, stream) -> None:
+    sp = getattr(stream, "cuda_stream", stream)
+    _check(load_library().bdm_set_stream(h.raw, ctypes.c_void_p(sp)), h.raw)
+
+
+def bdm_grid_build(h: Handle) -> None:
+    _check(load_library().bdm_grid_build(h.raw), h.raw)
+
+
+def bdm_mech_step(h: Handle, n_steps: int = 1) -> None:
+    _check(load_library().bdm_mech_step(h.raw, n_steps), h.raw)
+
+
+def bdm_sync(h: Handle) -> None:
+    _check(load_library().bdm_sync(h.raw), h.raw)
+
+
+def _out(h: Handle, shape, dtype, out):
+    if out is not None:
+        return out
+    if h.device_ptrs:
+        import torch
+
+        tdt = {np.float64: torch.float64, np.int32: torch.int32, np.int8: torch.int8, np.uint64: torch.int64}[dtype]
+        return torch.empty(shape, dtype=tdt, device="cuda")
+    return np.empty(shape, dtype=dtype)
+
+
+def bdm_get_displacements(h: Handle, out=None):
+    out = _out(h, (h.n, 3), np.float64, out)
+    _check(load_library().bdm_get_displacements(h.raw, _ptr(out)), h.raw)
+    return out
+
+
+def bdm_get_positions(h: Handle, out=None):
+    out = _out(h, (h.n, 3), np.float64, out)
+    _check(load_library().bdm_get_positions(h.raw, _ptr(out)), h.raw)
+    return out
+
+
+def bdm_get_box_coords(h: Handle, out=None):
+    out = _out(h, (h.n, 3), np.int32, out)
+    _check(load_library().bdm_get_box_coords(h.raw, _ptr(out)), h.raw)
+    return out
+
+
+def bdm_get_grid_info(h: Handle) -> dict:
+    g = bdm_grid_info()
+    _check(load_library().bdm_get_grid_info(h.raw, ctypes.byref(g)), h.raw)
+    return dict(L=g.L, L2=g.L2, inv=g.inv, lo=tuple(g.lo), hi=tuple(g.hi), n_boxes=g.n_boxes, n_agents=g.n_agents)
+
+
+def bdm_get_agent_stats(h: Handle) -> dict:
+    """Per-agent record of the last step (host NumPy arrays; requires BDM_RECORD)."""
+    if h.device_ptrs:
+        import torch
+
+        out = dict(n_cand=torch.empty(h.n, dtype=torch.int32, device="cuda"),
+                   n_nb=torch.empty(h.n, dtype=torch.int32, device="cuda"),
+                   n_ct=torch.empty(h.n, dtype=torch.int32, device="cuda"),
+                   branch=torch.empty(h.n, dtype=torch.int8, device="cuda"),
+                   nb_hash=torch.empty(h.n, dtype=torch.int64, device="cuda"),
+                   ct_hash=torch.empty(h.n, dtype=torch.int64, device="cuda"))
+    else:
+        out = dict(n_cand=np.empty(h.n, np.int32), n_nb=np.empty(h.n, np.int32), n_ct=np.empty(h.n, np.int32),
+                   branch=np.empty(h.n, np.int8), nb_hash=np.empty(h.n, np.uint64), ct_hash=np.empty(h.n, np.uint64))
+    st = bdm_agent_stats(*(_ptr(out[k]).value for k in ("n_cand", "n_nb", "n_ct", "branch", "nb_hash", "ct_hash")))
+    _check(load_library().bdm_get_agent_stats(h.raw, ctypes.byref(st)), h.raw)
+    return out
+
+
+def bdm_get_pairs(h: Handle, kind: int) -> np.ndarray:
+    """Sorted unordered pairs (min id, max id) as int64 [P, 2] (host)."""
+    lib = load_library()
+    cnt = ctypes.c_int64(0)
+    rc = lib.bdm_get_pairs(h.raw, kind, ctypes.byref(cnt), None, 0)
+    if rc not in (BDM_OK, BDM_ETRUNC):
+        _check(rc, h.raw)
+    out = np.empty((max(cnt.value, 1), 2), np.int64)
+    _check(lib.bdm_get_pairs(h.raw, kind, ctypes.byref(cnt), _ptr(out), cnt.value), h.raw)
+    return out[: cnt.value]
+
+
+def bdm_set_timing(h: Handle, enabled: bool = True) -> None:
+    _check(load_library().bdm_set_timing(h.raw, int(enabled)), h.raw)
+
+
+def bdm_get_timing(h: Handle) -> dict:
+    """Device ms of the grid-build and force kernels summed over the steps since the last call."""
+    out = np.zeros(4)
+    _check(load_library().bdm_get_timing(h.raw, _ptr(out)), h.raw)
+    return dict(grid_ms=float(out[0]), force_ms=float(out[1]), steps=int(out[2]), launches=int(out[3]))
+
+
+def bdm_generate_uniform(seed: int, id0: int, n: int, lo3, hi3, dlo: float, dhi: float, pos, diam, stream=None):
+    """Counter-hash population on the device (pos, diam are CUDA torch tensors)."""
+    lo = np.ascontiguousarray(lo3, np.float64)
+    hi = np.ascontiguousarray(hi3, np.float64)
+    sp = getattr(stream, "cuda_stream", stream) if stream is not None else None
+    _check(load_library().bdm_generate_uniform(seed, id0, n, _ptr(lo), _ptr(hi), dlo, dhi, _ptr(pos), _ptr(diam),
+                                               ctypes.c_void_p(sp) if sp else None))

@@ -1,0 +1,714 @@
+// bdm_capi.cu -- host runtime behind include/bdm.h (libbdm.so).
+//
+// Owns the device state of one population, sequences the kernels of bdm_kernels.cuh on one
+// CUDA stream and maps every failure to a BDM_E* code (never aborts).  Device layout:
+//   agents  double4 (x, y, z, D), 32 B = one sector per agent, two buffers (sorted / stepped)
+//   ids     uint32, two buffers (agent id = input index)
+//   table   uint32[n_boxes + 1]: per-box count, scanned in place into the start table
+//   sort    key / slot / tsrc / tid / tkey uint32 scratch
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/bdm.h"
+#include "bdm_kernels.cuh"
+
+using namespace bdm;
+
+namespace {
+
+thread_local std::string g_tls_error;
+
+enum class State { NoGrid, Fresh, Stepped };
+
+struct TimedStep {
+  cudaEvent_t e0, e1, e2;
+};
+
+}  // namespace
+
+struct bdm_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bdm_params prm{};
+  int64_t n = 0;
+  // state buffers: 'srt' holds the box-sorted agents after a grid build; 'cur' holds the newest
+  // positions (after a step: in srt's order, ids shared with srt).
+  double4* ag[2] = {nullptr, nullptr};
+  uint32_t* id[2] = {nullptr, nullptr};
+  int cur = 0;  // index of the buffer holding the newest state
+  uint32_t *key = nullptr, *slot = nullptr, *tsrc = nullptr, *tid = nullptr, *tkey = nullptr;
+  uint32_t* table = nullptr;
+  size_t table_cap = 0;  // entries
+  unsigned long long* scan_state = nullptr;
+  uint32_t* scan_ticket = nullptr;
+  size_t scan_tiles_cap = 0;
+  double* dp = nullptr;
+  double* stage = nullptr;  // 4n fp64 staging for host-pointer inputs/outputs (lazily allocated)
+  bool have_dp = false;
+  const uint32_t* out_ids = nullptr;  // id buffer matching the order of dp / record arrays
+  Extents* ext = nullptr;      // device
+  Extents* ext_host = nullptr;  // pinned mirror
+  bool ext_valid = false;       // ext describes ag[cur]
+  ErrDev* err = nullptr;
+  ErrDev* err_host = nullptr;
+  unsigned long long* maxd_bits = nullptr;
+  GridDev grid{};
+  bool have_grid = false;
+  State state = State::NoGrid;
+  bool poisoned = false;
+  // BDM_RECORD
+  int32_t *r_cand = nullptr, *r_nb = nullptr, *r_ct = nullptr;
+  int8_t* r_branch = nullptr;
+  unsigned long long *r_nbh = nullptr, *r_cth = nullptr;
+  bool have_record = false;
+  // timing
+  bool timing = false;
+  int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
+  std::vector<TimedStep> timed;
+  std::string error;
+};
+
+namespace {
+
+int fail(bdm_ctx* h, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (h)
+    h->error = buf;
+  g_tls_error = buf;
+  return code;
+}
+
+#define CU(h, call)                                                                           \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      (void)cudaGetLastError();                                                               \
+      return fail((h), e_ == cudaErrorMemoryAllocation ? BDM_ENOMEM : BDM_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
+    }                                                                                         \
+  } while (0)
+
+template <typename T>
+int dalloc(bdm_ctx* h, T** p, size_t count) {
+  if (count == 0) count = 1;
+  CU(h, cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T)));
+  return BDM_OK;
+}
+
+unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+bool params_ok(const bdm_params* p) {
+  auto fin = [](double v) { return std::isfinite(v); };
+  return p && p->eta > 0.0 && p->max_disp > 0.0 && fin(p->eta) && fin(p->max_disp) && p->k_rep >= 0.0 &&
+         fin(p->k_rep) && p->gamma_att >= 0.0 && fin(p->gamma_att) && p->adherence >= 0.0 && fin(p->adherence) &&
+         p->dt >= 0.0 && fin(p->dt) && p->box_edge_min >= 0.0 && fin(p->box_edge_min);
+}
+
+ParamsDev params_dev(const bdm_params& p) {
+  ParamsDev d;
+  d.k_rep = p.k_rep;
+  d.gamma_att = p.gamma_att;
+  d.adherence = p.adherence;
+  d.c = p.dt / p.eta;
+  d.max_disp = p.max_disp;
+  return d;
+}
+
+// Collect asynchronous device errors (after a stream sync).
+int check_async(bdm_ctx* h) {
+  CU(h, cudaMemcpyAsync(h->err_host, h->err, sizeof(ErrDev), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->err_host->code) {
+    h->poisoned = true;
+    if (h->err_host->code == 1u)
+      return fail(h, BDM_EINVAL, "invalid agent %u: diameter must be > 0 and finite, positions finite",
+                  h->err_host->first_bad);
+    if (h->err_host->code == 6u)
+      return fail(h, BDM_ENONFINITE, "non-finite force on agent %u", h->err_host->first_bad);
+    return fail(h, BDM_ECUDA, "device error code %u", h->err_host->code);
+  }
+  return BDM_OK;
+}
+
+int ensure_table(bdm_ctx* h, size_t entries) {
+  if (entries > h->table_cap) {
+    if (h->table) CU(h, cudaFree(h->table));
+    h->table = nullptr;
+    size_t cap = entries + entries / 8 + 1024;
+    CU(h, cudaMalloc(&h->table, cap * sizeof(uint32_t)));
+    h->table_cap = cap;
+  }
+  size_t tiles = (entries + SCAN_TILE - 1) / SCAN_TILE;
+  if (tiles > h->scan_tiles_cap) {
+    if (h->scan_state) CU(h, cudaFree(h->scan_state));
+    h->scan_state = nullptr;
+    size_t cap = tiles + tiles / 8 + 16;
+    CU(h, cudaMalloc(&h->scan_state, cap * sizeof(unsigned long long)));
+    h->scan_tiles_cap = cap;
+  }
+  return BDM_OK;
+}
+
+// Grid parameters from the (already reduced) extents of ag[cur]; one small D2H per build.
+int compute_extents(bdm_ctx* h) {
+  uint32_t n = (uint32_t)h->n;
+  if (!h->ext_valid) {
+    k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
+    k_extents<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], n, h->grid.inv, h->ext);
+    CU(h, cudaGetLastError());
+    h->launches += 2;
+  }
+  CU(h, cudaMemcpyAsync(h->ext_host, h->ext, sizeof(Extents), cudaMemcpyDeviceToHost, h->stream));
+  int rc = check_async(h);  // synchronises
+  if (rc) return rc;
+  if (h->ext_host->range_err) {
+    h->poisoned = true;
+    return fail(h, BDM_ERANGE, "an agent lies >= 2^20 boxes from the origin (|p*inv| >= 2^20, DESIGN.md R9)");
+  }
+  GridDev& g = h->grid;
+  int64_t dims[3];
+  for (int a = 0; a < 3; ++a) {
+    g.lo[a] = h->ext_host->lo[a];
+    g.hi[a] = h->ext_host->hi[a];
+    dims[a] = (int64_t)g.hi[a] - g.lo[a] + 1;
+  }
+  int64_t nb = dims[0] * dims[1] * dims[2];
+  if (nb >= (int64_t)0xffffffffll) return fail(h, BDM_ERANGE, "n_boxes = %lld >= 2^32", (long long)nb);
+  g.ny = (int32_t)dims[1];
+  g.nz = (int32_t)dims[2];
+  g.n_boxes = (uint32_t)nb;
+  h->ext_valid = true;
+  return BDM_OK;
+}
+
+int grid_build(bdm_ctx* h) {
+  if (h->poisoned) return fail(h, BDM_ESTATE, "handle poisoned by an earlier error: %s", h->error.c_str());
+  if (h->state == State::Fresh) return BDM_OK;  // positions unchanged since the last build
+  if (h->n == 0) {
+    h->state = State::Fresh;
+    h->have_grid = true;
+    return BDM_OK;
+  }
+  int rc = compute_extents(h);
+  if (rc) return rc;
+  const uint32_t n = (uint32_t)h->n;
+  const size_t items = (size_t)h->grid.n_boxes + 1;
+  rc = ensure_table(h, items);
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  const int src = h->cur, dst = 1 - h->cur;
+  CU(h, cudaMemsetAsync(h->table, 0, items * sizeof(uint32_t), s));
+  k_key_hist<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, h->grid, h->key, h->slot, h->table);
+  size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
+  CU(h, cudaMemsetAsync(h->scan_state, 0, tiles * sizeof(unsigned long long), s));
+  CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), s));
+  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(h->table, items, h->scan_state, h->scan_ticket);
+  k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
+  k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
+                                         h->id[dst]);
+  CU(h, cudaGetLastError());
+  h->launches += 4;
+  h->cur = dst;  // sorted buffer is now the newest state
+  h->state = State::Fresh;
+  h->have_grid = true;
+  return BDM_OK;
+}
+
+int force_step(bdm_ctx* h, bool want_dp) {
+  const uint32_t n = (uint32_t)h->n;
+  cudaStream_t s = h->stream;
+  const int src = h->cur, dst = 1 - h->cur;
+  k_ext_reset<<<1, 32, 0, s>>>(h->ext);
+  RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
+  ParamsDev pd = params_dev(h->prm);
+  double* dp = want_dp ? h->dp : nullptr;
+  if (h->prm.flags & BDM_RECORD)
+    k_force<true><<<blocks(n, FORCE_THREADS), FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, n, h->grid,
+                                                                    pd, h->ag[dst], dp, h->ext, h->err, rec);
+  else
+    k_force<false><<<blocks(n, FORCE_THREADS), FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, n,
+                                                                     h->grid, pd, h->ag[dst], dp, h->ext, h->err,
+                                                                     rec);
+  CU(h, cudaGetLastError());
+  h->launches += 2;
+  // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
+  // pointers (the kernel already captured its arguments) instead of copying.
+  h->out_ids = h->id[src];
+  std::swap(h->id[src], h->id[dst]);
+  h->cur = dst;
+  h->ext_valid = true;
+  h->state = State::Stepped;
+  if (want_dp) h->have_dp = true;
+  if (h->prm.flags & BDM_RECORD) h->have_record = true;
+  return BDM_OK;
+}
+
+int copy_out(bdm_ctx* h, void* dst, const void* dev_src, size_t bytes) {
+  if (h->prm.flags & BDM_DEVICE_PTRS) {
+    CU(h, cudaMemcpyAsync(dst, dev_src, bytes, cudaMemcpyDeviceToDevice, h->stream));
+    return BDM_OK;
+  }
+  CU(h, cudaMemcpyAsync(dst, dev_src, bytes, cudaMemcpyDeviceToHost, h->stream));
+  return check_async(h);  // synchronises and surfaces device-side errors
+}
+
+// Scratch device buffer for id-order outputs when the caller passed host pointers.
+struct Scratch {
+  void* p = nullptr;
+  ~Scratch() {
+    if (p) cudaFree(p);
+  }
+};
+
+int staging(bdm_ctx* h) {
+  if (!h->stage) return dalloc(h, &h->stage, 4 * (size_t)h->n);
+  return BDM_OK;
+}
+
+// Copy (or adopt) the population, validate it on the device and derive the box edge (O1).
+int upload(bdm_ctx* h, const double* pos, const double* diam) {
+  const int64_t n = h->n;
+  const size_t N = (size_t)n;
+  h->have_dp = false;
+  h->have_record = false;
+  h->ext_valid = false;
+  h->state = State::NoGrid;
+  h->have_grid = false;
+  h->cur = 0;
+  if (n > 0) {
+    const double *dpos = pos, *ddiam = diam;
+    if (!(h->prm.flags & BDM_DEVICE_PTRS)) {
+      int rc = staging(h);
+      if (rc) return rc;
+      CU(h, cudaMemcpyAsync(h->stage, pos, 3 * N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+      CU(h, cudaMemcpyAsync(h->stage + 3 * N, diam, N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+      dpos = h->stage;
+      ddiam = h->stage + 3 * N;
+    }
+    CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), h->stream));
+    k_pack<<<blocks(n, 256), 256, 0, h->stream>>>(dpos, ddiam, (uint32_t)n, h->ag[0], h->id[0], h->maxd_bits,
+                                                  h->err);
+    CU(h, cudaGetLastError());
+    CU(h, cudaMemcpyAsync(h->ext_host, h->maxd_bits, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          h->stream));
+    int rc = check_async(h);  // synchronises (the scratch copies are freed after)
+    if (rc) return rc;
+    double maxd;
+    std::memcpy(&maxd, h->ext_host, sizeof maxd);
+    // O1: L = max(max D, box_edge_min); inv = 1/(L*(1+2^-30))
+    double L = std::max(maxd, h->prm.box_edge_min);
+    h->grid.L = L;
+    h->grid.L2 = L * L;
+    h->grid.inv = 1.0 / (L * (1.0 + 0x1p-30));
+    h->grid.thr_pad = 0.5 * L;
+  } else {
+    double L = h->prm.box_edge_min;
+    h->grid.L = L;
+    h->grid.L2 = L * L;
+    h->grid.inv = L > 0 ? 1.0 / (L * (1.0 + 0x1p-30)) : 0.0;
+  }
+  return BDM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bdm_abi_version(void) { return BDM_ABI_VERSION; }
+
+int bdm_params_default(bdm_params* p) {
+  if (!p) return fail(nullptr, BDM_EINVAL, "bdm_params_default: NULL");
+  p->k_rep = 10.0;
+  p->gamma_att = 4.0;
+  p->adherence = 0.1;
+  p->dt = 1.0;
+  p->eta = 1.0;
+  p->max_disp = 3.0;
+  p->box_edge_min = 0.0;
+  p->flags = 0;
+  p->device = -1;
+  return BDM_OK;
+}
+
+const char* bdm_last_error(bdm_handle h) { return h ? h->error.c_str() : g_tls_error.c_str(); }
+
+void bdm_destroy(bdm_handle h) {
+  if (!h) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->stream);
+  for (auto& t : h->timed) {
+    cudaEventDestroy(t.e0);
+    cudaEventDestroy(t.e1);
+    cudaEventDestroy(t.e2);
+  }
+  void* ptrs[] = {h->ag[0], h->ag[1], h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->r_branch, h->r_nbh, h->r_cth};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (h->ext_host) cudaFreeHost(h->ext_host);
+  if (h->err_host) cudaFreeHost(h->err_host);
+  cudaSetDevice(prev);
+  delete h;
+}
+
+int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, const bdm_params* p) {
+  if (!out) return fail(nullptr, BDM_EINVAL, "bdm_init: handle pointer is NULL");
+  *out = nullptr;
+  if (n < 0) return fail(nullptr, BDM_EINVAL, "bdm_init: n = %lld < 0", (long long)n);
+  if (n > 0 && (!pos || !diam)) return fail(nullptr, BDM_EINVAL, "bdm_init: NULL array with n > 0");
+  if (!params_ok(p)) return fail(nullptr, BDM_EINVAL, "bdm_init: invalid params (eta, max_disp must be > 0; all finite, >= 0)");
+  if (n >= (int64_t)0xffffffffll) return fail(nullptr, BDM_ERANGE, "bdm_init: n >= 2^32 - 1 agents per handle");
+  bdm_ctx* h = new (std::nothrow) bdm_ctx();
+  if (!h) return fail(nullptr, BDM_ENOMEM, "bdm_init: host allocation");
+  h->prm = *p;
+  h->n = n;
+  int dev = p->device;
+  if (dev < 0) {
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+      (void)cudaGetLastError();
+      delete h;
+      return fail(nullptr, BDM_ECUDA, "bdm_init: no CUDA device");
+    }
+  }
+  h->device = dev;
+  int rc = BDM_OK;
+#define TRY(x)                   \
+  do {                           \
+    rc = (x);                    \
+    if (rc) {                    \
+      g_tls_error = h->error;    \
+      bdm_destroy(h);            \
+      return rc;                 \
+    }                            \
+  } while (0)
+  if (cudaSetDevice(dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    delete h;
+    return fail(nullptr, BDM_ECUDA, "bdm_init: cudaSetDevice(%d) failed", dev);
+  }
+  h->stream = nullptr;  // legacy default stream until bdm_set_stream
+  const size_t N = (size_t)n;
+  TRY(dalloc(h, &h->ag[0], N));
+  TRY(dalloc(h, &h->ag[1], N));
+  TRY(dalloc(h, &h->id[0], N));
+  TRY(dalloc(h, &h->id[1], N));
+  TRY(dalloc(h, &h->key, N));
+  TRY(dalloc(h, &h->slot, N));
+  TRY(dalloc(h, &h->tsrc, N));
+  TRY(dalloc(h, &h->tid, N));
+  TRY(dalloc(h, &h->tkey, N));
+  TRY(dalloc(h, &h->dp, 3 * N));
+  TRY(dalloc(h, &h->ext, 1));
+  TRY(dalloc(h, &h->err, 1));
+  TRY(dalloc(h, &h->maxd_bits, 1));
+  TRY(dalloc(h, &h->scan_ticket, 1));
+  if (p->flags & BDM_RECORD) {
+    TRY(dalloc(h, &h->r_cand, N));
+    TRY(dalloc(h, &h->r_nb, N));
+    TRY(dalloc(h, &h->r_ct, N));
+    TRY(dalloc(h, &h->r_branch, N));
+    TRY(dalloc(h, &h->r_nbh, N));
+    TRY(dalloc(h, &h->r_cth, N));
+  }
+  if (cudaMallocHost(&h->ext_host, sizeof(Extents)) != cudaSuccess ||
+      cudaMallocHost(&h->err_host, sizeof(ErrDev)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    TRY(fail(h, BDM_ENOMEM, "bdm_init: pinned host allocation"));
+  }
+  ErrDev e0{0u, 0xffffffffu, 0u, 0u};
+  if (cudaMemcpy(h->err, &e0, sizeof e0, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(h->maxd_bits, 0, sizeof(unsigned long long)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    TRY(fail(h, BDM_ECUDA, "bdm_init: device initialisation"));
+  }
+  TRY(upload(h, pos, diam));
+#undef TRY
+  h->cur = 0;
+  h->state = State::NoGrid;
+  *out = h;
+  return BDM_OK;
+}
+
+int bdm_set_agents(bdm_handle h, const double* pos, const double* diam) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_agents: NULL handle");
+  if (h->n > 0 && (!pos || !diam)) return fail(h, BDM_EINVAL, "bdm_set_agents: NULL array with n > 0");
+  CU(h, cudaSetDevice(h->device));
+  if (h->poisoned) {  // a fresh population clears an earlier data error
+    ErrDev e0{0u, 0xffffffffu, 0u, 0u};
+    CU(h, cudaMemcpyAsync(h->err, &e0, sizeof e0, cudaMemcpyHostToDevice, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    h->poisoned = false;
+  }
+  int rc = upload(h, pos, diam);
+  if (rc) h->poisoned = true;
+  return rc;
+}
+
+int bdm_set_stream(bdm_handle h, void* stream) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_stream: NULL handle");
+  h->stream = static_cast<cudaStream_t>(stream);
+  return BDM_OK;
+}
+
+int bdm_sync(bdm_handle h) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_sync: NULL handle");
+  CU(h, cudaSetDevice(h->device));
+  return check_async(h);
+}
+
+int bdm_grid_build(bdm_handle h) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_grid_build: NULL handle");
+  CU(h, cudaSetDevice(h->device));
+  return grid_build(h);
+}
+
+int bdm_mech_step(bdm_handle h, int32_t n_steps) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_mech_step: NULL handle");
+  if (n_steps < 0) return fail(h, BDM_EINVAL, "bdm_mech_step: n_steps = %d < 0", n_steps);
+  if (h->poisoned) return fail(h, BDM_ESTATE, "handle poisoned by an earlier error: %s", h->error.c_str());
+  CU(h, cudaSetDevice(h->device));
+  if (h->n == 0) {
+    if (n_steps > 0) h->have_dp = true;
+    return BDM_OK;
+  }
+  for (int32_t s = 0; s < n_steps; ++s) {
+    TimedStep ts{};
+    if (h->timing) {
+      CU(h, cudaEventCreate(&ts.e0));
+      CU(h, cudaEventCreate(&ts.e1));
+      CU(h, cudaEventCreate(&ts.e2));
+      h->timed.push_back(ts);
+      CU(h, cudaEventRecord(ts.e0, h->stream));
+    }
+    if (h->state != State::Fresh) {
+      int rc = grid_build(h);
+      if (rc) return rc;
+    }
+    if (h->timing) CU(h, cudaEventRecord(ts.e1, h->stream));
+    int rc = force_step(h, s == n_steps - 1);
+    if (rc) return rc;
+    if (h->timing) CU(h, cudaEventRecord(ts.e2, h->stream));
+  }
+  return BDM_OK;
+}
+
+int bdm_set_timing(bdm_handle h, int enabled) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_timing: NULL handle");
+  h->timing = enabled != 0;
+  return BDM_OK;
+}
+
+int bdm_get_timing(bdm_handle h, double* out4) {
+  if (!h || !out4) return fail(h, BDM_EINVAL, "bdm_get_timing: NULL argument");
+  CU(h, cudaSetDevice(h->device));
+  CU(h, cudaStreamSynchronize(h->stream));
+  double grid = 0.0, force = 0.0;
+  for (auto& t : h->timed) {
+    float a = 0.f, b = 0.f;
+    CU(h, cudaEventElapsedTime(&a, t.e0, t.e1));
+    CU(h, cudaEventElapsedTime(&b, t.e1, t.e2));
+    grid += a;
+    force += b;
+    cudaEventDestroy(t.e0);
+    cudaEventDestroy(t.e1);
+    cudaEventDestroy(t.e2);
+  }
+  out4[0] = grid;
+  out4[1] = force;
+  out4[2] = (double)h->timed.size();
+  out4[3] = (double)h->launches;
+  h->timed.clear();
+  h->launches = 0;
+  return BDM_OK;
+}
+
+int bdm_get_displacements(bdm_handle h, double* out) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_displacements: NULL handle");
+  if (!h->have_dp) return fail(h, BDM_ESTATE, "bdm_get_displacements: no step has been run");
+  if (h->n == 0) return BDM_OK;
+  if (!out) return fail(h, BDM_EINVAL, "bdm_get_displacements: NULL output");
+  CU(h, cudaSetDevice(h->device));
+  const uint32_t n = (uint32_t)h->n;
+  const size_t bytes = 3 * (size_t)n * sizeof(double);
+  double* dst = out;
+  if (!(h->prm.flags & BDM_DEVICE_PTRS)) {
+    int rc = staging(h);
+    if (rc) return rc;
+    dst = h->stage;
+  }
+  // dp is stored in the order of the buffer that was stepped into; ids of that order are id[cur]
+  k_unpermute3<<<blocks(n, 256), 256, 0, h->stream>>>(h->dp, h->out_ids, n, dst);
+  CU(h, cudaGetLastError());
+  if (dst != static_cast<void*>(out)) return copy_out(h, out, dst, bytes);
+  return BDM_OK;
+}
+
+int bdm_get_positions(bdm_handle h, double* out) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_positions: NULL handle");
+  if (h->n == 0) return BDM_OK;
+  if (!out) return fail(h, BDM_EINVAL, "bdm_get_positions: NULL output");
+  CU(h, cudaSetDevice(h->device));
+  const uint32_t n = (uint32_t)h->n;
+  const size_t bytes = 3 * (size_t)n * sizeof(double);
+  double* dst = out;
+  if (!(h->prm.flags & BDM_DEVICE_PTRS)) {
+    int rc = staging(h);
+    if (rc) return rc;
+    dst = h->stage;
+  }
+  k_unpermute_pos<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, dst);
+  CU(h, cudaGetLastError());
+  if (dst != static_cast<void*>(out)) return copy_out(h, out, dst, bytes);
+  return BDM_OK;
+}
+
+int bdm_get_box_coords(bdm_handle h, int32_t* out) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_box_coords: NULL handle");
+  if (h->n == 0) return BDM_OK;
+  if (!out) return fail(h, BDM_EINVAL, "bdm_get_box_coords: NULL output");
+  CU(h, cudaSetDevice(h->device));
+  if (h->state != State::Fresh) {
+    int rc = grid_build(h);
+    if (rc) return rc;
+  }
+  const uint32_t n = (uint32_t)h->n;
+  const size_t bytes = 3 * (size_t)n * sizeof(int32_t);
+  int32_t* dst = out;
+  if (!(h->prm.flags & BDM_DEVICE_PTRS)) {
+    int rc = staging(h);
+    if (rc) return rc;
+    dst = reinterpret_cast<int32_t*>(h->stage);
+  }
+  k_box_coords<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->grid.inv, dst);
+  CU(h, cudaGetLastError());
+  if (dst != static_cast<void*>(out)) return copy_out(h, out, dst, bytes);
+  return BDM_OK;
+}
+
+int bdm_get_grid_info(bdm_handle h, bdm_grid_info* out) {
+  if (!h || !out) return fail(h, BDM_EINVAL, "bdm_get_grid_info: NULL argument");
+  if (!h->have_grid) return fail(h, BDM_ESTATE, "bdm_get_grid_info: no grid built yet");
+  out->L = h->grid.L;
+  out->L2 = h->grid.L2;
+  out->inv = h->grid.inv;
+  int64_t nb = h->n ? 1 : 1;
+  for (int a = 0; a < 3; ++a) {
+    out->lo[a] = h->n ? h->grid.lo[a] : 0;
+    out->hi[a] = h->n ? h->grid.hi[a] : 0;
+    nb *= (int64_t)out->hi[a] - out->lo[a] + 1;
+  }
+  out->n_boxes = nb;
+  out->n_agents = h->n;
+  return BDM_OK;
+}
+
+int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out) {
+  if (!h || !out) return fail(h, BDM_EINVAL, "bdm_get_agent_stats: NULL argument");
+  if (!(h->prm.flags & BDM_RECORD) || !h->have_record)
+    return fail(h, BDM_ESTATE, "bdm_get_agent_stats: needs BDM_RECORD at init and one step");
+  if (h->n == 0) return BDM_OK;
+  CU(h, cudaSetDevice(h->device));
+  const uint32_t n = (uint32_t)h->n;
+  const uint32_t* ids = h->out_ids;
+  const bool dev = h->prm.flags & BDM_DEVICE_PTRS;
+  auto one = [&](auto* src, auto* dst) -> int {
+    using T = std::remove_pointer_t<decltype(src)>;
+    if (!dst) return BDM_OK;
+    Scratch sc;
+    T* d = reinterpret_cast<T*>(dst);
+    if (!dev) {
+      CU(h, cudaMalloc(&sc.p, n * sizeof(T)));
+      d = static_cast<T*>(sc.p);
+    }
+    k_unpermute1<T><<<blocks(n, 256), 256, 0, h->stream>>>(src, ids, n, d);
+    CU(h, cudaGetLastError());
+    if (!dev) return copy_out(h, dst, sc.p, n * sizeof(T));
+    return BDM_OK;
+  };
+  int rc;
+  if ((rc = one(h->r_cand, out->n_cand))) return rc;
+  if ((rc = one(h->r_nb, out->n_nb))) return rc;
+  if ((rc = one(h->r_ct, out->n_ct))) return rc;
+  if ((rc = one(h->r_branch, out->branch))) return rc;
+  if ((rc = one(h->r_nbh, reinterpret_cast<unsigned long long*>(out->nb_hash)))) return rc;
+  if ((rc = one(h->r_cth, reinterpret_cast<unsigned long long*>(out->ct_hash)))) return rc;
+  return check_async(h);
+}
+
+int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_t cap) {
+  if (!h || !n_pairs) return fail(h, BDM_EINVAL, "bdm_get_pairs: NULL argument");
+  if (kind != BDM_NEIGHBOR && kind != BDM_CONTACT) return fail(h, BDM_EINVAL, "bdm_get_pairs: bad kind %d", kind);
+  if (cap < 0 || (cap > 0 && !out)) return fail(h, BDM_EINVAL, "bdm_get_pairs: bad output buffer");
+  *n_pairs = 0;
+  if (h->n == 0) return BDM_OK;
+  CU(h, cudaSetDevice(h->device));
+  if (h->state != State::Fresh) {
+    int rc = grid_build(h);
+    if (rc) return rc;
+  }
+  const uint32_t n = (uint32_t)h->n;
+  ParamsDev pd = params_dev(h->prm);
+  Scratch sc_counts, sc_off, sc_out;
+  CU(h, cudaMalloc(&sc_counts.p, n * sizeof(uint32_t)));
+  k_pairs<<<blocks(n, 128), 128, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], h->table, n, h->grid, pd, kind,
+                                                 static_cast<uint32_t*>(sc_counts.p), nullptr, nullptr);
+  CU(h, cudaGetLastError());
+  std::vector<uint32_t> counts(n);
+  CU(h, cudaMemcpyAsync(counts.data(), sc_counts.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  std::vector<unsigned long long> off(n);
+  unsigned long long total = 0;
+  for (uint32_t i = 0; i < n; ++i) {
+    off[i] = total;
+    total += counts[i];
+  }
+  *n_pairs = (int64_t)total;
+  if ((int64_t)total > cap) return fail(h, BDM_ETRUNC, "bdm_get_pairs: %llu pairs > cap %lld", total, (long long)cap);
+  if (total == 0) return BDM_OK;
+  CU(h, cudaMalloc(&sc_off.p, n * sizeof(unsigned long long)));
+  CU(h, cudaMalloc(&sc_out.p, 2 * total * sizeof(long long)));
+  CU(h, cudaMemcpyAsync(sc_off.p, off.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, h->stream));
+  k_pairs<<<blocks(n, 128), 128, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], h->table, n, h->grid, pd, kind,
+                                                 nullptr, static_cast<unsigned long long*>(sc_off.p),
+                                                 static_cast<long long*>(sc_out.p));
+  CU(h, cudaGetLastError());
+  CU(h, cudaMemcpyAsync(out, sc_out.p, 2 * total * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  struct P {
+    int64_t a, b;
+  };
+  P* pp = reinterpret_cast<P*>(out);
+  std::sort(pp, pp + total, [](const P& x, const P& y) { return x.a != y.a ? x.a < y.a : x.b < y.b; });
+  return BDM_OK;
+}
+
+int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo3, const double* hi3, double dlo,
+                         double dhi, double* pos, double* diam, void* stream) {
+  if (n < 0 || id0 < 0 || !lo3 || !hi3 || (n > 0 && (!pos || !diam)))
+    return fail(nullptr, BDM_EINVAL, "bdm_generate_uniform: bad arguments");
+  if (n == 0) return BDM_OK;
+  unsigned nb = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 64);
+  k_gen_uniform<<<nb, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, id0, n, lo3[0], lo3[1], lo3[2], hi3[0],
+                                                                   hi3[1], hi3[2], dlo, dhi, pos, diam);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(nullptr, BDM_ECUDA, "bdm_generate_uniform: %s", cudaGetErrorString(e));
+  return BDM_OK;
+}
+
+}  // extern "C"
