@@ -1,0 +1,331 @@
+#!/usr/bin/env python
+"""bench.py -- agent mechanical updates/s of the B200-native BioDynaMo mechanical step.
+
+One bench "step" is one full pass of the hot path (grid rebuild, 27-box search, force,
+displacement, position update) over the whole population.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl bdm|reference]
+
+Default workload: BASELINE.json configs[2] (cfg3, 2e7 agents, Gaussian spheroid) -- the config
+BASELINE.json's metric ("at 1/2/4/8 B200") is quoted on; it fits one GPU.  Rank 0 prints ONE
+JSON line.  --impl reference times the CPU oracle (oracle/, the base contract's reference arm)
+on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import bdm_inputs  # noqa: E402
+
+METRIC = "agent mechanical updates/sec at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "agent-updates/s"
+WORKLOADS = {
+    1: "cfg1 (BASELINE configs[0]): 4096 agents U[0,160)^3 um, D~U[8,12)",
+    2: "cfg2 (BASELINE configs[1]): 1e6 agents, 100^3 lattice 10 um, jitter U[-2,2), D~U[9,11)",
+    3: "cfg3 (BASELINE configs[2]): 2e7 agents, Gaussian spheroid sigma=992.2 um, D=lognormal(10,0.15) clipped [6,16]",
+    4: "cfg4 (BASELINE configs[3]): 2e8 agents uniform 8:1:1 slab at 1e-3 um^-3, D~U[8,12)",
+    5: "cfg5 (BASELINE configs[4]): 1e9 agents uniform 1e4^3 um, D~U[8,12)",
+}
+
+# fp64-pipe instruction costs per unit of work (counted from the SASS of k_force)
+FP64_PER_CANDIDATE = 9
+FP64_PER_CONTACT = 44
+FP64_PER_AGENT = 40
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(cfg: int, n: int | None):
+    return bdm_inputs.make_config(cfg, n)
+
+
+# ------------------------------------------------------------------------------------ oracle arm
+def oracle_sample_run(pos, diam, stride: int):
+    """The CPU oracle as it stands on a bounded sample: the whole population is the environment
+    (the oracle rebuilds its grid over all N agents) and every stride-th agent id is updated."""
+    import oracle
+
+    sample = np.arange(0, len(diam), stride, dtype=np.int64)
+    t0 = time.perf_counter()
+    oracle.step(pos, diam, sample=sample, record=False)
+    dt = time.perf_counter() - t0
+    return len(sample), dt, oracle.threads()
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    pos, diam = make_inputs(args.config, args.n)
+    n = len(diam)
+    stride = args.cpu_stride
+    for _ in range(args.warmup):
+        oracle_sample_run(pos, diam, stride)
+    tot_agents, tot_t, threads = 0, 0.0, 1
+    for _ in range(args.steps):
+        m, dt, threads = oracle_sample_run(pos, diam, stride)
+        tot_agents += m
+        tot_t += dt
+    value = tot_agents / tot_t
+    sample = (f"every {stride}th agent id of the {n}-agent workload updated per step (the oracle rebuilds its "
+              f"grid over all {n} agents each step); value = sampled agent-updates / oracle wall time")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_obj(args, n, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_obj(args, n, world):
+    return {"workload": WORKLOADS[args.config], "n_agents": n, "config_index": args.config,
+            "parallelism": f"x-slabs x{world}" if world > 1 else "1 GPU",
+            "l2": "inputs larger than L2 (32 B/agent state)" if n * 32 > 126e6 else "L2 flushed between steps",
+            "params": "k=10 gamma=4 adherence=0.1 dt=1 eta=1 max_disp=3 (DESIGN.md R1-R5)"}
+
+
+# ------------------------------------------------------------------------------------ GPU arm
+def run_bdm(args):
+    import torch
+
+    import paper_2006_06775_b200 as bdm
+
+    world, rank, local = dist_env()
+    if world > 1:
+        from paper_2006_06775_b200 import dist as bdist
+
+        return bdist.bench_multi(args, METRIC, UNIT, config_obj, load_peaks, ClockSampler)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream()
+    pos_h, diam_h = make_inputs(args.config, args.n)
+    n = len(diam_h)
+    pos_d = torch.from_numpy(pos_h).to(dev)
+    diam_d = torch.from_numpy(diam_h).to(dev)
+    torch.cuda.synchronize()
+
+    # work units of one step (algorithmic fp64 ops), from one recorded step at the start state
+    prm = bdm.bdm_params_default(device=local)
+    prm.flags |= bdm.BDM_RECORD
+    hr = bdm.bdm_init(pos_d, diam_d, prm, stream=stream)
+    bdm.bdm_mech_step(hr, 1)
+    st = bdm.bdm_get_agent_stats(hr)
+    n_cand = int(st["n_cand"].sum().item())
+    n_ct = int(st["n_ct"].sum().item())
+    hr.close()
+    del st
+
+    h = bdm.bdm_init(pos_d, diam_d, bdm.bdm_params_default(device=local), stream=stream)
+    bdm.bdm_set_timing(h, True)
+    flush = None
+    if n * 32 <= 126e6:  # state fits in L2: flush it between timed steps
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:  # sampled from warm-up through the timed region
+        time.sleep(0.3)
+        for _ in range(args.warmup):
+            bdm.bdm_mech_step(h, 1)
+        bdm.bdm_sync(h)
+        bdm.bdm_get_timing(h)  # reset sums
+        torch.cuda.synchronize()
+        if flush is None:  # state larger than L2: time the K steps as one bdm_mech_step(K) call
+            evs[0][0].record(stream)
+            bdm.bdm_mech_step(h, args.steps)
+            evs[0][1].record(stream)
+            evs = evs[:1]
+        else:  # state fits in L2: flush it between steps, time each step
+            for k in range(args.steps):
+                flush.add_(1)
+                evs[k][0].record(stream)
+                bdm.bdm_mech_step(h, 1)
+                evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    bdm.bdm_sync(h)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    tm = bdm.bdm_get_timing(h)
+    total_s = sum(step_ms) / 1e3
+    value = n * args.steps / total_s
+
+    peaks, peak_kind = load_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp64_peak = 148 * 64 * sm_max * 1e6  # fp64 lanes x clock
+    force_s = tm["force_ms"] / 1e3 / max(tm["steps"], 1)
+    ops = FP64_PER_CANDIDATE * n_cand + FP64_PER_CONTACT * n_ct + FP64_PER_AGENT * n
+    achieved = ops / force_s
+    grid_s = tm["grid_ms"] / 1e3 / max(tm["steps"], 1)
+    rebuild_bytes = REBUILD_BYTES_PER_AGENT * n
+    rebuild = {"bound": "hbm", "achieved": rebuild_bytes / grid_s / 1e9, "peak": float(peaks["hbm_gbs"]),
+               "unit": "GB/s", "frac": rebuild_bytes / grid_s / 1e9 / float(peaks["hbm_gbs"]),
+               "ms_per_step": grid_s * 1e3, "bytes_per_agent": REBUILD_BYTES_PER_AGENT}
+    del pos_d, diam_d
+
+    # end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = run_e2e(bdm, torch, pos_h, diam_h, local, args)
+    h.close()
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        m, dt, threads = oracle_sample_run(pos_h, diam_h, args.cpu_stride)
+        cpu = {"value": m / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"every {args.cpu_stride}th agent id updated ({m} agents) with the full {n}-agent "
+                         f"population as environment; oracle grid rebuilt over all agents; {dt:.1f} s wall"}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_obj(args, n, 1),
+            "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_peak, "traffic": None, "kernel": "k_force",
+                         "ms_per_launch": force_s * 1e3,
+                         "note": "fp64-pipe ops (9/candidate + 44/contact + 40/agent, DESIGN.md §6.2) over the "
+                                 f"force kernel's event time; peak = 148 SM x 64 fp64 lanes x {sm_max:.0f} MHz "
+                                 f"({peak_kind} sm_max_mhz)",
+                         "units": {"candidates": n_cand, "contacts": n_ct, "agents": n}},
+            "roofline_rebuild": rebuild,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": tm["launches"],
+            "clocks": clk.summary(), "step_ms": [round(x, 4) for x in step_ms]}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# rebuild kernels (K2 key+hist, K3 scan, K4 scatter, place): algorithmic bytes per agent
+# (DESIGN.md §6.1): read state 32 + key/slot 8 | key/slot/id 12 + scatter 12 | place 12 + gather 32
+# + write 36  = 144 B/agent (the box table adds 12 B per box, counted separately in DESIGN.md)
+REBUILD_BYTES_PER_AGENT = 144
+
+
+def run_e2e(bdm, torch, pos_h, diam_h, local, args):
+    n = len(diam_h)
+    pin_pos = torch.from_numpy(pos_h).pin_memory()
+    pin_diam = torch.from_numpy(diam_h).pin_memory()
+    out = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    ppos, pdiam, pout = pin_pos.numpy(), pin_diam.numpy(), out.numpy()
+    h = bdm.bdm_init(ppos, pdiam, bdm.bdm_params_default(device=local))
+    stream = torch.cuda.current_stream()
+    bdm.bdm_set_stream(h, stream)
+
+    def one():
+        bdm.bdm_set_agents(h, ppos, pdiam)  # H2D of this step's inputs
+        bdm.bdm_mech_step(h, 1)
+        bdm.bdm_get_displacements(h, pout)  # D2H of the step's result
+
+    one()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    t0.record(stream)
+    for _ in range(args.e2e_steps):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    ms = t0.elapsed_time(t1)
+    h.close()
+    return {"value": n * args.e2e_steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(pos_h.nbytes + diam_h.nbytes),
+            "d2h_bytes_per_step": int(n * 3 * 8), "steps": args.e2e_steps, "wall_s": wall,
+            "path": "bdm_set_agents(host pinned) -> bdm_mech_step(1) -> bdm_get_displacements(host pinned)"}
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--n", type=int, default=None, help="override N (testing only)")
+    ap.add_argument("--impl", default="bdm", choices=["bdm", "reference"])
+    ap.add_argument("--cpu-stride", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "bdm":
+        print("note: timing rules need >= 3 warm-up steps; raising warmup to 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_bdm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

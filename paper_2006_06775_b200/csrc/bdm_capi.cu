@@ -72,6 +72,7 @@ struct bdm_ctx {
   bool have_record = false;
   // timing
   bool timing = false;
+  int sm_count = 0, force_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
   std::vector<TimedStep> timed;
   std::string error;
@@ -227,6 +228,19 @@ int grid_build(bdm_ctx* h) {
   return BDM_OK;
 }
 
+// Persistent grid: resident blocks per SM x SMs, no more than the work needs.
+unsigned force_grid(bdm_ctx* h, uint32_t n) {
+  if (!h->sm_count) {
+    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<false>, FORCE_THREADS, 0);
+    h->force_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  }
+  unsigned want = (n + FORCE_THREADS - 1) / FORCE_THREADS;
+  unsigned cap = (unsigned)(h->sm_count * h->force_blocks_per_sm);
+  return want < cap ? (want ? want : 1) : cap;
+}
+
 int force_step(bdm_ctx* h, bool want_dp) {
   const uint32_t n = (uint32_t)h->n;
   cudaStream_t s = h->stream;
@@ -235,13 +249,13 @@ int force_step(bdm_ctx* h, bool want_dp) {
   RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
   ParamsDev pd = params_dev(h->prm);
   double* dp = want_dp ? h->dp : nullptr;
+  const unsigned grid = force_grid(h, n);
   if (h->prm.flags & BDM_RECORD)
-    k_force<true><<<blocks(n, FORCE_THREADS), FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, n, h->grid,
-                                                                    pd, h->ag[dst], dp, h->ext, h->err, rec);
+    k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, 0u, n, h->grid, pd, h->ag[dst],
+                                                nullptr, dp, h->ext, h->err, rec);
   else
-    k_force<false><<<blocks(n, FORCE_THREADS), FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, n,
-                                                                     h->grid, pd, h->ag[dst], dp, h->ext, h->err,
-                                                                     rec);
+    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, 0u, n, h->grid, pd,
+                                                 h->ag[dst], nullptr, dp, h->ext, h->err, rec);
   CU(h, cudaGetLastError());
   h->launches += 2;
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id

@@ -41,7 +41,7 @@ struct ParamsDev {
 struct Extents {
   int32_t lo[3], hi[3];
   int32_t range_err;  // 1 if some |p*inv| >= 2^20
-  int32_t pad;
+  uint32_t work;      // chunk counter of the persistent force kernel
 };
 
 struct ErrDev {
@@ -115,16 +115,31 @@ __global__ void k_pack(const double* __restrict__ pos, const double* __restrict_
   if ((threadIdx.x & 31) == 0 && b) atomicMax(maxd_bits, b);
 }
 
-__device__ __forceinline__ void warp_minmax_atomic(Extents* ext, const int b[3], bool valid) {
+// Block-level min/max of integer box coordinates, then at most 6 atomics per block, each issued
+// only if it can still change the global value (ld.cg read of the current extent): a same-address
+// atomic per warp serialises at one L2 slice and cost milliseconds at 2e7 agents.
+// Must be called by every thread of the block.
+__device__ __forceinline__ void block_minmax_atomic(Extents* ext, const int b[3], bool valid) {
+  __shared__ int s_red[32][6];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    int lo = valid ? b[a] : INT32_MAX;
-    int hi = valid ? b[a] : INT32_MIN;
-    lo = __reduce_min_sync(FULL, lo);
-    hi = __reduce_max_sync(FULL, hi);
-    if ((threadIdx.x & 31) == 0 && lo != INT32_MAX) {
-      atomicMin(&ext->lo[a], lo);
-      atomicMax(&ext->hi[a], hi);
+    int lo = __reduce_min_sync(FULL, valid ? b[a] : INT32_MAX);
+    int hi = __reduce_max_sync(FULL, valid ? b[a] : INT32_MIN);
+    if (lane == 0) {
+      s_red[warp][a] = lo;
+      s_red[warp][3 + a] = hi;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 6) {
+    const int a = threadIdx.x;
+    int v = s_red[0][a];
+    for (int w = 1; w < nwarps; ++w) v = a < 3 ? min(v, s_red[w][a]) : max(v, s_red[w][a]);
+    if (a < 3) {
+      if (v != INT32_MAX && v < __ldcg(&ext->lo[a])) atomicMin(&ext->lo[a], v);
+    } else {
+      if (v != INT32_MIN && v > __ldcg(&ext->hi[a - 3])) atomicMax(&ext->hi[a - 3], v);
     }
   }
 }
@@ -147,7 +162,7 @@ __global__ void k_extents(const double4* __restrict__ ag, uint32_t n, double inv
     b[2] = box_coord(p.z, inv, bad);
   }
   if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) ext->range_err = 1;
-  warp_minmax_atomic(ext, b, valid);
+  block_minmax_atomic(ext, b, valid);
 }
 
 __global__ void k_ext_reset(Extents* ext) {
@@ -156,6 +171,7 @@ __global__ void k_ext_reset(Extents* ext) {
     ext->hi[threadIdx.x] = INT32_MIN;
   }
   if (threadIdx.x == 3) ext->range_err = 0;
+  if (threadIdx.x == 4) ext->work = 0u;
 }
 
 __device__ __forceinline__ uint32_t box_key(const GridDev& g, int bx, int by, int bz) {
@@ -320,8 +336,8 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
 // ------------------------------------------------------------------------------------------ K6
 constexpr int FORCE_THREADS = 256;
 constexpr int FORCE_WARPS = FORCE_THREADS / 32;
-constexpr int QCAP = 8;  // per-lane pending-contact FIFO depth (power of two)
-constexpr int QTHRESH = 16;
+constexpr int FORCE_MIN_BLOCKS = 3;  // 24 resident warps per SM
+constexpr int LCAP = 16;             // per-lane survivor list capacity (flushed before overflow)
 
 // One contact candidate of agent i (O4), returns false if delta <= 0.
 __device__ __forceinline__ bool pair_term(double xi, double yi, double zi, double ri, uint32_t idi, const double4& o,
@@ -352,159 +368,227 @@ __device__ __forceinline__ bool pair_term(double xi, double yi, double zi, doubl
   return true;
 }
 
-// Lane = agent (sorted order).  Each lane walks its 9 z-runs (27 boxes) in canonical order; the
-// cheap candidate test (d2 against a conservative per-lane bound) runs densely and pushes
-// possible contacts into a per-lane FIFO in shared memory; the expensive exact contact
-// evaluation (2 sqrt, 2 div) runs when at least QTHRESH lanes have work, so it is not paid by
-// the whole warp for one lane's contact.  FIFO order = candidate order, so each agent's force
-// is summed in the canonical order of DESIGN.md O5.
+struct ForceSmem {
+  uint32_t list[LCAP][32];  // survivors per lane (sorted index of the candidate), candidate order
+  double term[3][32];       // contact terms of one compacted batch
+  uint32_t cidx[32];        // candidate id of the batch entry, 0xffffffff = not a contact
+  uint32_t rb[9][32], re[9][32];
+};
+
+// Contact phase over the survivors of the warp (DESIGN.md §6.3 step 3).  The survivors of all lanes
+// are enumerated as one flat sequence (lane-major, candidate order inside a lane); each batch of 32
+// is evaluated with one entry per lane (owner found by a shuffle binary search over the inclusive
+// prefix of list lengths), then every owner adds its own entries of the batch in order -- so each
+// agent's force is summed in O5's canonical order.
 template <bool RECORD>
-__global__ void __launch_bounds__(FORCE_THREADS) k_force(const double4* __restrict__ ag,
-                                                         const uint32_t* __restrict__ ids,
-                                                         const uint32_t* __restrict__ start, uint32_t n, GridDev g,
-                                                         ParamsDev p, double4* __restrict__ ag_out,
-                                                         double* __restrict__ dp_out, Extents* ext_next,
-                                                         ErrDev* err, RecordDev rec) {
-  __shared__ uint32_t s_rb[FORCE_WARPS][9][32];
-  __shared__ uint32_t s_re[FORCE_WARPS][9][32];
-  __shared__ uint32_t s_q[FORCE_WARPS][QCAP][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t i = blockIdx.x * FORCE_THREADS + threadIdx.x;
-  const bool valid = i < n;
-  double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-  const double ri = 0.5 * me.w;
-  const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
-  // conservative bound: contact => d2 < (ri + rj)^2 <= (ri + L/2)^2 (exact reals); pad by 2^-50
-  double thr = (ri + g.thr_pad) * (ri + g.thr_pad);
-  thr = thr + thr * 0x1p-50;
-  const uint32_t myid = valid ? ids[i] : 0u;
-
-  // z-run ranges of the 9 columns, (dx, dy) lexicographic
+__device__ __forceinline__ void flush_contacts(ForceSmem& sm, int lane, int& cnt, double xi, double yi, double zi,
+                                               double ri, uint32_t idi, const double4* __restrict__ ag,
+                                               const uint32_t* __restrict__ ids, const ParamsDev& p, double& Fx,
+                                               double& Fy, double& Fz, int32_t& n_ct,
+                                               unsigned long long& ct_hash) {
+  const int incl = warp_incl_scan((uint32_t)cnt);
+  const int excl = incl - cnt;
+  const int total = __shfl_sync(FULL, incl, 31);
+  for (int b0 = 0; b0 < total; b0 += 32) {
+    const int e = b0 + lane;
+    int owner = 0;
 #pragma unroll
-  for (int c = 0; c < 9; ++c) {
-    int cx = bx + c / 3 - 1, cy = by + c % 3 - 1;
-    uint32_t b = 0, e = 0;
-    if (valid && cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1]) {
-      int z0 = bz - 1 < g.lo[2] ? g.lo[2] : bz - 1;
-      int z1 = bz + 1 > g.hi[2] ? g.hi[2] : bz + 1;
-      b = start[box_key(g, cx, cy, z0)];
-      e = start[box_key(g, cx, cy, z1) + 1];
+    for (int s = 16; s >= 1; s >>= 1) {
+      int v = __shfl_sync(FULL, incl, owner + s - 1);
+      if (v <= e) owner += s;
     }
-    s_rb[warp][c][lane] = b;
-    s_re[warp][c][lane] = e;
+    owner = owner > 31 ? 31 : owner;
+    const int oexcl = __shfl_sync(FULL, excl, owner);
+    const double ox = __shfl_sync(FULL, xi, owner);
+    const double oy = __shfl_sync(FULL, yi, owner);
+    const double oz = __shfl_sync(FULL, zi, owner);
+    const double orr = __shfl_sync(FULL, ri, owner);
+    const uint32_t oid = __shfl_sync(FULL, idi, owner);
+    uint32_t flag = 0xffffffffu;
+    if (e < total) {
+      const uint32_t j = sm.list[e - oexcl][owner];
+      const double4 o = ag[j];
+      const uint32_t idj = ids[j];
+      double tx, ty, tz, fa;
+      if (pair_term(ox, oy, oz, orr, oid, o, idj, p, tx, ty, tz, fa)) {
+        sm.term[0][lane] = tx;
+        sm.term[1][lane] = ty;
+        sm.term[2][lane] = tz;
+        flag = idj;
+      }
+    }
+    sm.cidx[lane] = flag;
+    __syncwarp();
+    const int lo = excl > b0 ? excl : b0;
+    const int hi = incl < b0 + 32 ? incl : b0 + 32;
+    for (int x = lo; x < hi; ++x) {
+      const int t = x - b0;
+      const uint32_t fl = sm.cidx[t];
+      if (fl != 0xffffffffu) {
+        Fx = Fx + sm.term[0][t];
+        Fy = Fy + sm.term[1][t];
+        Fz = Fz + sm.term[2][t];
+        if (RECORD) {
+          ++n_ct;
+          ct_hash += mix64(fl);
+        }
+      }
+    }
+    __syncwarp();
   }
-  __syncwarp();
+  cnt = 0;
+}
 
-  int c = 0;
-  uint32_t q = s_rb[warp][0][lane], e = s_re[warp][0][lane];
-  while (q >= e && c < 8) {
-    ++c;
-    q = s_rb[warp][c][lane];
-    e = s_re[warp][c][lane];
-  }
-  bool done = q >= e;
-  uint32_t qh = 0, qt = 0;  // FIFO head / tail
-  double Fx = 0.0, Fy = 0.0, Fz = 0.0;
-  int32_t n_cand = 0, n_nb = 0, n_ct = 0;
-  unsigned long long nb_hash = 0, ct_hash = 0;
-  double s_abs = 0.0;
-  (void)s_abs;
+// K6.  Persistent warps take chunks of 32 consecutive sorted agents from an atomic counter
+// (load balance without block barriers).  Lane = agent.  Candidate phase: warp-uniform loop over
+// the 9 columns (dx, dy) lexicographic; inside a column each lane walks its own z-run
+// [start(bz-1), start(bz+2)) two candidates per iteration (independent loads and d2 chains), and
+// keeps candidates passing the conservative bound d2 <= (r_i + L/2)^2 (1 + 2^-50) (contact implies
+// d2 < (r_i + r_j)^2 <= (r_i + L/2)^2).  Agents [a_begin, a_end) of the sorted array are updated
+// (the whole array is the environment, so slab ghosts are read but not moved); p' goes to
+// ag_out[i - a_begin] (and ids to id_out if given).
+template <bool RECORD>
+__global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
+    k_force(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, const uint32_t* __restrict__ start,
+            uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
+            uint32_t* __restrict__ id_out, double* __restrict__ dp_out, Extents* ext_next, ErrDev* err,
+            RecordDev rec) {
+  __shared__ ForceSmem s_all[FORCE_WARPS];
+  const int lane = threadIdx.x & 31;
+  ForceSmem& sm = s_all[threadIdx.x >> 5];
+  int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+  bool ebad = false;
 
   while (true) {
-    if (!done && qt - qh < QCAP) {
-      if (q != i) {
-        double4 o = ag[q];
-        double dx = me.x - o.x;
-        double dy = me.y - o.y;
-        double dz = me.z - o.z;
-        double d2 = (dx * dx + dy * dy) + dz * dz;
+    uint32_t chunk = 0;
+    if (lane == 0) chunk = atomicAdd(&ext_next->work, 1u);
+    chunk = __shfl_sync(FULL, chunk, 0);
+    const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
+    if (base >= a_end) break;
+    const uint32_t i = (uint32_t)base + lane;
+    const bool valid = i < a_end;
+    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const uint32_t myid = valid ? ids[i] : 0u;
+    const double ri = 0.5 * me.w;
+    const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+    double thr = (ri + g.thr_pad) * (ri + g.thr_pad);
+    thr = thr + thr * 0x1p-50;
+    {
+      const int z0 = bz - 1 < g.lo[2] ? g.lo[2] : bz - 1;
+      const int z1 = bz + 1 > g.hi[2] ? g.hi[2] : bz + 1;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) {
+        const int cx = bx + c / 3 - 1, cy = by + c % 3 - 1;
+        uint32_t b = 0, e = 0;
+        if (valid && cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1]) {
+          b = __ldg(&start[box_key(g, cx, cy, z0)]);
+          e = __ldg(&start[box_key(g, cx, cy, z1) + 1]);
+        }
+        sm.rb[c][lane] = b;
+        sm.re[c][lane] = e;
+      }
+    }
+    __syncwarp();
+    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+    int cnt = 0;
+    int32_t n_cand = 0, n_nb = 0, n_ct = 0;
+    unsigned long long nb_hash = 0, ct_hash = 0;
+    for (int c = 0; c < 9; ++c) {
+      uint32_t q = sm.rb[c][lane];
+      const uint32_t e = sm.re[c][lane];
+      while (__any_sync(FULL, q < e)) {
+        const bool a0 = q < e && q != i;
+        const bool a1 = q + 1 < e && q + 1 != i;
+        double3 o0 = make_double3(0.0, 0.0, 0.0), o1 = make_double3(0.0, 0.0, 0.0);
+        if (a0) {
+          const double2 xy = __ldg(reinterpret_cast<const double2*>(ag + q));
+          o0 = make_double3(xy.x, xy.y, __ldg(&ag[q].z));
+        }
+        if (a1) {
+          const double2 xy = __ldg(reinterpret_cast<const double2*>(ag + q + 1));
+          o1 = make_double3(xy.x, xy.y, __ldg(&ag[q + 1].z));
+        }
+        const double dx0 = me.x - o0.x, dy0 = me.y - o0.y, dz0 = me.z - o0.z;
+        const double dx1 = me.x - o1.x, dy1 = me.y - o1.y, dz1 = me.z - o1.z;
+        const double d20 = (dx0 * dx0 + dy0 * dy0) + dz0 * dz0;
+        const double d21 = (dx1 * dx1 + dy1 * dy1) + dz1 * dz1;
         if (RECORD) {
-          ++n_cand;
-          if (d2 <= g.L2) {
+          n_cand += (int)a0 + (int)a1;
+          if (a0 && d20 <= g.L2) {
             ++n_nb;
             nb_hash += mix64(ids[q]);
           }
-        }
-        if (d2 <= thr) {
-          s_q[warp][qt & (QCAP - 1)][lane] = q;
-          ++qt;
-        }
-      }
-      ++q;
-      while (q >= e && c < 8) {
-        ++c;
-        q = s_rb[warp][c][lane];
-        e = s_re[warp][c][lane];
-      }
-      done = q >= e;
-    }
-    const unsigned pend = __ballot_sync(FULL, qt != qh);
-    const unsigned fetching = __ballot_sync(FULL, !done);
-    if (!pend && !fetching) break;
-    const unsigned full = __ballot_sync(FULL, qt - qh == QCAP);
-    if (__popc(pend) >= QTHRESH || full || !fetching) {
-      if (qt != qh) {
-        uint32_t j = s_q[warp][qh & (QCAP - 1)][lane];
-        ++qh;
-        double4 o = ag[j];
-        uint32_t idj = ids[j];
-        double tx, ty, tz, fa;
-        if (pair_term(me.x, me.y, me.z, ri, myid, o, idj, p, tx, ty, tz, fa)) {
-          Fx = Fx + tx;
-          Fy = Fy + ty;
-          Fz = Fz + tz;
-          if (RECORD) {
-            ++n_ct;
-            ct_hash += mix64(idj);
+          if (a1 && d21 <= g.L2) {
+            ++n_nb;
+            nb_hash += mix64(ids[q + 1]);
           }
         }
+        if (a0 && d20 <= thr) sm.list[cnt++][lane] = q;
+        if (a1 && d21 <= thr) sm.list[cnt++][lane] = q + 1;
+        q += 2;
+        if (__any_sync(FULL, cnt > LCAP - 2))
+          flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+      }
+    }
+    if (__any_sync(FULL, cnt > 0))
+      flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+
+    // O6 displacement, O7 update
+    double dpx = 0.0, dpy = 0.0, dpz = 0.0;
+    int branch = 0;
+    const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
+    if (fn <= p.adherence) {
+      branch = 0;
+    } else if (fn * p.c > p.max_disp) {
+      const double scale = p.max_disp / fn;
+      dpx = Fx * scale;
+      dpy = Fy * scale;
+      dpz = Fz * scale;
+      branch = 1;
+    } else {
+      dpx = Fx * p.c;
+      dpy = Fy * p.c;
+      dpz = Fz * p.c;
+      branch = 2;
+    }
+    if (valid) {
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, myid);
+      const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
+      const uint32_t o = i - a_begin;
+      ag_out[o] = np;
+      if (id_out) id_out[o] = myid;
+      if (dp_out) {
+        dp_out[3 * (size_t)o] = dpx;
+        dp_out[3 * (size_t)o + 1] = dpy;
+        dp_out[3 * (size_t)o + 2] = dpz;
+      }
+      const int nb3[3] = {box_coord(np.x, g.inv, ebad), box_coord(np.y, g.inv, ebad), box_coord(np.z, g.inv, ebad)};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        elo[a] = min(elo[a], nb3[a]);
+        ehi[a] = max(ehi[a], nb3[a]);
+      }
+      if (RECORD) {
+        rec.n_cand[o] = n_cand;
+        rec.n_nb[o] = n_nb;
+        rec.n_ct[o] = n_ct;
+        rec.branch[o] = (int8_t)branch;
+        rec.nb_hash[o] = nb_hash;
+        rec.ct_hash[o] = ct_hash;
       }
     }
   }
-
-  // O6 displacement, O7 update
-  double dpx = 0.0, dpy = 0.0, dpz = 0.0;
-  int branch = 0;
-  double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
-  if (fn <= p.adherence) {
-    branch = 0;
-  } else if (fn * p.c > p.max_disp) {
-    double scale = p.max_disp / fn;
-    dpx = Fx * scale;
-    dpy = Fy * scale;
-    dpz = Fz * scale;
-    branch = 1;
-  } else {
-    dpx = Fx * p.c;
-    dpy = Fy * p.c;
-    dpz = Fz * p.c;
-    branch = 2;
-  }
-  bool bad = false;
-  int nb3[3] = {0, 0, 0};
-  if (valid) {
-    if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, myid);
-    double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
-    ag_out[i] = np;
-    if (dp_out) {
-      dp_out[3 * (size_t)i] = dpx;
-      dp_out[3 * (size_t)i + 1] = dpy;
-      dp_out[3 * (size_t)i + 2] = dpz;
-    }
-    nb3[0] = box_coord(np.x, g.inv, bad);
-    nb3[1] = box_coord(np.y, g.inv, bad);
-    nb3[2] = box_coord(np.z, g.inv, bad);
-    if (RECORD) {
-      rec.n_cand[i] = n_cand;
-      rec.n_nb[i] = n_nb;
-      rec.n_ct[i] = n_ct;
-      rec.branch[i] = (int8_t)branch;
-      rec.nb_hash[i] = nb_hash;
-      rec.ct_hash[i] = ct_hash;
+  // next step's extents: one guarded atomic set per warp (a few thousand warps per launch)
+  if (__any_sync(FULL, ebad) && lane == 0) ext_next->range_err = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int lo = __reduce_min_sync(FULL, elo[a]);
+    const int hi = __reduce_max_sync(FULL, ehi[a]);
+    if (lane == 0) {
+      if (lo != INT32_MAX && lo < __ldcg(&ext_next->lo[a])) atomicMin(&ext_next->lo[a], lo);
+      if (hi != INT32_MIN && hi > __ldcg(&ext_next->hi[a])) atomicMax(&ext_next->hi[a], hi);
     }
   }
-  if (__any_sync(FULL, bad) && lane == 0) ext_next->range_err = 1;
-  warp_minmax_atomic(ext_next, nb3, valid);
 }
 
 // ------------------------------------------------------------------------------------------ K7
