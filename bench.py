@@ -171,7 +171,7 @@ def run_bdm(args):
     import paper_2006_06775_b200 as bdm
 
     world, rank, local = dist_env()
-    if world > 1:
+    if world > 1 or args.slabs:
         from paper_2006_06775_b200 import dist as bdist
 
         return bdist.bench_multi(args, METRIC, UNIT, config_obj, load_peaks, ClockSampler)
@@ -318,6 +318,7 @@ def main():
     ap.add_argument("--cpu-stride", type=int, default=10)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--slabs", action="store_true", help="use the x-slab driver even at one rank (testing)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "bdm":
         print("note: timing rules need >= 3 warm-up steps; raising warmup to 3", file=sys.stderr)

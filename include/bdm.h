@@ -157,6 +157,59 @@ int bdm_get_timing(bdm_handle h, double* out4);
 int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo3, const double* hi3, double dlo,
                          double dhi, double* pos, double* diam, void* cuda_stream);
 
+/* ---------------------------------------------------------------------------------------------
+ * x-slab mode (multi-GPU; north_star "the domain is split into x-slabs. Each step does
+ * a halo exchange of boundary-box agents and migrates agents that cross slab boundaries").  One
+ * handle per rank owns the agents whose box-x lies in [x_begin, x_end) (rank 0: x_begin = INT32_MIN,
+ * last rank: x_end = INT32_MAX).  The exchange itself (counts, payloads, allreduce of L and the
+ * extents) is done by the caller -- paper_2006_06775_b200/dist.py over torch.distributed.  Every
+ * array is a DEVICE pointer (BDM_DEVICE_PTRS required).  Exchange records are 5 fp64 per agent
+ * (x, y, z, D, id).  Per step: local_extents -> allreduce -> pack(HALO) -> exchange -> step ->
+ * pack(MIGRANTS) -> exchange -> add.  Owned sums use ghosts with global ids in canonical order, so
+ * results are bit-identical to the single-handle path.
+ * --------------------------------------------------------------------------------------------- */
+#define BDM_HALO 0
+#define BDM_MIGRANTS 1
+#define BDM_OWNED_POSITIONS 0
+#define BDM_LAST_DISPLACEMENTS 1
+
+/* Create a slab handle with n_local owned agents (global ids < 2^32, positions n x 3, diameters n)
+ * and room for `capacity` owned + ghost agents.  EINVAL without BDM_DEVICE_PTRS. */
+int bdm_slab_init(bdm_handle* h, int64_t n_local, int64_t capacity, const uint32_t* ids, const double* pos,
+                  const double* diam, const bdm_params* p);
+
+/* Largest diameter among the owned agents (0 if none); the caller allreduces it (O1). */
+int bdm_slab_local_maxd(bdm_handle h, double* maxd);
+
+/* Set the global box edge (max over ranks of the local max D; box_edge_min still applies). */
+int bdm_slab_set_box_edge(bdm_handle h, double L);
+
+/* Integer box extents (lo[3], hi[3]) of the owned agents' current positions (after a step: of the
+ * positions the step produced, before migration).  INT32_MAX / INT32_MIN if none.  ERANGE as O2. */
+int bdm_slab_local_extents(bdm_handle h, int32_t* lohi6);
+
+/* Pack records to send to the lower (box-x below) and upper neighbour.  what = BDM_HALO: owned
+ * agents in the first / last box-x layer of the slab.  what = BDM_MIGRANTS: owned agents whose box-x
+ * left [x_begin, x_end); they are removed from the handle.  send_lo / send_hi hold cap records
+ * each; ETRUNC (state unchanged) if either count exceeds cap, with the counts written back. */
+int bdm_slab_pack(bdm_handle h, int what, int32_t x_begin, int32_t x_end, double* send_lo, double* send_hi,
+                  int64_t cap, int64_t* n_lo, int64_t* n_hi);
+
+/* Append received records (immigrants) to the owned agents.  ERANGE past the capacity. */
+int bdm_slab_add(bdm_handle h, const double* recv_lo, int64_t n_lo, const double* recv_hi, int64_t n_hi);
+
+/* One mechanical step of the owned agents: ghosts = the records received from the lower
+ * (box-x = x_begin - 1) and upper (box-x = x_end) neighbours; slab-local grid over box-x
+ * [x_begin-1, x_end] with the global y/z extents glo3/ghi3 (allreduced local extents); force,
+ * displacement and update of the owned agents only.  want_dp != 0 keeps the displacements. */
+int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_t x_begin, int32_t x_end,
+                  const double* recv_lo, int64_t n_lo, const double* recv_hi, int64_t n_hi, int want_dp);
+
+/* Owned agents (what = BDM_OWNED_POSITIONS: ids + n x 3 positions) or the displacements of the last
+ * step with want_dp (BDM_LAST_DISPLACEMENTS: ids + n x 3), in the handle's internal order; *n gets
+ * the count.  ids / vals may be NULL to query the count. */
+int bdm_slab_get(bdm_handle h, int what, int64_t* n, uint32_t* ids, double* vals);
+
 /* Human-readable message of the last failure on h (or of the calling thread when h is NULL). */
 const char* bdm_last_error(bdm_handle h);
 

@@ -33,6 +33,10 @@ BDM_DEVICE_PTRS = 0x1
 BDM_RECORD = 0x2
 BDM_NEIGHBOR = 0
 BDM_CONTACT = 1
+BDM_HALO = 0
+BDM_MIGRANTS = 1
+BDM_OWNED_POSITIONS = 0
+BDM_LAST_DISPLACEMENTS = 1
 
 ERRNAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -6: "ENONFINITE", -7: "ERANGE", -8: "ETRUNC"}
 
@@ -79,6 +83,17 @@ _SIGS = {
     "bdm_get_timing": ([_vp, _vp], ctypes.c_int),
     "bdm_generate_uniform": ([ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, ctypes.c_double,
                               ctypes.c_double, _vp, _vp, _vp], ctypes.c_int),
+    "bdm_slab_init": ([ctypes.POINTER(_vp), ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp,
+                       ctypes.POINTER(bdm_params)], ctypes.c_int),
+    "bdm_slab_local_maxd": ([_vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
+    "bdm_slab_set_box_edge": ([_vp, ctypes.c_double], ctypes.c_int),
+    "bdm_slab_local_extents": ([_vp, _vp], ctypes.c_int),
+    "bdm_slab_pack": ([_vp, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_int64,
+                       ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
+    "bdm_slab_add": ([_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64], ctypes.c_int),
+    "bdm_slab_step": ([_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
+                       ctypes.c_int], ctypes.c_int),
+    "bdm_slab_get": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, _vp], ctypes.c_int),
     "bdm_last_error": ([_vp], ctypes.c_char_p),
     "bdm_destroy": ([_vp], None),
 }
@@ -290,3 +305,79 @@ def bdm_generate_uniform(seed: int, id0: int, n: int, lo3, hi3, dlo: float, dhi:
     sp = getattr(stream, "cuda_stream", stream) if stream is not None else None
     _check(load_library().bdm_generate_uniform(seed, id0, n, _ptr(lo), _ptr(hi), dlo, dhi, _ptr(pos), _ptr(diam),
                                                ctypes.c_void_p(sp) if sp else None))
+
+
+# ------------------------------------------------------------------------------------ x-slab mode
+def bdm_slab_init(ids, pos, diam, capacity: int, params: bdm_params | None = None, stream=None) -> Handle:
+    """ids uint32-compatible (torch.int32 / int64 converted), pos [n,3], diam [n]: CUDA tensors."""
+    import torch
+
+    lib = load_library()
+    p = params if params is not None else bdm_params_default()
+    p.flags |= BDM_DEVICE_PTRS
+    if p.device < 0:
+        p.device = pos.device.index
+    n = pos.shape[0]
+    ids32 = ids.to(torch.int32).contiguous() if ids.dtype != torch.int32 else ids.contiguous()
+    raw = ctypes.c_void_p()
+    torch.cuda.current_stream(pos.device).synchronize()
+    _check(lib.bdm_slab_init(ctypes.byref(raw), n, capacity, _ptr(ids32), _ptr(pos.contiguous()),
+                             _ptr(diam.contiguous()), ctypes.byref(p)))
+    h = Handle(raw, n, True)
+    h.capacity = capacity
+    if stream is not None:
+        bdm_set_stream(h, stream)
+    return h
+
+
+def bdm_slab_local_maxd(h: Handle) -> float:
+    v = ctypes.c_double(0.0)
+    _check(load_library().bdm_slab_local_maxd(h.raw, ctypes.byref(v)), h.raw)
+    return v.value
+
+
+def bdm_slab_set_box_edge(h: Handle, L: float) -> None:
+    _check(load_library().bdm_slab_set_box_edge(h.raw, float(L)), h.raw)
+
+
+def bdm_slab_local_extents(h: Handle):
+    out = np.zeros(6, np.int32)
+    _check(load_library().bdm_slab_local_extents(h.raw, _ptr(out)), h.raw)
+    return out[:3].copy(), out[3:].copy()
+
+
+def bdm_slab_pack(h: Handle, what: int, x_begin: int, x_end: int, send_lo, send_hi, cap: int):
+    """Returns (rc, n_lo, n_hi); rc is BDM_OK or BDM_ETRUNC (buffers too small, nothing committed)."""
+    nlo, nhi = ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = load_library().bdm_slab_pack(h.raw, what, x_begin, x_end, _ptr(send_lo), _ptr(send_hi), cap,
+                                      ctypes.byref(nlo), ctypes.byref(nhi))
+    if rc not in (BDM_OK, BDM_ETRUNC):
+        _check(rc, h.raw)
+    return rc, nlo.value, nhi.value
+
+
+def bdm_slab_add(h: Handle, recv_lo, n_lo: int, recv_hi, n_hi: int) -> None:
+    _check(load_library().bdm_slab_add(h.raw, _ptr(recv_lo) if n_lo else None, n_lo,
+                                       _ptr(recv_hi) if n_hi else None, n_hi), h.raw)
+
+
+def bdm_slab_step(h: Handle, glo3, ghi3, x_begin: int, x_end: int, recv_lo, n_lo: int, recv_hi, n_hi: int,
+                  want_dp: bool = False) -> None:
+    lo = np.ascontiguousarray(glo3, np.int32)
+    hi = np.ascontiguousarray(ghi3, np.int32)
+    _check(load_library().bdm_slab_step(h.raw, _ptr(lo), _ptr(hi), x_begin, x_end,
+                                        _ptr(recv_lo) if n_lo else None, n_lo,
+                                        _ptr(recv_hi) if n_hi else None, n_hi, int(want_dp)), h.raw)
+
+
+def bdm_slab_get(h: Handle, what: int):
+    """(ids int64 CUDA tensor, values [n,3] fp64 CUDA tensor) of the owned agents / last displacements."""
+    import torch
+
+    lib = load_library()
+    n = ctypes.c_int64(0)
+    _check(lib.bdm_slab_get(h.raw, what, ctypes.byref(n), None, None), h.raw)
+    ids = torch.empty(n.value, dtype=torch.int32, device="cuda")
+    vals = torch.empty((n.value, 3), dtype=torch.float64, device="cuda")
+    _check(lib.bdm_slab_get(h.raw, what, ctypes.byref(n), _ptr(ids), _ptr(vals)), h.raw)
+    return ids.to(torch.int64) & 0xFFFFFFFF, vals

@@ -71,6 +71,13 @@ struct bdm_ctx {
   unsigned long long *r_nbh = nullptr, *r_cth = nullptr;
   bool have_record = false;
   // timing
+  // x-slab mode (multi-GPU)
+  bool slab = false;
+  int64_t cap = 0;            // capacity of owned + ghost agents
+  uint32_t* dp_ids = nullptr;  // ids in the order of dp (slab mode)
+  int64_t n_dp = 0;
+  uint32_t* cnt = nullptr;     // pack counters (device)
+  uint32_t* cnt_host = nullptr;
   bool timing = false;
   int sm_count = 0, force_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
@@ -195,6 +202,31 @@ int compute_extents(bdm_ctx* h) {
   return BDM_OK;
 }
 
+// Counting sort of ag[cur][0..n) by (box key under h->grid, id) into ag[1-cur]; box start table
+// in h->table.  cur flips to the sorted buffer.
+int sort_into(bdm_ctx* h, uint32_t n) {
+  const size_t items = (size_t)h->grid.n_boxes + 1;
+  int rc = ensure_table(h, items);
+  if (rc) return rc;
+  cudaStream_t s = h->stream;
+  const int src = h->cur, dst = 1 - h->cur;
+  CU(h, cudaMemsetAsync(h->table, 0, items * sizeof(uint32_t), s));
+  if (n > 0) k_key_hist<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, h->grid, h->key, h->slot, h->table);
+  size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
+  CU(h, cudaMemsetAsync(h->scan_state, 0, tiles * sizeof(unsigned long long), s));
+  CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), s));
+  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(h->table, items, h->scan_state, h->scan_ticket);
+  if (n > 0) {
+    k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
+    k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
+                                           h->id[dst]);
+  }
+  CU(h, cudaGetLastError());
+  h->launches += n > 0 ? 4 : 1;
+  h->cur = dst;
+  return BDM_OK;
+}
+
 int grid_build(bdm_ctx* h) {
   if (h->poisoned) return fail(h, BDM_ESTATE, "handle poisoned by an earlier error: %s", h->error.c_str());
   if (h->state == State::Fresh) return BDM_OK;  // positions unchanged since the last build
@@ -205,24 +237,8 @@ int grid_build(bdm_ctx* h) {
   }
   int rc = compute_extents(h);
   if (rc) return rc;
-  const uint32_t n = (uint32_t)h->n;
-  const size_t items = (size_t)h->grid.n_boxes + 1;
-  rc = ensure_table(h, items);
+  rc = sort_into(h, (uint32_t)h->n);
   if (rc) return rc;
-  cudaStream_t s = h->stream;
-  const int src = h->cur, dst = 1 - h->cur;
-  CU(h, cudaMemsetAsync(h->table, 0, items * sizeof(uint32_t), s));
-  k_key_hist<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, h->grid, h->key, h->slot, h->table);
-  size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
-  CU(h, cudaMemsetAsync(h->scan_state, 0, tiles * sizeof(unsigned long long), s));
-  CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), s));
-  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(h->table, items, h->scan_state, h->scan_ticket);
-  k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
-  k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
-                                         h->id[dst]);
-  CU(h, cudaGetLastError());
-  h->launches += 4;
-  h->cur = dst;  // sorted buffer is now the newest state
   h->state = State::Fresh;
   h->have_grid = true;
   return BDM_OK;
@@ -252,10 +268,10 @@ int force_step(bdm_ctx* h, bool want_dp) {
   const unsigned grid = force_grid(h, n);
   if (h->prm.flags & BDM_RECORD)
     k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, 0u, n, h->grid, pd, h->ag[dst],
-                                                nullptr, dp, h->ext, h->err, rec);
+                                                nullptr, dp, nullptr, h->ext, h->err, rec);
   else
     k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, 0u, n, h->grid, pd,
-                                                 h->ag[dst], nullptr, dp, h->ext, h->err, rec);
+                                                 h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec);
   CU(h, cudaGetLastError());
   h->launches += 2;
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
@@ -371,12 +387,13 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->ext_host) cudaFreeHost(h->ext_host);
   if (h->err_host) cudaFreeHost(h->err_host);
+  if (h->cnt_host) cudaFreeHost(h->cnt_host);
   cudaSetDevice(prev);
   delete h;
 }
@@ -710,6 +727,303 @@ int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_
   P* pp = reinterpret_cast<P*>(out);
   std::sort(pp, pp + total, [](const P& x, const P& y) { return x.a != y.a ? x.a < y.a : x.b < y.b; });
   return BDM_OK;
+}
+
+// ---------------------------------------------------------------------------------- x-slab mode
+// DESIGN.md §7.  The caller (paper_2006_06775_b200/dist.py) owns the exchange (torch.distributed);
+// these calls are the device-side halves: pack / unpack records, build the slab-local grid over
+// owned + ghost agents, run the force on the owned range only, and split off migrants.
+
+namespace {
+
+int slab_check(bdm_ctx* h, const char* fn) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "%s: NULL handle", fn);
+  if (!h->slab) return fail(h, BDM_ESTATE, "%s: handle was not created by bdm_slab_init", fn);
+  if (h->poisoned) return fail(h, BDM_ESTATE, "%s: handle poisoned by an earlier error: %s", fn, h->error.c_str());
+  CU(h, cudaSetDevice(h->device));
+  return BDM_OK;
+}
+
+int read_counts(bdm_ctx* h) {
+  CU(h, cudaMemcpyAsync(h->cnt_host, h->cnt, 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream));
+  return check_async(h);
+}
+
+}  // namespace
+
+int bdm_slab_init(bdm_handle* out, int64_t n_local, int64_t capacity, const uint32_t* ids, const double* pos,
+                  const double* diam, const bdm_params* p) {
+  if (!out) return fail(nullptr, BDM_EINVAL, "bdm_slab_init: handle pointer is NULL");
+  *out = nullptr;
+  if (!params_ok(p)) return fail(nullptr, BDM_EINVAL, "bdm_slab_init: invalid params");
+  if (!(p->flags & BDM_DEVICE_PTRS)) return fail(nullptr, BDM_EINVAL, "bdm_slab_init: slab mode needs BDM_DEVICE_PTRS");
+  if (n_local < 0 || capacity < n_local || capacity >= (int64_t)0xffffffffll)
+    return fail(nullptr, BDM_EINVAL, "bdm_slab_init: need 0 <= n_local <= capacity < 2^32");
+  if (n_local > 0 && (!pos || !diam || !ids)) return fail(nullptr, BDM_EINVAL, "bdm_slab_init: NULL array");
+  bdm_ctx* h = new (std::nothrow) bdm_ctx();
+  if (!h) return fail(nullptr, BDM_ENOMEM, "bdm_slab_init: host allocation");
+  h->prm = *p;
+  h->slab = true;
+  h->n = n_local;
+  h->cap = capacity;
+  int dev = p->device;
+  if (dev < 0 && cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    delete h;
+    return fail(nullptr, BDM_ECUDA, "bdm_slab_init: no CUDA device");
+  }
+  h->device = dev;
+  int rc = BDM_OK;
+#define TRY(x)                \
+  do {                        \
+    rc = (x);                 \
+    if (rc) {                 \
+      g_tls_error = h->error; \
+      bdm_destroy(h);         \
+      return rc;              \
+    }                         \
+  } while (0)
+  if (cudaSetDevice(dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    delete h;
+    return fail(nullptr, BDM_ECUDA, "bdm_slab_init: cudaSetDevice(%d) failed", dev);
+  }
+  const size_t N = (size_t)capacity;
+  TRY(dalloc(h, &h->ag[0], N));
+  TRY(dalloc(h, &h->ag[1], N));
+  TRY(dalloc(h, &h->id[0], N));
+  TRY(dalloc(h, &h->id[1], N));
+  TRY(dalloc(h, &h->key, N));
+  TRY(dalloc(h, &h->slot, N));
+  TRY(dalloc(h, &h->tsrc, N));
+  TRY(dalloc(h, &h->tid, N));
+  TRY(dalloc(h, &h->tkey, N));
+  TRY(dalloc(h, &h->dp, 3 * N));
+  TRY(dalloc(h, &h->dp_ids, N));
+  TRY(dalloc(h, &h->ext, 1));
+  TRY(dalloc(h, &h->err, 1));
+  TRY(dalloc(h, &h->maxd_bits, 1));
+  TRY(dalloc(h, &h->scan_ticket, 1));
+  TRY(dalloc(h, &h->cnt, 4));
+  if (cudaMallocHost(&h->ext_host, sizeof(Extents)) != cudaSuccess ||
+      cudaMallocHost(&h->err_host, sizeof(ErrDev)) != cudaSuccess ||
+      cudaMallocHost(&h->cnt_host, 4 * sizeof(uint32_t)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    TRY(fail(h, BDM_ENOMEM, "bdm_slab_init: pinned host allocation"));
+  }
+  ErrDev e0{0u, 0xffffffffu, 0u, 0u};
+  if (cudaMemcpy(h->err, &e0, sizeof e0, cudaMemcpyHostToDevice) != cudaSuccess) {
+    (void)cudaGetLastError();
+    TRY(fail(h, BDM_ECUDA, "bdm_slab_init: device initialisation"));
+  }
+  if (n_local > 0) {
+    CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), h->stream));
+    k_pack<<<blocks(n_local, 256), 256, 0, h->stream>>>(pos, diam, (uint32_t)n_local, h->ag[0], h->id[0],
+                                                        h->maxd_bits, h->err);
+    if (cudaGetLastError() != cudaSuccess) TRY(fail(h, BDM_ECUDA, "bdm_slab_init: k_pack launch"));
+    if (cudaMemcpyAsync(h->id[0], ids, (size_t)n_local * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream) !=
+        cudaSuccess)
+      TRY(fail(h, BDM_ECUDA, "bdm_slab_init: id copy"));
+    TRY(check_async(h));
+  }
+#undef TRY
+  h->cur = 0;
+  h->state = State::NoGrid;
+  *out = h;
+  return BDM_OK;
+}
+
+int bdm_slab_local_maxd(bdm_handle h, double* maxd) {
+  int rc = slab_check(h, "bdm_slab_local_maxd");
+  if (rc) return rc;
+  if (!maxd) return fail(h, BDM_EINVAL, "bdm_slab_local_maxd: NULL output");
+  CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), h->stream));
+  if (h->n > 0) k_maxd<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], (uint32_t)h->n, h->maxd_bits);
+  CU(h, cudaGetLastError());
+  CU(h, cudaMemcpyAsync(h->ext_host, h->maxd_bits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+  rc = check_async(h);
+  if (rc) return rc;
+  std::memcpy(maxd, h->ext_host, sizeof(double));
+  return BDM_OK;
+}
+
+int bdm_slab_set_box_edge(bdm_handle h, double L) {
+  int rc = slab_check(h, "bdm_slab_set_box_edge");
+  if (rc) return rc;
+  L = std::max(L, h->prm.box_edge_min);
+  if (!(L > 0.0) || !std::isfinite(L)) return fail(h, BDM_EINVAL, "bdm_slab_set_box_edge: L must be > 0 and finite");
+  h->grid.L = L;
+  h->grid.L2 = L * L;
+  h->grid.inv = 1.0 / (L * (1.0 + 0x1p-30));
+  h->grid.thr_pad = 0.5 * L;
+  h->ext_valid = false;
+  h->have_grid = true;
+  return BDM_OK;
+}
+
+int bdm_slab_local_extents(bdm_handle h, int32_t* lohi6) {
+  int rc = slab_check(h, "bdm_slab_local_extents");
+  if (rc) return rc;
+  if (!lohi6) return fail(h, BDM_EINVAL, "bdm_slab_local_extents: NULL output");
+  if (!(h->grid.inv > 0.0)) return fail(h, BDM_ESTATE, "bdm_slab_local_extents: call bdm_slab_set_box_edge first");
+  if (!h->ext_valid) {
+    k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
+    if (h->n > 0) k_extents<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], (uint32_t)h->n, h->grid.inv, h->ext);
+    CU(h, cudaGetLastError());
+    h->ext_valid = true;
+  }
+  CU(h, cudaMemcpyAsync(h->ext_host, h->ext, sizeof(Extents), cudaMemcpyDeviceToHost, h->stream));
+  rc = check_async(h);
+  if (rc) return rc;
+  if (h->ext_host->range_err) {
+    h->poisoned = true;
+    return fail(h, BDM_ERANGE, "an agent lies >= 2^20 boxes from the origin (DESIGN.md R9)");
+  }
+  for (int a = 0; a < 3; ++a) {
+    lohi6[a] = h->ext_host->lo[a];
+    lohi6[3 + a] = h->ext_host->hi[a];
+  }
+  return BDM_OK;
+}
+
+int bdm_slab_pack(bdm_handle h, int what, int32_t x_begin, int32_t x_end, double* send_lo, double* send_hi,
+                  int64_t cap, int64_t* n_lo, int64_t* n_hi) {
+  int rc = slab_check(h, "bdm_slab_pack");
+  if (rc) return rc;
+  if ((what != BDM_HALO && what != BDM_MIGRANTS) || !n_lo || !n_hi || cap < 0 || (cap > 0 && (!send_lo || !send_hi)))
+    return fail(h, BDM_EINVAL, "bdm_slab_pack: bad arguments");
+  if (x_begin >= x_end) return fail(h, BDM_EINVAL, "bdm_slab_pack: empty slab [%d, %d)", x_begin, x_end);
+  CU(h, cudaMemsetAsync(h->cnt, 0, 4 * sizeof(uint32_t), h->stream));
+  const uint32_t n = (uint32_t)h->n;
+  if (n > 0)
+    k_slab_pack<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->grid.inv,
+                                                        what == BDM_HALO ? 0 : 1, x_begin, x_end, send_lo, send_hi,
+                                                        (uint64_t)cap, h->cnt, h->ag[1 - h->cur], h->id[1 - h->cur]);
+  CU(h, cudaGetLastError());
+  h->launches += n > 0;
+  rc = read_counts(h);
+  if (rc) return rc;
+  *n_lo = h->cnt_host[0];
+  *n_hi = h->cnt_host[1];
+  if (*n_lo > cap || *n_hi > cap)
+    return fail(h, BDM_ETRUNC, "bdm_slab_pack: %lld / %lld records > cap %lld", (long long)*n_lo, (long long)*n_hi,
+                (long long)cap);
+  if (what == BDM_MIGRANTS) {  // commit the compaction of the agents that stay
+    h->cur = 1 - h->cur;
+    h->n = h->cnt_host[2];
+  }
+  return BDM_OK;
+}
+
+int bdm_slab_add(bdm_handle h, const double* recv_lo, int64_t n_lo, const double* recv_hi, int64_t n_hi) {
+  int rc = slab_check(h, "bdm_slab_add");
+  if (rc) return rc;
+  if (n_lo < 0 || n_hi < 0 || (n_lo && !recv_lo) || (n_hi && !recv_hi))
+    return fail(h, BDM_EINVAL, "bdm_slab_add: bad arguments");
+  if (h->n + n_lo + n_hi > h->cap)
+    return fail(h, BDM_ERANGE, "bdm_slab_add: %lld agents exceed the slab capacity %lld", (long long)(h->n + n_lo + n_hi),
+                (long long)h->cap);
+  uint32_t off = (uint32_t)h->n;
+  if (n_lo) k_unpack<<<blocks(n_lo, 256), 256, 0, h->stream>>>(recv_lo, (uint32_t)n_lo, h->ag[h->cur], h->id[h->cur], off);
+  if (n_hi)
+    k_unpack<<<blocks(n_hi, 256), 256, 0, h->stream>>>(recv_hi, (uint32_t)n_hi, h->ag[h->cur], h->id[h->cur],
+                                                       off + (uint32_t)n_lo);
+  CU(h, cudaGetLastError());
+  h->launches += (n_lo > 0) + (n_hi > 0);
+  h->n += n_lo + n_hi;
+  return BDM_OK;
+}
+
+int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_t x_begin, int32_t x_end,
+                  const double* recv_lo, int64_t n_lo, const double* recv_hi, int64_t n_hi, int want_dp) {
+  int rc = slab_check(h, "bdm_slab_step");
+  if (rc) return rc;
+  if (!glo3 || !ghi3 || n_lo < 0 || n_hi < 0 || (n_lo && !recv_lo) || (n_hi && !recv_hi) || x_begin >= x_end)
+    return fail(h, BDM_EINVAL, "bdm_slab_step: bad arguments");
+  if (!(h->grid.inv > 0.0)) return fail(h, BDM_ESTATE, "bdm_slab_step: call bdm_slab_set_box_edge first");
+  const int64_t n_own = h->n, n_tot = n_own + n_lo + n_hi;
+  if (n_tot > h->cap)
+    return fail(h, BDM_ERANGE, "bdm_slab_step: %lld owned + ghost agents exceed the capacity %lld", (long long)n_tot,
+                (long long)h->cap);
+  cudaStream_t s = h->stream;
+  // ghosts after the owned agents
+  if (n_lo) k_unpack<<<blocks(n_lo, 256), 256, 0, s>>>(recv_lo, (uint32_t)n_lo, h->ag[h->cur], h->id[h->cur], (uint32_t)n_own);
+  if (n_hi)
+    k_unpack<<<blocks(n_hi, 256), 256, 0, s>>>(recv_hi, (uint32_t)n_hi, h->ag[h->cur], h->id[h->cur],
+                                               (uint32_t)(n_own + n_lo));
+  CU(h, cudaGetLastError());
+  h->launches += (n_lo > 0) + (n_hi > 0);
+  // slab-local grid: box-x [x_begin-1, x_end] clipped to the global extents; y, z global
+  GridDev& g = h->grid;
+  const int64_t lox = std::max<int64_t>((int64_t)x_begin - 1, glo3[0]);
+  const int64_t hix = std::min<int64_t>((int64_t)x_end, ghi3[0]);
+  k_ext_reset<<<1, 32, 0, s>>>(h->ext);
+  h->launches += 1;
+  if (n_tot == 0 || lox > hix) {
+    if (n_tot) return fail(h, BDM_ESTATE, "bdm_slab_step: agents present but the slab lies outside the extents");
+    h->ext_valid = true;
+    h->n_dp = 0;
+    h->state = State::Stepped;
+    return BDM_OK;
+  }
+  g.lo[0] = (int32_t)lox;
+  g.hi[0] = (int32_t)hix;
+  for (int a = 1; a < 3; ++a) {
+    g.lo[a] = glo3[a];
+    g.hi[a] = ghi3[a];
+  }
+  const int64_t nb = (hix - lox + 1) * ((int64_t)g.hi[1] - g.lo[1] + 1) * ((int64_t)g.hi[2] - g.lo[2] + 1);
+  if (nb >= (int64_t)0xffffffffll) return fail(h, BDM_ERANGE, "bdm_slab_step: n_boxes = %lld >= 2^32", (long long)nb);
+  g.ny = g.hi[1] - g.lo[1] + 1;
+  g.nz = g.hi[2] - g.lo[2] + 1;
+  g.n_boxes = (uint32_t)nb;
+  rc = sort_into(h, (uint32_t)n_tot);  // cur -> sorted owned + ghosts
+  if (rc) return rc;
+  // ghosts_lo (box-x = x_begin-1) sort first, ghosts_hi (box-x = x_end) last: the owned agents are
+  // the contiguous range [n_lo, n_tot - n_hi) of the sorted array
+  const int src = h->cur, dst = 1 - h->cur;
+  RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
+  ParamsDev pd = params_dev(h->prm);
+  const unsigned grid = force_grid(h, (uint32_t)n_own);
+  if (n_own > 0) {
+    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, (uint32_t)n_lo,
+                                                 (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
+                                                 want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
+                                                 h->err, rec);
+    CU(h, cudaGetLastError());
+    h->launches += 1;
+  }
+  h->cur = dst;
+  h->n = n_own;
+  h->ext_valid = true;
+  if (want_dp) {
+    h->n_dp = n_own;
+    h->have_dp = true;
+  }
+  h->state = State::Stepped;
+  return BDM_OK;
+}
+
+int bdm_slab_get(bdm_handle h, int what, int64_t* n, uint32_t* ids, double* vals) {
+  int rc = slab_check(h, "bdm_slab_get");
+  if (rc) return rc;
+  if (!n || (what != BDM_OWNED_POSITIONS && what != BDM_LAST_DISPLACEMENTS))
+    return fail(h, BDM_EINVAL, "bdm_slab_get: bad arguments");
+  if (what == BDM_LAST_DISPLACEMENTS && !h->have_dp) return fail(h, BDM_ESTATE, "bdm_slab_get: no displacements yet");
+  const int64_t m = what == BDM_OWNED_POSITIONS ? h->n : h->n_dp;
+  *n = m;
+  if (m == 0 || (!ids && !vals)) return check_async(h);
+  if (what == BDM_OWNED_POSITIONS) {
+    if (ids) CU(h, cudaMemcpyAsync(ids, h->id[h->cur], m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream));
+    if (vals) {
+      CU(h, cudaMemcpy2DAsync(vals, 3 * sizeof(double), h->ag[h->cur], sizeof(double4), 3 * sizeof(double), m,
+                              cudaMemcpyDeviceToDevice, h->stream));
+    }
+  } else {
+    if (ids) CU(h, cudaMemcpyAsync(ids, h->dp_ids, m * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream));
+    if (vals) CU(h, cudaMemcpyAsync(vals, h->dp, 3 * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  }
+  return check_async(h);
 }
 
 int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo3, const double* hi3, double dlo,

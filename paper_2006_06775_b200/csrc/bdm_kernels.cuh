@@ -451,8 +451,8 @@ template <bool RECORD>
 __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     k_force(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, const uint32_t* __restrict__ start,
             uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
-            uint32_t* __restrict__ id_out, double* __restrict__ dp_out, Extents* ext_next, ErrDev* err,
-            RecordDev rec) {
+            uint32_t* __restrict__ id_out, double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
+            Extents* ext_next, ErrDev* err, RecordDev rec) {
   __shared__ ForceSmem s_all[FORCE_WARPS];
   const int lane = threadIdx.x & 31;
   ForceSmem& sm = s_all[threadIdx.x >> 5];
@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
         dp_out[3 * (size_t)o] = dpx;
         dp_out[3 * (size_t)o + 1] = dpy;
         dp_out[3 * (size_t)o + 2] = dpz;
+        if (dp_id_out) dp_id_out[o] = myid;
       }
       const int nb3[3] = {box_coord(np.x, g.inv, ebad), box_coord(np.y, g.inv, ebad), box_coord(np.z, g.inv, ebad)};
 #pragma unroll
@@ -589,6 +590,82 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       if (hi != INT32_MIN && hi > __ldcg(&ext_next->hi[a])) atomicMax(&ext_next->hi[a], hi);
     }
   }
+}
+
+// ------------------------------------------------------------------------------------------ K5/K9
+// x-slab exchange records: 5 fp64 per agent (x, y, z, D, id) -- ids < 2^32 are exact in fp64.
+constexpr int REC = 5;
+
+// Halo (mode 0): owned agents in the first box-x layer of the slab go to the lower neighbour, those
+// in the last layer to the upper one (both when the slab is one box wide).  Migration (mode 1):
+// agents whose box-x left [x_begin, x_end) go to the neighbour on that side; the others are
+// compacted into keep_ag/keep_id.  Order inside the buffers is irrelevant: the receiver sorts by
+// (box, id).  Counters: cnt[0] lo, cnt[1] hi, cnt[2] kept; records past a capacity are dropped
+// (the counts still tell the caller how much to allocate, and keep_* is only committed when both
+// sends fit).
+__global__ void k_slab_pack(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
+                            double inv, int mode, int32_t x_begin, int32_t x_end, double* __restrict__ send_lo,
+                            double* __restrict__ send_hi, uint64_t cap, uint32_t* __restrict__ cnt,
+                            double4* __restrict__ keep_ag, uint32_t* __restrict__ keep_id) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  double4 p = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+  const uint32_t id = valid ? ids[i] : 0u;
+  const int bx = (int)floor(p.x * inv);
+  bool to_lo, to_hi;
+  if (mode == 0) {
+    to_lo = valid && x_begin != INT32_MIN && bx == x_begin;
+    to_hi = valid && x_end != INT32_MAX && bx == x_end - 1;
+  } else {
+    to_lo = valid && bx < x_begin;
+    to_hi = valid && bx >= x_end;
+  }
+  const bool keep = mode == 1 && valid && !to_lo && !to_hi;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const unsigned mlo = __ballot_sync(FULL, to_lo), mhi = __ballot_sync(FULL, to_hi), mk = __ballot_sync(FULL, keep);
+  uint32_t blo = 0, bhi = 0, bk = 0;
+  if (lane == 0) {
+    if (mlo) blo = atomicAdd(&cnt[0], (uint32_t)__popc(mlo));
+    if (mhi) bhi = atomicAdd(&cnt[1], (uint32_t)__popc(mhi));
+    if (mk) bk = atomicAdd(&cnt[2], (uint32_t)__popc(mk));
+  }
+  blo = __shfl_sync(FULL, blo, 0) + __popc(mlo & lt);
+  bhi = __shfl_sync(FULL, bhi, 0) + __popc(mhi & lt);
+  bk = __shfl_sync(FULL, bk, 0) + __popc(mk & lt);
+  if (to_lo && blo < cap) {
+    double* r = send_lo + (size_t)REC * blo;
+    r[0] = p.x; r[1] = p.y; r[2] = p.z; r[3] = p.w; r[4] = (double)id;
+  }
+  if (to_hi && bhi < cap) {
+    double* r = send_hi + (size_t)REC * bhi;
+    r[0] = p.x; r[1] = p.y; r[2] = p.z; r[3] = p.w; r[4] = (double)id;
+  }
+  if (keep) {
+    keep_ag[bk] = p;
+    keep_id[bk] = id;
+  }
+}
+
+// Appends records (ghosts or immigrants) at ag[off..off+m).
+__global__ void k_unpack(const double* __restrict__ rec, uint32_t m, double4* __restrict__ ag,
+                         uint32_t* __restrict__ ids, uint32_t off) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= m) return;
+  const double* r = rec + (size_t)REC * t;
+  ag[off + t] = make_double4(r[0], r[1], r[2], r[3]);
+  ids[off + t] = (uint32_t)r[4];
+}
+
+// Max diameter of ag[0..n) (positive doubles order like their bit patterns).
+__global__ void k_maxd(const double4* __restrict__ ag, uint32_t n, unsigned long long* maxd_bits) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long b = i < n ? (unsigned long long)__double_as_longlong(ag[i].w) : 0ull;
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long v = __shfl_xor_sync(FULL, b, o);
+    b = v > b ? v : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b && b > __ldcg(maxd_bits)) atomicMax(maxd_bits, b);
 }
 
 // ------------------------------------------------------------------------------------------ K7

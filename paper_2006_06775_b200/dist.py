@@ -1,0 +1,339 @@
+"""x-slab decomposition of the mechanical step across ranks.
+
+north_star: "Across the 8 GPUs of one box the domain is split into x-slabs.  Each step does a halo
+exchange of boundary-box agents and migrates agents that cross slab boundaries, using NCCL
+send/recv over NVLink."
+
+Rank g owns the agents whose integer box-x lies in [bounds[g], bounds[g+1]) (bounds[0] = INT32_MIN,
+bounds[G] = INT32_MAX).  One step:
+  1. allreduce of the box extents (min lo / max hi of the owned agents' box coordinates, O2);
+  2. halo: every rank sends its first box-x layer to g-1 and its last to g+1 (ghosts);
+  3. bdm_slab_step: slab-local grid over owned + ghosts, force / displacement / update of the owned
+     agents (all in libbdm.so kernels);
+  4. migration: agents whose new box-x left the slab go to g-1 / g+1 and are appended there.
+Counts travel before payloads; records are 5 fp64 (x, y, z, D, id).  The arithmetic is unchanged
+from the single-GPU path and ghosts keep their global ids, so every owned agent's force is summed
+in the same canonical order: results are bit-identical to one GPU.
+
+This module is orchestration only (which buffer goes to which rank).  It runs against any engine
+with the interface of GpuSlabEngine and any communicator with the interface of TorchComm -- the
+CPU tests drive it with a gloo communicator and a test engine, the virtual-slab GPU test with
+LoopComm (several slabs in one process).
+"""
+from __future__ import annotations
+
+import json
+import time
+
+import numpy as np
+
+INT32_MIN = -(2 ** 31)
+INT32_MAX = 2 ** 31 - 1
+REC = 5
+
+
+def choose_bounds(hist: np.ndarray, x0: int, world: int, weights: np.ndarray | None = None) -> list[int]:
+    """Slab bounds on integer box-x from a global histogram (hist[k] = agents with box-x = x0 + k).
+
+    Cuts balance the (optionally weighted) agent count; every slab is at least one box wide."""
+    w = hist.astype(np.float64) if weights is None else weights.astype(np.float64)
+    nx = len(w)
+    bounds = [INT32_MIN]
+    if world > 1:
+        cum = np.cumsum(w)
+        total = cum[-1] if nx else 0.0
+        prev = x0
+        for g in range(1, world):
+            target = total * g / world
+            k = int(np.searchsorted(cum, target, side="left")) + 1  # first box of slab g (relative)
+            cut = x0 + k
+            cut = max(cut, prev + 1)
+            cut = min(cut, x0 + nx - (world - g)) if nx >= world else max(cut, prev + 1)
+            bounds.append(int(cut))
+            prev = cut
+    bounds.append(INT32_MAX)
+    return bounds
+
+
+# --------------------------------------------------------------------------------- communicators
+class TorchComm:
+    """One slab per process; exchange with ranks g-1 / g+1 over torch.distributed (NCCL or gloo)."""
+
+    def __init__(self, device=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        self.device = device
+
+    def slab_ids(self):
+        return [self.rank]
+
+    def _t(self, arr, dtype):
+        import torch
+
+        return torch.as_tensor(np.asarray(arr), dtype=dtype, device=self.device)
+
+    def allreduce_max(self, vals):
+        import torch
+
+        t = self._t([max(vals)], torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allreduce_sum(self, arrs):
+        import torch
+
+        t = self._t(np.sum(np.stack(arrs), axis=0), torch.int64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return t.cpu().numpy()
+
+    def allreduce_extents(self, exts):
+        import torch
+
+        (lo, hi), = exts
+        t = self._t(np.concatenate([np.asarray(lo, np.int64), -np.asarray(hi, np.int64)]), torch.int64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN)
+        v = t.cpu().numpy()
+        return v[:3].astype(np.int64), (-v[3:]).astype(np.int64)
+
+    def exchange(self, sends):
+        """sends = [(to_lower, to_upper)] ([m,5] fp64 tensors); returns [(from_lower, from_upper)]."""
+        import torch
+
+        dist = self.dist
+        (s_lo, s_hi), = sends
+        r, G = self.rank, self.world
+        dev = s_lo.device
+        peers = [(r - 1, s_lo), (r + 1, s_hi)]
+        cnt_out = {p: torch.tensor([t.shape[0]], dtype=torch.int64, device=dev) for p, t in peers if 0 <= p < G}
+        cnt_in = {p: torch.zeros(1, dtype=torch.int64, device=dev) for p, _ in peers if 0 <= p < G}
+        for p, t in peers:
+            if not (0 <= p < G):
+                assert t.shape[0] == 0, "records addressed to a rank outside the job"
+        ops = []
+        for p in cnt_out:
+            ops.append(dist.P2POp(dist.isend, cnt_out[p], p))
+            ops.append(dist.P2POp(dist.irecv, cnt_in[p], p))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        recv = {}
+        ops = []
+        for p, t in peers:
+            if not (0 <= p < G):
+                recv[p] = torch.empty((0, REC), dtype=torch.float64, device=dev)
+                continue
+            m = int(cnt_in[p].item())
+            recv[p] = torch.empty((m, REC), dtype=torch.float64, device=dev)
+            if t.shape[0]:
+                ops.append(dist.P2POp(dist.isend, t.contiguous(), p))
+            if m:
+                ops.append(dist.P2POp(dist.irecv, recv[p], p))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return [(recv[r - 1], recv[r + 1])]
+
+
+class LoopComm:
+    """All slabs in one process: exchanges are hand-overs between the local slabs (virtual slabs on
+    one GPU, or one CPU process).  Same interface as TorchComm with lists over all slabs."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+    def slab_ids(self):
+        return list(range(self.world))
+
+    def allreduce_max(self, vals):
+        return float(max(vals))
+
+    def allreduce_sum(self, arrs):
+        return np.sum(np.stack(arrs), axis=0)
+
+    def allreduce_extents(self, exts):
+        lo = np.min(np.stack([np.asarray(e[0], np.int64) for e in exts]), axis=0)
+        hi = np.max(np.stack([np.asarray(e[1], np.int64) for e in exts]), axis=0)
+        return lo, hi
+
+    def exchange(self, sends):
+        G = self.world
+        out = []
+        for g in range(G):
+            frm_lo = sends[g - 1][1] if g > 0 else sends[g][0][:0]
+            frm_hi = sends[g + 1][0] if g + 1 < G else sends[g][1][:0]
+            out.append((frm_lo, frm_hi))
+        assert sends[0][0].shape[0] == 0 and sends[G - 1][1].shape[0] == 0
+        return out
+
+
+# --------------------------------------------------------------------------------- GPU engine
+class GpuSlabEngine:
+    """One rank's slab on a GPU, through the C ABI (libbdm.so bdm_slab_*)."""
+
+    def __init__(self, ids, pos, diam, capacity: int, params=None, device=None, stream=None):
+        import torch
+
+        import paper_2006_06775_b200 as bdm
+
+        self.bdm = bdm
+        self.torch = torch
+        self.device = device if device is not None else pos.device
+        self.h = bdm.bdm_slab_init(ids, pos, diam, capacity, params, stream=stream)
+        self.buf_cap = max(1024, capacity // 16)
+        self._alloc()
+
+    def _alloc(self):
+        t = self.torch
+        self.s_lo = t.empty((self.buf_cap, REC), dtype=t.float64, device=self.device)
+        self.s_hi = t.empty((self.buf_cap, REC), dtype=t.float64, device=self.device)
+
+    def local_maxd(self):
+        return self.bdm.bdm_slab_local_maxd(self.h)
+
+    def set_box_edge(self, L):
+        self.bdm.bdm_slab_set_box_edge(self.h, L)
+
+    def local_extents(self):
+        return self.bdm.bdm_slab_local_extents(self.h)
+
+    def pack(self, what, xb, xe):
+        while True:
+            rc, nlo, nhi = self.bdm.bdm_slab_pack(self.h, what, xb, xe, self.s_lo, self.s_hi, self.buf_cap)
+            if rc == self.bdm.BDM_OK:
+                return self.s_lo[:nlo], self.s_hi[:nhi]
+            self.buf_cap = int(max(nlo, nhi) * 1.25) + 1024
+            self._alloc()
+
+    def step(self, glo, ghi, xb, xe, recv_lo, recv_hi, want_dp=False):
+        self.bdm.bdm_slab_step(self.h, glo, ghi, xb, xe, recv_lo, recv_lo.shape[0], recv_hi, recv_hi.shape[0],
+                               want_dp)
+
+    def add(self, recv_lo, recv_hi):
+        self.bdm.bdm_slab_add(self.h, recv_lo, recv_lo.shape[0], recv_hi, recv_hi.shape[0])
+
+    def owned(self):
+        ids, pos = self.bdm.bdm_slab_get(self.h, self.bdm.BDM_OWNED_POSITIONS)
+        return ids.cpu().numpy(), pos.cpu().numpy()
+
+    def last_dp(self):
+        ids, dp = self.bdm.bdm_slab_get(self.h, self.bdm.BDM_LAST_DISPLACEMENTS)
+        return ids.cpu().numpy(), dp.cpu().numpy()
+
+
+# --------------------------------------------------------------------------------- the protocol
+HALO, MIGRANTS = 0, 1
+
+
+class SlabDriver:
+    """Runs the per-step protocol over the local slabs `engines` (engine k is slab comm.slab_ids()[k])."""
+
+    def __init__(self, engines, comm, bounds):
+        self.engines = engines
+        self.comm = comm
+        self.bounds = bounds
+        self.slabs = [(bounds[g], bounds[g + 1]) for g in comm.slab_ids()]
+        L = comm.allreduce_max([e.local_maxd() for e in engines])  # O1 over all ranks
+        for e in engines:
+            e.set_box_edge(L)
+        self.L = L
+        self.migrated = 0  # agents moved between slabs by step() (diagnostics)
+        self.settle()
+
+    def migrate(self):
+        sends = [e.pack(MIGRANTS, xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]
+        moved = self.comm.allreduce_sum([np.array([s[0].shape[0] + s[1].shape[0]], np.int64) for s in sends])
+        recvs = self.comm.exchange(sends)
+        for e, (rl, rh) in zip(self.engines, recvs):
+            e.add(rl, rh)
+        return int(moved[0])
+
+    def settle(self, max_rounds: int | None = None):
+        """Move every agent to its owner (agents hop one slab per round)."""
+        rounds = 0
+        while self.migrate() > 0:
+            rounds += 1
+            if rounds > (max_rounds or len(self.bounds)):
+                raise RuntimeError("agents did not settle in their slabs")
+        return rounds
+
+    def step(self, want_dp: bool = False):
+        exts = [e.local_extents() for e in self.engines]
+        glo, ghi = self.comm.allreduce_extents(exts)
+        halos = [e.pack(HALO, xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]
+        ghosts = self.comm.exchange(halos)
+        self.ghosts = sum(gl.shape[0] + gh.shape[0] for gl, gh in ghosts)
+        for e, (xb, xe), (gl, gh) in zip(self.engines, self.slabs, ghosts):
+            e.step(glo, ghi, xb, xe, gl, gh, want_dp)
+        self.migrated += self.migrate()
+
+
+def initial_bounds(pos: np.ndarray, diam: np.ndarray, world: int, box_edge_min: float = 0.0):
+    """Setup helper (outside the hot path): global L and count-balanced bounds from the full population
+    known to every rank (the bench generates the whole seeded population on every rank)."""
+    L = max(float(diam.max()), box_edge_min)
+    inv = 1.0 / (L * (1.0 + 2.0 ** -30))
+    bx = np.floor(pos[:, 0] * inv).astype(np.int64)
+    x0 = int(bx.min())
+    hist = np.bincount(bx - x0)
+    return choose_bounds(hist, x0, world), bx
+
+
+# --------------------------------------------------------------------------------- bench (N > 1)
+def bench_multi(args, metric, unit, config_obj, load_peaks, ClockSampler):
+    """bench.py under torchrun: strong scaling of one config over x-slabs, one rank per GPU."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import bdm_inputs
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    rank, world = dist.get_rank(), dist.get_world_size()
+    pos_h, diam_h = bdm_inputs.make_config(args.config, args.n)
+    n = len(diam_h)
+    bounds, bx = initial_bounds(pos_h, diam_h, world)
+    mine = np.flatnonzero((bx >= bounds[rank]) & (bx < bounds[rank + 1]))
+    cap = int(max(len(mine) * 1.3, n / world * 1.3)) + 4096
+    ids = torch.from_numpy(mine.astype(np.int64)).to(dev)
+    pos = torch.from_numpy(np.ascontiguousarray(pos_h[mine])).to(dev)
+    diam = torch.from_numpy(np.ascontiguousarray(diam_h[mine])).to(dev)
+    del pos_h, diam_h, bx
+    stream = torch.cuda.current_stream()
+    eng = GpuSlabEngine(ids, pos, diam, cap, stream=stream)
+    drv = SlabDriver([eng], TorchComm(dev), bounds)
+    for _ in range(max(args.warmup, 3)):
+        drv.step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            drv.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    value = n * args.steps / (ms / 1e3)
+    if rank == 0:
+        line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_obj(args, n, world), "bounds": [int(b) for b in bounds[1:-1]],
+                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+                "clocks": clk.summary(), "timing": "CUDA events on each rank's stream, max over ranks"}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

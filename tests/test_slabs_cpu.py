@@ -1,0 +1,123 @@
+"""CPU tests of the x-slab protocol (paper_2006_06775_b200/dist.py), no GPU.
+
+* LoopComm with G slabs in one process;
+* world_size-2 torch.distributed over gloo (127.0.0.1), one slab per process;
+both with the oracle-backed test engine (tests/slab_cpu_engine.py).  After K steps the gathered
+positions must equal the single-process oracle trajectory bit for bit (north_star: halo exchange +
+migration must not change any agent's neighbourhood)."""
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import bdm_inputs
+import oracle
+from paper_2006_06775_b200 import dist as bdist
+from slab_cpu_engine import CpuSlabEngine
+
+
+def population(n=1500, seed=4):
+    # elongated in x so that slabs are several boxes wide and agents cross cuts
+    pos, diam = bdm_inputs.random_instance(seed, n, 1.0, 6.0, 14.0)
+    rng = np.random.default_rng(seed)
+    pos = np.stack([rng.uniform(0, 260, n), rng.uniform(0, 70, n), rng.uniform(0, 70, n)], axis=1)
+    return pos, diam
+
+
+def test_choose_bounds():
+    hist = np.array([5, 5, 5, 5, 5, 5, 5, 5])
+    b = bdist.choose_bounds(hist, 10, 4)
+    assert b[0] == bdist.INT32_MIN and b[-1] == bdist.INT32_MAX
+    assert b[1:-1] == [12, 14, 16]
+    b = bdist.choose_bounds(np.array([100, 0, 0, 1]), 0, 3)  # every slab at least one box wide
+    assert b[1:-1] == [1, 2]
+    b = bdist.choose_bounds(np.array([7]), 3, 4)  # more slabs than boxes: strictly increasing
+    assert all(x < y for x, y in zip(b, b[1:]))
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 5])
+def test_loop_slabs_match_single_process(G):
+    pos, diam = population()
+    steps = 3
+    ref, _ = oracle.run(pos, diam, steps)
+    bounds, bx = bdist.initial_bounds(pos, diam, G)
+    engines = []
+    for g in range(G):
+        m = np.flatnonzero((bx >= bounds[g]) & (bx < bounds[g + 1]))
+        engines.append(CpuSlabEngine(m, pos[m], diam[m]))
+    drv = bdist.SlabDriver(engines, bdist.LoopComm(G), bounds)
+    for _ in range(steps):
+        drv.step()
+    if G > 1:
+        assert drv.migrated > 0 and drv.ghosts > 0  # the protocol was exercised
+    ids = np.concatenate([e.owned()[0] for e in engines])
+    got = np.concatenate([e.owned()[1] for e in engines])
+    assert np.array_equal(np.sort(ids), np.arange(len(diam)))  # agents conserved, none duplicated
+    out = np.empty_like(got)
+    out[ids] = got
+    assert np.array_equal(out, ref)
+
+
+def test_loop_slabs_settle_from_arbitrary_distribution():
+    """Ranks may start with any subset (bdm_init_dist semantics): the setup migrates every agent to
+    its owner before the first step."""
+    pos, diam = population(900, 7)
+    G = 4
+    bounds, _ = bdist.initial_bounds(pos, diam, G)
+    assign = np.random.default_rng(0).integers(0, G, len(diam))
+    engines = [CpuSlabEngine(np.flatnonzero(assign == g), pos[assign == g], diam[assign == g]) for g in range(G)]
+    drv = bdist.SlabDriver(engines, bdist.LoopComm(G), bounds)
+    drv.step()
+    ref, _ = oracle.run(pos, diam, 1)
+    ids = np.concatenate([e.owned()[0] for e in engines])
+    got = np.concatenate([e.owned()[1] for e in engines])
+    out = np.empty_like(got)
+    out[ids] = got
+    assert np.array_equal(out, ref)
+
+
+def _worker(rank, world, port, steps, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pos, diam = population(1200, 11)
+        bounds, bx = bdist.initial_bounds(pos, diam, world)
+        m = np.flatnonzero((bx >= bounds[rank]) & (bx < bounds[rank + 1]))
+        eng = CpuSlabEngine(m, pos[m], diam[m])
+        drv = bdist.SlabDriver([eng], bdist.TorchComm(torch.device("cpu")), bounds)
+        for _ in range(steps):
+            drv.step()
+        ids, p = eng.owned()
+        got = [None] * world
+        dist.all_gather_object(got, (ids, p))
+        if rank == 0:
+            q.put(got)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks_match_single_process():
+    world, steps = 2, 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_worker, args=(r, world, port, steps, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    pos, diam = population(1200, 11)
+    ref, _ = oracle.run(pos, diam, steps)
+    ids = np.concatenate([g[0] for g in got])
+    vals = np.concatenate([g[1] for g in got])
+    assert np.array_equal(np.sort(ids), np.arange(len(diam)))
+    out = np.empty_like(vals)
+    out[ids] = vals
+    assert np.array_equal(out, ref)
+    # both ranks really owned agents (the cut is inside the population)
+    assert all(len(g[0]) > 100 for g in got)
