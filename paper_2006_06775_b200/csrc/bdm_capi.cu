@@ -71,6 +71,11 @@ struct bdm_ctx {
   unsigned long long *r_nbh = nullptr, *r_cth = nullptr;
   bool have_record = false;
   // timing
+  // ragged box table
+  int32_t *czlo = nullptr, *czhi = nullptr;
+  uint32_t* coff = nullptr;
+  size_t col_cap = 0;
+  int scan_blocks_per_sm = 0;
   // x-slab mode (multi-GPU)
   bool slab = false;
   int64_t cap = 0;            // capacity of owned + ghost agents
@@ -151,7 +156,7 @@ int check_async(bdm_ctx* h) {
   return BDM_OK;
 }
 
-int ensure_table(bdm_ctx* h, size_t entries) {
+int ensure_table(bdm_ctx* h, size_t entries, size_t min_scan_items) {
   if (entries > h->table_cap) {
     if (h->table) CU(h, cudaFree(h->table));
     h->table = nullptr;
@@ -159,7 +164,7 @@ int ensure_table(bdm_ctx* h, size_t entries) {
     CU(h, cudaMalloc(&h->table, cap * sizeof(uint32_t)));
     h->table_cap = cap;
   }
-  size_t tiles = (entries + SCAN_TILE - 1) / SCAN_TILE;
+  size_t tiles = (std::max(entries, min_scan_items) + SCAN_TILE - 1) / SCAN_TILE;
   if (tiles > h->scan_tiles_cap) {
     if (h->scan_state) CU(h, cudaFree(h->scan_state));
     h->scan_state = nullptr;
@@ -167,6 +172,48 @@ int ensure_table(bdm_ctx* h, size_t entries) {
     CU(h, cudaMalloc(&h->scan_state, cap * sizeof(unsigned long long)));
     h->scan_tiles_cap = cap;
   }
+  return BDM_OK;
+}
+
+int ensure_columns(bdm_ctx* h, size_t entries) {
+  if (entries > h->col_cap) {
+    for (void* p : {(void*)h->czlo, (void*)h->czhi, (void*)h->coff})
+      if (p) CU(h, cudaFree(p));
+    h->czlo = h->czhi = nullptr;
+    h->coff = nullptr;
+    size_t cap = entries + entries / 8 + 1024;
+    CU(h, cudaMalloc(&h->czlo, cap * sizeof(int32_t)));
+    CU(h, cudaMalloc(&h->czhi, cap * sizeof(int32_t)));
+    CU(h, cudaMalloc(&h->coff, cap * sizeof(uint32_t)));
+    h->col_cap = cap;
+  }
+  return BDM_OK;
+}
+
+void init_device_info(bdm_ctx* h) {
+  if (h->sm_count) return;
+  cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<false>, FORCE_THREADS, 0);
+  h->force_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan, SCAN_THREADS, 0);
+  h->scan_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+}
+
+// In-place exclusive scan of data[0 .. items) -- items given on the host, or read on the device as
+// *n_dev + 1 (persistent decoupled look-back, grid = resident capacity).
+int scan(bdm_ctx* h, uint32_t* data, uint64_t items, const uint32_t* n_dev) {
+  init_device_info(h);
+  size_t tiles_bound = h->scan_tiles_cap;
+  uint64_t want = items ? (items + SCAN_TILE - 1) / SCAN_TILE : tiles_bound;
+  CU(h, cudaMemsetAsync(h->scan_state, 0, std::min<uint64_t>(want, tiles_bound) * sizeof(unsigned long long),
+                        h->stream));
+  CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), h->stream));
+  const uint64_t cap = (uint64_t)h->sm_count * h->scan_blocks_per_sm;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
+  k_scan<<<grid, SCAN_THREADS, 0, h->stream>>>(data, n_dev, items, h->scan_state, h->scan_ticket);
+  CU(h, cudaGetLastError());
   return BDM_OK;
 }
 
@@ -202,27 +249,44 @@ int compute_extents(bdm_ctx* h) {
   return BDM_OK;
 }
 
-// Counting sort of ag[cur][0..n) by (box key under h->grid, id) into ag[1-cur]; box start table
-// in h->table.  cur flips to the sorted buffer.
+// Counting sort of ag[cur][0..n) by (box key under h->grid, id) into ag[1-cur]:
+//   column pass (occupied z-range per (bx, by) column) -> column offsets (scan) -> table zero ->
+//   key + histogram -> table scan (box starts) -> scatter -> in-box id order + payload gather.
+// The ragged table size T lives on the device (coff[nc]); no host round trip inside the build.
+// cur flips to the sorted buffer.
 int sort_into(bdm_ctx* h, uint32_t n) {
-  const size_t items = (size_t)h->grid.n_boxes + 1;
-  int rc = ensure_table(h, items);
+  GridDev& g = h->grid;
+  const uint64_t nc = (uint64_t)(g.hi[0] - g.lo[0] + 1) * (uint64_t)g.ny;
+  if (nc >= 0xffffffffull) return fail(h, BDM_ERANGE, "%llu grid columns >= 2^32", (unsigned long long)nc);
+  g.n_cols = (uint32_t)nc;
+  int rc = ensure_columns(h, nc + 1);
   if (rc) return rc;
+  rc = ensure_table(h, (size_t)g.n_boxes + 1, nc + 1);
+  if (rc) return rc;
+  g.czlo = h->czlo;
+  g.czhi = h->czhi;
+  g.coff = h->coff;
+  g.table = h->table;
   cudaStream_t s = h->stream;
   const int src = h->cur, dst = 1 - h->cur;
-  CU(h, cudaMemsetAsync(h->table, 0, items * sizeof(uint32_t), s));
-  if (n > 0) k_key_hist<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, h->grid, h->key, h->slot, h->table);
-  size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
-  CU(h, cudaMemsetAsync(h->scan_state, 0, tiles * sizeof(unsigned long long), s));
-  CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), s));
-  k_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(h->table, items, h->scan_state, h->scan_ticket);
+  init_device_info(h);
+  const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
+  k_col_reset<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols);
+  if (n > 0) k_col_ext<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
+  k_col_len<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols, h->coff);
+  rc = scan(h, h->coff, nc + 1, nullptr);  // exclusive: coff[c] = table offset, coff[nc] = T
+  if (rc) return rc;
+  k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
+  if (n > 0) k_key_hist<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table);
+  rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
+  if (rc) return rc;
   if (n > 0) {
     k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
     k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
                                            h->id[dst]);
   }
   CU(h, cudaGetLastError());
-  h->launches += n > 0 ? 4 : 1;
+  h->launches += n > 0 ? 8 : 4;
   h->cur = dst;
   return BDM_OK;
 }
@@ -246,12 +310,7 @@ int grid_build(bdm_ctx* h) {
 
 // Persistent grid: resident blocks per SM x SMs, no more than the work needs.
 unsigned force_grid(bdm_ctx* h, uint32_t n) {
-  if (!h->sm_count) {
-    cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<false>, FORCE_THREADS, 0);
-    h->force_blocks_per_sm = per_sm > 0 ? per_sm : 1;
-  }
+  init_device_info(h);
   unsigned want = (n + FORCE_THREADS - 1) / FORCE_THREADS;
   unsigned cap = (unsigned)(h->sm_count * h->force_blocks_per_sm);
   return want < cap ? (want ? want : 1) : cap;
@@ -267,10 +326,10 @@ int force_step(bdm_ctx* h, bool want_dp) {
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
   if (h->prm.flags & BDM_RECORD)
-    k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, 0u, n, h->grid, pd, h->ag[dst],
+    k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], 0u, n, h->grid, pd, h->ag[dst],
                                                 nullptr, dp, nullptr, h->ext, h->err, rec);
   else
-    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, 0u, n, h->grid, pd,
+    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], 0u, n, h->grid, pd,
                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec);
   CU(h, cudaGetLastError());
   h->launches += 2;
@@ -387,7 +446,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -697,7 +756,7 @@ int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_
   ParamsDev pd = params_dev(h->prm);
   Scratch sc_counts, sc_off, sc_out;
   CU(h, cudaMalloc(&sc_counts.p, n * sizeof(uint32_t)));
-  k_pairs<<<blocks(n, 128), 128, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], h->table, n, h->grid, pd, kind,
+  k_pairs<<<blocks(n, 128), 128, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->grid, pd, kind,
                                                  static_cast<uint32_t*>(sc_counts.p), nullptr, nullptr);
   CU(h, cudaGetLastError());
   std::vector<uint32_t> counts(n);
@@ -715,7 +774,7 @@ int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_
   CU(h, cudaMalloc(&sc_off.p, n * sizeof(unsigned long long)));
   CU(h, cudaMalloc(&sc_out.p, 2 * total * sizeof(long long)));
   CU(h, cudaMemcpyAsync(sc_off.p, off.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, h->stream));
-  k_pairs<<<blocks(n, 128), 128, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], h->table, n, h->grid, pd, kind,
+  k_pairs<<<blocks(n, 128), 128, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->grid, pd, kind,
                                                  nullptr, static_cast<unsigned long long*>(sc_off.p),
                                                  static_cast<long long*>(sc_out.p));
   CU(h, cudaGetLastError());
@@ -986,7 +1045,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   ParamsDev pd = params_dev(h->prm);
   const unsigned grid = force_grid(h, (uint32_t)n_own);
   if (n_own > 0) {
-    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], h->table, (uint32_t)n_lo,
+    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], (uint32_t)n_lo,
                                                  (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
                                                  h->err, rec);

@@ -25,12 +25,24 @@ namespace bdm {
 constexpr unsigned FULL = 0xffffffffu;
 
 // Grid parameters of one build, passed by value to kernels.
+//
+// Box table layout ("ragged" by column): a column is one (bx, by) pair; column c of the frame
+// [lo_x, hi_x] x [lo_y, hi_y] stores only its occupied z-range [czlo[c], czhi[c]], at table offset
+// coff[c].  Box (bx, by, bz) has key coff[c] + (bz - czlo[c]); keys keep x slowest, then y, then z,
+// so a slab is a contiguous key range and the 3 boxes (bx, by, bz-1..bz+1) are one contiguous range
+// of the sorted agents.  table[key] = first sorted agent of the box, table[T] = N.  For the
+// Gaussian cfg3 this is 3.8e7 entries instead of the 3.1e8 of the dense box lattice.
 struct GridDev {
   double L, L2, inv;
   double thr_pad;  // (L/2) used for the conservative contact prefilter
   int32_t lo[3], hi[3];
   int32_t ny, nz;
-  uint32_t n_boxes;
+  uint32_t n_boxes;  // dense lattice size (reported; the table itself is ragged)
+  uint32_t n_cols;   // nx * ny
+  const int32_t* czlo;
+  const int32_t* czhi;
+  const uint32_t* coff;  // n_cols + 1
+  const uint32_t* table;
 };
 
 struct ParamsDev {
@@ -174,9 +186,71 @@ __global__ void k_ext_reset(Extents* ext) {
   if (threadIdx.x == 4) ext->work = 0u;
 }
 
+__device__ __forceinline__ uint32_t col_of(const GridDev& g, int bx, int by) {
+  return (uint32_t)(bx - g.lo[0]) * (uint32_t)g.ny + (uint32_t)(by - g.lo[1]);
+}
+
+// key of an occupied box (the agent's own box)
 __device__ __forceinline__ uint32_t box_key(const GridDev& g, int bx, int by, int bz) {
-  return ((uint32_t)(bx - g.lo[0]) * (uint32_t)g.ny + (uint32_t)(by - g.lo[1])) * (uint32_t)g.nz +
-         (uint32_t)(bz - g.lo[2]);
+  const uint32_t c = col_of(g, bx, by);
+  return __ldg(&g.coff[c]) + (uint32_t)(bz - __ldg(&g.czlo[c]));
+}
+
+// Sorted-agent range [b, e) of the boxes (cx, cy, z0..z1) (O3's z-run of one column); false if empty.
+__device__ __forceinline__ bool zrun(const GridDev& g, int cx, int cy, int z0, int z1, uint32_t& b, uint32_t& e) {
+  if (cx < g.lo[0] || cx > g.hi[0] || cy < g.lo[1] || cy > g.hi[1]) return false;
+  const uint32_t c = col_of(g, cx, cy);
+  const int zl = __ldg(&g.czlo[c]), zh = __ldg(&g.czhi[c]);
+  const int a = z0 > zl ? z0 : zl, d = z1 < zh ? z1 : zh;
+  if (a > d) return false;
+  const uint32_t o = __ldg(&g.coff[c]);
+  b = __ldg(&g.table[o + (uint32_t)(a - zl)]);
+  e = __ldg(&g.table[o + (uint32_t)(d - zl) + 1u]);
+  return true;
+}
+
+// ---- column pass: occupied z-range of every column, then lengths for the offset scan
+__global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ czhi, uint32_t nc) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
+    czlo[c] = INT32_MAX;
+    czhi[c] = INT32_MIN;
+  }
+}
+
+__global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g, int32_t* __restrict__ czlo,
+                          int32_t* __restrict__ czhi) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  uint32_t c = 0xffffffffu;
+  int bz = 0;
+  if (valid) {
+    const double4 p = ag[i];
+    const int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv);
+    bz = (int)floor(p.z * g.inv);
+    c = col_of(g, bx, by);
+  }
+  // warp-aggregated: agents arrive mostly in box order, so a warp touches few columns; each group
+  // of lanes with the same column reduces with redux.sync over its own member mask
+  const unsigned peers = __match_any_sync(FULL, c);
+  const int zmin = __reduce_min_sync(peers, bz);
+  const int zmax = __reduce_max_sync(peers, bz);
+  const int lane = threadIdx.x & 31;
+  if (valid && lane == __ffs(peers) - 1) {
+    if (zmin < __ldcg(&czlo[c])) atomicMin(&czlo[c], zmin);
+    if (zmax > __ldcg(&czhi[c])) atomicMax(&czhi[c], zmax);
+  }
+}
+
+__global__ void k_col_len(const int32_t* __restrict__ czlo, const int32_t* __restrict__ czhi, uint32_t nc,
+                          uint32_t* __restrict__ len) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += gridDim.x * blockDim.x)
+    len[c] = c < nc && czhi[c] >= czlo[c] ? (uint32_t)(czhi[c] - czlo[c] + 1) : 0u;
+}
+
+// zero table[0 .. T] with T = coff[nc] read on the device (no host round trip)
+__global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __restrict__ coff, uint32_t nc) {
+  const uint32_t T = coff[nc];
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= T; k += gridDim.x * blockDim.x) table[k] = 0u;
 }
 
 // ------------------------------------------------------------------------------------------ K2
@@ -220,87 +294,94 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
 
 __device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_sync(FULL, v); }
 
-// In-place exclusive scan of data[0..n_items) (n_items = n_boxes + 1, last input 0 so that
-// data[n_boxes] becomes the total).  Tile order is taken from an atomic ticket so every
-// predecessor of a tile has started: the look-back cannot deadlock.
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan(uint32_t* __restrict__ data, uint64_t n_items,
-                                                       unsigned long long* __restrict__ state,
+// In-place exclusive scan of data[0..n_items) (the last input is 0 so that data[n_items-1] becomes
+// the total).  n_items = n_items_host, or *n_dev + 1 read on the device when n_items_host == 0.
+// Persistent blocks take tiles from an atomic ticket, so every predecessor of a tile is held by a
+// running block and the decoupled look-back cannot deadlock (the grid never exceeds the resident
+// capacity).
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan(uint32_t* __restrict__ data, const uint32_t* __restrict__ n_dev,
+                                                       uint64_t n_items_host, unsigned long long* __restrict__ state,
                                                        uint32_t* __restrict__ ticket) {
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[SCAN_THREADS / 32];
   __shared__ uint32_t s_prefix;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t base = (uint64_t)tile * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
-  uint32_t v[SCAN_ITEMS];
-  if (base + SCAN_ITEMS <= n_items) {
-    const uint4* src = reinterpret_cast<const uint4*>(data + base);
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS / 4; ++q) {
-      uint4 w = src[q];
-      v[4 * q] = w.x;
-      v[4 * q + 1] = w.y;
-      v[4 * q + 2] = w.z;
-      v[4 * q + 3] = w.w;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q) v[q] = base + q < n_items ? data[base + q] : 0u;
-  }
-  uint32_t tsum = 0;
-#pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += v[q];
+  const uint64_t n_items = n_items_host ? n_items_host : (uint64_t)(*n_dev) + 1;
+  const uint64_t n_tiles = (n_items + SCAN_TILE - 1) / SCAN_TILE;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t incl = warp_incl_scan(tsum);
-  if (lane == 31) s_warp[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t ws = lane < SCAN_THREADS / 32 ? s_warp[lane] : 0u;
-    uint32_t wi = warp_incl_scan(ws);
-    if (lane < SCAN_THREADS / 32) s_warp[lane] = wi - ws;  // exclusive warp offsets
-    uint32_t agg = __shfl_sync(FULL, wi, SCAN_THREADS / 32 - 1);
-    // decoupled look-back
-    uint32_t excl = 0;
-    if (tile == 0) {
-      if (lane == 0) atomicExch(&state[0], (2ull << 32) | agg);
-    } else {
-      if (lane == 0) atomicExch(&state[tile], (1ull << 32) | agg);
-      int64_t pred = (int64_t)tile - 1;
-      while (true) {
-        int64_t idx = pred - lane;
-        unsigned long long st = idx >= 0 ? atomicAdd(&state[idx], 0ull) : (2ull << 32);
-        uint32_t status = (uint32_t)(st >> 32);
-        if (__any_sync(FULL, status == 0u)) continue;
-        unsigned incl_mask = __ballot_sync(FULL, status == 2u);
-        if (incl_mask) {
-          int first = __ffs(incl_mask) - 1;
-          excl += warp_sum(lane <= first ? (uint32_t)st : 0u);
-          break;
-        }
-        excl += warp_sum((uint32_t)st);
-        pred -= 32;
+  while (true) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= n_tiles) return;
+    const uint64_t base = (uint64_t)tile * SCAN_TILE + (uint64_t)threadIdx.x * SCAN_ITEMS;
+    uint32_t v[SCAN_ITEMS];
+    if (base + SCAN_ITEMS <= n_items) {
+      const uint4* src = reinterpret_cast<const uint4*>(data + base);
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS / 4; ++q) {
+        uint4 w = src[q];
+        v[4 * q] = w.x;
+        v[4 * q + 1] = w.y;
+        v[4 * q + 2] = w.z;
+        v[4 * q + 3] = w.w;
       }
-      if (lane == 0) atomicExch(&state[tile], (2ull << 32) | (uint32_t)(excl + agg));
+    } else {
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q) v[q] = base + q < n_items ? data[base + q] : 0u;
     }
-    if (lane == 0) s_prefix = excl;
-  }
-  __syncthreads();
-  uint32_t run = s_prefix + s_warp[warp] + (incl - tsum);
-  uint32_t o[SCAN_ITEMS];
+    uint32_t tsum = 0;
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    o[q] = run;
-    run += v[q];
-  }
-  if (base + SCAN_ITEMS <= n_items) {
-    uint4* dst = reinterpret_cast<uint4*>(data + base);
+    for (int q = 0; q < SCAN_ITEMS; ++q) tsum += v[q];
+    uint32_t incl = warp_incl_scan(tsum);
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t ws = lane < SCAN_THREADS / 32 ? s_warp[lane] : 0u;
+      uint32_t wi = warp_incl_scan(ws);
+      if (lane < SCAN_THREADS / 32) s_warp[lane] = wi - ws;  // exclusive warp offsets
+      uint32_t agg = __shfl_sync(FULL, wi, SCAN_THREADS / 32 - 1);
+      uint32_t excl = 0;
+      if (tile == 0) {
+        if (lane == 0) atomicExch(&state[0], (2ull << 32) | agg);
+      } else {
+        if (lane == 0) atomicExch(&state[tile], (1ull << 32) | agg);
+        int64_t pred = (int64_t)tile - 1;
+        while (true) {
+          int64_t idx = pred - lane;
+          unsigned long long st = idx >= 0 ? atomicAdd(&state[idx], 0ull) : (2ull << 32);
+          uint32_t status = (uint32_t)(st >> 32);
+          if (__any_sync(FULL, status == 0u)) continue;
+          unsigned incl_mask = __ballot_sync(FULL, status == 2u);
+          if (incl_mask) {
+            int first = __ffs(incl_mask) - 1;
+            excl += warp_sum(lane <= first ? (uint32_t)st : 0u);
+            break;
+          }
+          excl += warp_sum((uint32_t)st);
+          pred -= 32;
+        }
+        if (lane == 0) atomicExch(&state[tile], (2ull << 32) | (uint32_t)(excl + agg));
+      }
+      if (lane == 0) s_prefix = excl;
+    }
+    __syncthreads();
+    uint32_t run = s_prefix + s_warp[warp] + (incl - tsum);
+    uint32_t o[SCAN_ITEMS];
 #pragma unroll
-    for (int q = 0; q < SCAN_ITEMS / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-  } else {
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      o[q] = run;
+      run += v[q];
+    }
+    if (base + SCAN_ITEMS <= n_items) {
+      uint4* dst = reinterpret_cast<uint4*>(data + base);
 #pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q)
-      if (base + q < n_items) data[base + q] = o[q];
+      for (int q = 0; q < SCAN_ITEMS / 4; ++q) dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q)
+        if (base + q < n_items) data[base + q] = o[q];
+    }
   }
 }
 
@@ -449,8 +530,7 @@ __device__ __forceinline__ void flush_contacts(ForceSmem& sm, int lane, int& cnt
 // ag_out[i - a_begin] (and ids to id_out if given).
 template <bool RECORD>
 __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
-    k_force(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, const uint32_t* __restrict__ start,
-            uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
+    k_force(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
             uint32_t* __restrict__ id_out, double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
             Extents* ext_next, ErrDev* err, RecordDev rec) {
   __shared__ ForceSmem s_all[FORCE_WARPS];
@@ -473,20 +553,12 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
     double thr = (ri + g.thr_pad) * (ri + g.thr_pad);
     thr = thr + thr * 0x1p-50;
-    {
-      const int z0 = bz - 1 < g.lo[2] ? g.lo[2] : bz - 1;
-      const int z1 = bz + 1 > g.hi[2] ? g.hi[2] : bz + 1;
 #pragma unroll
-      for (int c = 0; c < 9; ++c) {
-        const int cx = bx + c / 3 - 1, cy = by + c % 3 - 1;
-        uint32_t b = 0, e = 0;
-        if (valid && cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1]) {
-          b = __ldg(&start[box_key(g, cx, cy, z0)]);
-          e = __ldg(&start[box_key(g, cx, cy, z1) + 1]);
-        }
-        sm.rb[c][lane] = b;
-        sm.re[c][lane] = e;
-      }
+    for (int c = 0; c < 9; ++c) {
+      uint32_t b = 0, e = 0;
+      if (valid) zrun(g, bx + c / 3 - 1, by + c % 3 - 1, bz - 1, bz + 1, b, e);
+      sm.rb[c][lane] = b;
+      sm.re[c][lane] = e;
     }
     __syncwarp();
     double Fx = 0.0, Fy = 0.0, Fz = 0.0;
@@ -711,8 +783,7 @@ __global__ void k_unpermute1(const T* __restrict__ v, const uint32_t* __restrict
 
 // ------------------------------------------------------------------------------------------ K8
 // Pairs (id_i < id_j) per agent in canonical order; pass 0 counts, pass 1 writes at offsets.
-__global__ void k_pairs(const double4* __restrict__ ag, const uint32_t* __restrict__ ids,
-                        const uint32_t* __restrict__ start, uint32_t n, GridDev g, ParamsDev p, int kind,
+__global__ void k_pairs(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n, GridDev g, ParamsDev p, int kind,
                         uint32_t* __restrict__ counts, const unsigned long long* __restrict__ offsets,
                         long long* __restrict__ out) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -725,10 +796,8 @@ __global__ void k_pairs(const double4* __restrict__ ag, const uint32_t* __restri
   unsigned long long w = offsets ? offsets[i] : 0ull;
   for (int c = 0; c < 9; ++c) {
     int cx = bx + c / 3 - 1, cy = by + c % 3 - 1;
-    if (cx < g.lo[0] || cx > g.hi[0] || cy < g.lo[1] || cy > g.hi[1]) continue;
-    int z0 = bz - 1 < g.lo[2] ? g.lo[2] : bz - 1;
-    int z1 = bz + 1 > g.hi[2] ? g.hi[2] : bz + 1;
-    uint32_t b = start[box_key(g, cx, cy, z0)], e = start[box_key(g, cx, cy, z1) + 1];
+    uint32_t b, e;
+    if (!zrun(g, cx, cy, bz - 1, bz + 1, b, e)) continue;
     for (uint32_t q = b; q < e; ++q) {
       uint32_t idj = ids[q];
       if (idj <= myid) continue;
