@@ -43,6 +43,7 @@ struct bdm_ctx {
   // state buffers: 'srt' holds the box-sorted agents after a grid build; 'cur' holds the newest
   // positions (after a step: in srt's order, ids shared with srt).
   double4* ag[2] = {nullptr, nullptr};
+  float4* agf = nullptr;  // fp32 copy of the sorted positions (candidate prefilter)
   uint32_t* id[2] = {nullptr, nullptr};
   int cur = 0;  // index of the buffer holding the newest state
   uint32_t *key = nullptr, *slot = nullptr, *tsrc = nullptr, *tid = nullptr, *tkey = nullptr;
@@ -267,6 +268,13 @@ int sort_into(bdm_ctx* h, uint32_t n) {
   g.czhi = h->czhi;
   g.coff = h->coff;
   g.table = h->table;
+  {  // fp32 prefilter margin from the largest coordinate magnitude of this grid
+    double P = 0.0;
+    for (int a = 0; a < 3; ++a)
+      P = std::max(P, std::max(std::fabs((double)g.lo[a]), std::fabs((double)g.hi[a] + 1.0)) * g.L * (1.0 + 0x1p-20));
+    const double ulp32 = P > 0.0 ? std::ldexp(1.0, std::ilogb(P) - 23) : 0x1p-149;
+    g.m32 = 2.0 * ulp32 + 0x1p-18;
+  }
   cudaStream_t s = h->stream;
   const int src = h->cur, dst = 1 - h->cur;
   init_device_info(h);
@@ -283,7 +291,7 @@ int sort_into(bdm_ctx* h, uint32_t n) {
   if (n > 0) {
     k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
     k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
-                                           h->id[dst]);
+                                           h->id[dst], h->agf);
   }
   CU(h, cudaGetLastError());
   h->launches += n > 0 ? 8 : 4;
@@ -326,10 +334,10 @@ int force_step(bdm_ctx* h, bool want_dp) {
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
   if (h->prm.flags & BDM_RECORD)
-    k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], 0u, n, h->grid, pd, h->ag[dst],
+    k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
                                                 nullptr, dp, nullptr, h->ext, h->err, rec);
   else
-    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], 0u, n, h->grid, pd,
+    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec);
   CU(h, cudaGetLastError());
   h->launches += 2;
@@ -445,7 +453,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e1);
     cudaEventDestroy(t.e2);
   }
-  void* ptrs[] = {h->ag[0], h->ag[1], h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
+  void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
@@ -496,6 +504,7 @@ int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, 
   const size_t N = (size_t)n;
   TRY(dalloc(h, &h->ag[0], N));
   TRY(dalloc(h, &h->ag[1], N));
+  TRY(dalloc(h, &h->agf, N));
   TRY(dalloc(h, &h->id[0], N));
   TRY(dalloc(h, &h->id[1], N));
   TRY(dalloc(h, &h->key, N));
@@ -850,6 +859,7 @@ int bdm_slab_init(bdm_handle* out, int64_t n_local, int64_t capacity, const uint
   const size_t N = (size_t)capacity;
   TRY(dalloc(h, &h->ag[0], N));
   TRY(dalloc(h, &h->ag[1], N));
+  TRY(dalloc(h, &h->agf, N));
   TRY(dalloc(h, &h->id[0], N));
   TRY(dalloc(h, &h->id[1], N));
   TRY(dalloc(h, &h->key, N));
@@ -1045,7 +1055,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   ParamsDev pd = params_dev(h->prm);
   const unsigned grid = force_grid(h, (uint32_t)n_own);
   if (n_own > 0) {
-    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->id[src], (uint32_t)n_lo,
+    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
                                                  (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
                                                  h->err, rec);

@@ -35,6 +35,7 @@ constexpr unsigned FULL = 0xffffffffu;
 struct GridDev {
   double L, L2, inv;
   double thr_pad;  // (L/2) used for the conservative contact prefilter
+  double m32;      // fp32 prefilter margin: 2 ulp32(max |coordinate|) + 2^-18
   int32_t lo[3], hi[3];
   int32_t ny, nz;
   uint32_t n_boxes;  // dense lattice size (reported; the table itself is ragged)
@@ -402,7 +403,7 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __re
 __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __restrict__ tid,
                         const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ start,
                         const double4* __restrict__ ag_in, uint32_t n, double4* __restrict__ ag_out,
-                        uint32_t* __restrict__ ids_out) {
+                        uint32_t* __restrict__ ids_out, float4* __restrict__ agf_out) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   uint32_t k = tkey[q], id = tid[q];
@@ -410,8 +411,11 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
   uint32_t rank = 0;
   for (uint32_t t = b; t < e; ++t) rank += tid[t] < id;
   uint32_t dst = b + rank;
-  ag_out[dst] = ag_in[tsrc[q]];
+  const double4 p = ag_in[tsrc[q]];
+  ag_out[dst] = p;
   ids_out[dst] = id;
+  // fp32 copy of the position for the force kernel's conservative candidate filter
+  agf_out[dst] = make_float4(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z), 0.0f);
 }
 
 // ------------------------------------------------------------------------------------------ K6
@@ -530,7 +534,8 @@ __device__ __forceinline__ void flush_contacts(ForceSmem& sm, int lane, int& cnt
 // ag_out[i - a_begin] (and ids to id_out if given).
 template <bool RECORD>
 __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
-    k_force(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
+    k_force(const double4* __restrict__ ag, const float4* __restrict__ agf, const uint32_t* __restrict__ ids,
+            uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
             uint32_t* __restrict__ id_out, double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
             Extents* ext_next, ErrDev* err, RecordDev rec) {
   __shared__ ForceSmem s_all[FORCE_WARPS];
@@ -553,6 +558,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
     double thr = (ri + g.thr_pad) * (ri + g.thr_pad);
     thr = thr + thr * 0x1p-50;
+    // fp32 bound: (r_i + L/2 + m32)^2 (1 + 2^-20), rounded up
+    const double rp = (ri + g.thr_pad + g.m32) * (1.0 + 0x1p-20);
+    const float thr32 = __double2float_ru(rp * rp);
+    const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
       uint32_t b = 0, e = 0;
@@ -571,20 +580,21 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       while (__any_sync(FULL, q < e)) {
         const bool a0 = q < e && q != i;
         const bool a1 = q + 1 < e && q + 1 != i;
-        double3 o0 = make_double3(0.0, 0.0, 0.0), o1 = make_double3(0.0, 0.0, 0.0);
-        if (a0) {
-          const double2 xy = __ldg(reinterpret_cast<const double2*>(ag + q));
-          o0 = make_double3(xy.x, xy.y, __ldg(&ag[q].z));
-        }
-        if (a1) {
-          const double2 xy = __ldg(reinterpret_cast<const double2*>(ag + q + 1));
-          o1 = make_double3(xy.x, xy.y, __ldg(&ag[q + 1].z));
-        }
-        const double dx0 = me.x - o0.x, dy0 = me.y - o0.y, dz0 = me.z - o0.z;
-        const double dx1 = me.x - o1.x, dy1 = me.y - o1.y, dz1 = me.z - o1.z;
-        const double d20 = (dx0 * dx0 + dy0 * dy0) + dz0 * dz0;
-        const double d21 = (dx1 * dx1 + dy1 * dy1) + dz1 * dz1;
         if (RECORD) {
+          // exact fp64 test of every candidate: the per-agent neighbour statistics need d2 <= L2
+          double3 o0 = make_double3(0.0, 0.0, 0.0), o1 = make_double3(0.0, 0.0, 0.0);
+          if (a0) {
+            const double2 xy = __ldg(reinterpret_cast<const double2*>(ag + q));
+            o0 = make_double3(xy.x, xy.y, __ldg(&ag[q].z));
+          }
+          if (a1) {
+            const double2 xy = __ldg(reinterpret_cast<const double2*>(ag + q + 1));
+            o1 = make_double3(xy.x, xy.y, __ldg(&ag[q + 1].z));
+          }
+          const double dx0 = me.x - o0.x, dy0 = me.y - o0.y, dz0 = me.z - o0.z;
+          const double dx1 = me.x - o1.x, dy1 = me.y - o1.y, dz1 = me.z - o1.z;
+          const double d20 = (dx0 * dx0 + dy0 * dy0) + dz0 * dz0;
+          const double d21 = (dx1 * dx1 + dy1 * dy1) + dz1 * dz1;
           n_cand += (int)a0 + (int)a1;
           if (a0 && d20 <= g.L2) {
             ++n_nb;
@@ -594,11 +604,33 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
             ++n_nb;
             nb_hash += mix64(ids[q + 1]);
           }
+          if (a0 && d20 <= thr) sm.list[cnt++][lane] = q;
+          if (a1 && d21 <= thr) sm.list[cnt++][lane] = q + 1;
+        } else {
+          // conservative fp32 filter (never drops a contact); four candidates per
+          // iteration with clamped (unpredicated) loads keep four loads in flight per lane
+          const bool a2 = q + 2 < e && q + 2 != i;
+          const bool a3 = q + 3 < e && q + 3 != i;
+          const float4 o0 = __ldg(&agf[a0 ? q : i]);
+          const float4 o1 = __ldg(&agf[a1 ? q + 1 : i]);
+          const float4 o2 = __ldg(&agf[a2 ? q + 2 : i]);
+          const float4 o3 = __ldg(&agf[a3 ? q + 3 : i]);
+          const float dx0 = mf.x - o0.x, dy0 = mf.y - o0.y, dz0 = mf.z - o0.z;
+          const float dx1 = mf.x - o1.x, dy1 = mf.y - o1.y, dz1 = mf.z - o1.z;
+          const float dx2 = mf.x - o2.x, dy2 = mf.y - o2.y, dz2 = mf.z - o2.z;
+          const float dx3 = mf.x - o3.x, dy3 = mf.y - o3.y, dz3 = mf.z - o3.z;
+          const float d20 = __fmaf_rn(dz0, dz0, __fmaf_rn(dy0, dy0, dx0 * dx0));
+          const float d21 = __fmaf_rn(dz1, dz1, __fmaf_rn(dy1, dy1, dx1 * dx1));
+          const float d22 = __fmaf_rn(dz2, dz2, __fmaf_rn(dy2, dy2, dx2 * dx2));
+          const float d23 = __fmaf_rn(dz3, dz3, __fmaf_rn(dy3, dy3, dx3 * dx3));
+          if (a0 && d20 <= thr32) sm.list[cnt++][lane] = q;
+          if (a1 && d21 <= thr32) sm.list[cnt++][lane] = q + 1;
+          if (a2 && d22 <= thr32) sm.list[cnt++][lane] = q + 2;
+          if (a3 && d23 <= thr32) sm.list[cnt++][lane] = q + 3;
+          q += 2;  // + 2 more below
         }
-        if (a0 && d20 <= thr) sm.list[cnt++][lane] = q;
-        if (a1 && d21 <= thr) sm.list[cnt++][lane] = q + 1;
         q += 2;
-        if (__any_sync(FULL, cnt > LCAP - 2))
+        if (__any_sync(FULL, cnt > LCAP - 4))
           flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
       }
     }

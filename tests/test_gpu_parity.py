@@ -60,6 +60,10 @@ def assert_dp_contract(g_dp, o_dp, o_force=None, s_abs=None, adherence=0.1):
 
 def compare_full(bdm, pos, diam, pairs=True, **kw):
     g = run_gpu(bdm, pos, diam, pairs=pairs, **kw)
+    # the product kernel (fp32 candidate prefilter, no statistics) must give the recorded kernel's
+    # displacements bit for bit: the prefilter never drops a contact
+    fast = run_gpu(bdm, pos, diam, record=False, **kw)
+    assert np.array_equal(fast["dp"], g["dp"])
     prm = oracle.params(**{k: v for k, v in kw.items() if k in oracle.DEFAULTS})
     o = oracle.step(pos, diam, prm)
     gp = oracle.grid_params(pos, diam, prm.box_edge_min)
@@ -237,6 +241,30 @@ def test_device_generator_matches_numpy(bdm):
     assert np.array_equal(pos.cpu().numpy(), p_np) and np.array_equal(diam.cpu().numpy(), d_np)
 
 
+def test_prefilter_boundary_contacts(bdm):
+    """Adversarial case for the conservative fp32 filter: pairs of largest-diameter agents (r_j = L/2,
+    so the contact bound equals s) just inside contact (d = s (1 - 2^-40)) and just outside, far from
+    the origin where fp32 rounds positions to ~1e-3 um, in random directions."""
+    rng = np.random.default_rng(5)
+    m = 4000
+    base = rng.uniform(-9000.0, 9000.0, size=(m, 3))
+    base[:, 0] = np.where(np.arange(m) % 2, 9990.0, -9990.0) + rng.uniform(-5, 5, m)
+    u = rng.normal(size=(m, 3))
+    u /= np.linalg.norm(u, axis=1)[:, None]
+    D = 12.0
+    s = D  # two agents of diameter D: s = r_i + r_j = D
+    frac = np.where(np.arange(m) % 3 == 0, 1.0 + 2.0 ** -40, 1.0 - 2.0 ** -40)
+    # pairs 40 um apart along y, z (> 2 D: pairs do not interact)
+    base[:, 1] = (np.arange(m) % 60) * 40.0 - 9000.0
+    base[:, 2] = (np.arange(m) // 60) * 40.0 + 8000.0
+    pos = np.concatenate([base, base + u * (s * frac)[:, None]])
+    diam = np.full(2 * m, D)
+    o = oracle.step(pos, diam, oracle.params(max_disp=100.0), record=True)
+    assert (o["n_ct"] > 0).sum() > m  # most pairs are in contact
+    g = run_gpu(bdm, pos, diam, record=False, max_disp=100.0)
+    assert np.array_equal(g["dp"], o["dp"])
+
+
 @pytest.mark.slow
 def test_cfg3_full_size_sampled(bdm):
     """configs[2] at full size (2e7 agents) in the launch configuration bench.py times: every
@@ -244,6 +272,8 @@ def test_cfg3_full_size_sampled(bdm):
     oracle computed one by one on the same input."""
     pos, diam = bdm_inputs.make_config(3)
     g = run_gpu(bdm, pos, diam)
+    fast = run_gpu(bdm, pos, diam, record=False)
+    assert np.array_equal(fast["dp"], g["dp"])  # product kernel == recorded kernel, all 2e7 agents
     rng = np.random.default_rng(0)
     core = np.flatnonzero(np.linalg.norm(pos, axis=1) < 60.0)[:3000]
     sample = np.unique(np.concatenate([rng.choice(len(diam), 20000, replace=False), core]))
