@@ -273,7 +273,7 @@ int sort_into(bdm_ctx* h, uint32_t n) {
     for (int a = 0; a < 3; ++a)
       P = std::max(P, std::max(std::fabs((double)g.lo[a]), std::fabs((double)g.hi[a] + 1.0)) * g.L * (1.0 + 0x1p-20));
     const double ulp32 = P > 0.0 ? std::ldexp(1.0, std::ilogb(P) - 23) : 0x1p-149;
-    g.m32 = 2.0 * ulp32 + 0x1p-18;
+    g.m32 = 2.0 * ulp32 + 0x1p-18 + g.L * 0x1p-20;
   }
   cudaStream_t s = h->stream;
   const int src = h->cur, dst = 1 - h->cur;

@@ -35,7 +35,7 @@ constexpr unsigned FULL = 0xffffffffu;
 struct GridDev {
   double L, L2, inv;
   double thr_pad;  // (L/2) used for the conservative contact prefilter
-  double m32;      // fp32 prefilter margin: 2 ulp32(max |coordinate|) + 2^-18
+  double m32;      // fp32 prefilter margin: 2 ulp32(max |coord|) + 2^-18 + 2^-20 L
   int32_t lo[3], hi[3];
   int32_t ny, nz;
   uint32_t n_boxes;  // dense lattice size (reported; the table itself is ragged)
@@ -415,7 +415,8 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
   ag_out[dst] = p;
   ids_out[dst] = id;
   // fp32 copy of the position for the force kernel's conservative candidate filter
-  agf_out[dst] = make_float4(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z), 0.0f);
+  agf_out[dst] = make_float4(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z),
+                             __double2float_rn(0.5 * p.w));
 }
 
 // ------------------------------------------------------------------------------------------ K6
@@ -562,25 +563,56 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     const double rp = (ri + g.thr_pad + g.m32) * (1.0 + 0x1p-20);
     const float thr32 = __double2float_ru(rp * rp);
     const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    // Box culling (product kernel only): a neighbour box can hold a contact only if its region
+    // comes within R_i = r_i + L/2 of p_i (contact => d < r_i + r_j <= R_i).  fx/gx are the
+    // distances from p_i to the lower/upper x faces of its own box (clamped at 0 against rounding of
+    // floor(x*inv)); the bound is padded by the fp32 margin (>= 2^-18 um >> fp64 rounding here).
+    // RECORD counts all 27-box candidates (O3) and does not cull.
+    const double Lb = 1.0 / g.inv;
+    const double fx = fmax(me.x - bx * Lb, 0.0), gx = fmax((bx + 1) * Lb - me.x, 0.0);
+    const double fy = fmax(me.y - by * Lb, 0.0), gy = fmax((by + 1) * Lb - me.y, 0.0);
+    const double fz = fmax(me.z - bz * Lb, 0.0), gz = fmax((bz + 1) * Lb - me.z, 0.0);
+    const double Rc = rp + g.m32;
+    const double Rc2 = Rc * Rc;
+    int nr = 0;  // non-empty ranges of this lane, compacted in canonical (dx, dy) order
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
+      const int ddx = c / 3 - 1, ddy = c % 3 - 1;
       uint32_t b = 0, e = 0;
-      if (valid) zrun(g, bx + c / 3 - 1, by + c % 3 - 1, bz - 1, bz + 1, b, e);
-      sm.rb[c][lane] = b;
-      sm.re[c][lane] = e;
+      if (valid) {
+        int z0 = bz - 1, z1 = bz + 1;
+        bool keep = true;
+        if (!RECORD) {
+          const double ex = ddx < 0 ? fx : (ddx > 0 ? gx : 0.0);
+          const double ey = ddy < 0 ? fy : (ddy > 0 ? gy : 0.0);
+          const double exy2 = ex * ex + ey * ey;
+          keep = exy2 <= Rc2;
+          if (exy2 + fz * fz > Rc2) z0 = bz;
+          if (exy2 + gz * gz > Rc2) z1 = bz;
+        }
+        if (keep) zrun(g, bx + ddx, by + ddy, z0, z1, b, e);
+      }
+      if (RECORD) {
+        sm.rb[c][lane] = b;
+        sm.re[c][lane] = e;
+      } else if (b < e) {
+        sm.rb[nr][lane] = b;
+        sm.re[nr][lane] = e;
+        ++nr;
+      }
     }
     __syncwarp();
     double Fx = 0.0, Fy = 0.0, Fz = 0.0;
     int cnt = 0;
     int32_t n_cand = 0, n_nb = 0, n_ct = 0;
     unsigned long long nb_hash = 0, ct_hash = 0;
-    for (int c = 0; c < 9; ++c) {
-      uint32_t q = sm.rb[c][lane];
-      const uint32_t e = sm.re[c][lane];
-      while (__any_sync(FULL, q < e)) {
-        const bool a0 = q < e && q != i;
-        const bool a1 = q + 1 < e && q + 1 != i;
-        if (RECORD) {
+    if (RECORD) {
+      for (int c = 0; c < 9; ++c) {
+        uint32_t q = sm.rb[c][lane];
+        const uint32_t e = sm.re[c][lane];
+        while (__any_sync(FULL, q < e)) {
+          const bool a0 = q < e && q != i;
+          const bool a1 = q + 1 < e && q + 1 != i;
           // exact fp64 test of every candidate: the per-agent neighbour statistics need d2 <= L2
           double3 o0 = make_double3(0.0, 0.0, 0.0), o1 = make_double3(0.0, 0.0, 0.0);
           if (a0) {
@@ -606,30 +638,48 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           }
           if (a0 && d20 <= thr) sm.list[cnt++][lane] = q;
           if (a1 && d21 <= thr) sm.list[cnt++][lane] = q + 1;
-        } else {
-          // conservative fp32 filter (never drops a contact); four candidates per
-          // iteration with clamped (unpredicated) loads keep four loads in flight per lane
-          const bool a2 = q + 2 < e && q + 2 != i;
-          const bool a3 = q + 3 < e && q + 3 != i;
-          const float4 o0 = __ldg(&agf[a0 ? q : i]);
-          const float4 o1 = __ldg(&agf[a1 ? q + 1 : i]);
-          const float4 o2 = __ldg(&agf[a2 ? q + 2 : i]);
-          const float4 o3 = __ldg(&agf[a3 ? q + 3 : i]);
-          const float dx0 = mf.x - o0.x, dy0 = mf.y - o0.y, dz0 = mf.z - o0.z;
-          const float dx1 = mf.x - o1.x, dy1 = mf.y - o1.y, dz1 = mf.z - o1.z;
-          const float dx2 = mf.x - o2.x, dy2 = mf.y - o2.y, dz2 = mf.z - o2.z;
-          const float dx3 = mf.x - o3.x, dy3 = mf.y - o3.y, dz3 = mf.z - o3.z;
-          const float d20 = __fmaf_rn(dz0, dz0, __fmaf_rn(dy0, dy0, dx0 * dx0));
-          const float d21 = __fmaf_rn(dz1, dz1, __fmaf_rn(dy1, dy1, dx1 * dx1));
-          const float d22 = __fmaf_rn(dz2, dz2, __fmaf_rn(dy2, dy2, dx2 * dx2));
-          const float d23 = __fmaf_rn(dz3, dz3, __fmaf_rn(dy3, dy3, dx3 * dx3));
-          if (a0 && d20 <= thr32) sm.list[cnt++][lane] = q;
-          if (a1 && d21 <= thr32) sm.list[cnt++][lane] = q + 1;
-          if (a2 && d22 <= thr32) sm.list[cnt++][lane] = q + 2;
-          if (a3 && d23 <= thr32) sm.list[cnt++][lane] = q + 3;
-          q += 2;  // + 2 more below
+          q += 2;
+          if (__any_sync(FULL, cnt > LCAP - 2))
+            flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
         }
-        q += 2;
+      }
+    } else {
+      // Flattened cursor over this lane's culled non-empty ranges (canonical order), four candidate
+      // slots per iteration: the warp iterates max over lanes of the lane's TOTAL work rather than
+      // the sum over columns of per-column maxima.  Conservative fp32 test against the pair bound
+      // (r_i + r_j + m32)^2 (1 + 2^-20): only candidates that can be contacts reach
+      // the exact fp64 evaluation.
+      const float ri32 = __double2float_ru(ri + g.m32);
+      int k = 0;
+      bool live = nr > 0;
+      uint32_t q = live ? sm.rb[0][lane] : 0u, e = live ? sm.re[0][lane] : 0u;
+      while (__any_sync(FULL, live)) {
+        uint32_t qs[4];
+        bool as[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          as[t] = live && q != i;
+          qs[t] = live ? q : i;
+          if (live && ++q == e) {
+            ++k;
+            live = k < nr;
+            if (live) {
+              q = sm.rb[k][lane];
+              e = sm.re[k][lane];
+            }
+          }
+        }
+        float4 o[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) o[t] = __ldg(&agf[qs[t]]);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float dx = mf.x - o[t].x, dy = mf.y - o[t].y, dz = mf.z - o[t].z;
+          const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+          const float sp = ri32 + o[t].w;
+          const float s2 = sp * sp;
+          if (as[t] && d2 <= __fmaf_rn(s2, 0x1p-20f, s2)) sm.list[cnt++][lane] = qs[t];
+        }
         if (__any_sync(FULL, cnt > LCAP - 4))
           flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
       }

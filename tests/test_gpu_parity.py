@@ -258,7 +258,18 @@ def test_prefilter_boundary_contacts(bdm):
     base[:, 1] = (np.arange(m) % 60) * 40.0 - 9000.0
     base[:, 2] = (np.arange(m) // 60) * 40.0 + 8000.0
     pos = np.concatenate([base, base + u * (s * frac)[:, None]])
-    diam = np.full(2 * m, D)
+    # plus pairs straddling box corners / edges diagonally (exercise the box culling of the
+    # product kernel: the partner sits in a corner or edge neighbour box)
+    Lb = 1.0 / (D * (1.0 + 2.0 ** -30))
+    k = 600
+    corner = np.stack([np.full(k, 7000.0), (np.arange(k) % 30) * 48.0 + 100.0, (np.arange(k) // 30) * 48.0 + 100.0], 1)
+    corner = np.floor(corner * Lb) / Lb + 1e-9  # just above a box corner
+    dirs = np.array([[-1, -1, -1], [-1, -1, 0], [-1, 0, -1], [0, -1, -1], [-1, 1, -1], [-1, -1, 1]], float)
+    dd = dirs[np.arange(k) % len(dirs)]
+    dd /= np.linalg.norm(dd, axis=1)[:, None]
+    partner = corner + dd * (s * (1.0 - 2.0 ** -40))
+    pos = np.concatenate([pos, corner, partner])
+    diam = np.full(len(pos), D)
     o = oracle.step(pos, diam, oracle.params(max_disp=100.0), record=True)
     assert (o["n_ct"] > 0).sum() > m  # most pairs are in contact
     g = run_gpu(bdm, pos, diam, record=False, max_disp=100.0)
