@@ -194,8 +194,10 @@ int ensure_columns(bdm_ctx* h, size_t entries) {
 void init_device_info(bdm_ctx* h) {
   if (h->sm_count) return;
   cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, h->device);
+  cudaFuncSetAttribute(k_force<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FORCE_SMEM_BYTES);
+  cudaFuncSetAttribute(k_force<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FORCE_SMEM_BYTES);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<false>, FORCE_THREADS, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_force<false>, FORCE_THREADS, FORCE_SMEM_BYTES);
   h->force_blocks_per_sm = per_sm > 0 ? per_sm : 1;
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan, SCAN_THREADS, 0);
@@ -334,10 +336,10 @@ int force_step(bdm_ctx* h, bool want_dp) {
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
   if (h->prm.flags & BDM_RECORD)
-    k_force<true><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
+    k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
                                                 nullptr, dp, nullptr, h->ext, h->err, rec);
   else
-    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
+    k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec);
   CU(h, cudaGetLastError());
   h->launches += 2;
@@ -1055,7 +1057,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   ParamsDev pd = params_dev(h->prm);
   const unsigned grid = force_grid(h, (uint32_t)n_own);
   if (n_own > 0) {
-    k_force<false><<<grid, FORCE_THREADS, 0, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
+    k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
                                                  (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
                                                  h->err, rec);

@@ -454,12 +454,16 @@ __device__ __forceinline__ bool pair_term(double xi, double yi, double zi, doubl
   return true;
 }
 
+constexpr int TSPAN = 40;  // box-start window per neighbour column staged by a single-column chunk
+
 struct ForceSmem {
   uint32_t list[LCAP][32];  // survivors per lane (sorted index of the candidate), candidate order
   double term[3][32];       // contact terms of one compacted batch
   uint32_t cidx[32];        // candidate id of the batch entry, 0xffffffff = not a contact
   uint32_t rb[9][32], re[9][32];
+  uint32_t tab[9][TSPAN];   // box starts start(c, z) for z in [zf-1, zl+2] of the 9 neighbour columns
 };
+constexpr size_t FORCE_SMEM_BYTES = sizeof(ForceSmem) * FORCE_WARPS;
 
 // Contact phase over the survivors of the warp (DESIGN.md §6.3 step 3).  The survivors of all lanes
 // are enumerated as one flat sequence (lane-major, candidate order inside a lane); each batch of 32
@@ -539,7 +543,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
             uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
             uint32_t* __restrict__ id_out, double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
             Extents* ext_next, ErrDev* err, RecordDev rec) {
-  __shared__ ForceSmem s_all[FORCE_WARPS];
+  extern __shared__ __align__(16) unsigned char s_raw[];  // FORCE_WARPS x ForceSmem (dynamic)
+  ForceSmem* s_all = reinterpret_cast<ForceSmem*>(s_raw);
   const int lane = threadIdx.x & 31;
   ForceSmem& sm = s_all[threadIdx.x >> 5];
   int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
@@ -575,6 +580,52 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     const double Rc = rp + g.m32;
     const double Rc2 = Rc * Rc;
     int nr = 0;  // non-empty ranges of this lane, compacted in canonical (dx, dy) order
+    // Chunks whose agents all sit in one column (bx, by) -- most chunks in dense regions -- look
+    // the 9 neighbour columns up once per warp: lane c < 9 reads column c's descriptor, then the
+    // warp stages start(c, z) for z in [zf-1, zl+2] with coalesced loads; lanes then read their
+    // z-runs from shared memory instead of 9 dependent global lookups each.
+    const int bx0 = __shfl_sync(FULL, bx, 0), by0 = __shfl_sync(FULL, by, 0);
+    const int zf = __reduce_min_sync(FULL, valid ? bz : INT32_MAX);
+    const int zl = __reduce_max_sync(FULL, valid ? bz : INT32_MIN);
+    const bool coop = !RECORD && __all_sync(FULL, !valid || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
+    if (coop) {
+      int czl = 0, cze = 0;  // column descriptor: first occupied z, number of occupied z
+      uint32_t cof = 0;
+      if (lane < 9) {
+        const int cx = bx0 + lane / 3 - 1, cy = by0 + lane % 3 - 1;
+        if (cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1]) {
+          const uint32_t cc = col_of(g, cx, cy);
+          czl = __ldg(&g.czlo[cc]);
+          const int czh = __ldg(&g.czhi[cc]);
+          cof = __ldg(&g.coff[cc]);
+          cze = czh >= czl ? czh - czl + 1 : 0;
+        } else {
+          cof = 0xffffffffu;  // outside the grid: no agents
+        }
+      }
+      const int span = zl - zf + 4;
+      // stage start(c, z) = table[coff + clamp(z - zlo, 0, ext)] for all 9 x span entries at once
+      // (flattened so that every lane has its loads in flight together)
+      const int total = 9 * span;
+#pragma unroll 2
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int t = t0 + lane;
+        const int c = t / span < 8 ? t / span : 8;
+        const int zlo_c = __shfl_sync(FULL, czl, c), ext_c = __shfl_sync(FULL, cze, c);
+        const uint32_t off_c = __shfl_sync(FULL, cof, c);
+        if (t < total) {
+          uint32_t v = 0u;
+          const int tt = t - c * span;
+          if (off_c != 0xffffffffu) {
+            int k = zf - 1 + tt - zlo_c;
+            k = k < 0 ? 0 : (k > ext_c ? ext_c : k);
+            v = __ldg(&g.table[off_c + (uint32_t)k]);
+          }
+          sm.tab[c][tt] = v;
+        }
+      }
+      __syncwarp();
+    }
 #pragma unroll
     for (int c = 0; c < 9; ++c) {
       const int ddx = c / 3 - 1, ddy = c % 3 - 1;
@@ -590,7 +641,14 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           if (exy2 + fz * fz > Rc2) z0 = bz;
           if (exy2 + gz * gz > Rc2) z1 = bz;
         }
-        if (keep) zrun(g, bx + ddx, by + ddy, z0, z1, b, e);
+        if (keep) {
+          if (coop) {
+            b = sm.tab[c][z0 - zf + 1];
+            e = sm.tab[c][z1 - zf + 2];
+          } else {
+            zrun(g, bx + ddx, by + ddy, z0, z1, b, e);
+          }
+        }
       }
       if (RECORD) {
         sm.rb[c][lane] = b;
