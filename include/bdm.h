@@ -178,6 +178,10 @@ int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo
 int bdm_slab_init(bdm_handle* h, int64_t n_local, int64_t capacity, const uint32_t* ids, const double* pos,
                   const double* diam, const bdm_params* p);
 
+/* Replace the owned agents with a new batch (device arrays; same rules as bdm_slab_init), keeping
+ * every allocation.  The global box edge stays as set (call bdm_slab_set_box_edge if diameters grew). */
+int bdm_slab_load(bdm_handle h, int64_t n_local, const uint32_t* ids, const double* pos, const double* diam);
+
 /* Largest diameter among the owned agents (0 if none); the caller allreduces it (O1). */
 int bdm_slab_local_maxd(bdm_handle h, double* maxd);
 

@@ -85,6 +85,7 @@ _SIGS = {
                               ctypes.c_double, _vp, _vp, _vp], ctypes.c_int),
     "bdm_slab_init": ([ctypes.POINTER(_vp), ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp,
                        ctypes.POINTER(bdm_params)], ctypes.c_int),
+    "bdm_slab_load": ([_vp, ctypes.c_int64, _vp, _vp, _vp], ctypes.c_int),
     "bdm_slab_local_maxd": ([_vp, ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "bdm_slab_set_box_edge": ([_vp, ctypes.c_double], ctypes.c_int),
     "bdm_slab_local_extents": ([_vp, _vp], ctypes.c_int),
@@ -328,6 +329,16 @@ def bdm_slab_init(ids, pos, diam, capacity: int, params: bdm_params | None = Non
     if stream is not None:
         bdm_set_stream(h, stream)
     return h
+
+
+def bdm_slab_load(h: Handle, ids, pos, diam) -> None:
+    """Replace the owned agents (CUDA tensors; ids as int32/int64)."""
+    import torch
+
+    ids32 = ids.to(torch.int32).contiguous() if ids.dtype != torch.int32 else ids.contiguous()
+    _check(load_library().bdm_slab_load(h.raw, pos.shape[0], _ptr(ids32), _ptr(pos.contiguous()),
+                                        _ptr(diam.contiguous())), h.raw)
+    h.n = pos.shape[0]
 
 
 def bdm_slab_local_maxd(h: Handle) -> float:

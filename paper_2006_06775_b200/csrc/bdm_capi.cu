@@ -161,7 +161,7 @@ int ensure_table(bdm_ctx* h, size_t entries, size_t min_scan_items) {
   if (entries > h->table_cap) {
     if (h->table) CU(h, cudaFree(h->table));
     h->table = nullptr;
-    size_t cap = entries + entries / 8 + 1024;
+    size_t cap = entries + entries / 4 + (1u << 20);  // generous: no reallocation as extents drift
     CU(h, cudaMalloc(&h->table, cap * sizeof(uint32_t)));
     h->table_cap = cap;
   }
@@ -169,7 +169,7 @@ int ensure_table(bdm_ctx* h, size_t entries, size_t min_scan_items) {
   if (tiles > h->scan_tiles_cap) {
     if (h->scan_state) CU(h, cudaFree(h->scan_state));
     h->scan_state = nullptr;
-    size_t cap = tiles + tiles / 8 + 16;
+    size_t cap = tiles + tiles / 4 + 256;
     CU(h, cudaMalloc(&h->scan_state, cap * sizeof(unsigned long long)));
     h->scan_tiles_cap = cap;
   }
@@ -182,7 +182,7 @@ int ensure_columns(bdm_ctx* h, size_t entries) {
       if (p) CU(h, cudaFree(p));
     h->czlo = h->czhi = nullptr;
     h->coff = nullptr;
-    size_t cap = entries + entries / 8 + 1024;
+    size_t cap = entries + entries / 4 + (1u << 16);
     CU(h, cudaMalloc(&h->czlo, cap * sizeof(int32_t)));
     CU(h, cudaMalloc(&h->czhi, cap * sizeof(int32_t)));
     CU(h, cudaMalloc(&h->coff, cap * sizeof(uint32_t)));
@@ -904,6 +904,27 @@ int bdm_slab_init(bdm_handle* out, int64_t n_local, int64_t capacity, const uint
   return BDM_OK;
 }
 
+int bdm_slab_load(bdm_handle h, int64_t n_local, const uint32_t* ids, const double* pos, const double* diam) {
+  int rc = slab_check(h, "bdm_slab_load");
+  if (rc) return rc;
+  if (n_local < 0 || n_local > h->cap || (n_local > 0 && (!ids || !pos || !diam)))
+    return fail(h, BDM_EINVAL, "bdm_slab_load: need 0 <= n_local <= capacity and non-NULL arrays");
+  if (n_local > 0) {
+    k_pack<<<blocks(n_local, 256), 256, 0, h->stream>>>(pos, diam, (uint32_t)n_local, h->ag[0], h->id[0],
+                                                        h->maxd_bits, h->err);
+    CU(h, cudaGetLastError());
+    CU(h, cudaMemcpyAsync(h->id[0], ids, (size_t)n_local * sizeof(uint32_t), cudaMemcpyDeviceToDevice, h->stream));
+    h->launches += 1;
+  }
+  h->cur = 0;
+  h->n = n_local;
+  h->ext_valid = false;
+  h->have_dp = false;
+  h->n_dp = 0;
+  h->state = State::NoGrid;
+  return BDM_OK;
+}
+
 int bdm_slab_local_maxd(bdm_handle h, double* maxd) {
   int rc = slab_check(h, "bdm_slab_local_maxd");
   if (rc) return rc;
@@ -1017,6 +1038,14 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
     return fail(h, BDM_ERANGE, "bdm_slab_step: %lld owned + ghost agents exceed the capacity %lld", (long long)n_tot,
                 (long long)h->cap);
   cudaStream_t s = h->stream;
+  TimedStep ts{};
+  if (h->timing) {
+    CU(h, cudaEventCreate(&ts.e0));
+    CU(h, cudaEventCreate(&ts.e1));
+    CU(h, cudaEventCreate(&ts.e2));
+    h->timed.push_back(ts);
+    CU(h, cudaEventRecord(ts.e0, s));
+  }
   // ghosts after the owned agents
   if (n_lo) k_unpack<<<blocks(n_lo, 256), 256, 0, s>>>(recv_lo, (uint32_t)n_lo, h->ag[h->cur], h->id[h->cur], (uint32_t)n_own);
   if (n_hi)
@@ -1050,6 +1079,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   g.n_boxes = (uint32_t)nb;
   rc = sort_into(h, (uint32_t)n_tot);  // cur -> sorted owned + ghosts
   if (rc) return rc;
+  if (h->timing) CU(h, cudaEventRecord(ts.e1, s));
   // ghosts_lo (box-x = x_begin-1) sort first, ghosts_hi (box-x = x_end) last: the owned agents are
   // the contiguous range [n_lo, n_tot - n_hi) of the sorted array
   const int src = h->cur, dst = 1 - h->cur;
@@ -1064,6 +1094,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
     CU(h, cudaGetLastError());
     h->launches += 1;
   }
+  if (h->timing) CU(h, cudaEventRecord(ts.e2, s));
   h->cur = dst;
   h->n = n_own;
   h->ext_valid = true;

@@ -283,13 +283,17 @@ def initial_bounds(pos: np.ndarray, diam: np.ndarray, world: int, box_edge_min: 
 
 # --------------------------------------------------------------------------------- bench (N > 1)
 def bench_multi(args, metric, unit, config_obj, load_peaks, ClockSampler):
-    """bench.py under torchrun: strong scaling of one config over x-slabs, one rank per GPU."""
+    """bench.py under torchrun: strong scaling of one config over x-slabs, one rank per GPU.
+
+    Device time = CUDA events on each rank's stream around K full protocol steps (allreduce, halo,
+    slab step, migration), barrier + synchronize on both sides, max over ranks."""
     import os
 
     import torch
     import torch.distributed as dist
 
     import bdm_inputs
+    import paper_2006_06775_b200 as bdm
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -298,40 +302,111 @@ def bench_multi(args, metric, unit, config_obj, load_peaks, ClockSampler):
     rank, world = dist.get_rank(), dist.get_world_size()
     pos_h, diam_h = bdm_inputs.make_config(args.config, args.n)
     n = len(diam_h)
+    stream = torch.cuda.current_stream()
+    # algorithmic work units of one step (candidates, contacts) from one recorded single-handle step
+    units = torch.zeros(2, dtype=torch.float64, device=dev)
+    if rank == 0:
+        prm = bdm.bdm_params_default(device=local)
+        prm.flags |= bdm.BDM_RECORD
+        hr = bdm.bdm_init(torch.from_numpy(pos_h).to(dev), torch.from_numpy(diam_h).to(dev), prm, stream=stream)
+        bdm.bdm_mech_step(hr, 1)
+        st = bdm.bdm_get_agent_stats(hr)
+        units[0] = float(st["n_cand"].sum().item())
+        units[1] = float(st["n_ct"].sum().item())
+        hr.close()
+        del st
+        torch.cuda.empty_cache()
+    dist.broadcast(units, 0)
     bounds, bx = initial_bounds(pos_h, diam_h, world)
     mine = np.flatnonzero((bx >= bounds[rank]) & (bx < bounds[rank + 1]))
     cap = int(max(len(mine) * 1.3, n / world * 1.3)) + 4096
-    ids = torch.from_numpy(mine.astype(np.int64)).to(dev)
-    pos = torch.from_numpy(np.ascontiguousarray(pos_h[mine])).to(dev)
-    diam = torch.from_numpy(np.ascontiguousarray(diam_h[mine])).to(dev)
+    pos_mine = np.ascontiguousarray(pos_h[mine])
+    diam_mine = np.ascontiguousarray(diam_h[mine])
     del pos_h, diam_h, bx
-    stream = torch.cuda.current_stream()
-    eng = GpuSlabEngine(ids, pos, diam, cap, stream=stream)
+    ids = torch.from_numpy(mine.astype(np.int64)).to(dev)
+    eng = GpuSlabEngine(ids, torch.from_numpy(pos_mine).to(dev), torch.from_numpy(diam_mine).to(dev), cap,
+                        stream=stream)
     drv = SlabDriver([eng], TorchComm(dev), bounds)
-    for _ in range(max(args.warmup, 3)):
-        drv.step()
-    torch.cuda.synchronize()
-    dist.barrier()
+    bdm.bdm_set_timing(eng.h, True)
+    warm = max(args.warmup, 3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        for _ in range(warm):
+            drv.step()
         torch.cuda.synchronize()
+        bdm.bdm_get_timing(eng.h)  # reset
         dist.barrier()
+        torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(args.steps):
             drv.step()
         e1.record(stream)
         torch.cuda.synchronize()
         dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
+    tm = bdm.bdm_get_timing(eng.h)
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
     value = n * args.steps / (ms / 1e3)
+    launches = torch.tensor([tm["launches"]], dtype=torch.int64, device=dev)
+    dist.all_reduce(launches, op=dist.ReduceOp.SUM)
+
+    # end to end through the public API: per step each rank copies its slab's inputs from pinned
+    # host memory, loads them (bdm_slab_load), runs one protocol step and reads its displacements back
+    pin_pos = torch.from_numpy(pos_mine).pin_memory()
+    pin_diam = torch.from_numpy(diam_mine).pin_memory()
+    pin_ids = torch.from_numpy(mine.astype(np.int32)).pin_memory()
+    pin_dp = torch.empty((len(mine) + cap, 3), dtype=torch.float64).pin_memory()
+    e2e_ms = 0.0
+    h2d = d2h = 0
+    for rep in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dpos = pin_pos.to(dev, non_blocking=True)
+        ddiam = pin_diam.to(dev, non_blocking=True)
+        dids = pin_ids.to(dev, non_blocking=True)
+        bdm.bdm_slab_load(eng.h, dids, dpos, ddiam)
+        drv.settle()
+        drv.step(want_dp=True)
+        _, dp = bdm.bdm_slab_get(eng.h, bdm.BDM_LAST_DISPLACEMENTS)
+        dp_host = pin_dp[: dp.shape[0]]
+        dp_host.copy_(dp, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        if rep > 0:  # first round is warm-up
+            e2e_ms += a.elapsed_time(b)
+            h2d += pin_pos.numel() * 8 + pin_diam.numel() * 8 + pin_ids.numel() * 4
+            d2h += dp_host.numel() * 8
+    et = torch.tensor([e2e_ms, h2d, d2h], dtype=torch.float64, device=dev)
+    mx = et.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    dist.all_reduce(et, op=dist.ReduceOp.SUM)
+    e2e = {"value": n * args.e2e_steps / (float(mx[0].item()) / 1e3), "unit": unit,
+           "h2d_bytes_per_step": int(et[1].item() / max(args.e2e_steps, 1)),
+           "d2h_bytes_per_step": int(et[2].item() / max(args.e2e_steps, 1)), "steps": args.e2e_steps,
+           "path": "per rank: pinned H2D of the slab -> bdm_slab_load -> protocol step -> displacements D2H; "
+                   "max over ranks"}
     if rank == 0:
+        peaks, peak_kind = load_peaks()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        fp64_peak = 148 * 64 * sm_max * 1e6
+        share = len(mine) / n
+        ops = (9 * units[0].item() + 44 * units[1].item() + 40 * n) * share
+        force_s = tm["force_ms"] / 1e3 / max(tm["steps"], 1)
+        achieved = ops / force_s if force_s > 0 else 0.0
         line = {"metric": metric, "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
-                "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "warmup": warm, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_obj(args, n, world), "bounds": [int(b) for b in bounds[1:-1]],
-                "roofline": None, "cpu_baseline": None, "e2e": None, "gpu_launches": None,
+                "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
+                             "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None, "kernel": "k_force",
+                             "ms_per_launch": force_s * 1e3,
+                             "note": "rank 0's force kernel; its algorithmic fp64 ops taken as the rank's share of "
+                                     "agents x the whole-population per-agent mix (DESIGN.md §6.2)"},
+                "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches.item()),
                 "clocks": clk.summary(), "timing": "CUDA events on each rank's stream, max over ranks"}
         print(json.dumps(line), flush=True)
     dist.barrier()
