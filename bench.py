@@ -238,6 +238,12 @@ def run_bdm(args):
                "unit": "GB/s", "frac": rebuild_bytes / grid_s / 1e9 / float(peaks["hbm_gbs"]),
                "ms_per_step": grid_s * 1e3, "bytes_per_agent": REBUILD_BYTES_PER_AGENT}
     del pos_d, diam_d
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
+    if args.config == 3 and os.path.exists(tf):  # measured DRAM bytes of the force kernel (committed capture)
+        with open(tf) as f:
+            t = json.load(f)
+        traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
 
     # end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = run_e2e(bdm, torch, pos_h, diam_h, local, args)
@@ -255,7 +261,8 @@ def run_bdm(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_obj(args, n, 1),
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / fp64_peak, "traffic": None, "kernel": "k_force",
+                         "frac": achieved / fp64_peak, "traffic": traffic, "kernel": "k_force",
+                         "traffic_source": "profiles/r01_force_traffic.json" if traffic else None,
                          "ms_per_launch": force_s * 1e3,
                          "note": "fp64-pipe ops (9/candidate + 44/contact + 40/agent, DESIGN.md §6.2) over the "
                                  f"force kernel's event time; peak = 148 SM x 64 fp64 lanes x {sm_max:.0f} MHz "
