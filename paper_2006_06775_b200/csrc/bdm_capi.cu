@@ -282,12 +282,12 @@ int sort_into(bdm_ctx* h, uint32_t n) {
   init_device_info(h);
   const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
   k_col_reset<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols);
-  if (n > 0) k_col_ext<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
+  if (n > 0) k_col_ext<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
   k_col_len<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols, h->coff);
   rc = scan(h, h->coff, nc + 1, nullptr);  // exclusive: coff[c] = table offset, coff[nc] = T
   if (rc) return rc;
   k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
-  if (n > 0) k_key_hist<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table);
+  if (n > 0) k_key_hist<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table);
   rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
   if (rc) return rc;
   if (n > 0) {

@@ -70,6 +70,12 @@ struct RecordDev {
   unsigned long long *nb_hash, *ct_hash;
 };
 
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
@@ -220,25 +226,31 @@ __global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ cz
 
 __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g, int32_t* __restrict__ czlo,
                           int32_t* __restrict__ czhi) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < n;
-  uint32_t c = 0xffffffffu;
-  int bz = 0;
-  if (valid) {
-    const double4 p = ag[i];
-    const int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv);
-    bz = (int)floor(p.z * g.inv);
-    c = col_of(g, bx, by);
-  }
-  // warp-aggregated: agents arrive mostly in box order, so a warp touches few columns; each group
-  // of lanes with the same column reduces with redux.sync over its own member mask
-  const unsigned peers = __match_any_sync(FULL, c);
-  const int zmin = __reduce_min_sync(peers, bz);
-  const int zmax = __reduce_max_sync(peers, bz);
+  const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
+  const uint32_t ia[2] = {i0, i0 + blockDim.x};
+  double4 pa[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) pa[u] = ia[u] < n ? ag[ia[u]] : make_double4(0.0, 0.0, 0.0, 0.0);
   const int lane = threadIdx.x & 31;
-  if (valid && lane == __ffs(peers) - 1) {
-    if (zmin < __ldcg(&czlo[c])) atomicMin(&czlo[c], zmin);
-    if (zmax > __ldcg(&czhi[c])) atomicMax(&czhi[c], zmax);
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const bool valid = ia[u] < n;
+    uint32_t c = 0xffffffffu;
+    int bz = 0;
+    if (valid) {
+      const int bx = (int)floor(pa[u].x * g.inv), by = (int)floor(pa[u].y * g.inv);
+      bz = (int)floor(pa[u].z * g.inv);
+      c = col_of(g, bx, by);
+    }
+    // warp-aggregated: agents arrive mostly in box order, so a warp touches few columns; each group
+    // of lanes with the same column reduces with redux.sync over its own member mask
+    const unsigned peers = __match_any_sync(FULL, c);
+    const int zmin = __reduce_min_sync(peers, bz);
+    const int zmax = __reduce_max_sync(peers, bz);
+    if (valid && lane == __ffs(peers) - 1) {
+      if (zmin < __ldcg(&czlo[c])) atomicMin(&czlo[c], zmin);
+      if (zmax > __ldcg(&czhi[c])) atomicMax(&czhi[c], zmax);
+    }
   }
 }
 
@@ -255,26 +267,34 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
 }
 
 // ------------------------------------------------------------------------------------------ K2
+// Two agents per thread (block-strided, both loads coalesced and in flight together).
 __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g, uint32_t* __restrict__ key,
                            uint32_t* __restrict__ slot, uint32_t* __restrict__ count) {
-  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  bool valid = i < n;
-  uint32_t k = 0xffffffffu;
-  if (valid) {
-    double4 p = ag[i];
-    int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv), bz = (int)floor(p.z * g.inv);
-    k = box_key(g, bx, by, bz);
-  }
-  // warp-aggregated histogram: one atomic per distinct key in the warp
-  unsigned peers = __match_any_sync(FULL, k);
-  int leader = __ffs(peers) - 1;
-  int lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  if (valid && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
-  base = __shfl_sync(FULL, base, leader);
-  if (valid) {
-    key[i] = k;
-    slot[i] = base + __popc(peers & ((1u << lane) - 1u));
+  const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
+  const uint32_t ia[2] = {i0, i0 + blockDim.x};
+  double4 pa[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) pa[u] = ia[u] < n ? ag[ia[u]] : make_double4(0.0, 0.0, 0.0, 0.0);
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const bool valid = ia[u] < n;
+    uint32_t k = 0xffffffffu;
+    if (valid) {
+      const double4 p = pa[u];
+      const int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv), bz = (int)floor(p.z * g.inv);
+      k = box_key(g, bx, by, bz);
+    }
+    // warp-aggregated histogram: one atomic per distinct key in the warp
+    const unsigned peers = __match_any_sync(FULL, k);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (valid && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
+    base = __shfl_sync(FULL, base, leader);
+    if (valid) {
+      key[ia[u]] = k;
+      slot[ia[u]] = base + __popc(peers & ((1u << lane) - 1u));
+    }
   }
 }
 
@@ -416,7 +436,7 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
   ids_out[dst] = id;
   // fp32 copy of the position for the force kernel's conservative candidate filter
   agf_out[dst] = make_float4(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z),
-                             __double2float_rn(0.5 * p.w));
+                             -__double2float_rn(0.5 * p.w));  // -r: (z, -r) pairs with (z_i, r_i) in one FADD2
 }
 
 // ------------------------------------------------------------------------------------------ K6
@@ -708,6 +728,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       // (r_i + r_j + m32)^2 (1 + 2^-20): only candidates that can be contacts reach
       // the exact fp64 evaluation.
       const float ri32 = __double2float_ru(ri + g.m32);
+      const unsigned long long mxy = pack2(mf.x, mf.y), mzr = pack2(mf.z, ri32);
       int k = 0;
       bool live = nr > 0;
       uint32_t q = live ? sm.rb[0][lane] : 0u, e = live ? sm.re[0][lane] : 0u;
@@ -732,11 +753,19 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
         for (int t = 0; t < 4; ++t) o[t] = __ldg(&agf[qs[t]]);
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          const float dx = mf.x - o[t].x, dy = mf.y - o[t].y, dz = mf.z - o[t].z;
-          const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-          const float sp = ri32 + o[t].w;
-          const float s2 = sp * sp;
-          if (as[t] && d2 <= __fmaf_rn(s2, 0x1p-20f, s2)) sm.list[cnt++][lane] = qs[t];
+          // packed fp32x2 (FADD2/FMUL2): (dx, dy) = (x_i, y_i) - (x_j, y_j); (dz, s) = (z_i, r_i) - (z_j, -r_j)
+          float2 dxy, dzs;
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
+              : "l"(mxy), "l"(pack2(o[t].x, o[t].y)));
+          asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dzs))
+              : "l"(mzr), "l"(pack2(o[t].z, o[t].w)));
+          float2 sq, qz;
+          asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&sq))
+              : "l"(*reinterpret_cast<unsigned long long*>(&dxy)));
+          asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&qz))
+              : "l"(*reinterpret_cast<unsigned long long*>(&dzs)));
+          const float d2 = (sq.x + sq.y) + qz.x;
+          if (as[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) sm.list[cnt++][lane] = qs[t];
         }
         if (__any_sync(FULL, cnt > LCAP - 4))
           flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
