@@ -52,6 +52,9 @@ extern "C" {
 /* params.flags */
 #define BDM_DEVICE_PTRS 0x1u /* array arguments are CUDA device pointers */
 #define BDM_RECORD 0x2u      /* force kernel also records per-agent neighbour / contact statistics */
+#define BDM_SKIP_STATIONARY 0x4u /* NEXT-1: skip the neighbourhood search of agents no moving agent
+                                    could affect ("detect stationary regions ... and
+                                    skip the expensive collision detection"); bit-identical results */
 
 /* bdm_get_pairs kind */
 #define BDM_NEIGHBOR 0 /* unordered pairs with d2 <= L2 (O3) */
@@ -131,6 +134,11 @@ int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out);
  * max id) sorted lexicographically into out[2*cap] (HOST memory always).  *n_pairs receives the
  * count; ETRUNC (and nothing written) if it exceeds cap.  Builds the grid if not fresh. */
 int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_t cap);
+
+/* Stationary-region skip statistics of the last step (BDM_SKIP_STATIONARY): out3[0] agents that
+ * moved (dp != 0), out3[1] agents whose neighbourhood was searched, out3[2] N.  -1 entries when not
+ * available (no step yet, or the flag is off). */
+int bdm_get_skip_stats(bdm_handle h, int64_t* out3);
 
 /* Issue all later work on this CUDA stream (cudaStream_t; NULL = legacy default stream). */
 int bdm_set_stream(bdm_handle h, void* cuda_stream);

@@ -31,6 +31,7 @@ BDM_ERANGE = -7
 BDM_ETRUNC = -8
 BDM_DEVICE_PTRS = 0x1
 BDM_RECORD = 0x2
+BDM_SKIP_STATIONARY = 0x4
 BDM_NEIGHBOR = 0
 BDM_CONTACT = 1
 BDM_HALO = 0
@@ -77,6 +78,7 @@ _SIGS = {
     "bdm_get_agent_stats": ([_vp, ctypes.POINTER(bdm_agent_stats)], ctypes.c_int),
     "bdm_get_pairs": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, ctypes.c_int64], ctypes.c_int),
     "bdm_set_agents": ([_vp, _vp, _vp], ctypes.c_int),
+    "bdm_get_skip_stats": ([_vp, _vp], ctypes.c_int),
     "bdm_set_stream": ([_vp, _vp], ctypes.c_int),
     "bdm_sync": ([_vp], ctypes.c_int),
     "bdm_set_timing": ([_vp, ctypes.c_int], ctypes.c_int),
@@ -286,6 +288,13 @@ def bdm_get_pairs(h: Handle, kind: int) -> np.ndarray:
     out = np.empty((max(cnt.value, 1), 2), np.int64)
     _check(lib.bdm_get_pairs(h.raw, kind, ctypes.byref(cnt), _ptr(out), cnt.value), h.raw)
     return out[: cnt.value]
+
+
+def bdm_get_skip_stats(h: Handle) -> dict:
+    """NEXT-1 statistics of the last step: agents moved, agents searched, N."""
+    out = np.zeros(3, np.int64)
+    _check(load_library().bdm_get_skip_stats(h.raw, _ptr(out)), h.raw)
+    return dict(moved=int(out[0]), searched=int(out[1]), n=int(out[2]))
 
 
 def bdm_set_timing(h: Handle, enabled: bool = True) -> None:

@@ -84,6 +84,13 @@ struct bdm_ctx {
   int64_t n_dp = 0;
   uint32_t* cnt = nullptr;     // pack counters (device)
   uint32_t* cnt_host = nullptr;
+  // stationary-region skip (BDM_SKIP_STATIONARY, NEXT-1)
+  unsigned long long* hist[2] = {nullptr, nullptr};
+  uint8_t* hot = nullptr;  // one hot flag per box-table entry
+  size_t hot_cap = 0;
+  bool skip_valid = false;   // hist describes the last step
+  bool skip_active = false;  // the pending force kernel uses hot flags
+  uint32_t last_moved = 0, last_searched = 0;
   bool timing = false;
   int sm_count = 0, force_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
@@ -236,6 +243,8 @@ int compute_extents(bdm_ctx* h) {
     h->poisoned = true;
     return fail(h, BDM_ERANGE, "an agent lies >= 2^20 boxes from the origin (|p*inv| >= 2^20, DESIGN.md R9)");
   }
+  h->last_moved = h->ext_host->moved;
+  h->last_searched = h->ext_host->searched;
   GridDev& g = h->grid;
   int64_t dims[3];
   for (int a = 0; a < 3; ++a) {
@@ -292,8 +301,10 @@ int sort_into(bdm_ctx* h, uint32_t n) {
   if (rc) return rc;
   if (n > 0) {
     k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
+    const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
     k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
-                                           h->id[dst], h->agf);
+                                           h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
+                                           perm_hist ? h->hist[dst] : nullptr);
   }
   CU(h, cudaGetLastError());
   h->launches += n > 0 ? 8 : 4;
@@ -313,6 +324,23 @@ int grid_build(bdm_ctx* h) {
   if (rc) return rc;
   rc = sort_into(h, (uint32_t)h->n);
   if (rc) return rc;
+  // NEXT-1: mark agents near a moving agent; skip only while few agents move (else it costs more
+  // than it saves) and never in RECORD mode (statistics count every candidate)
+  h->skip_active = false;
+  if (h->hist[0] && h->skip_valid && !(h->prm.flags & BDM_RECORD) && (uint64_t)h->last_moved * 2 <= (uint64_t)h->n) {
+    if (h->hot_cap < h->table_cap + 4) {  // one flag byte per box-table entry
+      if (h->hot) CU(h, cudaFree(h->hot));
+      h->hot = nullptr;
+      CU(h, cudaMalloc(&h->hot, h->table_cap + 4));
+      h->hot_cap = h->table_cap + 4;
+    }
+    k_flag_zero<<<h->sm_count * 4, 256, 0, h->stream>>>(h->hot, h->coff, h->grid.n_cols);
+    k_mark_hot<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->hist[h->cur], (uint32_t)h->n, h->grid,
+                                                         h->hot);
+    CU(h, cudaGetLastError());
+    h->launches += 2;
+    h->skip_active = true;
+  }
   h->state = State::Fresh;
   h->have_grid = true;
   return BDM_OK;
@@ -337,10 +365,13 @@ int force_step(bdm_ctx* h, bool want_dp) {
   const unsigned grid = force_grid(h, n);
   if (h->prm.flags & BDM_RECORD)
     k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
-                                                nullptr, dp, nullptr, h->ext, h->err, rec);
+                                                nullptr, dp, nullptr, h->ext, h->err, rec, nullptr,
+                                                h->hist[0] ? h->hist[dst] : nullptr);
   else
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
-                                                 h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec);
+                                                 h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
+                                                 h->skip_active ? h->hot : nullptr,
+                                                 h->hist[0] ? h->hist[dst] : nullptr);
   CU(h, cudaGetLastError());
   h->launches += 2;
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
@@ -348,6 +379,8 @@ int force_step(bdm_ctx* h, bool want_dp) {
   h->out_ids = h->id[src];
   std::swap(h->id[src], h->id[dst]);
   h->cur = dst;
+  if (h->hist[0]) h->skip_valid = true;
+  h->skip_active = false;
   h->ext_valid = true;
   h->state = State::Stepped;
   if (want_dp) h->have_dp = true;
@@ -384,6 +417,7 @@ int upload(bdm_ctx* h, const double* pos, const double* diam) {
   h->have_dp = false;
   h->have_record = false;
   h->ext_valid = false;
+  h->skip_valid = false;
   h->state = State::NoGrid;
   h->have_grid = false;
   h->cur = 0;
@@ -456,7 +490,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -519,6 +553,10 @@ int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, 
   TRY(dalloc(h, &h->err, 1));
   TRY(dalloc(h, &h->maxd_bits, 1));
   TRY(dalloc(h, &h->scan_ticket, 1));
+  if (p->flags & BDM_SKIP_STATIONARY) {
+    TRY(dalloc(h, &h->hist[0], N));
+    TRY(dalloc(h, &h->hist[1], N));
+  }
   if (p->flags & BDM_RECORD) {
     TRY(dalloc(h, &h->r_cand, N));
     TRY(dalloc(h, &h->r_nb, N));
@@ -1090,7 +1128,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
                                                  (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
-                                                 h->err, rec);
+                                                 h->err, rec, nullptr, nullptr);
     CU(h, cudaGetLastError());
     h->launches += 1;
   }
@@ -1126,6 +1164,22 @@ int bdm_slab_get(bdm_handle h, int what, int64_t* n, uint32_t* ids, double* vals
     if (vals) CU(h, cudaMemcpyAsync(vals, h->dp, 3 * m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   }
   return check_async(h);
+}
+
+int bdm_get_skip_stats(bdm_handle h, int64_t* out3) {
+  if (!h || !out3) return fail(h, BDM_EINVAL, "bdm_get_skip_stats: NULL argument");
+  CU(h, cudaSetDevice(h->device));
+  if (!h->ext_valid || h->state != State::Stepped) {
+    out3[0] = out3[1] = out3[2] = -1;
+    return BDM_OK;
+  }
+  CU(h, cudaMemcpyAsync(h->ext_host, h->ext, sizeof(Extents), cudaMemcpyDeviceToHost, h->stream));
+  int rc = check_async(h);
+  if (rc) return rc;
+  out3[0] = h->hist[0] ? (int64_t)h->ext_host->moved : -1;
+  out3[1] = h->hist[0] ? (int64_t)h->ext_host->searched : -1;
+  out3[2] = h->n;
+  return BDM_OK;
 }
 
 int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo3, const double* hi3, double dlo,

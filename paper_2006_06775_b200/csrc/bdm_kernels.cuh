@@ -55,6 +55,8 @@ struct Extents {
   int32_t lo[3], hi[3];
   int32_t range_err;  // 1 if some |p*inv| >= 2^20
   uint32_t work;      // chunk counter of the persistent force kernel
+  uint32_t moved;     // agents with dp != 0 in the step that produced these extents (skip mode)
+  uint32_t searched;  // agents whose neighbourhood was searched in that step (skip mode)
 };
 
 struct ErrDev {
@@ -191,6 +193,8 @@ __global__ void k_ext_reset(Extents* ext) {
   }
   if (threadIdx.x == 3) ext->range_err = 0;
   if (threadIdx.x == 4) ext->work = 0u;
+  if (threadIdx.x == 5) ext->moved = 0u;
+  if (threadIdx.x == 6) ext->searched = 0u;
 }
 
 __device__ __forceinline__ uint32_t col_of(const GridDev& g, int bx, int by) {
@@ -423,7 +427,8 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __re
 __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __restrict__ tid,
                         const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ start,
                         const double4* __restrict__ ag_in, uint32_t n, double4* __restrict__ ag_out,
-                        uint32_t* __restrict__ ids_out, float4* __restrict__ agf_out) {
+                        uint32_t* __restrict__ ids_out, float4* __restrict__ agf_out,
+                        const unsigned long long* __restrict__ hist_in, unsigned long long* __restrict__ hist_out) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
   uint32_t k = tkey[q], id = tid[q];
@@ -431,12 +436,85 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
   uint32_t rank = 0;
   for (uint32_t t = b; t < e; ++t) rank += tid[t] < id;
   uint32_t dst = b + rank;
-  const double4 p = ag_in[tsrc[q]];
+  const uint32_t src = tsrc[q];
+  const double4 p = ag_in[src];
   ag_out[dst] = p;
   ids_out[dst] = id;
+  if (hist_out) hist_out[dst] = hist_in[src];
   // fp32 copy of the position for the force kernel's conservative candidate filter
   agf_out[dst] = make_float4(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z),
                              -__double2float_rn(0.5 * p.w));  // -r: (z, -r) pairs with (z_i, r_i) in one FADD2
+}
+
+// ------------------------------------------------------------------------------------------ NEXT-1
+// Stationary-region skip (§2.3(iv)).  Per agent the previous
+// step leaves hist = moved-bit (bit 63, dp != 0) | packed box of the position before that step.
+// A box is hot if some moved agent's new or old box lies within Chebyshev distance 1 of it.  An
+// agent in a quiet box had no moving agent in its 27-box neighbourhood before or after the last
+// step, so its candidate set, pair terms and canonical order are unchanged, and since it did not
+// move its displacement was and stays exactly 0: the force kernel skips it, bit-identically.
+constexpr int HB = 21;  // bits per packed box coordinate (|b| < 2^20)
+
+__device__ __forceinline__ unsigned long long pack_box(int bx, int by, int bz) {
+  const unsigned long long m = (1ull << HB) - 1ull;
+  return ((unsigned long long)(bx + (1 << 20)) & m) | (((unsigned long long)(by + (1 << 20)) & m) << HB) |
+         (((unsigned long long)(bz + (1 << 20)) & m) << (2 * HB));
+}
+
+__device__ __forceinline__ void unpack_box(unsigned long long v, int& bx, int& by, int& bz) {
+  const unsigned long long m = (1ull << HB) - 1ull;
+  bx = (int)(v & m) - (1 << 20);
+  by = (int)((v >> HB) & m) - (1 << 20);
+  bz = (int)((v >> (2 * HB)) & m) - (1 << 20);
+}
+
+// Warp per 32 sorted agents: the bounding region of the warp's movers' new and old boxes, grown by
+// one box, is marked hot (conservative superset of every mover's two 3x3x3 neighbourhoods).
+// Only boxes inside their column's occupied z-range exist (and only they can hold agents).
+__global__ void k_mark_hot(const double4* __restrict__ ag, const unsigned long long* __restrict__ hist, uint32_t n,
+                           GridDev g, uint8_t* __restrict__ bflag) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const unsigned long long h = i < n ? hist[i] : 0ull;
+  const bool moved = (h >> 63) != 0;
+  if (!__any_sync(FULL, moved)) return;
+  int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+  if (moved) {
+    const double4 p = ag[i];
+    const int nb[3] = {(int)floor(p.x * g.inv), (int)floor(p.y * g.inv), (int)floor(p.z * g.inv)};
+    int ob[3];
+    unpack_box(h & ~(1ull << 63), ob[0], ob[1], ob[2]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      lo[a] = min(nb[a], ob[a]) - 1;
+      hi[a] = max(nb[a], ob[a]) + 1;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = __reduce_min_sync(FULL, lo[a]);
+    hi[a] = __reduce_max_sync(FULL, hi[a]);
+  }
+  lo[0] = max(lo[0], g.lo[0]);
+  hi[0] = min(hi[0], g.hi[0]);
+  lo[1] = max(lo[1], g.lo[1]);
+  hi[1] = min(hi[1], g.hi[1]);
+  for (int cx = lo[0]; cx <= hi[0]; ++cx)
+    for (int cy = lo[1]; cy <= hi[1]; ++cy) {
+      const uint32_t c = col_of(g, cx, cy);
+      const int zl = __ldg(&g.czlo[c]), zh = __ldg(&g.czhi[c]);
+      const int a = max(lo[2], zl), d = min(hi[2], zh);
+      if (a > d) continue;
+      const uint32_t o = __ldg(&g.coff[c]) + (uint32_t)(a - zl);
+      for (int t = lane; t <= d - a; t += 32) bflag[o + t] = 1;
+    }
+}
+
+// zero box flags [0 .. T] (T = coff[nc] on the device)
+__global__ void k_flag_zero(uint8_t* __restrict__ bflag, const uint32_t* __restrict__ coff, uint32_t nc) {
+  const uint32_t T = coff[nc];
+  uint32_t* w = reinterpret_cast<uint32_t*>(bflag);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= T / 4; k += gridDim.x * blockDim.x) w[k] = 0u;
 }
 
 // ------------------------------------------------------------------------------------------ K6
@@ -562,7 +640,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     k_force(const double4* __restrict__ ag, const float4* __restrict__ agf, const uint32_t* __restrict__ ids,
             uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
             uint32_t* __restrict__ id_out, double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
-            Extents* ext_next, ErrDev* err, RecordDev rec) {
+            Extents* ext_next, ErrDev* err, RecordDev rec, const uint8_t* __restrict__ hot,
+            unsigned long long* __restrict__ hist_out) {
   extern __shared__ __align__(16) unsigned char s_raw[];  // FORCE_WARPS x ForceSmem (dynamic)
   ForceSmem* s_all = reinterpret_cast<ForceSmem*>(s_raw);
   const int lane = threadIdx.x & 31;
@@ -582,6 +661,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     const uint32_t myid = valid ? ids[i] : 0u;
     const double ri = 0.5 * me.w;
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+    // skip mode: quiet agents (no moving agent around them, NEXT-1) do not search: F = 0 exactly
+    const bool search = valid && (hot == nullptr || hot[box_key(g, bx, by, bz)] != 0);
     double thr = (ri + g.thr_pad) * (ri + g.thr_pad);
     thr = thr + thr * 0x1p-50;
     // fp32 bound: (r_i + L/2 + m32)^2 (1 + 2^-20), rounded up
@@ -604,10 +685,13 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     // the 9 neighbour columns up once per warp: lane c < 9 reads column c's descriptor, then the
     // warp stages start(c, z) for z in [zf-1, zl+2] with coalesced loads; lanes then read their
     // z-runs from shared memory instead of 9 dependent global lookups each.
-    const int bx0 = __shfl_sync(FULL, bx, 0), by0 = __shfl_sync(FULL, by, 0);
-    const int zf = __reduce_min_sync(FULL, valid ? bz : INT32_MAX);
-    const int zl = __reduce_max_sync(FULL, valid ? bz : INT32_MIN);
-    const bool coop = !RECORD && __all_sync(FULL, !valid || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
+    const unsigned smask = __ballot_sync(FULL, search);
+    const int src0 = smask ? __ffs(smask) - 1 : 0;
+    const int bx0 = __shfl_sync(FULL, bx, src0), by0 = __shfl_sync(FULL, by, src0);
+    const int zf = __reduce_min_sync(FULL, search ? bz : INT32_MAX);
+    const int zl = __reduce_max_sync(FULL, search ? bz : INT32_MIN);
+    const bool coop = !RECORD && __any_sync(FULL, search) &&
+                      __all_sync(FULL, !search || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
     if (coop) {
       int czl = 0, cze = 0;  // column descriptor: first occupied z, number of occupied z
       uint32_t cof = 0;
@@ -650,7 +734,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     for (int c = 0; c < 9; ++c) {
       const int ddx = c / 3 - 1, ddy = c % 3 - 1;
       uint32_t b = 0, e = 0;
-      if (valid) {
+      if (search) {
         int z0 = bz - 1, z1 = bz + 1;
         bool keep = true;
         if (!RECORD) {
@@ -797,6 +881,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
       ag_out[o] = np;
+      if (hist_out) {
+        const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
+        hist_out[o] = ((unsigned long long)moved << 63) | pack_box(bx, by, bz);
+      }
       if (id_out) id_out[o] = myid;
       if (dp_out) {
         dp_out[3 * (size_t)o] = dpx;
@@ -817,6 +905,14 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
         rec.branch[o] = (int8_t)branch;
         rec.nb_hash[o] = nb_hash;
         rec.ct_hash[o] = ct_hash;
+      }
+    }
+    if (hist_out) {
+      const unsigned mv = __ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0));
+      const unsigned se = __ballot_sync(FULL, search);
+      if (lane == 0) {
+        if (mv) atomicAdd(&ext_next->moved, (uint32_t)__popc(mv));
+        if (se) atomicAdd(&ext_next->searched, (uint32_t)__popc(se));
       }
     }
   }
