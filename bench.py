@@ -275,10 +275,10 @@ def run_bdm(args):
     return 0
 
 
-# rebuild kernels (K2 key+hist, K3 scan, K4 scatter, place): algorithmic bytes per agent
-# (DESIGN.md §6.1): read state 32 + key/slot 8 | key/slot/id 12 + scatter 12 | place 12 + gather 32
-# + write 36  = 144 B/agent (the box table adds 12 B per box, counted separately in DESIGN.md)
-REBUILD_BYTES_PER_AGENT = 144
+# rebuild kernels, algorithmic bytes per agent: column pass 32 | key + histogram
+# 32 + 8 | scatter 12 + 12 | place 12 + 32 gather + 32 + 4 + 16 (fp32 copy) = 192 B/agent (the
+# ragged box table adds ~12 B per box, not counted)
+REBUILD_BYTES_PER_AGENT = 192
 
 
 def run_e2e(bdm, torch, pos_h, diam_h, local, args):
