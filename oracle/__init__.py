@@ -30,6 +30,10 @@ class Params(ctypes.Structure):
                 ("k_rep", "gamma_att", "adherence", "dt", "eta", "max_disp", "box_edge_min")]
 
 
+class Growth(ctypes.Structure):
+    _fields_ = [("growth", ctypes.c_double), ("div_diam", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
 class Grid(ctypes.Structure):
     _fields_ = [("L", ctypes.c_double), ("L2", ctypes.c_double), ("inv", ctypes.c_double),
                 ("lo", ctypes.c_int64 * 3), ("hi", ctypes.c_int64 * 3)]
@@ -72,6 +76,12 @@ def lib():
                                      ctypes.c_int64, ctypes.POINTER(Params), _f64p]
         L.orc_displacement.argtypes = [_f64p, ctypes.POINTER(Params), _f64p]
         L.orc_box_coords.argtypes = [ctypes.c_int64, _f64p, ctypes.POINTER(Grid), _i64p]
+        L.orc_grow_divide.argtypes = [ctypes.c_int64, _f64p, _f64p, ctypes.POINTER(Growth), ctypes.c_int64,
+                                      ctypes.c_int64]
+        L.orc_grow_divide.restype = ctypes.c_int64
+        L.orc_run_growth.argtypes = [ctypes.c_int64, _f64p, _f64p, ctypes.POINTER(Params), ctypes.POINTER(Growth),
+                                     ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _f64p, ctypes.c_int]
+        L.orc_run_growth.restype = ctypes.c_int64
         L.orc_mix64.argtypes = [ctypes.c_uint64]
         L.orc_mix64.restype = ctypes.c_uint64
         _lib = L
@@ -194,3 +204,33 @@ def mix64(x: int) -> int:
 
 def threads() -> int:
     return int(lib().orc_threads())
+
+
+def grow_divide(pos, diam, growth, div_diam, seed, step):
+    """NEXT-2 G1-G2 on copies; returns (pos, diam) with daughters appended (ids n, n+1, ...)."""
+    n = len(diam)
+    cap = 2 * n + 1
+    P = np.zeros((cap, 3))
+    Dm = np.zeros(cap)
+    P[:n] = pos
+    Dm[:n] = diam
+    m = lib().orc_grow_divide(n, _ptr(P), _ptr(Dm), ctypes.byref(Growth(growth, div_diam, seed)), step, cap)
+    if m < 0:
+        raise OracleError(m)
+    return P[:m].copy(), Dm[:m].copy()
+
+
+def run_growth(pos, diam, n_steps, growth, div_diam, seed, prm=None, step0=0, cap=None):
+    """n_steps of (mechanics, growth + division).  Returns (pos, diam, dp of the last mechanics)."""
+    n = len(diam)
+    cap = cap or max(4 * n, 16) * (2 ** min(n_steps, 6))
+    P = np.zeros((cap, 3))
+    Dm = np.zeros(cap)
+    P[:n] = pos
+    Dm[:n] = diam
+    dp = np.zeros((cap, 3))
+    m = lib().orc_run_growth(n, _ptr(P), _ptr(Dm), ctypes.byref(prm or params()),
+                             ctypes.byref(Growth(growth, div_diam, seed)), n_steps, step0, cap, _ptr(dp), 0)
+    if m < 0:
+        raise OracleError(m)
+    return P[:m].copy(), Dm[:m].copy(), dp

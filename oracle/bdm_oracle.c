@@ -449,3 +449,86 @@ int orc_threads(void) {
   return 1;
 #endif
 }
+
+/* ------------------------------------------------------------------------------------------------
+ * NEXT-2: cell growth and division (readings G1-G3).  PAPER.md:711-712, 772 (the
+ * "cell growth and division" GPU benchmark); SPEC.md:82-91 (CellDivision: volume-conserving split,
+ * daughter displaced so the two spheres touch), SPEC.md:101 (2^n doubling oracle).
+ *   G1 growth   D <- D + growth                                   (diameter rate, um per step)
+ *   G2 division if D >= div_diam: D' = D * c, c = 2^(-1/3) (binary64 nearest), h = 0.5 * D',
+ *               u = v/|v|, v_a = 2 * U(seed, step, id, a) - 1 (counter hash, a = 0..2; v = 0 -> x_hat),
+ *               mother p - h*u (same id), daughter p + h*u with id N + (rank of the mother among this
+ *               step's dividers in ascending id order)
+ *   G3 order    a growth step runs after the mechanics of the same step (new agents are visible from
+ *               the next step on)
+ * ---------------------------------------------------------------------------------------------- */
+typedef struct {
+  double growth;   /* diameter increase per step, um */
+  double div_diam; /* division threshold on the grown diameter, um */
+  uint64_t seed;
+} orc_growth;
+
+static const double ORC_CBRT_HALF = 0.79370052598409973737585281963615; /* 2^(-1/3) */
+
+static double orc_u01(uint64_t seed, uint64_t step, uint64_t id, uint64_t a) {
+  uint64_t h = orc_mix64(seed * 0x9E3779B97F4A7C15ULL + ((step << 32) + id) * 4ULL + a);
+  return (double)(h >> 11) * 0x1p-53;
+}
+
+/* One growth + division pass in id order.  pos (3*cap), diam (cap) are updated in place; returns the
+ * new agent count, or ORC_ERANGE when cap is too small. */
+int64_t orc_grow_divide(int64_t n, double* pos, double* diam, const orc_growth* gp, int64_t step, int64_t cap) {
+  int64_t nd = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    diam[i] = diam[i] + gp->growth;
+    if (diam[i] >= gp->div_diam) ++nd;
+  }
+  if (n + nd > cap) return ORC_ERANGE;
+  int64_t k = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (!(diam[i] >= gp->div_diam)) continue;
+    double v[3], u[3];
+    for (int a = 0; a < 3; ++a) v[a] = 2.0 * orc_u01(gp->seed, (uint64_t)step, (uint64_t)i, (uint64_t)a) - 1.0;
+    double norm = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+    if (norm == 0.0) {
+      u[0] = 1.0;
+      u[1] = 0.0;
+      u[2] = 0.0;
+    } else {
+      for (int a = 0; a < 3; ++a) u[a] = v[a] / norm;
+    }
+    double Dd = diam[i] * ORC_CBRT_HALF;
+    double h = 0.5 * Dd;
+    int64_t d = n + k;
+    for (int a = 0; a < 3; ++a) {
+      double p = pos[3 * i + a];
+      double off = h * u[a];
+      pos[3 * i + a] = p - off;
+      pos[3 * d + a] = p + off;
+    }
+    diam[i] = Dd;
+    diam[d] = Dd;
+    ++k;
+  }
+  return n + nd;
+}
+
+/* n_steps of (mechanics O1-O7, then growth + division); returns the final count (<0: error).
+ * dp (3*cap) receives the mechanics displacement of the last step for the agents of that step. */
+int64_t orc_run_growth(int64_t n, double* pos, double* diam, const orc_params* p, const orc_growth* gp,
+                       int32_t n_steps, int64_t step0, int64_t cap, double* dp, int nthreads) {
+  double* tmp = (double*)malloc(sizeof(double) * 3 * (cap > 0 ? cap : 1));
+  if (!tmp) return ORC_ENOMEM;
+  for (int32_t s = 0; s < n_steps; ++s) {
+    int rc = orc_step(n, pos, diam, p, dp, tmp, NULL, nthreads);
+    if (rc) {
+      free(tmp);
+      return rc;
+    }
+    memcpy(pos, tmp, sizeof(double) * 3 * n);
+    n = orc_grow_divide(n, pos, diam, gp, step0 + s, cap);
+    if (n < 0) break;
+  }
+  free(tmp);
+  return n;
+}
