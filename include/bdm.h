@@ -119,6 +119,9 @@ int bdm_get_displacements(bdm_handle h, double* out);
 /* Current positions, n x 3 fp64, id order. */
 int bdm_get_positions(bdm_handle h, double* out);
 
+/* Current diameters, n fp64, id order (they change under bdm_set_growth). */
+int bdm_get_diameters(bdm_handle h, double* out);
+
 /* Integer box coordinates floor(p * inv) of the current positions under the current grid,
  * n x 3 int32, id order.  Builds the grid if it is not fresh. */
 int bdm_get_box_coords(bdm_handle h, int32_t* out);
@@ -134,6 +137,21 @@ int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out);
  * max id) sorted lexicographically into out[2*cap] (HOST memory always).  *n_pairs receives the
  * count; ETRUNC (and nothing written) if it exceeds cap.  Builds the grid if not fresh. */
 int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_t cap);
+
+/* NEXT-2, cell growth and division ("cell growth and
+ * division" benchmark; SPEC.md:82-91 volume-conserving division).  After the mechanics of every
+ * later step: D <- D + growth; agents with D >= div_diam divide into two spheres of diameter
+ * D * 2^(-1/3) touching along a counter-hash direction (seed, step, id); the k-th divider in id
+ * order creates agent id N + k.  growth = 0 and div_diam = +inf switch it off.  The population
+ * grows (capacity doubles as needed); displacements refer to the agents of the last mechanics. */
+int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed);
+
+/* Make room for `capacity` agents (dynamic populations).  Never shrinks. */
+int bdm_reserve(bdm_handle h, int64_t capacity);
+
+/* out2[0] = current number of agents, out2[1] = agents of the last mechanics step (rows of
+ * bdm_get_displacements / bdm_get_agent_stats). */
+int bdm_get_count(bdm_handle h, int64_t* out2);
 
 /* Stationary-region skip statistics of the last step (BDM_SKIP_STATIONARY): out3[0] agents that
  * moved (dp != 0), out3[1] agents whose neighbourhood was searched, out3[2] N.  -1 entries when not

@@ -74,11 +74,15 @@ _SIGS = {
     "bdm_get_displacements": ([_vp, _vp], ctypes.c_int),
     "bdm_get_positions": ([_vp, _vp], ctypes.c_int),
     "bdm_get_box_coords": ([_vp, _vp], ctypes.c_int),
+    "bdm_get_diameters": ([_vp, _vp], ctypes.c_int),
     "bdm_get_grid_info": ([_vp, ctypes.POINTER(bdm_grid_info)], ctypes.c_int),
     "bdm_get_agent_stats": ([_vp, ctypes.POINTER(bdm_agent_stats)], ctypes.c_int),
     "bdm_get_pairs": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, ctypes.c_int64], ctypes.c_int),
     "bdm_set_agents": ([_vp, _vp, _vp], ctypes.c_int),
     "bdm_get_skip_stats": ([_vp, _vp], ctypes.c_int),
+    "bdm_set_growth": ([_vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
+    "bdm_reserve": ([_vp, ctypes.c_int64], ctypes.c_int),
+    "bdm_get_count": ([_vp, _vp], ctypes.c_int),
     "bdm_set_stream": ([_vp, _vp], ctypes.c_int),
     "bdm_sync": ([_vp], ctypes.c_int),
     "bdm_set_timing": ([_vp, ctypes.c_int], ctypes.c_int),
@@ -151,6 +155,13 @@ def _ptr(a):
     return ctypes.c_void_p(a.ctypes.data)
 
 
+class _Sized:
+    """View of a handle with another row count (for last-step outputs)."""
+
+    def __init__(self, h, n):
+        self.raw, self.n, self.device_ptrs = h.raw, n, h.device_ptrs
+
+
 class Handle:
     """Owns a bdm_handle; destroyed with the object."""
 
@@ -218,6 +229,7 @@ def bdm_grid_build(h: Handle) -> None:
 
 def bdm_mech_step(h: Handle, n_steps: int = 1) -> None:
     _check(load_library().bdm_mech_step(h.raw, n_steps), h.raw)
+    bdm_get_count(h)
 
 
 def bdm_sync(h: Handle) -> None:
@@ -235,15 +247,40 @@ def _out(h: Handle, shape, dtype, out):
     return np.empty(shape, dtype=dtype)
 
 
+def bdm_get_count(h: Handle):
+    """(current agents, agents of the last mechanics step)."""
+    out = np.zeros(2, np.int64)
+    _check(load_library().bdm_get_count(h.raw, _ptr(out)), h.raw)
+    h.n = int(out[0])
+    return int(out[0]), int(out[1])
+
+
+def bdm_set_growth(h: Handle, growth: float, div_diam: float, seed: int = 0) -> None:
+    _check(load_library().bdm_set_growth(h.raw, growth, div_diam, seed), h.raw)
+
+
+def bdm_reserve(h: Handle, capacity: int) -> None:
+    _check(load_library().bdm_reserve(h.raw, capacity), h.raw)
+
+
 def bdm_get_displacements(h: Handle, out=None):
-    out = _out(h, (h.n, 3), np.float64, out)
+    _, n_dp = bdm_get_count(h)
+    out = _out(h, (n_dp, 3), np.float64, out)
     _check(load_library().bdm_get_displacements(h.raw, _ptr(out)), h.raw)
     return out
 
 
 def bdm_get_positions(h: Handle, out=None):
+    bdm_get_count(h)
     out = _out(h, (h.n, 3), np.float64, out)
     _check(load_library().bdm_get_positions(h.raw, _ptr(out)), h.raw)
+    return out
+
+
+def bdm_get_diameters(h: Handle, out=None):
+    bdm_get_count(h)
+    out = _out(h, (h.n,), np.float64, out)
+    _check(load_library().bdm_get_diameters(h.raw, _ptr(out)), h.raw)
     return out
 
 
@@ -261,6 +298,8 @@ def bdm_get_grid_info(h: Handle) -> dict:
 
 def bdm_get_agent_stats(h: Handle) -> dict:
     """Per-agent record of the last step (host NumPy arrays; requires BDM_RECORD)."""
+    n_cur, n_dp = bdm_get_count(h)
+    h = _Sized(h, n_dp or n_cur)
     if h.device_ptrs:
         import torch
 

@@ -26,6 +26,7 @@ using namespace bdm;
 namespace {
 
 thread_local std::string g_tls_error;
+const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after every launch
 
 enum class State { NoGrid, Fresh, Stepped };
 
@@ -84,6 +85,12 @@ struct bdm_ctx {
   int64_t n_dp = 0;
   uint32_t* cnt = nullptr;     // pack counters (device)
   uint32_t* cnt_host = nullptr;
+  // cell growth and division (NEXT-2): dynamic population up to cap agents
+  bool growth_on = false;
+  double growth = 0.0, div_diam = 0.0;
+  uint64_t gseed = 0;
+  uint64_t step_count = 0;   // mechanics steps since init / set_agents (division hash)
+  uint32_t* gflag = nullptr;  // id-indexed division flags -> ranks (cap + 1)
   // stationary-region skip (BDM_SKIP_STATIONARY, NEXT-1)
   unsigned long long* hist[2] = {nullptr, nullptr};
   uint8_t* hot = nullptr;  // one hot flag per box-table entry
@@ -120,6 +127,18 @@ int fail(bdm_ctx* h, int code, const char* fmt, ...) {
       return fail((h), e_ == cudaErrorMemoryAllocation ? BDM_ENOMEM : BDM_ECUDA, "%s: %s (%s:%d)", \
                   #call, cudaGetErrorString(e_), __FILE__, __LINE__);                         \
     }                                                                                         \
+  } while (0)
+
+// BDM_DEBUG=1: synchronise after a launch and name the kernel that failed.
+#define DBG(h, name)                                                                                   \
+  do {                                                                                                 \
+    if (g_debug) {                                                                                     \
+      cudaError_t e_ = cudaStreamSynchronize((h)->stream);                                             \
+      if (e_ == cudaSuccess) e_ = cudaGetLastError();                                                  \
+      if (e_ != cudaSuccess)                                                                           \
+        return fail((h), BDM_ECUDA, "%s (n=%lld cap=%lld step=%llu): %s", name, (long long)(h)->n,     \
+                    (long long)(h)->cap, (unsigned long long)(h)->step_count, cudaGetErrorString(e_)); \
+    }                                                                                                  \
   } while (0)
 
 template <typename T>
@@ -215,6 +234,16 @@ void init_device_info(bdm_ctx* h) {
 // *n_dev + 1 (persistent decoupled look-back, grid = resident capacity).
 int scan(bdm_ctx* h, uint32_t* data, uint64_t items, const uint32_t* n_dev) {
   init_device_info(h);
+  if (items) {  // host-sized scans (column offsets, division ranks) may need more tile slots
+    const size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
+    if (tiles > h->scan_tiles_cap) {
+      if (h->scan_state) CU(h, cudaFree(h->scan_state));
+      h->scan_state = nullptr;
+      const size_t cap = tiles + tiles / 4 + 256;
+      CU(h, cudaMalloc(&h->scan_state, cap * sizeof(unsigned long long)));
+      h->scan_tiles_cap = cap;
+    }
+  }
   size_t tiles_bound = h->scan_tiles_cap;
   uint64_t want = items ? (items + SCAN_TILE - 1) / SCAN_TILE : tiles_bound;
   CU(h, cudaMemsetAsync(h->scan_state, 0, std::min<uint64_t>(want, tiles_bound) * sizeof(unsigned long long),
@@ -223,6 +252,7 @@ int scan(bdm_ctx* h, uint32_t* data, uint64_t items, const uint32_t* n_dev) {
   const uint64_t cap = (uint64_t)h->sm_count * h->scan_blocks_per_sm;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
   k_scan<<<grid, SCAN_THREADS, 0, h->stream>>>(data, n_dev, items, h->scan_state, h->scan_ticket);
+  DBG(h, "k_scan");
   CU(h, cudaGetLastError());
   return BDM_OK;
 }
@@ -233,6 +263,7 @@ int compute_extents(bdm_ctx* h) {
   if (!h->ext_valid) {
     k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
     k_extents<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], n, h->grid.inv, h->ext);
+    DBG(h, "k_extents");
     CU(h, cudaGetLastError());
     h->launches += 2;
   }
@@ -291,20 +322,27 @@ int sort_into(bdm_ctx* h, uint32_t n) {
   init_device_info(h);
   const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
   k_col_reset<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols);
+  DBG(h, "k_col_reset");
   if (n > 0) k_col_ext<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
+  DBG(h, "k_col_ext");
   k_col_len<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols, h->coff);
+  DBG(h, "k_col_len");
   rc = scan(h, h->coff, nc + 1, nullptr);  // exclusive: coff[c] = table offset, coff[nc] = T
   if (rc) return rc;
   k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
+  DBG(h, "k_table_zero");
   if (n > 0) k_key_hist<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table);
+  DBG(h, "k_key_hist");
   rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
   if (rc) return rc;
   if (n > 0) {
     k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
+    DBG(h, "k_scatter");
     const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
     k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
                                            h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
                                            perm_hist ? h->hist[dst] : nullptr);
+    DBG(h, "k_place");
   }
   CU(h, cudaGetLastError());
   h->launches += n > 0 ? 8 : 4;
@@ -337,6 +375,7 @@ int grid_build(bdm_ctx* h) {
     k_flag_zero<<<h->sm_count * 4, 256, 0, h->stream>>>(h->hot, h->coff, h->grid.n_cols);
     k_mark_hot<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->hist[h->cur], (uint32_t)h->n, h->grid,
                                                          h->hot);
+    DBG(h, "k_mark_hot");
     CU(h, cudaGetLastError());
     h->launches += 2;
     h->skip_active = true;
@@ -373,6 +412,7 @@ int force_step(bdm_ctx* h, bool want_dp) {
                                                  h->skip_active ? h->hot : nullptr,
                                                  h->hist[0] ? h->hist[dst] : nullptr);
   CU(h, cudaGetLastError());
+  DBG(h, "k_force");
   h->launches += 2;
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
   // pointers (the kernel already captured its arguments) instead of copying.
@@ -383,8 +423,90 @@ int force_step(bdm_ctx* h, bool want_dp) {
   h->skip_active = false;
   h->ext_valid = true;
   h->state = State::Stepped;
-  if (want_dp) h->have_dp = true;
+  if (want_dp) {
+    h->have_dp = true;
+    h->n_dp = h->n;
+  }
   if (h->prm.flags & BDM_RECORD) h->have_record = true;
+  return BDM_OK;
+}
+
+// Reallocate every per-agent buffer of a single handle for new_cap agents, keeping the live data
+// (agents and ids of both buffers, displacements / statistics of the last step).
+template <typename T>
+int regrow(bdm_ctx* h, T** p, size_t keep, size_t new_count) {
+  if (!*p) return BDM_OK;
+  T* q = nullptr;
+  CU(h, cudaMalloc(&q, std::max<size_t>(new_count, 1) * sizeof(T)));
+  if (keep) CU(h, cudaMemcpyAsync(q, *p, keep * sizeof(T), cudaMemcpyDeviceToDevice, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  CU(h, cudaFree(*p));
+  *p = q;
+  return BDM_OK;
+}
+
+int grow_capacity(bdm_ctx* h, int64_t new_cap) {
+  if (new_cap <= h->cap) return BDM_OK;
+  if (new_cap >= (int64_t)0xffffffffll) return fail(h, BDM_ERANGE, "population would exceed 2^32 - 1 agents");
+  const size_t N = (size_t)new_cap, n = (size_t)h->n, nd = (size_t)h->n_dp;
+  const int oi = h->out_ids == h->id[0] ? 0 : (h->out_ids == h->id[1] ? 1 : -1);
+  int rc;
+  if ((rc = regrow(h, &h->ag[0], n, N)) || (rc = regrow(h, &h->ag[1], n, N)) || (rc = regrow(h, &h->agf, 0, N)) ||
+      (rc = regrow(h, &h->id[0], n, N)) || (rc = regrow(h, &h->id[1], n, N)) || (rc = regrow(h, &h->key, 0, N)) ||
+      (rc = regrow(h, &h->slot, 0, N)) || (rc = regrow(h, &h->tsrc, 0, N)) || (rc = regrow(h, &h->tid, 0, N)) ||
+      (rc = regrow(h, &h->tkey, 0, N)) || (rc = regrow(h, &h->dp, 3 * nd, 3 * N)) ||
+      (rc = regrow(h, &h->r_cand, nd, N)) || (rc = regrow(h, &h->r_nb, nd, N)) || (rc = regrow(h, &h->r_ct, nd, N)) ||
+      (rc = regrow(h, &h->r_branch, nd, N)) || (rc = regrow(h, &h->r_nbh, nd, N)) ||
+      (rc = regrow(h, &h->r_cth, nd, N)) || (rc = regrow(h, &h->hist[0], 0, N)) ||
+      (rc = regrow(h, &h->hist[1], 0, N)) || (rc = regrow(h, &h->gflag, 0, N + 1)))
+    return rc;
+  if (oi >= 0) h->out_ids = h->id[oi];
+  if (h->stage) {
+    CU(h, cudaFree(h->stage));
+    h->stage = nullptr;
+  }
+  h->cap = new_cap;
+  return BDM_OK;
+}
+
+// NEXT-2: growth + division after the mechanics of a step (G1-G3).
+int grow_divide_step(bdm_ctx* h) {
+  const uint32_t n = (uint32_t)h->n;
+  if (h->cap < 2 * h->n) {
+    int rc = grow_capacity(h, std::max<int64_t>(2 * h->n, h->cap + h->cap / 2));
+    if (rc) return rc;
+  }
+  if (!h->gflag) CU(h, cudaMalloc(&h->gflag, ((size_t)h->cap + 1) * sizeof(uint32_t)));
+  cudaStream_t s = h->stream;
+  const int cur = h->cur;  // stepped buffer, sorted order of the step, ids in id[cur]
+  k_grow<<<blocks(n, 256), 256, 0, s>>>(h->ag[cur], h->id[cur], n, h->growth, h->div_diam, h->gflag);
+  DBG(h, "k_grow");
+  CU(h, cudaMemsetAsync(h->gflag + n, 0, sizeof(uint32_t), s));
+  int rc = scan(h, h->gflag, (uint64_t)n + 1, nullptr);
+  if (rc) return rc;
+  CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), s));
+  k_divide<<<blocks(n, 256), 256, 0, s>>>(h->ag[cur], h->id[cur], n, h->div_diam, h->gseed, h->step_count, h->gflag,
+                                          h->maxd_bits);
+  DBG(h, "k_divide");
+  CU(h, cudaGetLastError());
+  h->launches += 3;
+  uint32_t* hostbuf = reinterpret_cast<uint32_t*>(h->ext_host);  // pinned scratch: total, then max D
+  CU(h, cudaMemcpyAsync(hostbuf, h->gflag + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+  CU(h, cudaMemcpyAsync(hostbuf + 2, h->maxd_bits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+  rc = check_async(h);
+  if (rc) return rc;
+  const uint32_t born = hostbuf[0];
+  double maxd;
+  std::memcpy(&maxd, hostbuf + 2, sizeof maxd);
+  h->n += born;
+  // O1 for the new population: the box edge follows the largest diameter
+  const double L = std::max(maxd, h->prm.box_edge_min);
+  h->grid.L = L;
+  h->grid.L2 = L * L;
+  h->grid.inv = 1.0 / (L * (1.0 + 0x1p-30));
+  h->grid.thr_pad = 0.5 * L;
+  h->ext_valid = false;  // extents were reduced with the old box edge
+  h->skip_valid = false;
   return BDM_OK;
 }
 
@@ -405,8 +527,8 @@ struct Scratch {
   }
 };
 
-int staging(bdm_ctx* h) {
-  if (!h->stage) return dalloc(h, &h->stage, 4 * (size_t)h->n);
+int staging(bdm_ctx* h) {  // sized for the capacity, so it stays valid while the population grows
+  if (!h->stage) return dalloc(h, &h->stage, 4 * (size_t)std::max(h->n, h->cap));
   return BDM_OK;
 }
 
@@ -418,6 +540,8 @@ int upload(bdm_ctx* h, const double* pos, const double* diam) {
   h->have_record = false;
   h->ext_valid = false;
   h->skip_valid = false;
+  h->step_count = 0;
+  h->n_dp = 0;
   h->state = State::NoGrid;
   h->have_grid = false;
   h->cur = 0;
@@ -490,7 +614,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -512,6 +636,7 @@ int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, 
   if (!h) return fail(nullptr, BDM_ENOMEM, "bdm_init: host allocation");
   h->prm = *p;
   h->n = n;
+  h->cap = n;
   int dev = p->device;
   if (dev < 0) {
     if (cudaGetDevice(&dev) != cudaSuccess) {
@@ -642,8 +767,39 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
     if (h->timing) CU(h, cudaEventRecord(ts.e1, h->stream));
     int rc = force_step(h, s == n_steps - 1);
     if (rc) return rc;
+    if (h->growth_on) {
+      rc = grow_divide_step(h);
+      if (rc) return rc;
+    }
+    ++h->step_count;
     if (h->timing) CU(h, cudaEventRecord(ts.e2, h->stream));
   }
+  return BDM_OK;
+}
+
+int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_growth: NULL handle");
+  if (h->slab) return fail(h, BDM_EINVAL, "bdm_set_growth: not available in slab mode");
+  if (!(growth >= 0.0) || !std::isfinite(growth) || !(div_diam > 0.0))
+    return fail(h, BDM_EINVAL, "bdm_set_growth: need growth >= 0 (finite) and div_diam > 0");
+  h->growth_on = std::isfinite(div_diam) || growth > 0.0;
+  h->growth = growth;
+  h->div_diam = div_diam;
+  h->gseed = seed;
+  return BDM_OK;
+}
+
+int bdm_reserve(bdm_handle h, int64_t capacity) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_reserve: NULL handle");
+  if (h->slab) return fail(h, BDM_EINVAL, "bdm_reserve: not available in slab mode");
+  CU(h, cudaSetDevice(h->device));
+  return grow_capacity(h, capacity);
+}
+
+int bdm_get_count(bdm_handle h, int64_t* out2) {
+  if (!h || !out2) return fail(h, BDM_EINVAL, "bdm_get_count: NULL argument");
+  out2[0] = h->n;
+  out2[1] = h->n_dp;
   return BDM_OK;
 }
 
@@ -680,10 +836,10 @@ int bdm_get_timing(bdm_handle h, double* out4) {
 int bdm_get_displacements(bdm_handle h, double* out) {
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_displacements: NULL handle");
   if (!h->have_dp) return fail(h, BDM_ESTATE, "bdm_get_displacements: no step has been run");
-  if (h->n == 0) return BDM_OK;
+  if (h->n_dp == 0) return BDM_OK;
   if (!out) return fail(h, BDM_EINVAL, "bdm_get_displacements: NULL output");
   CU(h, cudaSetDevice(h->device));
-  const uint32_t n = (uint32_t)h->n;
+  const uint32_t n = (uint32_t)h->n_dp;
   const size_t bytes = 3 * (size_t)n * sizeof(double);
   double* dst = out;
   if (!(h->prm.flags & BDM_DEVICE_PTRS)) {
@@ -714,6 +870,25 @@ int bdm_get_positions(bdm_handle h, double* out) {
   k_unpermute_pos<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, dst);
   CU(h, cudaGetLastError());
   if (dst != static_cast<void*>(out)) return copy_out(h, out, dst, bytes);
+  return BDM_OK;
+}
+
+int bdm_get_diameters(bdm_handle h, double* out) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_diameters: NULL handle");
+  if (h->n == 0) return BDM_OK;
+  if (!out) return fail(h, BDM_EINVAL, "bdm_get_diameters: NULL output");
+  CU(h, cudaSetDevice(h->device));
+  const uint32_t n = (uint32_t)h->n;
+  const size_t bytes = (size_t)n * sizeof(double);
+  double* dst = out;
+  if (!(h->prm.flags & BDM_DEVICE_PTRS)) {
+    int rc = staging(h);
+    if (rc) return rc;
+    dst = h->stage;
+  }
+  k_unpermute_diam<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, dst);
+  CU(h, cudaGetLastError());
+  if (dst != out) return copy_out(h, out, dst, bytes);
   return BDM_OK;
 }
 
@@ -761,9 +936,9 @@ int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out) {
   if (!h || !out) return fail(h, BDM_EINVAL, "bdm_get_agent_stats: NULL argument");
   if (!(h->prm.flags & BDM_RECORD) || !h->have_record)
     return fail(h, BDM_ESTATE, "bdm_get_agent_stats: needs BDM_RECORD at init and one step");
-  if (h->n == 0) return BDM_OK;
+  if (h->n_dp == 0 && h->n == 0) return BDM_OK;
   CU(h, cudaSetDevice(h->device));
-  const uint32_t n = (uint32_t)h->n;
+  const uint32_t n = (uint32_t)(h->n_dp ? h->n_dp : h->n);
   const uint32_t* ids = h->out_ids;
   const bool dev = h->prm.flags & BDM_DEVICE_PTRS;
   auto one = [&](auto* src, auto* dst) -> int {
@@ -999,6 +1174,7 @@ int bdm_slab_local_extents(bdm_handle h, int32_t* lohi6) {
   if (!h->ext_valid) {
     k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
     if (h->n > 0) k_extents<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], (uint32_t)h->n, h->grid.inv, h->ext);
+    DBG(h, "k_extents");
     CU(h, cudaGetLastError());
     h->ext_valid = true;
   }

@@ -1005,6 +1005,65 @@ __global__ void k_maxd(const double4* __restrict__ ag, uint32_t n, unsigned long
   if ((threadIdx.x & 31) == 0 && b && b > __ldcg(maxd_bits)) atomicMax(maxd_bits, b);
 }
 
+// ------------------------------------------------------------------------------------------ NEXT-2
+// Cell growth and division (G1-G3), after the mechanics of a step, on the stepped
+// buffer (sorted order of that step, ids alongside).  Daughters are appended behind the n agents
+// (unsorted; the next build sorts them).
+__global__ void k_grow(double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n, double growth,
+                       double div_diam, uint32_t* __restrict__ flag_by_id) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double D = ag[i].w + growth;  // G1
+  ag[i].w = D;
+  flag_by_id[ids[i]] = D >= div_diam ? 1u : 0u;
+}
+
+__device__ __forceinline__ double div_u01(uint64_t seed, uint64_t step, uint64_t id, uint64_t a) {
+  return (double)(mix64(seed * 0x9E3779B97F4A7C15ull + ((step << 32) + id) * 4ull + a) >> 11) * 0x1p-53;
+}
+
+// G2.  rank_by_id = exclusive scan of the division flags in id order, so the k-th divider in
+// ascending id order creates daughter id n + k at position n + k.  Also reduces the new max D (O1).
+__global__ void k_divide(double4* __restrict__ ag, uint32_t* __restrict__ ids, uint32_t n, double div_diam,
+                         uint64_t seed, uint64_t step, const uint32_t* __restrict__ rank_by_id,
+                         unsigned long long* maxd_bits) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  double Dfin = 0.0;
+  if (i < n) {
+    double4 p = ag[i];
+    Dfin = p.w;
+    if (p.w >= div_diam) {
+      const uint32_t id = ids[i];
+      const uint32_t d = n + rank_by_id[id];
+      double v[3], u[3];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) v[a] = 2.0 * div_u01(seed, step, id, (uint64_t)a) - 1.0;
+      const double norm = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+      if (norm == 0.0) {
+        u[0] = 1.0;
+        u[1] = 0.0;
+        u[2] = 0.0;
+      } else {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) u[a] = v[a] / norm;
+      }
+      const double Dd = p.w * 0.79370052598409973737585281963615;  // 2^(-1/3)
+      const double h = 0.5 * Dd;
+      const double ox = h * u[0], oy = h * u[1], oz = h * u[2];
+      ag[i] = make_double4(p.x - ox, p.y - oy, p.z - oz, Dd);
+      ag[d] = make_double4(p.x + ox, p.y + oy, p.z + oz, Dd);
+      ids[d] = d;
+      Dfin = Dd;
+    }
+  }
+  unsigned long long b = __double_as_longlong(Dfin);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(FULL, b, o);
+    b = v > b ? v : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b && b > __ldcg(maxd_bits)) atomicMax(maxd_bits, b);
+}
+
 // ------------------------------------------------------------------------------------------ K7
 __global__ void k_unpermute_pos(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
                                 double* __restrict__ out) {
@@ -1025,6 +1084,13 @@ __global__ void k_unpermute3(const double* __restrict__ v, const uint32_t* __res
   out[d] = v[3 * (size_t)i];
   out[d + 1] = v[3 * (size_t)i + 1];
   out[d + 2] = v[3 * (size_t)i + 2];
+}
+
+__global__ void k_unpermute_diam(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
+                                 double* __restrict__ out) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[ids[i]] = ag[i].w;
 }
 
 __global__ void k_box_coords(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
