@@ -34,6 +34,16 @@ class Growth(ctypes.Structure):
     _fields_ = [("growth", ctypes.c_double), ("div_diam", ctypes.c_double), ("seed", ctypes.c_uint64)]
 
 
+class Fields(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_double), ("origin", ctypes.c_double * 3), ("dims", ctypes.c_int32 * 3),
+                ("diff", ctypes.c_double), ("decay", ctypes.c_double), ("dt", ctypes.c_double),
+                ("secretion", ctypes.c_double), ("speed", ctypes.c_double)]
+
+
+def fields(h, origin, dims, diff, decay, dt, secretion, speed) -> "Fields":
+    return Fields(h, (ctypes.c_double * 3)(*origin), (ctypes.c_int32 * 3)(*dims), diff, decay, dt, secretion, speed)
+
+
 class Grid(ctypes.Structure):
     _fields_ = [("L", ctypes.c_double), ("L2", ctypes.c_double), ("inv", ctypes.c_double),
                 ("lo", ctypes.c_int64 * 3), ("hi", ctypes.c_int64 * 3)]
@@ -82,6 +92,13 @@ def lib():
         L.orc_run_growth.argtypes = [ctypes.c_int64, _f64p, _f64p, ctypes.POINTER(Params), ctypes.POINTER(Growth),
                                      ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, _f64p, ctypes.c_int]
         L.orc_run_growth.restype = ctypes.c_int64
+        _i8p = ctypes.POINTER(ctypes.c_int8)
+        L.orc_secrete.argtypes = [ctypes.c_int64, _f64p, _i8p, ctypes.POINTER(Fields), _f64p, _f64p]
+        L.orc_diffuse.argtypes = [ctypes.POINTER(Fields), _f64p, _f64p]
+        L.orc_gradient_at.argtypes = [ctypes.POINTER(Fields), _f64p, _f64p, _f64p]
+        L.orc_chemotaxis.argtypes = [ctypes.c_int64, _f64p, _i8p, ctypes.POINTER(Fields), _f64p, _f64p]
+        L.orc_run_soma.argtypes = [ctypes.c_int64, _f64p, _f64p, _i8p, ctypes.POINTER(Params), ctypes.POINTER(Fields),
+                                   _f64p, _f64p, ctypes.c_int32, _f64p, ctypes.c_int]
         L.orc_mix64.argtypes = [ctypes.c_uint64]
         L.orc_mix64.restype = ctypes.c_uint64
         _lib = L
@@ -234,3 +251,44 @@ def run_growth(pos, diam, n_steps, growth, div_diam, seed, prm=None, step0=0, ca
     if m < 0:
         raise OracleError(m)
     return P[:m].copy(), Dm[:m].copy(), dp
+
+
+_i8p = ctypes.POINTER(ctypes.c_int8)
+
+
+def diffuse(fp, c):
+    """S2 on a copy of field c (shape dims)."""
+    c = _c(c)
+    out = np.zeros_like(c)
+    lib().orc_diffuse(ctypes.byref(fp), _ptr(c), _ptr(out))
+    return out
+
+
+def secrete(fp, pos, types, c0, c1):
+    pos = _c(pos)
+    t = _c(types, np.int8)
+    c0, c1 = _c(c0).copy(), _c(c1).copy()
+    lib().orc_secrete(len(t), _ptr(pos), _ptr(t, _i8p), ctypes.byref(fp), _ptr(c0), _ptr(c1))
+    return c0, c1
+
+
+def gradient_at(fp, c, p):
+    c, p = _c(c), _c(p)
+    g = np.zeros(3)
+    lib().orc_gradient_at(ctypes.byref(fp), _ptr(c), _ptr(p), _ptr(g))
+    return g
+
+
+def run_soma(pos, diam, types, fp, n_steps, c0=None, c1=None, prm=None):
+    """n_steps of S1-S4.  Returns (pos, c0, c1, dp of the last mechanics)."""
+    pos, diam = _c(pos).copy(), _c(diam)
+    t = _c(types, np.int8)
+    dims = tuple(fp.dims)
+    c0 = np.zeros(dims) if c0 is None else _c(c0).copy()
+    c1 = np.zeros(dims) if c1 is None else _c(c1).copy()
+    dp = np.zeros_like(pos)
+    rc = lib().orc_run_soma(len(diam), _ptr(pos), _ptr(diam), _ptr(t, _i8p), ctypes.byref(prm or params()),
+                            ctypes.byref(fp), _ptr(c0), _ptr(c1), n_steps, _ptr(dp), 0)
+    if rc:
+        raise OracleError(rc)
+    return pos, c0, c1, dp

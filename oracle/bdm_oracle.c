@@ -532,3 +532,146 @@ int64_t orc_run_growth(int64_t n, double* pos, double* diam, const orc_params* p
   free(tmp);
   return n;
 }
+
+/* ------------------------------------------------------------------------------------------------
+ * NEXT-3: soma clustering (readings S1-S5).  PAPER.md:711-712, 773 (the "soma
+ * clustering" GPU benchmark: two cell types, each secreting its own substance and moving up its
+ * gradient); SPEC.md:260-329 (diffusion-field: explicit Euler, 7-point stencil, closed boundary,
+ * trilinear sampling, central-difference gradients), SPEC.md:477 (soma_clustering benchmark).
+ *   S1 secretion  every agent of type t adds `secretion` to the node nearest to it in field t:
+ *                 node_a = clamp(floor((p_a - origin_a) * (1/h) + 0.5), 0, dims_a - 1);
+ *                 c[node] += count(node) * secretion  (one multiply per node)
+ *   S2 diffusion  c' = c + dt * (D * lap - mu * c), lap = (((xm + xp) + (ym + yp)) + (zm + zp) - 6c) * (1/h^2),
+ *                 closed boundary: a missing neighbour is the node itself; both fields
+ *   S3 chemotaxis g = grad c_t(p): central differences (g_a = (c[+1] - c[-1]) * (0.5/h), one-sided
+ *                 (c[+1]-c[0])/h or (c[0]-c[-1])/h on the boundary layers) at the 8 nodes of the cell
+ *                 containing p, trilinearly interpolated (weights clamped to the lattice);
+ *                 p <- p + speed * g / |g| (no move if |g| == 0)
+ *   S4 mechanics  O1-O7 on the moved agents
+ * ---------------------------------------------------------------------------------------------- */
+typedef struct {
+  double h, origin[3];
+  int32_t dims[3];
+  double diff, decay, dt, secretion, speed;
+} orc_fields;
+
+static int64_t fidx(const orc_fields* f, int64_t x, int64_t y, int64_t z) {
+  return (x * f->dims[1] + y) * f->dims[2] + z;
+}
+
+static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+void orc_secrete(int64_t n, const double* pos, const int8_t* type, const orc_fields* f, double* c0, double* c1) {
+  int64_t nn = (int64_t)f->dims[0] * f->dims[1] * f->dims[2];
+  uint32_t* cnt = (uint32_t*)calloc((size_t)(2 * nn), sizeof(uint32_t));
+  double invh = 1.0 / f->h;
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t b[3];
+    for (int a = 0; a < 3; ++a)
+      b[a] = clampi((int64_t)floor((pos[3 * i + a] - f->origin[a]) * invh + 0.5), 0, f->dims[a] - 1);
+    cnt[(type[i] ? nn : 0) + fidx(f, b[0], b[1], b[2])] += 1;
+  }
+  for (int64_t k = 0; k < nn; ++k) {
+    if (cnt[k]) c0[k] = c0[k] + (double)cnt[k] * f->secretion;
+    if (cnt[nn + k]) c1[k] = c1[k] + (double)cnt[nn + k] * f->secretion;
+  }
+  free(cnt);
+}
+
+void orc_diffuse(const orc_fields* f, const double* c, double* out) {
+  double ih2 = 1.0 / (f->h * f->h);
+  for (int64_t x = 0; x < f->dims[0]; ++x)
+    for (int64_t y = 0; y < f->dims[1]; ++y)
+      for (int64_t z = 0; z < f->dims[2]; ++z) {
+        double c0 = c[fidx(f, x, y, z)];
+        double xm = c[fidx(f, x > 0 ? x - 1 : x, y, z)], xp = c[fidx(f, x + 1 < f->dims[0] ? x + 1 : x, y, z)];
+        double ym = c[fidx(f, x, y > 0 ? y - 1 : y, z)], yp = c[fidx(f, x, y + 1 < f->dims[1] ? y + 1 : y, z)];
+        double zm = c[fidx(f, x, y, z > 0 ? z - 1 : z)], zp = c[fidx(f, x, y, z + 1 < f->dims[2] ? z + 1 : z)];
+        double lap = ((((xm + xp) + (ym + yp)) + (zm + zp)) - 6.0 * c0) * ih2;
+        out[fidx(f, x, y, z)] = c0 + f->dt * (f->diff * lap - f->decay * c0);
+      }
+}
+
+/* central-difference gradient component a at node (x,y,z), one-sided on the boundary layers */
+static double node_grad(const orc_fields* f, const double* c, int64_t x, int64_t y, int64_t z, int a) {
+  int64_t v[3] = {x, y, z};
+  int64_t lo[3] = {x, y, z}, hi[3] = {x, y, z};
+  if (v[a] > 0) lo[a] = v[a] - 1;
+  if (v[a] + 1 < f->dims[a]) hi[a] = v[a] + 1;
+  double cl = c[fidx(f, lo[0], lo[1], lo[2])], ch = c[fidx(f, hi[0], hi[1], hi[2])];
+  if (lo[a] == v[a] && hi[a] == v[a]) return 0.0;
+  if (lo[a] == v[a] || hi[a] == v[a]) return (ch - cl) * (1.0 / f->h);
+  return (ch - cl) * (0.5 / f->h);
+}
+
+void orc_gradient_at(const orc_fields* f, const double* c, const double* p, double* g) {
+  double invh = 1.0 / f->h;
+  int64_t b[3];
+  double w[3];
+  for (int a = 0; a < 3; ++a) {
+    double q = (p[a] - f->origin[a]) * invh;
+    double fl = floor(q);
+    int64_t i0 = (int64_t)fl;
+    double t = q - fl;
+    if (i0 < 0) {
+      i0 = 0;
+      t = 0.0;
+    }
+    if (i0 > f->dims[a] - 2) {
+      i0 = f->dims[a] - 2 >= 0 ? f->dims[a] - 2 : 0;
+      t = f->dims[a] >= 2 ? 1.0 : 0.0;
+    }
+    b[a] = i0;
+    w[a] = t;
+  }
+  for (int a = 0; a < 3; ++a) {
+    double acc = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
+      int64_t x = b[0] + dx, y = b[1] + dy, z = b[2] + dz;
+      if (x >= f->dims[0]) x = f->dims[0] - 1;
+      if (y >= f->dims[1]) y = f->dims[1] - 1;
+      if (z >= f->dims[2]) z = f->dims[2] - 1;
+      double wk = (dx ? w[0] : 1.0 - w[0]) * (dy ? w[1] : 1.0 - w[1]);
+      wk = wk * (dz ? w[2] : 1.0 - w[2]);
+      acc = acc + wk * node_grad(f, c, x, y, z, a);
+    }
+    g[a] = acc;
+  }
+}
+
+void orc_chemotaxis(int64_t n, double* pos, const int8_t* type, const orc_fields* f, const double* c0,
+                    const double* c1) {
+  for (int64_t i = 0; i < n; ++i) {
+    double g[3];
+    orc_gradient_at(f, type[i] ? c1 : c0, pos + 3 * i, g);
+    double gn = sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2]);
+    if (!(gn > 0.0)) continue;
+    double sc = f->speed / gn;
+    for (int a = 0; a < 3; ++a) pos[3 * i + a] = pos[3 * i + a] + g[a] * sc;
+  }
+}
+
+/* n_steps of S1-S4; c0/c1 are updated in place (scratch allocated here). */
+int orc_run_soma(int64_t n, double* pos, const double* diam, const int8_t* type, const orc_params* p,
+                 const orc_fields* f, double* c0, double* c1, int32_t n_steps, double* dp, int nthreads) {
+  int64_t nn = (int64_t)f->dims[0] * f->dims[1] * f->dims[2];
+  double* tmp = (double*)malloc(sizeof(double) * (size_t)(nn > 3 * n ? nn : 3 * n + 1));
+  if (!tmp) return ORC_ENOMEM;
+  for (int32_t s = 0; s < n_steps; ++s) {
+    orc_secrete(n, pos, type, f, c0, c1);
+    orc_diffuse(f, c0, tmp);
+    memcpy(c0, tmp, sizeof(double) * nn);
+    orc_diffuse(f, c1, tmp);
+    memcpy(c1, tmp, sizeof(double) * nn);
+    orc_chemotaxis(n, pos, type, f, c0, c1);
+    int rc = orc_step(n, pos, diam, p, dp, tmp, NULL, nthreads);
+    if (rc) {
+      free(tmp);
+      return rc;
+    }
+    memcpy(pos, tmp, sizeof(double) * 3 * n);
+  }
+  free(tmp);
+  return ORC_OK;
+}
