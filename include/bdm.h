@@ -146,6 +146,30 @@ int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_
  * grows (capacity doubles as needed); displacements refer to the agents of the last mechanics. */
 int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed);
 
+/* NEXT-3, soma clustering ("soma clustering" benchmark;
+ * SPEC.md:260-329 diffusion-field).  Two substances on a lattice of dims nodes at spacing h from
+ * origin (node (i,j,k) at origin + h*(i,j,k)), closed boundary.  Every later step, before the
+ * mechanics: agents of type t add `secretion` to their nearest node of field t; both fields take one
+ * explicit-Euler step c += dt*(diff*lap(c) - decay*c) (7-point stencil; needs diff*dt/h^2 <= 1/6,
+ * else EINVAL); every agent moves `speed` along the normalised gradient of its own field. */
+typedef struct {
+  double h;         /* lattice spacing, um */
+  double origin[3]; /* position of node (0,0,0), um */
+  int32_t dims[3];  /* nodes per axis */
+  double diff;      /* diffusion coefficient, um^2/step */
+  double decay;     /* decay rate, 1/step */
+  double dt;        /* time step of the diffusion update */
+  double secretion; /* amount added per agent per step */
+  double speed;     /* chemotaxis displacement per step, um */
+} bdm_field_params;
+
+/* Enable the soma-clustering operations; types: n int8 (0 or 1) in id order (host or device per
+ * BDM_DEVICE_PTRS).  Both fields start at 0. */
+int bdm_set_fields(bdm_handle h, const bdm_field_params* fp, const int8_t* types);
+
+/* Field `which` (0 or 1), dims[0]*dims[1]*dims[2] fp64 with z fastest. */
+int bdm_get_field(bdm_handle h, int which, double* out);
+
 /* Make room for `capacity` agents (dynamic populations).  Never shrinks. */
 int bdm_reserve(bdm_handle h, int64_t capacity);
 

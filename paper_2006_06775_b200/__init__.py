@@ -60,6 +60,12 @@ class bdm_grid_info(ctypes.Structure):
                 ("n_agents", ctypes.c_int64)]
 
 
+class bdm_field_params(ctypes.Structure):
+    _fields_ = [("h", ctypes.c_double), ("origin", ctypes.c_double * 3), ("dims", ctypes.c_int32 * 3),
+                ("diff", ctypes.c_double), ("decay", ctypes.c_double), ("dt", ctypes.c_double),
+                ("secretion", ctypes.c_double), ("speed", ctypes.c_double)]
+
+
 class bdm_agent_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("n_cand", "n_nb", "n_ct", "branch", "nb_hash", "ct_hash")]
 
@@ -82,6 +88,8 @@ _SIGS = {
     "bdm_get_skip_stats": ([_vp, _vp], ctypes.c_int),
     "bdm_set_growth": ([_vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
     "bdm_reserve": ([_vp, ctypes.c_int64], ctypes.c_int),
+    "bdm_set_fields": ([_vp, ctypes.POINTER(bdm_field_params), _vp], ctypes.c_int),
+    "bdm_get_field": ([_vp, ctypes.c_int, _vp], ctypes.c_int),
     "bdm_get_count": ([_vp, _vp], ctypes.c_int),
     "bdm_set_stream": ([_vp, _vp], ctypes.c_int),
     "bdm_sync": ([_vp], ctypes.c_int),
@@ -257,6 +265,29 @@ def bdm_get_count(h: Handle):
 
 def bdm_set_growth(h: Handle, growth: float, div_diam: float, seed: int = 0) -> None:
     _check(load_library().bdm_set_growth(h.raw, growth, div_diam, seed), h.raw)
+
+
+def bdm_set_fields(h: Handle, h_spacing: float, origin, dims, diff: float, decay: float, dt: float,
+                   secretion: float, speed: float, types) -> None:
+    """Soma clustering (NEXT-3): two substance lattices + chemotaxis before each mechanics step."""
+    fp = bdm_field_params(h_spacing, (ctypes.c_double * 3)(*origin), (ctypes.c_int32 * 3)(*dims), diff, decay, dt,
+                          secretion, speed)
+    if not h.device_ptrs:
+        types = np.ascontiguousarray(types, dtype=np.int8)
+    h.field_dims = tuple(int(d) for d in dims)
+    _check(load_library().bdm_set_fields(h.raw, ctypes.byref(fp), _ptr(types)), h.raw)
+
+
+def bdm_get_field(h: Handle, which: int, out=None):
+    if out is None:
+        if h.device_ptrs:
+            import torch
+
+            out = torch.empty(h.field_dims, dtype=torch.float64, device="cuda")
+        else:
+            out = np.empty(h.field_dims, np.float64)
+    _check(load_library().bdm_get_field(h.raw, which, _ptr(out)), h.raw)
+    return out
 
 
 def bdm_reserve(h: Handle, capacity: int) -> None:

@@ -91,6 +91,13 @@ struct bdm_ctx {
   uint64_t gseed = 0;
   uint64_t step_count = 0;   // mechanics steps since init / set_agents (division hash)
   uint32_t* gflag = nullptr;  // id-indexed division flags -> ranks (cap + 1)
+  // soma clustering (NEXT-3): two substance fields on a lattice, agent types by id
+  bool fields_on = false;
+  FieldDev fd{};
+  double* field[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [substance][buffer]
+  int fcur = 0;
+  uint32_t* fcnt = nullptr;  // 2 x nn secretion counts
+  int8_t* type_by_id = nullptr;
   // stationary-region skip (BDM_SKIP_STATIONARY, NEXT-1)
   unsigned long long* hist[2] = {nullptr, nullptr};
   uint8_t* hot = nullptr;  // one hot flag per box-table entry
@@ -469,6 +476,35 @@ int grow_capacity(bdm_ctx* h, int64_t new_cap) {
   return BDM_OK;
 }
 
+// NEXT-3: secretion + diffusion of both substances, then chemotaxis of every agent (S1-S3,
+// DESIGN.md §12), on the current positions before the step's grid build.
+int fields_step(bdm_ctx* h) {
+  const uint32_t n = (uint32_t)h->n;
+  cudaStream_t s = h->stream;
+  const FieldDev& f = h->fd;
+  CU(h, cudaMemsetAsync(h->fcnt, 0, 2 * (size_t)f.nn * sizeof(uint32_t), s));
+  if (n) k_secrete<<<blocks(n, 256), 256, 0, s>>>(h->ag[h->cur], h->id[h->cur], n, h->type_by_id, f, h->fcnt);
+  DBG(h, "k_secrete");
+  const int src = h->fcur, dst = 1 - h->fcur;
+  for (int t = 0; t < 2; ++t) {
+    k_diffuse<<<blocks(f.nn, 256), 256, 0, s>>>(h->field[t][src], h->fcnt + (size_t)t * f.nn, h->field[t][dst], f);
+    DBG(h, "k_diffuse");
+  }
+  h->fcur = dst;
+  if (n) {
+    k_chemotaxis<<<blocks(n, 256), 256, 0, s>>>(h->ag[h->cur], h->id[h->cur], n, h->type_by_id, f, h->field[0][dst],
+                                                h->field[1][dst]);
+    DBG(h, "k_chemotaxis");
+  }
+  CU(h, cudaGetLastError());
+  h->launches += 3 + (n ? 2 : 0);
+  // the agents moved: new extents and a fresh grid are needed
+  h->ext_valid = false;
+  h->skip_valid = false;
+  if (h->state == State::Fresh) h->state = State::Stepped;
+  return BDM_OK;
+}
+
 // NEXT-2: growth + division after the mechanics of a step (G1-G3).
 int grow_divide_step(bdm_ctx* h) {
   const uint32_t n = (uint32_t)h->n;
@@ -614,7 +650,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -760,6 +796,10 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
       h->timed.push_back(ts);
       CU(h, cudaEventRecord(ts.e0, h->stream));
     }
+    if (h->fields_on) {
+      int rc = fields_step(h);
+      if (rc) return rc;
+    }
     if (h->state != State::Fresh) {
       int rc = grid_build(h);
       if (rc) return rc;
@@ -779,7 +819,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
 
 int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed) {
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_growth: NULL handle");
-  if (h->slab) return fail(h, BDM_EINVAL, "bdm_set_growth: not available in slab mode");
+  if (h->slab || h->fields_on) return fail(h, BDM_EINVAL, "bdm_set_growth: not available with slabs or fields");
   if (!(growth >= 0.0) || !std::isfinite(growth) || !(div_diam > 0.0))
     return fail(h, BDM_EINVAL, "bdm_set_growth: need growth >= 0 (finite) and div_diam > 0");
   h->growth_on = std::isfinite(div_diam) || growth > 0.0;
@@ -787,6 +827,69 @@ int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed) 
   h->div_diam = div_diam;
   h->gseed = seed;
   return BDM_OK;
+}
+
+int bdm_set_fields(bdm_handle h, const bdm_field_params* fp, const int8_t* types) {
+  if (!h || !fp) return fail(h, BDM_EINVAL, "bdm_set_fields: NULL argument");
+  if (h->slab || h->growth_on) return fail(h, BDM_EINVAL, "bdm_set_fields: not available with slabs or growth");
+  const double h_ = fp->h;
+  if (!(h_ > 0.0) || !std::isfinite(h_) || fp->dims[0] < 1 || fp->dims[1] < 1 || fp->dims[2] < 1 ||
+      !(fp->diff >= 0.0) || !(fp->decay >= 0.0) || !(fp->dt >= 0.0) || !std::isfinite(fp->secretion) ||
+      !(fp->speed >= 0.0) || !std::isfinite(fp->speed))
+    return fail(h, BDM_EINVAL, "bdm_set_fields: bad field parameters");
+  if (fp->diff * fp->dt / (h_ * h_) > 1.0 / 6.0)
+    return fail(h, BDM_EINVAL, "bdm_set_fields: explicit Euler unstable, need D dt / h^2 <= 1/6 (SPEC.md:266), got %g",
+                fp->diff * fp->dt / (h_ * h_));
+  const uint64_t nn = (uint64_t)fp->dims[0] * fp->dims[1] * fp->dims[2];
+  if (2 * nn >= 0xffffffffull) return fail(h, BDM_ERANGE, "bdm_set_fields: lattice too large");
+  if (h->n > 0 && !types) return fail(h, BDM_EINVAL, "bdm_set_fields: NULL types");
+  CU(h, cudaSetDevice(h->device));
+  FieldDev& f = h->fd;
+  f.h = h_;
+  f.invh = 1.0 / h_;
+  f.ih2 = 1.0 / (h_ * h_);
+  f.gh1 = 1.0 / h_;
+  f.gh2 = 0.5 / h_;
+  f.ox = fp->origin[0];
+  f.oy = fp->origin[1];
+  f.oz = fp->origin[2];
+  f.nx = fp->dims[0];
+  f.ny = fp->dims[1];
+  f.nz = fp->dims[2];
+  f.nn = (uint32_t)nn;
+  f.diff = fp->diff;
+  f.decay = fp->decay;
+  f.dt = fp->dt;
+  f.secretion = fp->secretion;
+  f.speed = fp->speed;
+  for (int t = 0; t < 2; ++t)
+    for (int b = 0; b < 2; ++b) {
+      if (h->field[t][b]) CU(h, cudaFree(h->field[t][b]));
+      CU(h, cudaMalloc(&h->field[t][b], nn * sizeof(double)));
+      CU(h, cudaMemsetAsync(h->field[t][b], 0, nn * sizeof(double), h->stream));
+    }
+  h->fcur = 0;
+  if (h->fcnt) CU(h, cudaFree(h->fcnt));
+  CU(h, cudaMalloc(&h->fcnt, 2 * nn * sizeof(uint32_t)));
+  if (h->type_by_id) CU(h, cudaFree(h->type_by_id));
+  CU(h, cudaMalloc(&h->type_by_id, std::max<size_t>(1, (size_t)h->n)));
+  if (h->n > 0)
+    CU(h, cudaMemcpyAsync(h->type_by_id, types, (size_t)h->n,
+                          (h->prm.flags & BDM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                          h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  h->fields_on = true;
+  return BDM_OK;
+}
+
+int bdm_get_field(bdm_handle h, int which, double* out) {
+  if (!h || !out || (which != 0 && which != 1)) return fail(h, BDM_EINVAL, "bdm_get_field: bad arguments");
+  if (!h->fields_on) return fail(h, BDM_ESTATE, "bdm_get_field: no fields (bdm_set_fields)");
+  CU(h, cudaSetDevice(h->device));
+  const size_t bytes = (size_t)h->fd.nn * sizeof(double);
+  CU(h, cudaMemcpyAsync(out, h->field[which][h->fcur], bytes,
+                        (h->prm.flags & BDM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  return check_async(h);
 }
 
 int bdm_reserve(bdm_handle h, int64_t capacity) {

@@ -1064,6 +1064,124 @@ __global__ void k_divide(double4* __restrict__ ag, uint32_t* __restrict__ ids, u
   if ((threadIdx.x & 31) == 0 && b && b > __ldcg(maxd_bits)) atomicMax(maxd_bits, b);
 }
 
+// ------------------------------------------------------------------------------------------ NEXT-3
+// Soma clustering (S1-S4): two substances on a regular lattice, secreted by the
+// agents of their type, diffused by explicit Euler with the 7-point stencil (closed boundary), and
+// followed by chemotaxis before the mechanics.  Arithmetic written exactly as the oracle's.
+struct FieldDev {
+  double h, invh, ih2, gh1, gh2;  // h, 1/h, 1/(h*h), 1/h (one-sided), 0.5/h (central)
+  double ox, oy, oz;
+  int32_t nx, ny, nz;
+  uint32_t nn;
+  double diff, decay, dt, secretion, speed;
+};
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// S1: integer count of secreting agents per nearest node (warp-aggregated atomics)
+__global__ void k_secrete(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
+                          const int8_t* __restrict__ type_by_id, FieldDev f, uint32_t* __restrict__ counts) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t k = 0xffffffffu;
+  if (i < n) {
+    const double4 p = ag[i];
+    const int bx = clampi((int)floor((p.x - f.ox) * f.invh + 0.5), 0, f.nx - 1);
+    const int by = clampi((int)floor((p.y - f.oy) * f.invh + 0.5), 0, f.ny - 1);
+    const int bz = clampi((int)floor((p.z - f.oz) * f.invh + 0.5), 0, f.nz - 1);
+    k = (type_by_id[ids[i]] ? f.nn : 0u) + ((uint32_t)bx * f.ny + by) * f.nz + bz;
+  }
+  const unsigned peers = __match_any_sync(FULL, k);
+  if (i < n && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&counts[k], (uint32_t)__popc(peers));
+}
+
+__device__ __forceinline__ double secreted(const double* __restrict__ c, const uint32_t* __restrict__ cnt,
+                                           uint32_t k, double s) {
+  const uint32_t m = cnt[k];
+  const double v = c[k];
+  return m ? v + (double)m * s : v;
+}
+
+// S1 + S2 fused: every stencil value is the secreted value of that node (c + count * s).  One
+// thread per node, z fastest (coalesced); neighbours come from L1/L2.
+__global__ void k_diffuse(const double* __restrict__ c, const uint32_t* __restrict__ cnt, double* __restrict__ out,
+                          FieldDev f) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= f.nn) return;
+  const int z = (int)(k % (uint32_t)f.nz);
+  const int y = (int)((k / (uint32_t)f.nz) % (uint32_t)f.ny);
+  const int x = (int)(k / ((uint32_t)f.nz * (uint32_t)f.ny));
+  const uint32_t sx = (uint32_t)f.ny * f.nz, sy = (uint32_t)f.nz;
+  const double s = f.secretion;
+  const double c0 = secreted(c, cnt, k, s);
+  const double xm = secreted(c, cnt, x > 0 ? k - sx : k, s), xp = secreted(c, cnt, x + 1 < f.nx ? k + sx : k, s);
+  const double ym = secreted(c, cnt, y > 0 ? k - sy : k, s), yp = secreted(c, cnt, y + 1 < f.ny ? k + sy : k, s);
+  const double zm = secreted(c, cnt, z > 0 ? k - 1 : k, s), zp = secreted(c, cnt, z + 1 < f.nz ? k + 1 : k, s);
+  const double lap = ((((xm + xp) + (ym + yp)) + (zm + zp)) - 6.0 * c0) * f.ih2;
+  out[k] = c0 + f.dt * (f.diff * lap - f.decay * c0);
+}
+
+__device__ __forceinline__ double node_grad(const double* __restrict__ c, const FieldDev& f, int x, int y, int z,
+                                            int a) {
+  int v[3] = {x, y, z}, lo[3] = {x, y, z}, hi[3] = {x, y, z};
+  const int dim[3] = {f.nx, f.ny, f.nz};
+  if (v[a] > 0) lo[a] = v[a] - 1;
+  if (v[a] + 1 < dim[a]) hi[a] = v[a] + 1;
+  if (lo[a] == v[a] && hi[a] == v[a]) return 0.0;
+  const double cl = c[((uint32_t)lo[0] * f.ny + lo[1]) * f.nz + lo[2]];
+  const double ch = c[((uint32_t)hi[0] * f.ny + hi[1]) * f.nz + hi[2]];
+  if (lo[a] == v[a] || hi[a] == v[a]) return (ch - cl) * f.gh1;
+  return (ch - cl) * f.gh2;
+}
+
+// S3: gradient of the own substance at p (trilinear interpolation of node gradients), then
+// p <- p + speed * g / |g|.  In place on the agents.
+__global__ void k_chemotaxis(double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
+                             const int8_t* __restrict__ type_by_id, FieldDev f, const double* __restrict__ c0,
+                             const double* __restrict__ c1) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double4 p = ag[i];
+  const double* c = type_by_id[ids[i]] ? c1 : c0;
+  const double pp[3] = {p.x, p.y, p.z}, org[3] = {f.ox, f.oy, f.oz};
+  const int dim[3] = {f.nx, f.ny, f.nz};
+  int b[3];
+  double w[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double q = (pp[a] - org[a]) * f.invh;
+    const double fl = floor(q);
+    int i0 = (int)fl;
+    double t = q - fl;
+    if (i0 < 0) {
+      i0 = 0;
+      t = 0.0;
+    }
+    if (i0 > dim[a] - 2) {
+      i0 = dim[a] - 2 >= 0 ? dim[a] - 2 : 0;
+      t = dim[a] >= 2 ? 1.0 : 0.0;
+    }
+    b[a] = i0;
+    w[a] = t;
+  }
+  double g[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    double acc = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      const int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
+      const int x = min(b[0] + dx, f.nx - 1), y = min(b[1] + dy, f.ny - 1), z = min(b[2] + dz, f.nz - 1);
+      double wk = (dx ? w[0] : 1.0 - w[0]) * (dy ? w[1] : 1.0 - w[1]);
+      wk = wk * (dz ? w[2] : 1.0 - w[2]);
+      acc = acc + wk * node_grad(c, f, x, y, z, a);
+    }
+    g[a] = acc;
+  }
+  const double gn = sqrt((g[0] * g[0] + g[1] * g[1]) + g[2] * g[2]);
+  if (!(gn > 0.0)) return;
+  const double sc = f.speed / gn;
+  ag[i] = make_double4(p.x + g[0] * sc, p.y + g[1] * sc, p.z + g[2] * sc, p.w);
+}
+
 // ------------------------------------------------------------------------------------------ K7
 __global__ void k_unpermute_pos(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
                                 double* __restrict__ out) {
