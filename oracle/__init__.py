@@ -99,6 +99,9 @@ def lib():
         L.orc_chemotaxis.argtypes = [ctypes.c_int64, _f64p, _i8p, ctypes.POINTER(Fields), _f64p, _f64p]
         L.orc_run_soma.argtypes = [ctypes.c_int64, _f64p, _f64p, _i8p, ctypes.POINTER(Params), ctypes.POINTER(Fields),
                                    _f64p, _f64p, ctypes.c_int32, _f64p, ctypes.c_int]
+        L.orc_neurite_step.argtypes = [ctypes.c_int64, _f64p, _f64p, ctypes.c_int64, _f64p, _f64p, _f64p, _f64p,
+                                       _i64p, _i64p, _i64p, ctypes.POINTER(Params), ctypes.POINTER(ctypes.c_double),
+                                       _f64p, _f64p]
         L.orc_mix64.argtypes = [ctypes.c_uint64]
         L.orc_mix64.restype = ctypes.c_uint64
         _lib = L
@@ -292,3 +295,20 @@ def run_soma(pos, diam, types, fp, n_steps, c0=None, c1=None, prm=None):
     if rc:
         raise OracleError(rc)
     return pos, c0, c1, dp
+
+
+def neurite_step(pos, diam, Q, de, l0, anchor, mother, c1, c2, k_spring, prm=None, steps=1):
+    """NEXT-4 (N1-N6): spheres + neurite elements, `steps` Jacobi steps.  Returns (pos, Q, dp, dQ)."""
+    pos, diam = _c(pos).copy(), _c(diam)
+    Q, de, l0, A = _c(Q).copy(), _c(de), _c(l0), _c(anchor)
+    m, a1, a2 = _c(mother, np.int64), _c(c1, np.int64), _c(c2, np.int64)
+    dp = np.zeros_like(pos)
+    dQ = np.zeros_like(Q)
+    ks = ctypes.c_double(k_spring)
+    for _ in range(steps):
+        rc = lib().orc_neurite_step(len(diam), _ptr(pos), _ptr(diam), len(de), _ptr(Q), _ptr(de), _ptr(l0), _ptr(A),
+                                    _ptr(m, _i64p), _ptr(a1, _i64p), _ptr(a2, _i64p), ctypes.byref(prm or params()),
+                                    ctypes.byref(ks), _ptr(dp), _ptr(dQ))
+        if rc:
+            raise OracleError(rc)
+    return pos, Q, dp, dQ

@@ -675,3 +675,183 @@ int orc_run_soma(int64_t n, double* pos, const double* diam, const int8_t* type,
   free(tmp);
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------------------------------------------
+ * NEXT-4: neurite elements (cylinders) -- sphere-cylinder contacts and spring chains (DESIGN.md §13,
+ * readings N1-N6).  PAPER.md:402-415 (§2.2 "approximated as a spring with a point mass on its distal
+ * end ... springs are connected to each other to transmit forces along the chain")
+ * (the paper's GPU kernel lacks cylinders); SPEC.md:230-238 (sphere_cylinder_force: closest point on
+ * the axis segment, then the sphere law; reaction on the distal point mass)
+ * (neurite_mechanics_op: axial spring force k_s (actual - resting)/resting).
+ *   N1 element e: distal point Q_e, diameter d_e, resting length l0_e, mother m_e (-1: root with
+ *      fixed proximal anchor A_e), daughters c1_e, c2_e; P_e = Q_{m_e} or A_e; v = Q - P;
+ *      len = sqrt((vx*vx + vy*vy) + vz*vz); centre C_e = P + 0.5*v
+ *   N2 box edge L = max(max_s D_s, max_e (len_e + d_e), box_edge_min), one frame for both grids
+ *   N3 spring: T_e = k_s * ((len - l0)/l0); u = v * (1/len); on Q_e: -T_e*u; on Q_{m_e}: +T_e*u
+ *   N4 sphere-cylinder: t = clamp(((c-P).v)/(v.v), 0, 1) (v.v = 0: t = 0); X = P + t*v; w = c - X;
+ *      d2 = (wx*wx + wy*wy) + wz*wz; d = sqrt(d2); delta = (r_s + r_e) - d; contact iff delta > 0 and
+ *      d2 > 0; r = (r_s*r_e)/(r_s + r_e); f = k*delta - gamma*sqrt(r*delta); on the sphere (f/d)*w,
+ *      on Q_e the reaction -(f/d)*w
+ *   N5 sums: sphere: sphere-sphere sum (O5), then element terms over the 27 element boxes around its
+ *      box in (dx,dy,dz) order, ascending element id.  Distal point Q_e: -T_e*u_e, then +T_c*u_c for
+ *      daughters c in ascending id, then sphere reactions over the 27 sphere boxes around box(C_e),
+ *      ascending sphere id
+ *   N6 displacement O6 for spheres and distal points alike; p' = p + dp, Q' = Q + dQ (Jacobi)
+ * ---------------------------------------------------------------------------------------------- */
+typedef struct {
+  double k_spring;
+} orc_neurite;
+
+static void el_geom(int64_t e, const double* Q, const double* A, const int64_t* mother, double* P, double* v,
+                    double* len, double* C) {
+  const double* pp = mother[e] >= 0 ? Q + 3 * mother[e] : A + 3 * e;
+  for (int a = 0; a < 3; ++a) {
+    P[a] = pp[a];
+    v[a] = Q[3 * e + a] - pp[a];
+  }
+  *len = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+  for (int a = 0; a < 3; ++a) C[a] = P[a] + 0.5 * v[a];
+}
+
+/* N4: force on the sphere at c (radius rs) from element (P, v, re); returns 1 on contact */
+static int sc_term(const double* c, double rs, const double* P, const double* v, double re, const orc_params* p,
+                   double* t3) {
+  double cp[3] = {c[0] - P[0], c[1] - P[1], c[2] - P[2]};
+  double vv = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+  double t = 0.0;
+  if (vv > 0.0) {
+    t = ((cp[0] * v[0] + cp[1] * v[1]) + cp[2] * v[2]) / vv;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  }
+  double w[3];
+  for (int a = 0; a < 3; ++a) w[a] = c[a] - (P[a] + t * v[a]);
+  double d2 = (w[0] * w[0] + w[1] * w[1]) + w[2] * w[2];
+  if (!(d2 > 0.0)) return 0;
+  double d = sqrt(d2);
+  double s = rs + re;
+  double delta = s - d;
+  if (!(delta > 0.0)) return 0;
+  double r = (rs * re) / s;
+  double f = p->k_rep * delta - p->gamma_att * sqrt(r * delta);
+  double m = f / d;
+  for (int a = 0; a < 3; ++a) t3[a] = m * w[a];
+  return 1;
+}
+
+/* One step of spheres + neurite elements.  Sphere arrays as orc_step; elements: Q (3E), d (E),
+ * l0 (E), anchor A (3E), mother/c1/c2 (E).  Outputs dp_s (3n), dQ (3E); positions updated in place. */
+int orc_neurite_step(int64_t n, double* pos, const double* diam, int64_t E, double* Q, const double* de,
+                     const double* l0, const double* A, const int64_t* mother, const int64_t* c1, const int64_t* c2,
+                     const orc_params* p, const orc_neurite* np, double* dp_s, double* dQ) {
+  double* P = (double*)malloc(sizeof(double) * 3 * (E > 0 ? E : 1));
+  double* V = (double*)malloc(sizeof(double) * 3 * (E > 0 ? E : 1));
+  double* LEN = (double*)malloc(sizeof(double) * (E > 0 ? E : 1));
+  double* C = (double*)malloc(sizeof(double) * 3 * (E > 0 ? E : 1));
+  double* Ce_d = (double*)malloc(sizeof(double) * (E > 0 ? E : 1));
+  double* F = (double*)malloc(sizeof(double) * 3 * (n > 0 ? n : 1));
+  if (!P || !V || !LEN || !C || !Ce_d || !F) return ORC_ENOMEM;
+  double L = p->box_edge_min;
+  for (int64_t i = 0; i < n; ++i)
+    if (diam[i] > L) L = diam[i];
+  for (int64_t e = 0; e < E; ++e) {
+    el_geom(e, Q, A, mother, P + 3 * e, V + 3 * e, LEN + e, C + 3 * e);
+    Ce_d[e] = LEN[e] + de[e];
+    if (Ce_d[e] > L) L = Ce_d[e];
+  }
+  /* sphere-sphere sums with the common box edge (N2) */
+  orc_params ps = *p;
+  ps.box_edge_min = L;
+  orc_record rec;
+  memset(&rec, 0, sizeof rec);
+  rec.force = F;
+  double* scratch = (double*)malloc(sizeof(double) * 3 * (n > 0 ? n : 1));
+  int rc = n > 0 ? orc_step_sample(n, pos, diam, &ps, n, NULL, scratch, NULL, &rec, 0) : ORC_OK;
+  free(scratch);
+  if (rc) return rc;
+  orc_index sx, ex;
+  memset(&sx, 0, sizeof sx);
+  memset(&ex, 0, sizeof ex);
+  if (n > 0 && (rc = build_index(&sx, n, pos, diam, L))) return rc;
+  if (E > 0 && (rc = build_index(&ex, E, C, Ce_d, L))) return rc;
+  /* spheres: + element terms (N5), O6 */
+  for (int64_t i = 0; i < n; ++i) {
+    double Fi[3] = {F[3 * i], F[3 * i + 1], F[3 * i + 2]};
+    if (E > 0) {
+      int64_t b[3];
+      for (int a = 0; a < 3; ++a) b[a] = (int64_t)floor(pos[3 * i + a] * ex.g.inv);
+      for (int ddx = -1; ddx <= 1; ++ddx)
+        for (int ddy = -1; ddy <= 1; ++ddy)
+          for (int ddz = -1; ddz <= 1; ++ddz) {
+            int64_t cx = b[0] + ddx, cy = b[1] + ddy, cz = b[2] + ddz;
+            if (cx < ex.g.lo[0] || cx > ex.g.hi[0] || cy < ex.g.lo[1] || cy > ex.g.hi[1] || cz < ex.g.lo[2] ||
+                cz > ex.g.hi[2])
+              continue;
+            uint64_t k = key_of(&ex, cx, cy, cz);
+            for (int64_t q = lower_bound(&ex, k); q < E && ex.sorted[q].key == k; ++q) {
+              int64_t e = ex.sorted[q].id;
+              double t3[3];
+              if (sc_term(pos + 3 * i, 0.5 * diam[i], P + 3 * e, V + 3 * e, 0.5 * de[e], p, t3)) {
+                Fi[0] = Fi[0] + t3[0];
+                Fi[1] = Fi[1] + t3[1];
+                Fi[2] = Fi[2] + t3[2];
+              }
+            }
+          }
+    }
+    displacement(Fi, p, dp_s + 3 * i);
+  }
+  /* distal points (N3, N5), O6 */
+  for (int64_t e = 0; e < E; ++e) {
+    double Fe[3] = {0.0, 0.0, 0.0};
+    double T = np->k_spring * ((LEN[e] - l0[e]) / l0[e]);
+    double inv = 1.0 / LEN[e];
+    for (int a = 0; a < 3; ++a) Fe[a] = Fe[a] + (-T) * (V[3 * e + a] * inv);
+    int64_t ch[2] = {c1[e], c2[e]};
+    if (ch[0] > ch[1] && ch[1] >= 0) {
+      int64_t t = ch[0];
+      ch[0] = ch[1];
+      ch[1] = t;
+    }
+    for (int k = 0; k < 2; ++k) {
+      int64_t c = ch[k];
+      if (c < 0) continue;
+      double Tc = np->k_spring * ((LEN[c] - l0[c]) / l0[c]);
+      double invc = 1.0 / LEN[c];
+      for (int a = 0; a < 3; ++a) Fe[a] = Fe[a] + Tc * (V[3 * c + a] * invc);
+    }
+    if (n > 0) {
+      int64_t b[3];
+      for (int a = 0; a < 3; ++a) b[a] = (int64_t)floor(C[3 * e + a] * sx.g.inv);
+      for (int ddx = -1; ddx <= 1; ++ddx)
+        for (int ddy = -1; ddy <= 1; ++ddy)
+          for (int ddz = -1; ddz <= 1; ++ddz) {
+            int64_t cx = b[0] + ddx, cy = b[1] + ddy, cz = b[2] + ddz;
+            if (cx < sx.g.lo[0] || cx > sx.g.hi[0] || cy < sx.g.lo[1] || cy > sx.g.hi[1] || cz < sx.g.lo[2] ||
+                cz > sx.g.hi[2])
+              continue;
+            uint64_t k = key_of(&sx, cx, cy, cz);
+            for (int64_t q = lower_bound(&sx, k); q < n && sx.sorted[q].key == k; ++q) {
+              int64_t s = sx.sorted[q].id;
+              double t3[3];
+              if (sc_term(pos + 3 * s, 0.5 * diam[s], P + 3 * e, V + 3 * e, 0.5 * de[e], p, t3)) {
+                Fe[0] = Fe[0] - t3[0];
+                Fe[1] = Fe[1] - t3[1];
+                Fe[2] = Fe[2] - t3[2];
+              }
+            }
+          }
+    }
+    displacement(Fe, p, dQ + 3 * e);
+  }
+  for (int64_t i = 0; i < 3 * n; ++i) pos[i] = pos[i] + dp_s[i];
+  for (int64_t i = 0; i < 3 * E; ++i) Q[i] = Q[i] + dQ[i];
+  if (n > 0) free_index(&sx);
+  if (E > 0) free_index(&ex);
+  free(P);
+  free(V);
+  free(LEN);
+  free(C);
+  free(Ce_d);
+  free(F);
+  return ORC_OK;
+}
