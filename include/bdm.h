@@ -170,6 +170,20 @@ int bdm_set_fields(bdm_handle h, const bdm_field_params* fp, const int8_t* types
 /* Field `which` (0 or 1), dims[0]*dims[1]*dims[2] fp64 with z fastest. */
 int bdm_get_field(bdm_handle h, int which, double* out);
 
+/* NEXT-4, neurite elements (PAPER.md:402-415 springs with a distal point mass,
+ * PAPER.md:768-769; SPEC.md:230-238 sphere-cylinder force, SPEC.md:377-386 spring chains).
+ * n_el cylinders (HOST arrays, element id = index): distal point (n_el x 3), diameter, resting length,
+ * anchor (n_el x 3, the proximal point of roots), mother (-1 for roots), daughters (n_el x 2, -1 =
+ * none).  Every later step moves spheres and distal points together: sphere-sphere and
+ * sphere-cylinder contacts, axial springs k_spring*(len - rest)/rest, one box edge for both grids.
+ * n_el = 0 removes them. */
+int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const double* diam, const double* rest_len,
+                     const double* anchor, const int64_t* mother, const int64_t* daughters, double k_spring);
+
+/* Distal points (n_el x 3) and their displacements of the last step (n_el x 3), HOST arrays; either
+ * pointer may be NULL. */
+int bdm_get_neurites(bdm_handle h, double* distal, double* ddistal);
+
 /* Make room for `capacity` agents (dynamic populations).  Never shrinks. */
 int bdm_reserve(bdm_handle h, int64_t capacity);
 

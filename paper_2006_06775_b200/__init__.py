@@ -88,6 +88,8 @@ _SIGS = {
     "bdm_get_skip_stats": ([_vp, _vp], ctypes.c_int),
     "bdm_set_growth": ([_vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
     "bdm_reserve": ([_vp, ctypes.c_int64], ctypes.c_int),
+    "bdm_set_neurites": ([_vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double], ctypes.c_int),
+    "bdm_get_neurites": ([_vp, _vp, _vp], ctypes.c_int),
     "bdm_set_fields": ([_vp, ctypes.POINTER(bdm_field_params), _vp], ctypes.c_int),
     "bdm_get_field": ([_vp, ctypes.c_int, _vp], ctypes.c_int),
     "bdm_get_count": ([_vp, _vp], ctypes.c_int),
@@ -288,6 +290,25 @@ def bdm_get_field(h: Handle, which: int, out=None):
             out = np.empty(h.field_dims, np.float64)
     _check(load_library().bdm_get_field(h.raw, which, _ptr(out)), h.raw)
     return out
+
+
+def bdm_set_neurites(h: Handle, distal, diam, rest_len, anchor, mother, daughters, k_spring: float) -> None:
+    """NEXT-4: neurite elements (host arrays; element id = index; -1 = no mother / daughter)."""
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in (distal, diam, rest_len, anchor)]
+    m = np.ascontiguousarray(mother, dtype=np.int64)
+    d = np.ascontiguousarray(daughters, dtype=np.int64).reshape(-1, 2)
+    h.n_el = len(m)
+    _check(load_library().bdm_set_neurites(h.raw, len(m), *(_ptr(a) for a in arrs), _ptr(m), _ptr(d), k_spring),
+           h.raw)
+
+
+def bdm_get_neurites(h: Handle):
+    """(distal points [E,3], their displacements of the last step [E,3])."""
+    E = getattr(h, "n_el", 0)
+    q = np.zeros((E, 3))
+    dq = np.zeros((E, 3))
+    _check(load_library().bdm_get_neurites(h.raw, _ptr(q), _ptr(dq)), h.raw)
+    return q, dq
 
 
 def bdm_reserve(h: Handle, capacity: int) -> None:

@@ -98,6 +98,19 @@ struct bdm_ctx {
   int fcur = 0;
   uint32_t* fcnt = nullptr;  // 2 x nn secretion counts
   int8_t* type_by_id = nullptr;
+  // neurite elements (NEXT-4): by element id; element grid in a sub-handle over element centres
+  int64_t n_el = 0;
+  double4* eq[2] = {nullptr, nullptr};  // distal point + diameter (Jacobi double buffer)
+  double4* ea = nullptr;                // anchor + resting length
+  int4* et = nullptr;                   // mother, daughter1, daughter2
+  double* edq = nullptr;                // distal displacements of the last step
+  double* cpos = nullptr;               // element centres (3E) and extents len + d (E)
+  double* cdiam = nullptr;
+  double* fss = nullptr;                // sphere-sphere forces of the force-only pass (3 cap)
+  int eqc = 0;
+  double k_spring = 0.0;
+  double sphere_L = 0.0;  // O1 box edge of the spheres alone
+  bdm_ctx* el = nullptr;
   // stationary-region skip (BDM_SKIP_STATIONARY, NEXT-1)
   unsigned long long* hist[2] = {nullptr, nullptr};
   uint8_t* hot = nullptr;  // one hot flag per box-table entry
@@ -412,12 +425,12 @@ int force_step(bdm_ctx* h, bool want_dp) {
   if (h->prm.flags & BDM_RECORD)
     k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
                                                 nullptr, dp, nullptr, h->ext, h->err, rec, nullptr,
-                                                h->hist[0] ? h->hist[dst] : nullptr);
+                                                h->hist[0] ? h->hist[dst] : nullptr, nullptr);
   else
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
                                                  h->skip_active ? h->hot : nullptr,
-                                                 h->hist[0] ? h->hist[dst] : nullptr);
+                                                 h->hist[0] ? h->hist[dst] : nullptr, nullptr);
   CU(h, cudaGetLastError());
   DBG(h, "k_force");
   h->launches += 2;
@@ -546,6 +559,71 @@ int grow_divide_step(bdm_ctx* h) {
   return BDM_OK;
 }
 
+// NEXT-4 step (N1-N6): element geometry -> element grid (sub-handle) with the common box edge ->
+// sphere grid -> sphere-sphere forces (force-only pass) -> spheres + element terms, O6/O7 ->
+// distal points (springs + reactions), O6.  Called instead of grid_build + force_step.
+void set_box_edge(GridDev& g, double L) {
+  g.L = L;
+  g.L2 = L * L;
+  g.inv = 1.0 / (L * (1.0 + 0x1p-30));
+  g.thr_pad = 0.5 * L;
+}
+
+int upload(bdm_ctx* h, const double* pos, const double* diam);
+
+int neurite_step(bdm_ctx* h, bool want_dp) {
+  const uint32_t n = (uint32_t)h->n, E = (uint32_t)h->n_el;
+  cudaStream_t s = h->stream;
+  const int ec = h->eqc;
+  k_el_geom<<<blocks(E, 256), 256, 0, s>>>(h->eq[ec], h->ea, h->et, E, h->cpos, h->cdiam);
+  CU(h, cudaGetLastError());
+  DBG(h, "k_el_geom");
+  bdm_ctx* el = h->el;
+  int rc = upload(el, h->cpos, h->cdiam);  // re-bin the elements (synchronises; L of the elements)
+  if (rc) return fail(h, rc, "element grid: %s", el->error.c_str());
+  const double L = std::max(h->sphere_L, el->grid.L);  // N2: one box edge for both grids
+  set_box_edge(el->grid, L);
+  if (h->grid.L != L) {
+    set_box_edge(h->grid, L);
+    h->ext_valid = false;
+    if (h->state == State::Fresh) h->state = State::Stepped;
+  }
+  if ((rc = grid_build(el))) return fail(h, rc, "element grid: %s", el->error.c_str());
+  if (h->state != State::Fresh && (rc = grid_build(h))) return rc;
+  const int src = h->cur, dst = 1 - h->cur;
+  k_ext_reset<<<1, 32, 0, s>>>(h->ext);
+  RecordDev rec{};
+  ParamsDev pd = params_dev(h->prm);
+  if (n > 0) {
+    k_force<false><<<force_grid(h, n), FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(
+        h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst], nullptr, nullptr, nullptr, h->ext, h->err, rec,
+        nullptr, nullptr, h->fss);
+    DBG(h, "k_force (force-only)");
+    k_sc_sphere<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], h->fss, n, h->grid, el->grid, el->id[el->cur],
+                                               h->eq[ec], h->ea, h->et, pd, h->ag[dst], want_dp ? h->dp : nullptr,
+                                               h->ext);
+    DBG(h, "k_sc_sphere");
+  }
+  GridDev gs = h->grid;
+  if (n == 0) gs.table = nullptr;
+  k_el_update<<<blocks(E, 256), 256, 0, s>>>(h->eq[ec], h->ea, h->et, E, h->k_spring, h->ag[src], gs, pd,
+                                             h->eq[1 - ec], h->edq);
+  CU(h, cudaGetLastError());
+  DBG(h, "k_el_update");
+  h->launches += 5;
+  h->eqc = 1 - ec;
+  h->out_ids = h->id[src];
+  std::swap(h->id[src], h->id[dst]);
+  h->cur = dst;
+  h->ext_valid = true;
+  h->state = State::Stepped;
+  if (want_dp) {
+    h->have_dp = true;
+    h->n_dp = h->n;
+  }
+  return BDM_OK;
+}
+
 int copy_out(bdm_ctx* h, void* dst, const void* dev_src, size_t bytes) {
   if (h->prm.flags & BDM_DEVICE_PTRS) {
     CU(h, cudaMemcpyAsync(dst, dev_src, bytes, cudaMemcpyDeviceToDevice, h->stream));
@@ -603,6 +681,7 @@ int upload(bdm_ctx* h, const double* pos, const double* diam) {
     std::memcpy(&maxd, h->ext_host, sizeof maxd);
     // O1: L = max(max D, box_edge_min); inv = 1/(L*(1+2^-30))
     double L = std::max(maxd, h->prm.box_edge_min);
+    h->sphere_L = L;
     h->grid.L = L;
     h->grid.L2 = L * L;
     h->grid.inv = 1.0 / (L * (1.0 + 0x1p-30));
@@ -640,6 +719,7 @@ const char* bdm_last_error(bdm_handle h) { return h ? h->error.c_str() : g_tls_e
 
 void bdm_destroy(bdm_handle h) {
   if (!h) return;
+  if (h->el) bdm_destroy(h->el);
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
@@ -650,7 +730,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -783,7 +863,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
   if (n_steps < 0) return fail(h, BDM_EINVAL, "bdm_mech_step: n_steps = %d < 0", n_steps);
   if (h->poisoned) return fail(h, BDM_ESTATE, "handle poisoned by an earlier error: %s", h->error.c_str());
   CU(h, cudaSetDevice(h->device));
-  if (h->n == 0) {
+  if (h->n == 0 && h->n_el == 0) {
     if (n_steps > 0) h->have_dp = true;
     return BDM_OK;
   }
@@ -799,6 +879,14 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
     if (h->fields_on) {
       int rc = fields_step(h);
       if (rc) return rc;
+    }
+    if (h->n_el > 0) {  // NEXT-4: spheres + neurite elements
+      if (h->timing) CU(h, cudaEventRecord(ts.e1, h->stream));
+      int rc = neurite_step(h, s == n_steps - 1);
+      if (rc) return rc;
+      ++h->step_count;
+      if (h->timing) CU(h, cudaEventRecord(ts.e2, h->stream));
+      continue;
     }
     if (h->state != State::Fresh) {
       int rc = grid_build(h);
@@ -819,7 +907,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
 
 int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed) {
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_growth: NULL handle");
-  if (h->slab || h->fields_on) return fail(h, BDM_EINVAL, "bdm_set_growth: not available with slabs or fields");
+  if (h->slab || h->fields_on || h->n_el) return fail(h, BDM_EINVAL, "bdm_set_growth: not available with slabs, fields or neurites");
   if (!(growth >= 0.0) || !std::isfinite(growth) || !(div_diam > 0.0))
     return fail(h, BDM_EINVAL, "bdm_set_growth: need growth >= 0 (finite) and div_diam > 0");
   h->growth_on = std::isfinite(div_diam) || growth > 0.0;
@@ -889,6 +977,95 @@ int bdm_get_field(bdm_handle h, int which, double* out) {
   const size_t bytes = (size_t)h->fd.nn * sizeof(double);
   CU(h, cudaMemcpyAsync(out, h->field[which][h->fcur], bytes,
                         (h->prm.flags & BDM_DEVICE_PTRS) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+  return check_async(h);
+}
+
+int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const double* diam, const double* rest_len,
+                     const double* anchor, const int64_t* mother, const int64_t* daughters, double k_spring) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_neurites: NULL handle");
+  if (h->slab || h->growth_on || h->fields_on)
+    return fail(h, BDM_EINVAL, "bdm_set_neurites: not available with slabs, growth or fields");
+  if (n_el < 0 || n_el >= (int64_t)0x7fffffff || !(k_spring >= 0.0) || !std::isfinite(k_spring))
+    return fail(h, BDM_EINVAL, "bdm_set_neurites: bad count or spring constant");
+  if (n_el > 0 && (!distal || !diam || !rest_len || !anchor || !mother || !daughters))
+    return fail(h, BDM_EINVAL, "bdm_set_neurites: NULL array");
+  const size_t E = (size_t)n_el;
+  std::vector<double4> q(E), a(E);
+  std::vector<int4> t(E);
+  for (size_t e = 0; e < E; ++e) {
+    int64_t m = mother[e], d1 = daughters[2 * e], d2 = daughters[2 * e + 1];
+    if (!(diam[e] > 0.0) || !std::isfinite(diam[e]) || !(rest_len[e] > 0.0) || !std::isfinite(rest_len[e]) ||
+        m < -1 || m >= n_el || m == (int64_t)e || d1 < -1 || d1 >= n_el || d2 < -1 || d2 >= n_el)
+      return fail(h, BDM_EINVAL, "bdm_set_neurites: bad element %zu (diameter, resting length > 0; indices)", e);
+    for (int k = 0; k < 3; ++k)
+      if (!std::isfinite(distal[3 * e + k]) || !std::isfinite(anchor[3 * e + k]))
+        return fail(h, BDM_EINVAL, "bdm_set_neurites: non-finite coordinate of element %zu", e);
+    if (d1 >= 0 && d2 >= 0 && d2 < d1) std::swap(d1, d2);
+    if (d1 < 0 && d2 >= 0) std::swap(d1, d2);
+    q[e] = make_double4(distal[3 * e], distal[3 * e + 1], distal[3 * e + 2], diam[e]);
+    a[e] = make_double4(anchor[3 * e], anchor[3 * e + 1], anchor[3 * e + 2], rest_len[e]);
+    t[e] = make_int4((int)m, (int)d1, (int)d2, 0);
+  }
+  CU(h, cudaSetDevice(h->device));
+  auto fr = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  fr(h->eq[0]); fr(h->eq[1]); fr(h->ea); fr(h->et); fr(h->edq); fr(h->cpos); fr(h->cdiam); fr(h->fss);
+  h->eq[0] = h->eq[1] = h->ea = nullptr;
+  h->et = nullptr;
+  h->edq = h->cpos = h->cdiam = h->fss = nullptr;
+  if (h->el) {
+    bdm_destroy(h->el);
+    h->el = nullptr;
+  }
+  h->n_el = n_el;
+  if (n_el == 0) return BDM_OK;
+  int rc;
+  if ((rc = dalloc(h, &h->eq[0], E)) || (rc = dalloc(h, &h->eq[1], E)) || (rc = dalloc(h, &h->ea, E)) ||
+      (rc = dalloc(h, &h->et, E)) || (rc = dalloc(h, &h->edq, 3 * E)) || (rc = dalloc(h, &h->cpos, 3 * E)) ||
+      (rc = dalloc(h, &h->cdiam, E)) || (rc = dalloc(h, &h->fss, 3 * (size_t)std::max<int64_t>(h->cap, 1))))
+    return rc;
+  CU(h, cudaMemcpy(h->eq[0], q.data(), E * sizeof(double4), cudaMemcpyHostToDevice));
+  CU(h, cudaMemcpy(h->ea, a.data(), E * sizeof(double4), cudaMemcpyHostToDevice));
+  CU(h, cudaMemcpy(h->et, t.data(), E * sizeof(int4), cudaMemcpyHostToDevice));
+  CU(h, cudaMemset(h->edq, 0, 3 * E * sizeof(double)));
+  h->eqc = 0;
+  h->k_spring = k_spring;
+  k_el_geom<<<blocks(E, 256), 256, 0, h->stream>>>(h->eq[0], h->ea, h->et, (uint32_t)E, h->cpos, h->cdiam);
+  CU(h, cudaGetLastError());
+  CU(h, cudaStreamSynchronize(h->stream));
+  bdm_params ep = h->prm;
+  ep.flags = BDM_DEVICE_PTRS;
+  ep.device = h->device;
+  bdm_ctx* el = nullptr;
+  rc = bdm_init(&el, n_el, h->cpos, h->cdiam, &ep);
+  if (rc) return fail(h, rc, "bdm_set_neurites: element grid: %s", bdm_last_error(nullptr));
+  el->stream = h->stream;
+  h->el = el;
+  h->state = State::NoGrid;
+  h->ext_valid = false;
+  return BDM_OK;
+}
+
+int bdm_get_neurites(bdm_handle h, double* distal, double* ddistal) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_neurites: NULL handle");
+  if (h->n_el == 0) return BDM_OK;
+  CU(h, cudaSetDevice(h->device));
+  const size_t E = (size_t)h->n_el;
+  if (distal) {
+    std::vector<double4> q(E);
+    CU(h, cudaMemcpyAsync(q.data(), h->eq[h->eqc], E * sizeof(double4), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    for (size_t e = 0; e < E; ++e) {
+      distal[3 * e] = q[e].x;
+      distal[3 * e + 1] = q[e].y;
+      distal[3 * e + 2] = q[e].z;
+    }
+  }
+  if (ddistal) {
+    CU(h, cudaMemcpyAsync(ddistal, h->edq, 3 * E * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+  }
   return check_async(h);
 }
 
@@ -1407,7 +1584,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
                                                  (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
-                                                 h->err, rec, nullptr, nullptr);
+                                                 h->err, rec, nullptr, nullptr, nullptr);
     CU(h, cudaGetLastError());
     h->launches += 1;
   }

@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
             uint32_t a_begin, uint32_t a_end, GridDev g, ParamsDev p, double4* __restrict__ ag_out,
             uint32_t* __restrict__ id_out, double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
             Extents* ext_next, ErrDev* err, RecordDev rec, const uint8_t* __restrict__ hot,
-            unsigned long long* __restrict__ hist_out) {
+            unsigned long long* __restrict__ hist_out, double* __restrict__ f_out) {
   extern __shared__ __align__(16) unsigned char s_raw[];  // FORCE_WARPS x ForceSmem (dynamic)
   ForceSmem* s_all = reinterpret_cast<ForceSmem*>(s_raw);
   const int lane = threadIdx.x & 31;
@@ -858,6 +858,15 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     if (__any_sync(FULL, cnt > 0))
       flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
 
+    if (f_out) {  // force-only mode (NEXT-4): the sphere-sphere sum goes to a later kernel
+      if (valid) {
+        const uint32_t o = i - a_begin;
+        f_out[3 * (size_t)o] = Fx;
+        f_out[3 * (size_t)o + 1] = Fy;
+        f_out[3 * (size_t)o + 2] = Fz;
+      }
+      continue;
+    }
     // O6 displacement, O7 update
     double dpx = 0.0, dpy = 0.0, dpz = 0.0;
     int branch = 0;
@@ -1180,6 +1189,183 @@ __global__ void k_chemotaxis(double4* __restrict__ ag, const uint32_t* __restric
   if (!(gn > 0.0)) return;
   const double sc = f.speed / gn;
   ag[i] = make_double4(p.x + g[0] * sc, p.y + g[1] * sc, p.z + g[2] * sc, p.w);
+}
+
+// ------------------------------------------------------------------------------------------ NEXT-4
+// Neurite elements (cylinders): sphere-cylinder contacts and spring chains (N1-N6).
+// Element e by id: eq[e] = (distal Q, diameter d), ea[e] = (anchor A, resting length l0),
+// et[e] = (mother, daughter1, daughter2) with daughter1 < daughter2 when both exist.
+
+__device__ __forceinline__ void el_geom(uint32_t e, const double4* __restrict__ eq, const double4* __restrict__ ea,
+                                        const int4* __restrict__ et, double P[3], double v[3], double& len) {
+  const double4 q = eq[e];
+  const int m = et[e].x;
+  const double4 pp = m >= 0 ? eq[m] : ea[e];
+  P[0] = pp.x;
+  P[1] = pp.y;
+  P[2] = pp.z;
+  v[0] = q.x - pp.x;
+  v[1] = q.y - pp.y;
+  v[2] = q.z - pp.z;
+  len = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
+}
+
+// N1/N2: element centres (for the element grid) and their extent len + d
+__global__ void k_el_geom(const double4* __restrict__ eq, const double4* __restrict__ ea, const int4* __restrict__ et,
+                          uint32_t E, double* __restrict__ cpos, double* __restrict__ cdiam) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  double P[3], v[3], len;
+  el_geom(e, eq, ea, et, P, v, len);
+  cpos[3 * (size_t)e] = P[0] + 0.5 * v[0];
+  cpos[3 * (size_t)e + 1] = P[1] + 0.5 * v[1];
+  cpos[3 * (size_t)e + 2] = P[2] + 0.5 * v[2];
+  cdiam[e] = len + eq[e].w;
+}
+
+// N4: force on the sphere at c (radius rs) from the element (P, v, re); false without contact
+__device__ __forceinline__ bool sc_term(const double c[3], double rs, const double P[3], const double v[3], double re,
+                                        const ParamsDev& p, double t3[3]) {
+  const double cp0 = c[0] - P[0], cp1 = c[1] - P[1], cp2 = c[2] - P[2];
+  const double vv = (v[0] * v[0] + v[1] * v[1]) + v[2] * v[2];
+  double t = 0.0;
+  if (vv > 0.0) {
+    t = ((cp0 * v[0] + cp1 * v[1]) + cp2 * v[2]) / vv;
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+  }
+  const double w0 = c[0] - (P[0] + t * v[0]), w1 = c[1] - (P[1] + t * v[1]), w2 = c[2] - (P[2] + t * v[2]);
+  const double d2 = (w0 * w0 + w1 * w1) + w2 * w2;
+  if (!(d2 > 0.0)) return false;
+  const double d = sqrt(d2);
+  const double s = rs + re;
+  const double delta = s - d;
+  if (!(delta > 0.0)) return false;
+  const double r = (rs * re) / s;
+  const double f = p.k_rep * delta - p.gamma_att * sqrt(r * delta);
+  const double m = f / d;
+  t3[0] = m * w0;
+  t3[1] = m * w1;
+  t3[2] = m * w2;
+  return true;
+}
+
+__device__ __forceinline__ int disp_rule(double Fx, double Fy, double Fz, const ParamsDev& p, double& dx, double& dy,
+                                         double& dz) {
+  dx = dy = dz = 0.0;
+  const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
+  if (fn <= p.adherence) return 0;
+  if (fn * p.c > p.max_disp) {
+    const double scale = p.max_disp / fn;
+    dx = Fx * scale;
+    dy = Fy * scale;
+    dz = Fz * scale;
+    return 1;
+  }
+  dx = Fx * p.c;
+  dy = Fy * p.c;
+  dz = Fz * p.c;
+  return 2;
+}
+
+// N5 (spheres) + O6/O7: sphere-sphere sum from the force-only pass, then the element terms over the
+// 27 element boxes (canonical order, ascending element id inside a box).
+__global__ void k_sc_sphere(const double4* __restrict__ ag, const double* __restrict__ fss, uint32_t n, GridDev gs,
+                            GridDev ge, const uint32_t* __restrict__ el_ids, const double4* __restrict__ eq,
+                            const double4* __restrict__ ea, const int4* __restrict__ et, ParamsDev p,
+                            double4* __restrict__ ag_out, double* __restrict__ dp_out, Extents* ext_next) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  int nb3[3] = {0, 0, 0};
+  bool bad = false;
+  if (valid) {
+    const double4 me = ag[i];
+    const double c[3] = {me.x, me.y, me.z};
+    const double rs = 0.5 * me.w;
+    double Fx = fss[3 * (size_t)i], Fy = fss[3 * (size_t)i + 1], Fz = fss[3 * (size_t)i + 2];
+    const int bx = (int)floor(me.x * ge.inv), by = (int)floor(me.y * ge.inv), bz = (int)floor(me.z * ge.inv);
+    for (int col = 0; col < 9; ++col) {
+      uint32_t b, e;
+      if (!zrun(ge, bx + col / 3 - 1, by + col % 3 - 1, bz - 1, bz + 1, b, e)) continue;
+      for (uint32_t q = b; q < e; ++q) {
+        const uint32_t el = el_ids[q];
+        double P[3], v[3], len, t3[3];
+        el_geom(el, eq, ea, et, P, v, len);
+        if (sc_term(c, rs, P, v, 0.5 * eq[el].w, p, t3)) {
+          Fx = Fx + t3[0];
+          Fy = Fy + t3[1];
+          Fz = Fz + t3[2];
+        }
+      }
+    }
+    double dx, dy, dz;
+    disp_rule(Fx, Fy, Fz, p, dx, dy, dz);
+    const double4 np = make_double4(me.x + dx, me.y + dy, me.z + dz, me.w);
+    ag_out[i] = np;
+    if (dp_out) {
+      dp_out[3 * (size_t)i] = dx;
+      dp_out[3 * (size_t)i + 1] = dy;
+      dp_out[3 * (size_t)i + 2] = dz;
+    }
+    nb3[0] = box_coord(np.x, gs.inv, bad);
+    nb3[1] = box_coord(np.y, gs.inv, bad);
+    nb3[2] = box_coord(np.z, gs.inv, bad);
+  }
+  if (__any_sync(FULL, bad) && (threadIdx.x & 31) == 0) ext_next->range_err = 1;
+  block_minmax_atomic(ext_next, nb3, valid);
+}
+
+// N3 + N5 (distal points) + O6: own spring, daughters' springs (ascending id), sphere reactions over
+// the 27 sphere boxes around box(C_e) (canonical order, ascending sphere id).
+__global__ void k_el_update(const double4* __restrict__ eq, const double4* __restrict__ ea,
+                            const int4* __restrict__ et, uint32_t E, double k_spring, const double4* __restrict__ ag,
+                            GridDev gs, ParamsDev p, double4* __restrict__ eq_out, double* __restrict__ dq_out) {
+  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  double P[3], v[3], len;
+  el_geom(e, eq, ea, et, P, v, len);
+  const double4 a = ea[e];
+  const double T = k_spring * ((len - a.w) / a.w);
+  const double inv = 1.0 / len;
+  double F[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) F[k] = F[k] + (-T) * (v[k] * inv);
+  const int4 tp = et[e];
+  const int ch[2] = {tp.y, tp.z};
+  for (int k = 0; k < 2; ++k) {
+    if (ch[k] < 0) continue;
+    double Pc[3], vc[3], lc;
+    el_geom((uint32_t)ch[k], eq, ea, et, Pc, vc, lc);
+    const double Tc = k_spring * ((lc - ea[ch[k]].w) / ea[ch[k]].w);
+    const double ic = 1.0 / lc;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) F[j] = F[j] + Tc * (vc[j] * ic);
+  }
+  const double re = 0.5 * eq[e].w;
+  const double C[3] = {P[0] + 0.5 * v[0], P[1] + 0.5 * v[1], P[2] + 0.5 * v[2]};
+  if (gs.table) {
+    const int bx = (int)floor(C[0] * gs.inv), by = (int)floor(C[1] * gs.inv), bz = (int)floor(C[2] * gs.inv);
+    for (int col = 0; col < 9; ++col) {
+      uint32_t b, en;
+      if (!zrun(gs, bx + col / 3 - 1, by + col % 3 - 1, bz - 1, bz + 1, b, en)) continue;
+      for (uint32_t q = b; q < en; ++q) {
+        const double4 sp = ag[q];
+        const double c[3] = {sp.x, sp.y, sp.z};
+        double t3[3];
+        if (sc_term(c, 0.5 * sp.w, P, v, re, p, t3)) {
+          F[0] = F[0] - t3[0];
+          F[1] = F[1] - t3[1];
+          F[2] = F[2] - t3[2];
+        }
+      }
+    }
+  }
+  double dx, dy, dz;
+  disp_rule(F[0], F[1], F[2], p, dx, dy, dz);
+  const double4 q = eq[e];
+  eq_out[e] = make_double4(q.x + dx, q.y + dy, q.z + dz, q.w);
+  dq_out[3 * (size_t)e] = dx;
+  dq_out[3 * (size_t)e + 1] = dy;
+  dq_out[3 * (size_t)e + 2] = dz;
 }
 
 // ------------------------------------------------------------------------------------------ K7
