@@ -178,24 +178,31 @@ def run_bdm(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
-    pos_h, diam_h = make_inputs(args.config, args.n)
-    n = len(diam_h)
-    pos_d = torch.from_numpy(pos_h).to(dev)
-    diam_d = torch.from_numpy(diam_h).to(dev)
-    torch.cuda.synchronize()
+    n = config_size(args.config, args.n)
+    big = n > BIG_N
+    pos_d, diam_d, pos_h, diam_h = device_inputs(bdm, torch, args.config, n, dev, stream)
 
-    # work units of one step (algorithmic fp64 ops), from one recorded step at the start state
+    # work units of one step (algorithmic fp64 ops), from one recorded step at the start state; for
+    # the 1e8-1e9-agent configs on a 2e7-agent sub-volume of the same density (per-agent averages)
     prm = bdm.bdm_params_default(device=local)
     prm.flags |= bdm.BDM_RECORD
-    hr = bdm.bdm_init(pos_d, diam_d, prm, stream=stream)
+    if big:
+        sp, sd, _, _ = device_inputs(bdm, torch, args.config, SUB_N, dev, stream, scale_from=n)
+        hr = bdm.bdm_init(sp, sd, prm, stream=stream)
+        del sp, sd
+    else:
+        hr = bdm.bdm_init(pos_d, diam_d, prm, stream=stream)
     bdm.bdm_mech_step(hr, 1)
     st = bdm.bdm_get_agent_stats(hr)
-    n_cand = int(st["n_cand"].sum().item())
-    n_ct = int(st["n_ct"].sum().item())
+    scale = n / (SUB_N if big else n)
+    n_cand = int(st["n_cand"].sum().item() * scale)
+    n_ct = int(st["n_ct"].sum().item() * scale)
     hr.close()
     del st
-
+    torch.cuda.empty_cache()
     h = bdm.bdm_init(pos_d, diam_d, bdm.bdm_params_default(device=local), stream=stream)
+    del pos_d, diam_d  # the handle holds its own copy (frees 32 B/agent for the 1e9-agent config)
+    torch.cuda.empty_cache()
     bdm.bdm_set_timing(h, True)
     flush = None
     if n * 32 <= 126e6:  # state fits in L2: flush it between timed steps
@@ -237,7 +244,6 @@ def run_bdm(args):
     rebuild = {"bound": "hbm", "achieved": rebuild_bytes / grid_s / 1e9, "peak": float(peaks["hbm_gbs"]),
                "unit": "GB/s", "frac": rebuild_bytes / grid_s / 1e9 / float(peaks["hbm_gbs"]),
                "ms_per_step": grid_s * 1e3, "bytes_per_agent": REBUILD_BYTES_PER_AGENT}
-    del pos_d, diam_d
     traffic = None
     tf = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
     if args.config == 3 and os.path.exists(tf):  # measured DRAM bytes of the force kernel (committed capture)
@@ -245,16 +251,28 @@ def run_bdm(args):
             t = json.load(f)
         traffic = t["dram_bytes_read"] + t["dram_bytes_write"]
 
-    # end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
-    e2e = run_e2e(bdm, torch, pos_h, diam_h, local, args)
     h.close()
+    torch.cuda.empty_cache()
+    # end-to-end through the C ABI with host buffers (pinned), copies inside the timed region
+    if pos_h is None:  # device-generated config: bring the inputs to (pinned) host memory once
+        pd, dd, _, _ = device_inputs(bdm, torch, args.config, n, dev, stream)
+        pos_h, diam_h = pd.cpu().numpy(), dd.cpu().numpy()
+        del pd, dd
+        torch.cuda.empty_cache()
+    e2e = run_e2e(bdm, torch, pos_h, diam_h, local, args)
 
     cpu = None
     if not args.no_cpu_baseline:
-        m, dt, threads = oracle_sample_run(pos_h, diam_h, args.cpu_stride)
+        if big:  # the oracle on a 2e7-agent sub-volume of the same density
+            ps, ds = sub_volume(args.config, n)
+            m, dt, threads = oracle_sample_run(ps, ds, args.cpu_stride)
+            what = f"a {SUB_N}-agent sub-volume at the same density"
+        else:
+            m, dt, threads = oracle_sample_run(pos_h, diam_h, args.cpu_stride)
+            what = f"the full {n}-agent population"
         cpu = {"value": m / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"every {args.cpu_stride}th agent id updated ({m} agents) with the full {n}-agent "
-                         f"population as environment; oracle grid rebuilt over all agents; {dt:.1f} s wall"}
+               "sample": f"every {args.cpu_stride}th agent id updated ({m} agents) with {what} as environment; "
+                         f"oracle grid rebuilt over all of them; {dt:.1f} s wall"}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
@@ -273,6 +291,43 @@ def run_bdm(args):
             "clocks": clk.summary(), "step_ms": [round(x, 4) for x in step_ms]}
     print(json.dumps(line), flush=True)
     return 0
+
+
+BIG_N = 50_000_000  # above this: device generation, statistics and CPU baseline on a sub-volume
+SUB_N = 20_000_000
+
+
+def config_size(cfg, n):
+    if n is not None:
+        return n
+    return bdm_inputs.CFG_N[cfg]
+
+
+def sub_volume(cfg, n_full):
+    """Host population: the first SUB_N ids of a counter-hash config in a box shrunk so that the
+    density is unchanged (cfg4 / cfg5 are uniform)."""
+    lo, hi = bdm_inputs.box_of(cfg, n_full)
+    f = (SUB_N / n_full) ** (1.0 / 3.0)
+    hi = tuple(lo[a] + (hi[a] - lo[a]) * f for a in range(3))
+    return bdm_inputs.uniform_population(cfg, np.arange(SUB_N), lo, hi, 8.0, 12.0)
+
+
+def device_inputs(bdm, torch, cfg, n, dev, stream, scale_from=None):
+    """(pos_d, diam_d, pos_h, diam_h): counter-hash configs (1, 4, 5) are generated on the device by
+    bdm_generate_uniform (kernel K0, bit-identical to bdm_inputs); cfg2 / cfg3 on the host."""
+    if cfg in (1, 4, 5):
+        nfull = scale_from or n
+        lo, hi = bdm_inputs.box_of(cfg, nfull) if cfg != 1 else bdm_inputs.box_of(1)
+        if scale_from:
+            f = (n / scale_from) ** (1.0 / 3.0)
+            hi = tuple(lo[a] + (hi[a] - lo[a]) * f for a in range(3))
+        pos = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        diam = torch.empty(n, dtype=torch.float64, device=dev)
+        bdm.bdm_generate_uniform(cfg, 0, n, lo, hi, 8.0, 12.0, pos, diam, stream)
+        torch.cuda.synchronize()
+        return pos, diam, None, None
+    pos_h, diam_h = make_inputs(cfg, n if n != bdm_inputs.CFG_N[cfg] else None)
+    return torch.from_numpy(pos_h).to(dev), torch.from_numpy(diam_h).to(dev), pos_h, diam_h
 
 
 # rebuild kernels, algorithmic bytes per agent (DESIGN.md §6.1): column pass 32 | key + histogram

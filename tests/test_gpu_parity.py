@@ -296,3 +296,33 @@ def test_cfg3_full_size_sampled(bdm):
     # whole-population properties: every agent's box is its floor(p*inv), |dp| <= max_disp
     assert np.array_equal(g["boxes"], np.floor(pos * g["info"]["inv"]).astype(np.int32))
     assert np.all(np.linalg.norm(g["dp"], axis=1) <= 3.0 * (1 + 4 * U))
+
+
+@pytest.mark.slow
+def test_cfg4_full_size_window(bdm):
+    """configs[3] at full size (2e8 agents, generated on the device by K0) in the launch
+    configuration bench.py times: the displacements of every agent inside a window are checked
+    against the oracle run on that window plus a margin of two box edges (the window's agents have
+    their complete 27-box neighbourhood in the oracle's input), with the global box edge."""
+    import torch
+
+    n = bdm_inputs.CFG_N[4]
+    lo, hi = bdm_inputs.box_of(4, n)
+    pos = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    diam = torch.empty(n, dtype=torch.float64, device="cuda")
+    bdm.bdm_generate_uniform(4, 0, n, lo, hi, 8.0, 12.0, pos, diam)
+    h = bdm.bdm_init(pos, diam, bdm.bdm_params_default())
+    bdm.bdm_mech_step(h, 1)
+    dp = bdm.bdm_get_displacements(h)
+    torch.cuda.synchronize()
+    L = float(diam.max().item())
+    c = np.array([4000.0, 1500.0, 1500.0])
+    w, m = 60.0, 2.2 * L
+    sel = torch.all((pos > torch.tensor(c - w - m, device="cuda")) & (pos < torch.tensor(c + w + m, device="cuda")),
+                    dim=1)
+    idx = torch.nonzero(sel).squeeze(1)
+    ps, ds, dps = pos[idx].cpu().numpy(), diam[idx].cpu().numpy(), dp[idx].cpu().numpy()
+    inner = np.all(np.abs(ps - c) < w, axis=1)
+    o = oracle.step(ps, ds, oracle.params(box_edge_min=L), sample=np.flatnonzero(inner), record=False)
+    assert inner.sum() > 100
+    assert np.array_equal(dps[inner], o["dp"])
