@@ -242,18 +242,21 @@ class SlabDriver:
         self.migrated = 0  # agents moved between slabs by step() (diagnostics)
         self.settle()
 
-    def migrate(self):
+    def migrate(self, count_global: bool = False):
+        """Send emigrants to g-1 / g+1 and append the immigrants.  Returns the number of agents moved
+        (globally when count_global -- an extra allreduce only the setup needs)."""
         sends = [e.pack(MIGRANTS, xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]
-        moved = self.comm.allreduce_sum([np.array([s[0].shape[0] + s[1].shape[0]], np.int64) for s in sends])
+        local = sum(s[0].shape[0] + s[1].shape[0] for s in sends)
+        moved = self.comm.allreduce_sum([np.array([local], np.int64)])[0] if count_global else local
         recvs = self.comm.exchange(sends)
         for e, (rl, rh) in zip(self.engines, recvs):
             e.add(rl, rh)
-        return int(moved[0])
+        return int(moved)
 
     def settle(self, max_rounds: int | None = None):
         """Move every agent to its owner (agents hop one slab per round)."""
         rounds = 0
-        while self.migrate() > 0:
+        while self.migrate(count_global=True) > 0:
             rounds += 1
             if rounds > (max_rounds or len(self.bounds)):
                 raise RuntimeError("agents did not settle in their slabs")

@@ -52,7 +52,7 @@ def test_loop_slabs_match_single_process(G):
     for _ in range(steps):
         drv.step()
     if G > 1:
-        assert drv.migrated > 0 and drv.ghosts > 0  # the protocol was exercised
+        assert drv.migrated > 0 and drv.ghosts > 0  # the protocol was exercised (counts of the local slabs)
     ids = np.concatenate([e.owned()[0] for e in engines])
     got = np.concatenate([e.owned()[1] for e in engines])
     assert np.array_equal(np.sort(ids), np.arange(len(diam)))  # agents conserved, none duplicated
