@@ -18,7 +18,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libbdm.so")
+LIB_PATH = os.environ.get("BDM_LIBRARY") or os.path.join(HERE, "libbdm.so")  # override: kernel-variant experiments
 HEADER = os.path.join(ROOT, "include", "bdm.h")
 
 BDM_OK = 0

@@ -520,7 +520,17 @@ __global__ void k_flag_zero(uint8_t* __restrict__ bflag, const uint32_t* __restr
 // ------------------------------------------------------------------------------------------ K6
 constexpr int FORCE_THREADS = 256;
 constexpr int FORCE_WARPS = FORCE_THREADS / 32;
-constexpr int FORCE_MIN_BLOCKS = 3;  // 24 resident warps per SM
+#ifndef BDM_FORCE_MIN_BLOCKS
+#define BDM_FORCE_MIN_BLOCKS 3
+#endif
+constexpr int FORCE_MIN_BLOCKS = BDM_FORCE_MIN_BLOCKS;  // 3: 24 resident warps per SM
+#ifndef BDM_NSLOT
+#define BDM_NSLOT 4  // candidate slots per iteration of the k_force candidate loop
+#endif
+constexpr int NSLOT = BDM_NSLOT;
+#ifndef BDM_CURSOR
+#define BDM_CURSOR 0  // candidate cursor of k_force: 0 flattened per slot, 1 range-granular
+#endif
 constexpr int LCAP = 16;             // per-lane survivor list capacity (flushed before overflow)
 
 // One contact candidate of agent i (O4), returns false if delta <= 0.
@@ -817,10 +827,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       bool live = nr > 0;
       uint32_t q = live ? sm.rb[0][lane] : 0u, e = live ? sm.re[0][lane] : 0u;
       while (__any_sync(FULL, live)) {
-        uint32_t qs[4];
-        bool as[4];
+        uint32_t qs[NSLOT];
+        bool as[NSLOT];
+#if BDM_CURSOR == 0
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < NSLOT; ++t) {
           as[t] = live && q != i;
           qs[t] = live ? q : i;
           if (live && ++q == e) {
@@ -832,11 +843,30 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
             }
           }
         }
-        float4 o[4];
+#else
+        // range-granular cursor: the NSLOT slots come from the current range only (slots past its end
+        // idle); one range switch per iteration at most
 #pragma unroll
-        for (int t = 0; t < 4; ++t) o[t] = __ldg(&agf[qs[t]]);
+        for (int t = 0; t < NSLOT; ++t) {
+          const uint32_t qt = q + (uint32_t)t;
+          as[t] = live && qt < e && qt != i;
+          qs[t] = as[t] ? qt : i;
+        }
+        q += (uint32_t)NSLOT;
+        if (live && q >= e) {
+          ++k;
+          live = k < nr;
+          if (live) {
+            q = sm.rb[k][lane];
+            e = sm.re[k][lane];
+          }
+        }
+#endif
+        float4 o[NSLOT];
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
+        for (int t = 0; t < NSLOT; ++t) o[t] = __ldg(&agf[qs[t]]);
+#pragma unroll
+        for (int t = 0; t < NSLOT; ++t) {
           // packed fp32x2 (FADD2/FMUL2): (dx, dy) = (x_i, y_i) - (x_j, y_j); (dz, s) = (z_i, r_i) - (z_j, -r_j)
           float2 dxy, dzs;
           asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
@@ -851,7 +881,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           const float d2 = (sq.x + sq.y) + qz.x;
           if (as[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) sm.list[cnt++][lane] = qs[t];
         }
-        if (__any_sync(FULL, cnt > LCAP - 4))
+        if (__any_sync(FULL, cnt > LCAP - NSLOT))
           flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
       }
     }

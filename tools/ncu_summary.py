@@ -56,11 +56,19 @@ def kernel(path):
     if len(rows) > 2:
         h = rows[1]
         si, wi, ei = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-        data = rows[2:]
-        tot = sum(int(x[wi]) for x in data) or 1
+        def num(v):
+            try:
+                return int(float(v.replace(",", "")))
+            except ValueError:
+                return 0
+
+        data = [x for x in rows[2:] if len(x) > max(si, wi, ei)]
+        for x in data:
+            x[wi], x[ei] = num(x[wi]), num(x[ei])
+        tot = sum(x[wi] for x in data) or 1
         print("  hottest SASS (share of stall samples):")
-        for x in sorted(data, key=lambda x: -int(x[wi]))[:12]:
-            print(f"    {100 * int(x[wi]) / tot:5.1f}%  exec {int(x[ei]) / 1e6:8.2f}M  {x[si].strip()[:70]}")
+        for x in sorted(data, key=lambda x: -x[wi])[:25]:
+            print(f"    {100 * x[wi] / tot:5.1f}%  exec {x[ei] / 1e6:8.2f}M  {x[si].strip()[:70]}")
 
 
 if __name__ == "__main__":
