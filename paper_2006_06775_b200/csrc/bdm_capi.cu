@@ -27,6 +27,8 @@ namespace {
 
 thread_local std::string g_tls_error;
 const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after every launch
+// BDM_HALF=0 selects the single-pass k_force for plain steps (A/B measurements of the half-shell path)
+const bool g_no_half = std::getenv("BDM_HALF") != nullptr && std::getenv("BDM_HALF")[0] == '0';
 
 enum class State { NoGrid, Fresh, Stepped };
 
@@ -119,7 +121,12 @@ struct bdm_ctx {
   bool skip_active = false;  // the pending force kernel uses hot flags
   uint32_t last_moved = 0, last_searched = 0;
   bool timing = false;
-  int sm_count = 0, force_blocks_per_sm = 0;
+  // half-shell force path (k_half_search + k_half_sum): pair rows, sized to cap
+  uint32_t *h_fwd = nullptr, *h_bwd = nullptr, *h_bcnt = nullptr;
+  uint8_t* h_fcnt = nullptr;
+  int64_t h_cap = 0;
+  bool half_off = false;  // BDM_HALF=0, or the rows could not be allocated: k_force only
+  int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
   std::vector<TimedStep> timed;
   std::string error;
@@ -248,6 +255,62 @@ void init_device_info(bdm_ctx* h) {
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan, SCAN_THREADS, 0);
   h->scan_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  cudaFuncSetAttribute(k_half_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HA_SMEM_BYTES);
+  cudaFuncSetAttribute(k_half_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
+  per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_search, HA_THREADS, HA_SMEM_BYTES);
+  h->half_a_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_sum, FORCE_THREADS, HB_SMEM_BYTES);
+  h->half_b_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+}
+
+// Pair rows of the half-shell path for cap agents (16 + 16 u32 + counters: 133 B/agent).  An
+// allocation failure is not an error: the handle falls back to k_force (no rows needed).
+bool ensure_half(bdm_ctx* h) {
+  if (h->half_off || g_no_half) return false;
+  if (h->h_cap >= h->cap && h->h_fwd) return true;
+  for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt})
+    if (q) cudaFree(q);
+  h->h_fwd = h->h_bwd = h->h_bcnt = nullptr;
+  h->h_fcnt = nullptr;
+  const size_t N = (size_t)std::max<int64_t>(h->cap, 1);
+  if (cudaMalloc(&h->h_fwd, N * HFC * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&h->h_bwd, N * HBC * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&h->h_bcnt, N * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->h_fcnt, N) != cudaSuccess) {
+    (void)cudaGetLastError();
+    for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt})
+      if (q) cudaFree(q);
+    h->h_fwd = h->h_bwd = h->h_bcnt = nullptr;
+    h->h_fcnt = nullptr;
+    h->half_off = true;
+    return false;
+  }
+  h->h_cap = h->cap;
+  return true;
+}
+
+// Half-shell force step over the owned sorted range [a_begin, a_end) of ag[src]; pass A searches
+// from s_begin (slab mode: the lower ghost layer searches too, its pairs with owned agents are
+// forward pairs of the ghost).
+int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t a_end, uint32_t n_all,
+               const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids) {
+  cudaStream_t s = h->stream;
+  CU(h, cudaMemsetAsync(h->h_bcnt, 0, (size_t)std::max<uint32_t>(n_all, 1) * sizeof(uint32_t), s));
+  const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
+                                                   std::max<uint64_t>(1, (a_end - s_begin + HA_THREADS - 1) / HA_THREADS));
+  k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, s>>>(h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
+                                                       h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext);
+  DBG(h, "k_half_search");
+  const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
+                                                   std::max<uint64_t>(1, (a_end - a_begin + FORCE_THREADS - 1) / FORCE_THREADS));
+  k_half_sum<<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd, ag_out,
+                                                       id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt,
+                                                       h->h_bwd, h->h_bcnt);
+  DBG(h, "k_half_sum");
+  CU(h, cudaGetLastError());
+  h->launches += 2;
+  return BDM_OK;
 }
 
 // In-place exclusive scan of data[0 .. items) -- items given on the host, or read on the device as
@@ -422,7 +485,10 @@ int force_step(bdm_ctx* h, bool want_dp) {
   ParamsDev pd = params_dev(h->prm);
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
-  if (h->prm.flags & BDM_RECORD)
+  if (!(h->prm.flags & BDM_RECORD) && !h->skip_active && !h->hist[0] && n > 0 && ensure_half(h)) {
+    int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr);
+    if (rc) return rc;
+  } else if (h->prm.flags & BDM_RECORD)
     k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
                                                 nullptr, dp, nullptr, h->ext, h->err, rec, nullptr,
                                                 h->hist[0] ? h->hist[dst] : nullptr, nullptr);
@@ -731,7 +797,7 @@ void bdm_destroy(bdm_handle h) {
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
-                  h->r_branch, h->r_nbh, h->r_cth};
+                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->ext_host) cudaFreeHost(h->ext_host);

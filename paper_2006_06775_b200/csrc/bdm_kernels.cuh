@@ -57,6 +57,7 @@ struct Extents {
   uint32_t work;      // chunk counter of the persistent force kernel
   uint32_t moved;     // agents with dp != 0 in the step that produced these extents (skip mode)
   uint32_t searched;  // agents whose neighbourhood was searched in that step (skip mode)
+  uint32_t work_a;    // chunk counter of the half-shell search pass (k_half_search)
 };
 
 struct ErrDev {
@@ -195,6 +196,7 @@ __global__ void k_ext_reset(Extents* ext) {
   if (threadIdx.x == 4) ext->work = 0u;
   if (threadIdx.x == 5) ext->moved = 0u;
   if (threadIdx.x == 6) ext->searched = 0u;
+  if (threadIdx.x == 7) ext->work_a = 0u;
 }
 
 __device__ __forceinline__ uint32_t col_of(const GridDev& g, int bx, int by) {
@@ -578,8 +580,8 @@ constexpr size_t FORCE_SMEM_BYTES = sizeof(ForceSmem) * FORCE_WARPS;
 // is evaluated with one entry per lane (owner found by a shuffle binary search over the inclusive
 // prefix of list lengths), then every owner adds its own entries of the batch in order -- so each
 // agent's force is summed in O5's canonical order.
-template <bool RECORD>
-__device__ __forceinline__ void flush_contacts(ForceSmem& sm, int lane, int& cnt, double xi, double yi, double zi,
+template <bool RECORD, class Smem>
+__device__ __forceinline__ void flush_contacts(Smem& sm, int lane, int& cnt, double xi, double yi, double zi,
                                                double ri, uint32_t idi, const double4* __restrict__ ag,
                                                const uint32_t* __restrict__ ids, const ParamsDev& p, double& Fx,
                                                double& Fy, double& Fz, int32_t& n_ct,
@@ -812,7 +814,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           if (a1 && d21 <= thr) sm.list[cnt++][lane] = q + 1;
           q += 2;
           if (__any_sync(FULL, cnt > LCAP - 2))
-            flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+            flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
         }
       }
     } else {
@@ -882,11 +884,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           if (as[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) sm.list[cnt++][lane] = qs[t];
         }
         if (__any_sync(FULL, cnt > LCAP - NSLOT))
-          flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+          flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
       }
     }
     if (__any_sync(FULL, cnt > 0))
-      flush_contacts<RECORD>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+      flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
 
     if (f_out) {  // force-only mode (NEXT-4): the sphere-sphere sum goes to a later kernel
       if (valid) {
@@ -967,6 +969,343 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     }
   }
 }
+
+// ------------------------------------------------------------------------------------------ K6h
+// Half-shell force path, used for plain steps (no statistics, no stationary-region
+// skip, no neurites).  Newton's third law (R2: F_ji = -F_ij bit-exactly) lets each candidate pair
+// be TESTED once instead of twice:
+//   pass A, k_half_search: agent i walks only the half of its 27-box neighbourhood that follows it in
+//     the sorted order (the rest of its own box after i, the box above in its column, and the 13
+//     boxes of larger key: columns (0,+1), (+1,-1), (+1,0), (+1,+1)), with the conservative fp32
+//     filter of k_force.  A surviving pair (i, j), i < j in sorted order, goes to i's forward row
+//     (ascending j: the walk is in sorted order) and, through an atomic slot, to j's backward row;
+//   pass B, k_half_sum: agent i evaluates the exact fp64 term (O4) of every pair of its backward row
+//     (sorted ascending first) then of its forward row -- i.e. of all its contacts in ascending
+//     sorted order = O5's canonical order (boxes in key order, ascending id inside a box) -- with
+//     the balanced contact phase of k_force, then O6/O7.  So Δp is bit-identical to k_force's.
+// Rows hold HFC / HBC entries; an agent whose row overflowed takes a slow path in pass B (a full
+// 27-box canonical search of its own), so the result does not depend on the capacities.
+constexpr int HFC = 16;  // forward row capacity (entries per agent)
+constexpr int HBC = 16;  // backward row capacity
+constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
+constexpr int HA_THREADS = 256;
+constexpr int HA_MIN_BLOCKS = 4;
+
+struct HalfASmem {
+  uint32_t list[HLA][32];  // survivors (sorted index j) of this lane, ascending
+  uint2 rr[7][32];         // this lane's non-empty forward z-runs [b, e), then the sentinel (0, 0)
+  uint32_t tab[5][TSPAN];  // box starts of the 5 forward columns (single-column chunks)
+};
+constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
+
+// forward row of i, backward rows of its partners; list drained
+__device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int& cnt, uint32_t i, uint32_t& nf,
+                                          uint32_t* __restrict__ fwd, uint32_t* __restrict__ bwd,
+                                          uint32_t* __restrict__ bcnt) {
+  for (int x0 = 0; x0 < cnt; x0 += 4) {
+    uint32_t j[4], slot[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      j[u] = x0 + u < cnt ? sm.list[x0 + u][lane] : 0u;
+      if (x0 + u < cnt) slot[u] = atomicAdd(&bcnt[j[u]], 1u);  // four atomics in flight
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (x0 + u < cnt) {
+        if (nf < (uint32_t)HFC) fwd[(size_t)i * HFC + nf] = j[u];
+        ++nf;
+        if (slot[u] < (uint32_t)HBC) bwd[(size_t)j[u] * HBC + slot[u]] = i;
+      }
+    }
+  }
+  cnt = 0;
+}
+
+__global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
+    k_half_search(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin, uint32_t s_end,
+                  GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
+                  uint32_t* __restrict__ bcnt, Extents* ext) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const uint32_t rr_base = (uint32_t)__cvta_generic_to_shared(&sm.rr[0][lane]);
+  while (true) {
+    uint32_t chunk = 0;
+    if (lane == 0) chunk = atomicAdd(&ext->work_a, 1u);
+    chunk = __shfl_sync(FULL, chunk, 0);
+    const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
+    if (base >= s_end) break;
+    const uint32_t i = (uint32_t)base + lane;
+    const bool valid = i < s_end;
+    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const double ri = 0.5 * me.w;
+    const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+    // box culling of k_force, for the 5 forward columns q = 0..4 <-> (dx, dy) = (0,0), (0,+1),
+    // (+1,-1), (+1,0), (+1,+1): bit q kept, bit 8+q z-1 box culled, bit 16+q z+1 box culled
+    uint32_t cull = 0u;
+    {
+      const double rp = (ri + g.thr_pad + g.m32) * (1.0 + 0x1p-20);
+      const double Rc = rp + g.m32;
+      const double Rc2 = Rc * Rc;
+      const double Lb = 1.0 / g.inv;
+      const double fy = fmax(me.y - by * Lb, 0.0), gy = fmax((by + 1) * Lb - me.y, 0.0);
+      const double gx = fmax((bx + 1) * Lb - me.x, 0.0);
+      const double fz = fmax(me.z - bz * Lb, 0.0), gz = fmax((bz + 1) * Lb - me.z, 0.0);
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const double ex = q >= 2 ? gx : 0.0;
+        const double ey = q == 1 || q == 4 ? gy : (q == 2 ? fy : 0.0);
+        const double exy2 = ex * ex + ey * ey;
+        cull |= (uint32_t)(exy2 <= Rc2) << q;
+        cull |= (uint32_t)(exy2 + fz * fz > Rc2) << (8 + q);
+        cull |= (uint32_t)(exy2 + gz * gz > Rc2) << (16 + q);
+      }
+    }
+    // single-column chunks stage the box starts of the 5 forward columns (as k_force does for 9)
+    const int bx0 = __shfl_sync(FULL, bx, 0), by0 = __shfl_sync(FULL, by, 0);
+    const int zf = __reduce_min_sync(FULL, valid ? bz : INT32_MAX);
+    const int zl = __reduce_max_sync(FULL, valid ? bz : INT32_MIN);
+    const bool coop = __all_sync(FULL, !valid || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
+    const int span = zl - zf + 4;
+    if (coop) {
+      int czl = 0, cze = 0;
+      uint32_t cof = 0xffffffffu;
+      if (lane < 5) {
+        const int cx = bx0 + (lane >= 2 ? 1 : 0);
+        const int cy = by0 + (lane == 1 || lane == 4 ? 1 : (lane == 2 ? -1 : 0));
+        if (cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1]) {
+          const uint32_t cc = col_of(g, cx, cy);
+          czl = __ldg(&g.czlo[cc]);
+          const int czh = __ldg(&g.czhi[cc]);
+          cof = __ldg(&g.coff[cc]);
+          cze = czh >= czl ? czh - czl + 1 : 0;
+        }
+      }
+      const int total = 5 * span;
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int t = t0 + lane;
+        const int c = t / span < 4 ? t / span : 4;
+        const int zlo_c = __shfl_sync(FULL, czl, c), ext_c = __shfl_sync(FULL, cze, c);
+        const uint32_t off_c = __shfl_sync(FULL, cof, c);
+        if (t < total) {
+          uint32_t v = 0u;
+          const int tt = t - c * span;
+          if (off_c != 0xffffffffu) {
+            int k = zf - 1 + tt - zlo_c;
+            k = k < 0 ? 0 : (k > ext_c ? ext_c : k);
+            v = __ldg(&g.table[off_c + (uint32_t)k]);
+          }
+          sm.tab[c][tt] = v;
+        }
+      }
+      __syncwarp();
+    }
+    // this lane's forward z-runs in canonical (= ascending sorted) order
+    int nr = 0;
+    uint32_t w = 0;
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        if (!((cull >> q) & 1u)) continue;
+        const int z0 = q == 0 ? bz : bz - 1 + (int)((cull >> (8 + q)) & 1u);
+        const int z1 = bz + 1 - (int)((cull >> (16 + q)) & 1u);
+        uint32_t b = 0, e = 0;
+        if (coop) {
+          b = sm.tab[q][z0 - zf + 1];
+          e = sm.tab[q][z1 - zf + 2];
+        } else {
+          const int cx = bx + (q >= 2 ? 1 : 0), cy = by + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
+          zrun(g, cx, cy, z0, z1, b, e);
+        }
+        if (q == 0) b = i + 1;  // own box: only the agents after i
+        if (b < e) {
+          sm.rr[nr][lane] = make_uint2(b, e);
+          w += e - b;
+          ++nr;
+        }
+      }
+    }
+    sm.rr[nr][lane] = make_uint2(0u, 0u);  // sentinel: after the last run q never meets e again
+    __syncwarp();
+    const uint32_t wmax = __reduce_max_sync(FULL, w);
+    const float ri32 = __double2float_ru(ri + g.m32);
+    const unsigned long long mxy = pack2(mf.x, mf.y), mzr = pack2(mf.z, ri32);
+    int cnt = 0;
+    uint32_t nf = 0;
+    uint2 cur = sm.rr[0][lane];
+    uint32_t q = cur.x, e = cur.y;
+    uint2 nx = sm.rr[1][lane];
+    uint32_t kaddr = rr_base + 2u * 256u;  // address of the run after nx
+    for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
+      uint32_t qs[NSLOT];
+      bool ok[NSLOT];
+#pragma unroll
+      for (int t = 0; t < NSLOT; ++t) {
+        ok[t] = s0 + t < w;
+        qs[t] = ok[t] ? q : 0u;
+        ++q;
+        const uint32_t sw = q == e;
+        q = sw ? nx.x : q;
+        e = sw ? nx.y : e;
+        // predicated refill of the next run (no branch): nx = rr[k], k advanced on a switch
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.v2.u32 {%0, %1}, [%3];\n\t}"
+                     : "+r"(nx.x), "+r"(nx.y) : "r"(sw), "r"(kaddr));
+        kaddr += sw * 256u;
+      }
+      float4 o[NSLOT];
+#pragma unroll
+      for (int t = 0; t < NSLOT; ++t) o[t] = __ldg(&agf[qs[t]]);
+#pragma unroll
+      for (int t = 0; t < NSLOT; ++t) {
+        float2 dxy, dzs;
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
+            : "l"(mxy), "l"(pack2(o[t].x, o[t].y)));
+        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dzs))
+            : "l"(mzr), "l"(pack2(o[t].z, o[t].w)));
+        float2 sq, qz;
+        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&sq))
+            : "l"(*reinterpret_cast<unsigned long long*>(&dxy)));
+        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&qz))
+            : "l"(*reinterpret_cast<unsigned long long*>(&dzs)));
+        const float d2 = (sq.x + sq.y) + qz.x;
+        if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) sm.list[cnt++][lane] = qs[t];
+      }
+      if (__any_sync(FULL, cnt > HLA - NSLOT)) half_emit(sm, lane, cnt, i, nf, fwd, bwd, bcnt);
+    }
+    half_emit(sm, lane, cnt, i, nf, fwd, bwd, bcnt);
+    if (valid) fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+    __syncwarp();
+  }
+}
+
+struct HalfBSmem {
+  uint32_t list[HFC + HBC][32];  // all contact candidates of this lane, ascending sorted index
+  double term[3][32];
+  uint32_t cidx[32];
+};
+constexpr size_t HB_SMEM_BYTES = sizeof(HalfBSmem) * FORCE_WARPS;
+
+// Full canonical 27-box sum of agent i (O3-O5 as written): the overflow path of pass B.
+__device__ __noinline__ void full_force(const GridDev& g, const double4* __restrict__ ag, const uint32_t* __restrict__ ids,
+                                        const ParamsDev& p, uint32_t i, double4 me, uint32_t myid, double& Fx,
+                                        double& Fy, double& Fz) {
+  const double ri = 0.5 * me.w;
+  const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+  Fx = 0.0;
+  Fy = 0.0;
+  Fz = 0.0;
+  for (int c = 0; c < 9; ++c) {
+    uint32_t b = 0, e = 0;
+    if (!zrun(g, bx + c / 3 - 1, by + c % 3 - 1, bz - 1, bz + 1, b, e)) continue;
+    for (uint32_t j = b; j < e; ++j) {
+      if (j == i) continue;
+      double tx, ty, tz, fa;
+      if (pair_term(me.x, me.y, me.z, ri, myid, ag[j], ids[j], p, tx, ty, tz, fa)) {
+        Fx = Fx + tx;
+        Fy = Fy + ty;
+        Fz = Fz + tz;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
+    k_half_sum(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t a_begin, uint32_t a_end,
+               GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
+               double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
+               const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
+               const uint32_t* __restrict__ bcnt) {
+  extern __shared__ __align__(16) unsigned char s_raw[];
+  HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+  bool ebad = false;
+  while (true) {
+    uint32_t chunk = 0;
+    if (lane == 0) chunk = atomicAdd(&ext_next->work, 1u);
+    chunk = __shfl_sync(FULL, chunk, 0);
+    const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
+    if (base >= a_end) break;
+    const uint32_t i = (uint32_t)base + lane;
+    const bool valid = i < a_end;
+    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const uint32_t myid = valid ? ids[i] : 0u;
+    const double ri = 0.5 * me.w;
+    const uint32_t nf = valid ? fcnt[i] : 0u;
+    const uint32_t nb = valid ? bcnt[i] : 0u;
+    const bool slow = nf > (uint32_t)HFC || nb > (uint32_t)HBC;
+    int cnt = 0;
+    if (!slow) {
+      // backward partners (all < i) sorted ascending, then forward partners (all > i, ascending)
+      const uint32_t* brow = bwd + (size_t)i * HBC;
+      for (uint32_t t = 0; t < nb; ++t) {
+        const uint32_t v = brow[t];
+        int x = (int)t;
+        while (x > 0 && sm.list[x - 1][lane] > v) {
+          sm.list[x][lane] = sm.list[x - 1][lane];
+          --x;
+        }
+        sm.list[x][lane] = v;
+      }
+      const uint32_t* frow = fwd + (size_t)i * HFC;
+      for (uint32_t t = 0; t < nf; ++t) sm.list[nb + t][lane] = frow[t];
+      cnt = (int)(nb + nf);
+    }
+    __syncwarp();
+    double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+    int32_t n_ct = 0;
+    unsigned long long ct_hash = 0;
+    if (__any_sync(FULL, cnt > 0))
+      flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct,
+                                       ct_hash);
+    if (slow) full_force(g, ag, ids, p, i, me, myid, Fx, Fy, Fz);
+    // O6 displacement, O7 update (as k_force)
+    double dpx = 0.0, dpy = 0.0, dpz = 0.0;
+    const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
+    if (fn <= p.adherence) {
+    } else if (fn * p.c > p.max_disp) {
+      const double scale = p.max_disp / fn;
+      dpx = Fx * scale;
+      dpy = Fy * scale;
+      dpz = Fz * scale;
+    } else {
+      dpx = Fx * p.c;
+      dpy = Fy * p.c;
+      dpz = Fz * p.c;
+    }
+    if (valid) {
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, myid);
+      const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
+      const uint32_t o = i - a_begin;
+      ag_out[o] = np;
+      if (id_out) id_out[o] = myid;
+      if (dp_out) {
+        dp_out[3 * (size_t)o] = dpx;
+        dp_out[3 * (size_t)o + 1] = dpy;
+        dp_out[3 * (size_t)o + 2] = dpz;
+        if (dp_id_out) dp_id_out[o] = myid;
+      }
+      const int nb3[3] = {box_coord(np.x, g.inv, ebad), box_coord(np.y, g.inv, ebad), box_coord(np.z, g.inv, ebad)};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        elo[a] = min(elo[a], nb3[a]);
+        ehi[a] = max(ehi[a], nb3[a]);
+      }
+    }
+  }
+  if (__any_sync(FULL, ebad) && lane == 0) ext_next->range_err = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int lo = __reduce_min_sync(FULL, elo[a]);
+    const int hi = __reduce_max_sync(FULL, ehi[a]);
+    if (lane == 0) {
+      if (lo != INT32_MAX && lo < __ldcg(&ext_next->lo[a])) atomicMin(&ext_next->lo[a], lo);
+      if (hi != INT32_MIN && hi > __ldcg(&ext_next->hi[a])) atomicMax(&ext_next->hi[a], hi);
+    }
+  }
+}
+
 
 // ------------------------------------------------------------------------------------------ K5/K9
 // x-slab exchange records: 5 fp64 per agent (x, y, z, D, id) -- ids < 2^32 are exact in fp64.
