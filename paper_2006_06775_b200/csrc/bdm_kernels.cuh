@@ -536,9 +536,10 @@ constexpr int NSLOT = BDM_NSLOT;
 constexpr int LCAP = 16;             // per-lane survivor list capacity (flushed before overflow)
 
 // One contact candidate of agent i (O4), returns false if delta <= 0.
-__device__ __forceinline__ bool pair_term(double xi, double yi, double zi, double ri, uint32_t idi, const double4& o,
-                                          uint32_t idj, const ParamsDev& p, double& tx, double& ty, double& tz,
-                                          double& fabs_out) {
+// i, j are sorted indices; ids[] is read only for coincident centres (the R8 tie-break, rare).
+__device__ __forceinline__ bool pair_term(double xi, double yi, double zi, double ri, uint32_t i, const double4& o,
+                                          const uint32_t* __restrict__ ids, uint32_t j, const ParamsDev& p, double& tx,
+                                          double& ty, double& tz, double& fabs_out) {
   double dx = xi - o.x;
   double dy = yi - o.y;
   double dz = zi - o.z;
@@ -552,7 +553,7 @@ __device__ __forceinline__ bool pair_term(double xi, double yi, double zi, doubl
   double f = p.k_rep * delta - p.gamma_att * sqrt(r * delta);
   fabs_out = fabs(f);
   if (d2 == 0.0) {  // coincident centres (R8)
-    tx = idi > idj ? f : -f;
+    tx = __ldg(&ids[i]) > __ldg(&ids[j]) ? f : -f;
     ty = 0.0;
     tz = 0.0;
     return true;
@@ -582,7 +583,7 @@ constexpr size_t FORCE_SMEM_BYTES = sizeof(ForceSmem) * FORCE_WARPS;
 // agent's force is summed in O5's canonical order.
 template <bool RECORD, class Smem>
 __device__ __forceinline__ void flush_contacts(Smem& sm, int lane, int& cnt, double xi, double yi, double zi,
-                                               double ri, uint32_t idi, const double4* __restrict__ ag,
+                                               double ri, uint32_t ii, const double4* __restrict__ ag,
                                                const uint32_t* __restrict__ ids, const ParamsDev& p, double& Fx,
                                                double& Fy, double& Fz, int32_t& n_ct,
                                                unsigned long long& ct_hash) {
@@ -603,18 +604,17 @@ __device__ __forceinline__ void flush_contacts(Smem& sm, int lane, int& cnt, dou
     const double oy = __shfl_sync(FULL, yi, owner);
     const double oz = __shfl_sync(FULL, zi, owner);
     const double orr = __shfl_sync(FULL, ri, owner);
-    const uint32_t oid = __shfl_sync(FULL, idi, owner);
+    const uint32_t oidx = __shfl_sync(FULL, ii, owner);
     uint32_t flag = 0xffffffffu;
     if (e < total) {
       const uint32_t j = sm.list[e - oexcl][owner];
       const double4 o = ag[j];
-      const uint32_t idj = ids[j];
       double tx, ty, tz, fa;
-      if (pair_term(ox, oy, oz, orr, oid, o, idj, p, tx, ty, tz, fa)) {
+      if (pair_term(ox, oy, oz, orr, oidx, o, ids, j, p, tx, ty, tz, fa)) {
         sm.term[0][lane] = tx;
         sm.term[1][lane] = ty;
         sm.term[2][lane] = tz;
-        flag = idj;
+        flag = RECORD ? ids[j] : 0u;  // id for the contact digest; any value != ~0 marks a contact
       }
     }
     sm.cidx[lane] = flag;
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           if (a1 && d21 <= thr) sm.list[cnt++][lane] = q + 1;
           q += 2;
           if (__any_sync(FULL, cnt > LCAP - 2))
-            flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+            flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
         }
       }
     } else {
@@ -884,11 +884,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
           if (as[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) sm.list[cnt++][lane] = qs[t];
         }
         if (__any_sync(FULL, cnt > LCAP - NSLOT))
-          flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+          flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
       }
     }
     if (__any_sync(FULL, cnt > 0))
-      flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
+      flush_contacts<RECORD, ForceSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct, ct_hash);
 
     if (f_out) {  // force-only mode (NEXT-4): the sphere-sphere sum goes to a later kernel
       if (valid) {
@@ -989,19 +989,70 @@ constexpr int HFC = 16;  // forward row capacity (entries per agent)
 constexpr int HBC = 16;  // backward row capacity
 constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
 constexpr int HA_THREADS = 256;
-constexpr int HA_MIN_BLOCKS = 4;
+#ifndef BDM_HA_MIN_BLOCKS
+#define BDM_HA_MIN_BLOCKS 4
+#endif
+#ifndef BDM_HB_MIN_BLOCKS
+#define BDM_HB_MIN_BLOCKS 3
+#endif
+constexpr int HA_MIN_BLOCKS = BDM_HA_MIN_BLOCKS;  // pass A: 4 x 8 resident warps per SM
+constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
+
+#ifndef BDM_HSTAGE
+#define BDM_HSTAGE 0  // 1: pass A single-column chunks read candidates from a TMA-staged shared copy (measured slower)
+#endif
+#ifndef BDM_HPCAP
+#define BDM_HPCAP 256
+#endif
+constexpr int HPCAP = BDM_HPCAP;  // staged candidates (float4) per warp
 
 struct HalfASmem {
-  uint32_t list[HLA][32];  // survivors (sorted index j) of this lane, ascending
+#if BDM_HSTAGE
+  float4 buf[HPCAP];        // fp32 candidates of the 5 forward columns' union z-runs (staged chunks)
+  unsigned long long bar;   // mbarrier of the bulk copies into buf
+  uint32_t off[6];          // buffer offset of each column's union run (off[5] = total)
+  uint32_t ub[5];           // global sorted index of each union run's first agent
+  uint32_t pad_;
+#endif
+  uint32_t list[HLA][32];  // survivors (sorted index j, or staged buffer index) of this lane, ascending
   uint2 rr[7][32];         // this lane's non-empty forward z-runs [b, e), then the sentinel (0, 0)
   uint32_t tab[5][TSPAN];  // box starts of the 5 forward columns (single-column chunks)
 };
+
+// ---- TMA bulk copies (cp.async.bulk, async proxy) completing on a per-warp mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
 constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 
-// forward row of i, backward rows of its partners; list drained
-__device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int& cnt, uint32_t i, uint32_t& nf,
-                                          uint32_t* __restrict__ fwd, uint32_t* __restrict__ bwd,
-                                          uint32_t* __restrict__ bcnt) {
+// End of a chunk: the forward row of i as whole 32-byte sectors (entries past cnt are don't-care;
+// full sectors avoid read-modify-write of partially written sectors in DRAM), and one backward-row
+// entry per pair through an atomic slot of the partner.
+__device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint32_t i, uint32_t* __restrict__ fwd,
+                                          uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
+  uint4* frow = reinterpret_cast<uint4*>(fwd + (size_t)i * HFC);
+#pragma unroll
+  for (int v = 0; v < HFC / 4; ++v)
+    if (cnt > 8 * (v / 2))
+      frow[v] = make_uint4(sm.list[4 * v][lane], sm.list[4 * v + 1][lane], sm.list[4 * v + 2][lane],
+                           sm.list[4 * v + 3][lane]);
   for (int x0 = 0; x0 < cnt; x0 += 4) {
     uint32_t j[4], slot[4];
 #pragma unroll
@@ -1010,15 +1061,83 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int& cnt, uin
       if (x0 + u < cnt) slot[u] = atomicAdd(&bcnt[j[u]], 1u);  // four atomics in flight
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (x0 + u < cnt) {
-        if (nf < (uint32_t)HFC) fwd[(size_t)i * HFC + nf] = j[u];
-        ++nf;
-        if (slot[u] < (uint32_t)HBC) bwd[(size_t)j[u] * HBC + slot[u]] = i;
+    for (int u = 0; u < 4; ++u)
+      if (x0 + u < cnt && slot[u] < (uint32_t)HBC) bwd[(size_t)j[u] * HBC + slot[u]] = i;
+  }
+}
+
+// Candidate loop of pass A over this lane's runs rr[] (flattened, branch-free run switch): fp32
+// conservative filter of k_force; survivors to the lane's list (STAGED: runs and survivors are
+// buffer indices of sm.buf).  A survivor beyond the list (rare) gets its backward entry at once.
+template <bool STAGED>
+__device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restrict__ agf, uint32_t rr_base,
+                                          uint32_t wmax, uint32_t w, uint32_t i, unsigned long long mxy,
+                                          unsigned long long mzr, int& cnt, uint32_t& extra, uint32_t* __restrict__ bwd,
+                                          uint32_t* __restrict__ bcnt) {
+  const int lane = threadIdx.x & 31;
+  uint2 cur = sm.rr[0][lane];
+  uint32_t q = cur.x, e = cur.y;
+  uint2 nx = sm.rr[1][lane];
+  uint32_t kaddr = rr_base + 2u * 256u;  // address of the run after nx
+  for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
+    uint32_t qs[NSLOT];
+    bool ok[NSLOT];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+      ok[t] = s0 + t < w;
+      qs[t] = ok[t] ? q : 0u;
+      ++q;
+      const uint32_t sw = q == e;
+      q = sw ? nx.x : q;
+      e = sw ? nx.y : e;
+      // predicated refill of the next run (no branch): nx = rr[k], k advanced on a switch
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.v2.u32 {%0, %1}, [%3];\n\t}"
+                   : "+r"(nx.x), "+r"(nx.y) : "r"(sw), "r"(kaddr));
+      kaddr += sw * 256u;
+    }
+    float4 o[NSLOT];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+#if BDM_HSTAGE
+      if (STAGED)
+        o[t] = sm.buf[qs[t]];
+      else
+#endif
+        o[t] = __ldg(&agf[qs[t]]);
+    }
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+      float2 dxy, dzs;
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
+          : "l"(mxy), "l"(pack2(o[t].x, o[t].y)));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dzs))
+          : "l"(mzr), "l"(pack2(o[t].z, o[t].w)));
+      float2 sq, qz;
+      asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&sq))
+          : "l"(*reinterpret_cast<unsigned long long*>(&dxy)));
+      asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&qz))
+          : "l"(*reinterpret_cast<unsigned long long*>(&dzs)));
+      const float d2 = (sq.x + sq.y) + qz.x;
+      if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) {
+        if (cnt < HLA) {
+          sm.list[cnt++][lane] = qs[t];
+        } else {  // rare: the partner still gets its backward entry
+          uint32_t j = qs[t];
+#if BDM_HSTAGE
+          if (STAGED) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int u = 1; u < 5; ++u) c += j >= sm.off[u] ? 1u : 0u;
+            j = j - sm.off[c] + sm.ub[c];
+          }
+#endif
+          const uint32_t sl = atomicAdd(&bcnt[j], 1u);
+          if (sl < (uint32_t)HBC) bwd[(size_t)j * HBC + sl] = i;
+          ++extra;
+        }
       }
     }
   }
-  cnt = 0;
 }
 
 __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
@@ -1029,6 +1148,11 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const uint32_t rr_base = (uint32_t)__cvta_generic_to_shared(&sm.rr[0][lane]);
+#if BDM_HSTAGE
+  uint32_t phase = 0;  // parity of this warp's staging mbarrier
+  if (lane == 0) mbar_init(&sm.bar);
+  __syncwarp();
+#endif
   while (true) {
     uint32_t chunk = 0;
     if (lane == 0) chunk = atomicAdd(&ext->work_a, 1u);
@@ -1101,6 +1225,42 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
       }
       __syncwarp();
     }
+    bool staged = false;
+#if BDM_HSTAGE
+    uint32_t stage_ub[5] = {0u, 0u, 0u, 0u, 0u}, stage_off[5] = {0u, 0u, 0u, 0u, 0u};
+    if (coop) {
+      // union runs of the 5 forward columns over the chunk: own column from box zf (the agents
+      // before a lane are never its candidates, but the union is simpler), the others from zf-1,
+      // all to the end of box zl+1.  If they fit, one lane copies them into sm.buf (TMA bulk
+      // copies, completing on the warp's mbarrier) while the lanes set up their runs.
+      uint32_t ub[5], off[6];
+      off[0] = 0u;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        ub[q] = sm.tab[q][q == 0 ? 1 : 0];
+        off[q + 1] = off[q] + (sm.tab[q][span - 1] - ub[q]);
+      }
+      staged = off[5] > 0u && off[5] <= (uint32_t)HPCAP;
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        stage_ub[q] = ub[q];
+        stage_off[q] = off[q];
+      }
+      if (staged && lane == 0) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          sm.off[q] = off[q];
+          sm.ub[q] = ub[q];
+        }
+        sm.off[5] = off[5];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&sm.bar, off[5] * 16u);
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+          if (off[q + 1] > off[q]) bulk_g2s(&sm.buf[off[q]], agf + ub[q], (off[q + 1] - off[q]) * 16u, &sm.bar);
+      }
+    }
+#endif
     // this lane's forward z-runs in canonical (= ascending sorted) order
     int nr = 0;
     uint32_t w = 0;
@@ -1120,6 +1280,13 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
         }
         if (q == 0) b = i + 1;  // own box: only the agents after i
         if (b < e) {
+#if BDM_HSTAGE
+          if (staged) {  // the run in buffer indices of its column's union run
+            const uint32_t d = stage_ub[q] - stage_off[q];
+            b -= d;
+            e -= d;
+          }
+#endif
           sm.rr[nr][lane] = make_uint2(b, e);
           w += e - b;
           ++nr;
@@ -1132,49 +1299,29 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     const float ri32 = __double2float_ru(ri + g.m32);
     const unsigned long long mxy = pack2(mf.x, mf.y), mzr = pack2(mf.z, ri32);
     int cnt = 0;
-    uint32_t nf = 0;
-    uint2 cur = sm.rr[0][lane];
-    uint32_t q = cur.x, e = cur.y;
-    uint2 nx = sm.rr[1][lane];
-    uint32_t kaddr = rr_base + 2u * 256u;  // address of the run after nx
-    for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
-      uint32_t qs[NSLOT];
-      bool ok[NSLOT];
+    uint32_t extra = 0;  // survivors beyond the buffer (forward row overflow: pass B's slow path)
+#if BDM_HSTAGE
+    if (staged) {
+      mbar_wait(&sm.bar, phase);
+      phase ^= 1u;
+      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+      // buffer index -> global sorted index (each union run is contiguous in both)
+      for (int x = 0; x < cnt; ++x) {
+        const uint32_t v = sm.list[x][lane];
+        uint32_t c = 0;
 #pragma unroll
-      for (int t = 0; t < NSLOT; ++t) {
-        ok[t] = s0 + t < w;
-        qs[t] = ok[t] ? q : 0u;
-        ++q;
-        const uint32_t sw = q == e;
-        q = sw ? nx.x : q;
-        e = sw ? nx.y : e;
-        // predicated refill of the next run (no branch): nx = rr[k], k advanced on a switch
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.v2.u32 {%0, %1}, [%3];\n\t}"
-                     : "+r"(nx.x), "+r"(nx.y) : "r"(sw), "r"(kaddr));
-        kaddr += sw * 256u;
+        for (int q = 1; q < 5; ++q) c += v >= sm.off[q] ? 1u : 0u;
+        sm.list[x][lane] = v - sm.off[c] + sm.ub[c];
       }
-      float4 o[NSLOT];
-#pragma unroll
-      for (int t = 0; t < NSLOT; ++t) o[t] = __ldg(&agf[qs[t]]);
-#pragma unroll
-      for (int t = 0; t < NSLOT; ++t) {
-        float2 dxy, dzs;
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
-            : "l"(mxy), "l"(pack2(o[t].x, o[t].y)));
-        asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dzs))
-            : "l"(mzr), "l"(pack2(o[t].z, o[t].w)));
-        float2 sq, qz;
-        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&sq))
-            : "l"(*reinterpret_cast<unsigned long long*>(&dxy)));
-        asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&qz))
-            : "l"(*reinterpret_cast<unsigned long long*>(&dzs)));
-        const float d2 = (sq.x + sq.y) + qz.x;
-        if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) sm.list[cnt++][lane] = qs[t];
-      }
-      if (__any_sync(FULL, cnt > HLA - NSLOT)) half_emit(sm, lane, cnt, i, nf, fwd, bwd, bcnt);
+      __syncwarp();  // every lane is done with buf before the next chunk's copies overwrite it
+    } else
+#endif
+      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+    if (valid) {
+      half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
+      const uint32_t nf = (uint32_t)cnt + extra;
+      fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
     }
-    half_emit(sm, lane, cnt, i, nf, fwd, bwd, bcnt);
-    if (valid) fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
     __syncwarp();
   }
 }
@@ -1188,7 +1335,7 @@ constexpr size_t HB_SMEM_BYTES = sizeof(HalfBSmem) * FORCE_WARPS;
 
 // Full canonical 27-box sum of agent i (O3-O5 as written): the overflow path of pass B.
 __device__ __noinline__ void full_force(const GridDev& g, const double4* __restrict__ ag, const uint32_t* __restrict__ ids,
-                                        const ParamsDev& p, uint32_t i, double4 me, uint32_t myid, double& Fx,
+                                        const ParamsDev& p, uint32_t i, double4 me, double& Fx,
                                         double& Fy, double& Fz) {
   const double ri = 0.5 * me.w;
   const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
@@ -1201,7 +1348,7 @@ __device__ __noinline__ void full_force(const GridDev& g, const double4* __restr
     for (uint32_t j = b; j < e; ++j) {
       if (j == i) continue;
       double tx, ty, tz, fa;
-      if (pair_term(me.x, me.y, me.z, ri, myid, ag[j], ids[j], p, tx, ty, tz, fa)) {
+      if (pair_term(me.x, me.y, me.z, ri, i, ag[j], ids, j, p, tx, ty, tz, fa)) {
         Fx = Fx + tx;
         Fy = Fy + ty;
         Fz = Fz + tz;
@@ -1210,7 +1357,7 @@ __device__ __noinline__ void full_force(const GridDev& g, const double4* __restr
   }
 }
 
-__global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
+__global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     k_half_sum(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t a_begin, uint32_t a_end,
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
@@ -1229,27 +1376,55 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     if (base >= a_end) break;
     const uint32_t i = (uint32_t)base + lane;
     const bool valid = i < a_end;
+    // the agent and both counts, then the first 4 entries of each non-empty row (one vector load;
+    // entries past a count are stale and ignored)
+    const uint4* brow = reinterpret_cast<const uint4*>(bwd + (size_t)i * HBC);
+    const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
     const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const uint32_t myid = valid ? ids[i] : 0u;
-    const double ri = 0.5 * me.w;
     const uint32_t nf = valid ? fcnt[i] : 0u;
     const uint32_t nb = valid ? bcnt[i] : 0u;
+    // (rows are read only where the count says so: a speculative read of every row costs more DRAM
+    // traffic than the round trip it saves)
+    const uint4 b4 = nb ? __ldg(brow) : make_uint4(0u, 0u, 0u, 0u);
+    const uint4 f4 = nf ? __ldg(frow) : make_uint4(0u, 0u, 0u, 0u);
+    const double ri = 0.5 * me.w;
     const bool slow = nf > (uint32_t)HFC || nb > (uint32_t)HBC;
     int cnt = 0;
     if (!slow) {
       // backward partners (all < i) sorted ascending, then forward partners (all > i, ascending)
-      const uint32_t* brow = bwd + (size_t)i * HBC;
-      for (uint32_t t = 0; t < nb; ++t) {
-        const uint32_t v = brow[t];
+      uint32_t* col = &sm.list[0][lane];
+      col[0] = b4.x;
+      col[32] = b4.y;
+      col[64] = b4.z;
+      col[96] = b4.w;
+      for (uint32_t v = 1; 4 * v < nb; ++v) {
+        const uint4 t4 = __ldg(brow + v);
+        col[32 * (4 * v)] = t4.x;
+        col[32 * (4 * v + 1)] = t4.y;
+        col[32 * (4 * v + 2)] = t4.z;
+        col[32 * (4 * v + 3)] = t4.w;
+      }
+      for (uint32_t t = 1; t < nb; ++t) {  // insertion sort (rows hold a handful of entries)
+        const uint32_t v = col[32 * t];
         int x = (int)t;
-        while (x > 0 && sm.list[x - 1][lane] > v) {
-          sm.list[x][lane] = sm.list[x - 1][lane];
+        while (x > 0 && col[32 * (x - 1)] > v) {
+          col[32 * x] = col[32 * (x - 1)];
           --x;
         }
-        sm.list[x][lane] = v;
+        col[32 * x] = v;
       }
-      const uint32_t* frow = fwd + (size_t)i * HFC;
-      for (uint32_t t = 0; t < nf; ++t) sm.list[nb + t][lane] = frow[t];
+      uint32_t* fc = col + 32 * nb;
+      if (nf > 0) fc[0] = f4.x;
+      if (nf > 1) fc[32] = f4.y;
+      if (nf > 2) fc[64] = f4.z;
+      if (nf > 3) fc[96] = f4.w;
+      for (uint32_t v = 1; 4 * v < nf; ++v) {
+        const uint4 t4 = __ldg(frow + v);
+        const uint32_t u[4] = {t4.x, t4.y, t4.z, t4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (4 * v + k < nf) fc[32 * (4 * v + k)] = u[k];
+      }
       cnt = (int)(nb + nf);
     }
     __syncwarp();
@@ -1257,9 +1432,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     int32_t n_ct = 0;
     unsigned long long ct_hash = 0;
     if (__any_sync(FULL, cnt > 0))
-      flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, myid, ag, ids, p, Fx, Fy, Fz, n_ct,
+      flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct,
                                        ct_hash);
-    if (slow) full_force(g, ag, ids, p, i, me, myid, Fx, Fy, Fz);
+    if (slow) full_force(g, ag, ids, p, i, me, Fx, Fy, Fz);
     // O6 displacement, O7 update (as k_force)
     double dpx = 0.0, dpy = 0.0, dpz = 0.0;
     const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
@@ -1275,16 +1450,16 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       dpz = Fz * p.c;
     }
     if (valid) {
-      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, myid);
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
       ag_out[o] = np;
-      if (id_out) id_out[o] = myid;
+      if (id_out) id_out[o] = ids[i];
       if (dp_out) {
         dp_out[3 * (size_t)o] = dpx;
         dp_out[3 * (size_t)o + 1] = dpy;
         dp_out[3 * (size_t)o + 2] = dpz;
-        if (dp_id_out) dp_id_out[o] = myid;
+        if (dp_id_out) dp_id_out[o] = ids[i];
       }
       const int nb3[3] = {box_coord(np.x, g.inv, ebad), box_coord(np.y, g.inv, ebad), box_coord(np.z, g.inv, ebad)};
 #pragma unroll
@@ -1811,7 +1986,7 @@ __global__ void k_pairs(const double4* __restrict__ ag, const uint32_t* __restri
       if (!(d2 <= g.L2)) continue;
       if (kind == 1) {
         double tx, ty, tz, fa;
-        if (!pair_term(me.x, me.y, me.z, ri, myid, o, idj, p, tx, ty, tz, fa)) continue;
+        if (!pair_term(me.x, me.y, me.z, ri, i, o, ids, q, p, tx, ty, tz, fa)) continue;
       }
       if (out) {
         out[2 * w] = myid;
