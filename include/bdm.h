@@ -196,6 +196,13 @@ int bdm_get_count(bdm_handle h, int64_t* out2);
  * available (no step yet, or the flag is off). */
 int bdm_get_skip_stats(bdm_handle h, int64_t* out3);
 
+/* Force path of the last step: out2[0] = 1 if it ran the half-shell pair path
+ * (k_half_search + k_half_sum: each candidate pair tested once, Newton's third law), 0 if the
+ * single-pass k_force (BDM_RECORD, BDM_SKIP_STATIONARY, neurites, BDM_HALF=0, or the pair rows
+ * could not be allocated); out2[1] = agents of that step whose pair rows overflowed and took the
+ * exact full-search path (results are identical either way).  -1 entries before the first step. */
+int bdm_get_path_stats(bdm_handle h, int64_t* out2);
+
 /* Issue all later work on this CUDA stream (cudaStream_t; NULL = legacy default stream). */
 int bdm_set_stream(bdm_handle h, void* cuda_stream);
 

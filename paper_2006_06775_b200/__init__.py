@@ -86,6 +86,7 @@ _SIGS = {
     "bdm_get_pairs": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, ctypes.c_int64], ctypes.c_int),
     "bdm_set_agents": ([_vp, _vp, _vp], ctypes.c_int),
     "bdm_get_skip_stats": ([_vp, _vp], ctypes.c_int),
+    "bdm_get_path_stats": ([_vp, _vp], ctypes.c_int),
     "bdm_set_growth": ([_vp, ctypes.c_double, ctypes.c_double, ctypes.c_uint64], ctypes.c_int),
     "bdm_reserve": ([_vp, ctypes.c_int64], ctypes.c_int),
     "bdm_set_neurites": ([_vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _vp, _vp, ctypes.c_double], ctypes.c_int),
@@ -386,6 +387,14 @@ def bdm_get_skip_stats(h: Handle) -> dict:
     out = np.zeros(3, np.int64)
     _check(load_library().bdm_get_skip_stats(h.raw, _ptr(out)), h.raw)
     return dict(moved=int(out[0]), searched=int(out[1]), n=int(out[2]))
+
+
+def bdm_get_path_stats(h: Handle) -> dict:
+    """Force path of the last step: half-shell pair path used (1/0), agents that overflowed their
+    pair rows and took the exact full-search path."""
+    out = np.zeros(2, np.int64)
+    _check(load_library().bdm_get_path_stats(h.raw, _ptr(out)), h.raw)
+    return dict(half=int(out[0]), slow=int(out[1]))
 
 
 def bdm_set_timing(h: Handle, enabled: bool = True) -> None:

@@ -126,6 +126,7 @@ struct bdm_ctx {
   uint8_t* h_fcnt = nullptr;
   int64_t h_cap = 0;
   bool half_off = false;  // BDM_HALF=0, or the rows could not be allocated: k_force only
+  bool last_half = false;  // the last step used the half-shell path
   int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
   std::vector<TimedStep> timed;
@@ -485,7 +486,8 @@ int force_step(bdm_ctx* h, bool want_dp) {
   ParamsDev pd = params_dev(h->prm);
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
-  if (!(h->prm.flags & BDM_RECORD) && !h->skip_active && !h->hist[0] && n > 0 && ensure_half(h)) {
+  h->last_half = !(h->prm.flags & BDM_RECORD) && !h->skip_active && !h->hist[0] && n > 0 && ensure_half(h);
+  if (h->last_half) {
     int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr);
     if (rc) return rc;
   } else if (h->prm.flags & BDM_RECORD)
@@ -1701,6 +1703,21 @@ int bdm_get_skip_stats(bdm_handle h, int64_t* out3) {
   out3[0] = h->hist[0] ? (int64_t)h->ext_host->moved : -1;
   out3[1] = h->hist[0] ? (int64_t)h->ext_host->searched : -1;
   out3[2] = h->n;
+  return BDM_OK;
+}
+
+int bdm_get_path_stats(bdm_handle h, int64_t* out2) {
+  if (!h || !out2) return fail(h, BDM_EINVAL, "bdm_get_path_stats: NULL argument");
+  CU(h, cudaSetDevice(h->device));
+  if (!h->ext_valid || h->state != State::Stepped) {
+    out2[0] = out2[1] = -1;
+    return BDM_OK;
+  }
+  CU(h, cudaMemcpyAsync(h->ext_host, h->ext, sizeof(Extents), cudaMemcpyDeviceToHost, h->stream));
+  int rc = check_async(h);
+  if (rc) return rc;
+  out2[0] = h->last_half ? 1 : 0;
+  out2[1] = h->last_half ? (int64_t)h->ext_host->slow : 0;
   return BDM_OK;
 }
 

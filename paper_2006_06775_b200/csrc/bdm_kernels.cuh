@@ -58,6 +58,7 @@ struct Extents {
   uint32_t moved;     // agents with dp != 0 in the step that produced these extents (skip mode)
   uint32_t searched;  // agents whose neighbourhood was searched in that step (skip mode)
   uint32_t work_a;    // chunk counter of the half-shell search pass (k_half_search)
+  uint32_t slow;      // agents of the half-shell sum pass whose pair rows overflowed (full search)
 };
 
 struct ErrDev {
@@ -197,6 +198,7 @@ __global__ void k_ext_reset(Extents* ext) {
   if (threadIdx.x == 5) ext->moved = 0u;
   if (threadIdx.x == 6) ext->searched = 0u;
   if (threadIdx.x == 7) ext->work_a = 0u;
+  if (threadIdx.x == 8) ext->slow = 0u;
 }
 
 __device__ __forceinline__ uint32_t col_of(const GridDev& g, int bx, int by) {
@@ -1435,6 +1437,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct,
                                        ct_hash);
     if (slow) full_force(g, ag, ids, p, i, me, Fx, Fy, Fz);
+    {
+      const unsigned sm_ = __ballot_sync(FULL, slow);
+      if (sm_ && lane == 0) atomicAdd(&ext_next->slow, (uint32_t)__popc(sm_));
+    }
     // O6 displacement, O7 update (as k_force)
     double dpx = 0.0, dpy = 0.0, dpz = 0.0;
     const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
