@@ -1648,7 +1648,14 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
   ParamsDev pd = params_dev(h->prm);
   const unsigned grid = force_grid(h, (uint32_t)n_own);
-  if (n_own > 0) {
+  h->last_half = n_own > 0 && ensure_half(h);
+  if (h->last_half) {
+    // pass A from the first lower ghost (their forward pairs with owned agents are the owned
+    // agents' backward pairs); owned agents' forward runs reach into the upper ghosts
+    rc = half_force(h, src, 0u, (uint32_t)n_lo, (uint32_t)(n_tot - n_hi), (uint32_t)n_tot, pd, h->ag[dst], h->id[dst],
+                    want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr);
+    if (rc) return rc;
+  } else if (n_own > 0) {
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
                                                  (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
