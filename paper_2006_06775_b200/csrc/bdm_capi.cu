@@ -78,7 +78,14 @@ struct bdm_ctx {
   // ragged box table
   int32_t *czlo = nullptr, *czhi = nullptr;
   uint32_t* coff = nullptr;
-  size_t col_cap = 0;
+  size_t col_cap = 0, coff_cap = 0;
+  // next build's column z-ranges, accumulated by the half-shell sum pass (fused column pass):
+  // frame [nlo[0], nlo[0]+nnx) x [nlo[1], nlo[1]+nny) = tight extents of the step start +- 1 box
+  int32_t *czlo2 = nullptr, *czhi2 = nullptr;
+  size_t col2_cap = 0;
+  bool cols_next = false;
+  int32_t nlo[2] = {0, 0}, nnx = 0, nny = 0;
+  int32_t tlo[3] = {0, 0, 0}, thi[3] = {0, 0, 0};  // tight extents of the last build (reported)
   int scan_blocks_per_sm = 0;
   // x-slab mode (multi-GPU)
   bool slab = false;
@@ -230,17 +237,26 @@ int ensure_table(bdm_ctx* h, size_t entries, size_t min_scan_items) {
   return BDM_OK;
 }
 
-int ensure_columns(bdm_ctx* h, size_t entries) {
-  if (entries > h->col_cap) {
-    for (void* p : {(void*)h->czlo, (void*)h->czhi, (void*)h->coff})
+// Column arrays for `entries` columns: z-range pair czlo/czhi (second: the next build's pair
+// czlo2/czhi2, filled by the fused column pass) and the offsets coff (own capacity: the pairs swap).
+int ensure_columns(bdm_ctx* h, size_t entries, bool second = false) {
+  int32_t** lo = second ? &h->czlo2 : &h->czlo;
+  int32_t** hi = second ? &h->czhi2 : &h->czhi;
+  size_t* capp = second ? &h->col2_cap : &h->col_cap;
+  const size_t cap = entries + entries / 4 + (1u << 16);
+  if (entries > *capp) {
+    for (void* p : {(void*)*lo, (void*)*hi})
       if (p) CU(h, cudaFree(p));
-    h->czlo = h->czhi = nullptr;
+    *lo = *hi = nullptr;
+    CU(h, cudaMalloc(lo, cap * sizeof(int32_t)));
+    CU(h, cudaMalloc(hi, cap * sizeof(int32_t)));
+    *capp = cap;
+  }
+  if (!second && entries > h->coff_cap) {
+    if (h->coff) CU(h, cudaFree(h->coff));
     h->coff = nullptr;
-    size_t cap = entries + entries / 4 + (1u << 16);
-    CU(h, cudaMalloc(&h->czlo, cap * sizeof(int32_t)));
-    CU(h, cudaMalloc(&h->czhi, cap * sizeof(int32_t)));
     CU(h, cudaMalloc(&h->coff, cap * sizeof(uint32_t)));
-    h->col_cap = cap;
+    h->coff_cap = cap;
   }
   return BDM_OK;
 }
@@ -295,8 +311,29 @@ bool ensure_half(bdm_ctx* h) {
 // from s_begin (slab mode: the lower ghost layer searches too, its pairs with owned agents are
 // forward pairs of the ghost).
 int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t a_end, uint32_t n_all,
-               const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids) {
+               const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids,
+               bool fuse_cols = false) {
   cudaStream_t s = h->stream;
+  ColNext cn{0, 0, 0, 0, nullptr, nullptr};
+  h->cols_next = false;
+  if (fuse_cols) {  // next build's frame: this step's tight extents +- 1 box (|dp| < L)
+    cn.lo0 = h->tlo[0] - 1;
+    cn.lo1 = h->tlo[1] - 1;
+    cn.nx = h->thi[0] - h->tlo[0] + 3;
+    cn.ny = h->thi[1] - h->tlo[1] + 3;
+    const size_t nc2 = (size_t)cn.nx * (size_t)cn.ny;
+    int rc = ensure_columns(h, nc2 + 1, true);
+    if (rc) return rc;
+    cn.czlo = h->czlo2;
+    cn.czhi = h->czhi2;
+    const unsigned gs = (unsigned)std::min<uint64_t>((nc2 + 256) / 256, 148u * 16u);
+    k_col_reset<<<gs, 256, 0, s>>>(h->czlo2, h->czhi2, (uint32_t)nc2);
+    h->launches += 1;
+    h->nlo[0] = cn.lo0;
+    h->nlo[1] = cn.lo1;
+    h->nnx = cn.nx;
+    h->nny = cn.ny;
+  }
   CU(h, cudaMemsetAsync(h->h_bcnt, 0, (size_t)std::max<uint32_t>(n_all, 1) * sizeof(uint32_t), s));
   const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
                                                    std::max<uint64_t>(1, (a_end - s_begin + HA_THREADS - 1) / HA_THREADS));
@@ -307,10 +344,11 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
                                                    std::max<uint64_t>(1, (a_end - a_begin + FORCE_THREADS - 1) / FORCE_THREADS));
   k_half_sum<<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd, ag_out,
                                                        id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt,
-                                                       h->h_bwd, h->h_bcnt);
+                                                       h->h_bwd, h->h_bcnt, cn);
   DBG(h, "k_half_sum");
   CU(h, cudaGetLastError());
   h->launches += 2;
+  h->cols_next = fuse_cols;
   return BDM_OK;
 }
 
@@ -363,10 +401,24 @@ int compute_extents(bdm_ctx* h) {
   GridDev& g = h->grid;
   int64_t dims[3];
   for (int a = 0; a < 3; ++a) {
-    g.lo[a] = h->ext_host->lo[a];
-    g.hi[a] = h->ext_host->hi[a];
-    dims[a] = (int64_t)g.hi[a] - g.lo[a] + 1;
+    g.lo[a] = h->tlo[a] = h->ext_host->lo[a];
+    g.hi[a] = h->thi[a] = h->ext_host->hi[a];
   }
+  // fused column pass of the last step: its frame (tight extents of that step's start +- 1 box)
+  // becomes this grid's x/y frame; it contains every box by construction (|dp| < L), verified
+  if (h->cols_next) {
+    const bool inside = h->ext_host->col_bad == 0u && g.lo[0] >= h->nlo[0] && g.lo[1] >= h->nlo[1] &&
+                        g.hi[0] < h->nlo[0] + h->nnx && g.hi[1] < h->nlo[1] + h->nny;
+    if (inside) {
+      g.lo[0] = h->nlo[0];
+      g.lo[1] = h->nlo[1];
+      g.hi[0] = h->nlo[0] + h->nnx - 1;
+      g.hi[1] = h->nlo[1] + h->nny - 1;
+    } else {
+      h->cols_next = false;
+    }
+  }
+  for (int a = 0; a < 3; ++a) dims[a] = (int64_t)g.hi[a] - g.lo[a] + 1;
   int64_t nb = dims[0] * dims[1] * dims[2];
   if (nb >= (int64_t)0xffffffffll) return fail(h, BDM_ERANGE, "n_boxes = %lld >= 2^32", (long long)nb);
   g.ny = (int32_t)dims[1];
@@ -405,10 +457,23 @@ int sort_into(bdm_ctx* h, uint32_t n) {
   const int src = h->cur, dst = 1 - h->cur;
   init_device_info(h);
   const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
-  k_col_reset<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols);
-  DBG(h, "k_col_reset");
-  if (n > 0) k_col_ext<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
-  DBG(h, "k_col_ext");
+  if (h->cols_next) {  // z-ranges already accumulated by the last step's sum pass
+    std::swap(h->czlo, h->czlo2);
+    std::swap(h->czhi, h->czhi2);
+    std::swap(h->col_cap, h->col2_cap);
+    h->cols_next = false;
+    rc = ensure_columns(h, nc + 1);  // no-op for the swapped pair (sized for this frame by force_step)
+    if (rc) return rc;
+    g.czlo = h->czlo;
+    g.czhi = h->czhi;
+    g.coff = h->coff;
+    h->launches -= 2;
+  } else {
+    k_col_reset<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols);
+    DBG(h, "k_col_reset");
+    if (n > 0) k_col_ext<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
+    DBG(h, "k_col_ext");
+  }
   k_col_len<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols, h->coff);
   DBG(h, "k_col_len");
   rc = scan(h, h->coff, nc + 1, nullptr);  // exclusive: coff[c] = table offset, coff[nc] = T
@@ -487,8 +552,13 @@ int force_step(bdm_ctx* h, bool want_dp) {
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
   h->last_half = !(h->prm.flags & BDM_RECORD) && !h->skip_active && !h->hist[0] && n > 0 && ensure_half(h);
+  h->cols_next = false;
   if (h->last_half) {
-    int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr);
+    // fuse the next build's column pass when nothing moves agents between this step and that build
+    // and one step moves an agent by less than a box (|dp| <= max_disp (1 + 4u) < L)
+    const bool fuse = !h->growth_on && !h->fields_on && h->n_el == 0 && !h->slab &&
+                      h->prm.max_disp < h->grid.L * (1.0 - 0x1p-20);
+    int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr, fuse);
     if (rc) return rc;
   } else if (h->prm.flags & BDM_RECORD)
     k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
@@ -581,6 +651,7 @@ int fields_step(bdm_ctx* h) {
   h->launches += 3 + (n ? 2 : 0);
   // the agents moved: new extents and a fresh grid are needed
   h->ext_valid = false;
+  h->cols_next = false;
   h->skip_valid = false;
   if (h->state == State::Fresh) h->state = State::Stepped;
   return BDM_OK;
@@ -623,6 +694,7 @@ int grow_divide_step(bdm_ctx* h) {
   h->grid.inv = 1.0 / (L * (1.0 + 0x1p-30));
   h->grid.thr_pad = 0.5 * L;
   h->ext_valid = false;  // extents were reduced with the old box edge
+  h->cols_next = false;
   h->skip_valid = false;
   return BDM_OK;
 }
@@ -654,6 +726,7 @@ int neurite_step(bdm_ctx* h, bool want_dp) {
   if (h->grid.L != L) {
     set_box_edge(h->grid, L);
     h->ext_valid = false;
+    h->cols_next = false;
     if (h->state == State::Fresh) h->state = State::Stepped;
   }
   if ((rc = grid_build(el))) return fail(h, rc, "element grid: %s", el->error.c_str());
@@ -721,6 +794,7 @@ int upload(bdm_ctx* h, const double* pos, const double* diam) {
   h->have_dp = false;
   h->have_record = false;
   h->ext_valid = false;
+  h->cols_next = false;
   h->skip_valid = false;
   h->step_count = 0;
   h->n_dp = 0;
@@ -799,7 +873,7 @@ void bdm_destroy(bdm_handle h) {
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
-                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt};
+                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->czlo2, h->czhi2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->ext_host) cudaFreeHost(h->ext_host);
@@ -1112,6 +1186,7 @@ int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const dou
   h->el = el;
   h->state = State::NoGrid;
   h->ext_valid = false;
+  h->cols_next = false;
   return BDM_OK;
 }
 
@@ -1270,9 +1345,9 @@ int bdm_get_grid_info(bdm_handle h, bdm_grid_info* out) {
   out->L2 = h->grid.L2;
   out->inv = h->grid.inv;
   int64_t nb = h->n ? 1 : 1;
-  for (int a = 0; a < 3; ++a) {
-    out->lo[a] = h->n ? h->grid.lo[a] : 0;
-    out->hi[a] = h->n ? h->grid.hi[a] : 0;
+  for (int a = 0; a < 3; ++a) {  // tight extents (a fused build's x/y frame is one box wider)
+    out->lo[a] = h->n ? (h->slab ? h->grid.lo[a] : h->tlo[a]) : 0;
+    out->hi[a] = h->n ? (h->slab ? h->grid.hi[a] : h->thi[a]) : 0;
     nb *= (int64_t)out->hi[a] - out->lo[a] + 1;
   }
   out->n_boxes = nb;
@@ -1480,6 +1555,7 @@ int bdm_slab_load(bdm_handle h, int64_t n_local, const uint32_t* ids, const doub
   h->cur = 0;
   h->n = n_local;
   h->ext_valid = false;
+  h->cols_next = false;
   h->have_dp = false;
   h->n_dp = 0;
   h->state = State::NoGrid;
@@ -1510,6 +1586,7 @@ int bdm_slab_set_box_edge(bdm_handle h, double L) {
   h->grid.inv = 1.0 / (L * (1.0 + 0x1p-30));
   h->grid.thr_pad = 0.5 * L;
   h->ext_valid = false;
+  h->cols_next = false;
   h->have_grid = true;
   return BDM_OK;
 }

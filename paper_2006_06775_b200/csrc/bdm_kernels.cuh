@@ -59,6 +59,15 @@ struct Extents {
   uint32_t searched;  // agents whose neighbourhood was searched in that step (skip mode)
   uint32_t work_a;    // chunk counter of the half-shell search pass (k_half_search)
   uint32_t slow;      // agents of the half-shell sum pass whose pair rows overflowed (full search)
+  uint32_t col_bad;   // fused column pass: some agent's new box left its frame (columns invalid)
+};
+
+// Fused column pass (k_half_sum): occupied z-range of every column (bx, by) of the NEXT build's
+// frame [lo0, lo0+nx) x [lo1, lo1+ny), accumulated from the stepped positions (czlo = nullptr: off).
+struct ColNext {
+  int32_t lo0, lo1, nx, ny;
+  int32_t* czlo;
+  int32_t* czhi;
 };
 
 struct ErrDev {
@@ -199,6 +208,7 @@ __global__ void k_ext_reset(Extents* ext) {
   if (threadIdx.x == 6) ext->searched = 0u;
   if (threadIdx.x == 7) ext->work_a = 0u;
   if (threadIdx.x == 8) ext->slow = 0u;
+  if (threadIdx.x == 9) ext->col_bad = 0u;
 }
 
 __device__ __forceinline__ uint32_t col_of(const GridDev& g, int bx, int by) {
@@ -1364,7 +1374,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
                const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
-               const uint32_t* __restrict__ bcnt) {
+               const uint32_t* __restrict__ bcnt, ColNext cn) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1455,6 +1465,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       dpy = Fy * p.c;
       dpz = Fz * p.c;
     }
+    int nb3[3] = {INT32_MAX, INT32_MAX, INT32_MAX};  // box of p'
     if (valid) {
       if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
@@ -1467,12 +1478,33 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
         dp_out[3 * (size_t)o + 2] = dpz;
         if (dp_id_out) dp_id_out[o] = ids[i];
       }
-      const int nb3[3] = {box_coord(np.x, g.inv, ebad), box_coord(np.y, g.inv, ebad), box_coord(np.z, g.inv, ebad)};
+      nb3[0] = box_coord(np.x, g.inv, ebad);
+      nb3[1] = box_coord(np.y, g.inv, ebad);
+      nb3[2] = box_coord(np.z, g.inv, ebad);
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         elo[a] = min(elo[a], nb3[a]);
         ehi[a] = max(ehi[a], nb3[a]);
       }
+    }
+    if (cn.czlo) {  // fused column pass (warp-aggregated: a chunk touches one or two columns)
+      uint32_t c = 0xffffffffu;
+      bool out = false;
+      if (valid) {
+        const int ux = nb3[0] - cn.lo0, uy = nb3[1] - cn.lo1;
+        if (ux >= 0 && ux < cn.nx && uy >= 0 && uy < cn.ny)
+          c = (uint32_t)ux * (uint32_t)cn.ny + (uint32_t)uy;
+        else
+          out = true;
+      }
+      const unsigned peers = __match_any_sync(FULL, c);
+      const int zmin = __reduce_min_sync(peers, valid ? nb3[2] : INT32_MAX);
+      const int zmax = __reduce_max_sync(peers, valid ? nb3[2] : INT32_MIN);
+      if (c != 0xffffffffu && lane == __ffs(peers) - 1) {  // fire-and-forget reductions (RED)
+        atomicMin(&cn.czlo[c], zmin);
+        atomicMax(&cn.czhi[c], zmax);
+      }
+      if (__any_sync(FULL, out) && lane == 0) ext_next->col_bad = 1u;
     }
   }
   if (__any_sync(FULL, ebad) && lane == 0) ext_next->range_err = 1;
