@@ -279,12 +279,15 @@ def run_bdm(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_obj(args, n, 1),
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / fp64_peak, "traffic": traffic, "kernel": "k_force",
+                         "frac": achieved / fp64_peak, "traffic": traffic,
+                         "kernel": "force phase: k_half_search + k_half_sum" if tm["search_ms"] > 0 else "k_force",
                          "traffic_source": "profiles/r01_force_traffic.json" if traffic else None,
                          "ms_per_launch": force_s * 1e3,
-                         "note": "fp64-pipe ops (9/candidate + 44/contact + 40/agent, DESIGN.md §6.2) over the "
-                                 f"force kernel's event time; peak = 148 SM x 64 fp64 lanes x {sm_max:.0f} MHz "
-                                 f"({peak_kind} sm_max_mhz)",
+                         "passes_ms": {"search": tm["search_ms"] / max(tm["steps"], 1),
+                                       "sum": tm["sum_ms"] / max(tm["steps"], 1)},
+                         "note": "the method's fp64-pipe ops (9 per 27-box candidate + 44 per contact + 40 per "
+                                 "agent, DESIGN.md §6.2) over the force phase's event time (both passes); peak = "
+                                 f"148 SM x 64 fp64 lanes x {sm_max:.0f} MHz ({peak_kind} sm_max_mhz)",
                          "units": {"candidates": n_cand, "contacts": n_ct, "agents": n}},
             "roofline_rebuild": rebuild,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": tm["launches"],
@@ -333,7 +336,7 @@ def device_inputs(bdm, torch, cfg, n, dev, stream, scale_from=None):
 # rebuild kernels, algorithmic bytes per agent: column pass 32 | key + histogram
 # 32 + 8 | scatter 12 + 12 | place 12 + 32 gather + 32 + 4 + 16 (fp32 copy) = 192 B/agent (the
 # ragged box table adds ~12 B per box, not counted)
-REBUILD_BYTES_PER_AGENT = 192
+REBUILD_BYTES_PER_AGENT = 160  # key+hist 40, scatter 24, place 96 (column pass fused into the sum pass)
 
 
 def run_e2e(bdm, torch, pos_h, diam_h, local, args):

@@ -220,6 +220,10 @@ int bdm_set_agents(bdm_handle h, const double* pos, const double* diam);
  * launched (counted whether or not timing is enabled); then resets the sums. */
 int bdm_set_timing(bdm_handle h, int enabled);
 int bdm_get_timing(bdm_handle h, double* out4);
+/* As bdm_get_timing, plus the force phase split of the half-shell path:
+ * out6[4] ms of the search pass (row-counter and fused-column resets + k_half_search), out6[5] ms of
+ * the sum pass (k_half_sum); both 0 for steps that ran k_force.  Resets the sums. */
+int bdm_get_timing_ex(bdm_handle h, double* out6);
 
 /* Counter-based uniform population on the device (kernel K0; bdm_inputs/__init__.py holds the
  * NumPy twin): for ids [id0, id0+n): pos[i][a] = lo[a] + (hi[a]-lo[a])*u(seed, id, a),

@@ -98,6 +98,7 @@ _SIGS = {
     "bdm_sync": ([_vp], ctypes.c_int),
     "bdm_set_timing": ([_vp, ctypes.c_int], ctypes.c_int),
     "bdm_get_timing": ([_vp, _vp], ctypes.c_int),
+    "bdm_get_timing_ex": ([_vp, _vp], ctypes.c_int),
     "bdm_generate_uniform": ([ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, ctypes.c_double,
                               ctypes.c_double, _vp, _vp, _vp], ctypes.c_int),
     "bdm_slab_init": ([ctypes.POINTER(_vp), ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp,
@@ -402,10 +403,12 @@ def bdm_set_timing(h: Handle, enabled: bool = True) -> None:
 
 
 def bdm_get_timing(h: Handle) -> dict:
-    """Device ms of the grid-build and force kernels summed over the steps since the last call."""
-    out = np.zeros(4)
-    _check(load_library().bdm_get_timing(h.raw, _ptr(out)), h.raw)
-    return dict(grid_ms=float(out[0]), force_ms=float(out[1]), steps=int(out[2]), launches=int(out[3]))
+    """Device ms of the grid-build and force kernels summed over the steps since the last call
+    (force split into the half-shell search and sum passes where that path ran)."""
+    out = np.zeros(6)
+    _check(load_library().bdm_get_timing_ex(h.raw, _ptr(out)), h.raw)
+    return dict(grid_ms=float(out[0]), force_ms=float(out[1]), steps=int(out[2]), launches=int(out[3]),
+                search_ms=float(out[4]), sum_ms=float(out[5]))
 
 
 def bdm_generate_uniform(seed: int, id0: int, n: int, lo3, hi3, dlo: float, dhi: float, pos, diam, stream=None):

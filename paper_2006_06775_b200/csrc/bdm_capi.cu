@@ -34,6 +34,7 @@ enum class State { NoGrid, Fresh, Stepped };
 
 struct TimedStep {
   cudaEvent_t e0, e1, e2;
+  cudaEvent_t e3 = nullptr;  // half-shell path: between the search and the sum pass
 };
 
 }  // namespace
@@ -342,6 +343,10 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   DBG(h, "k_half_search");
   const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
                                                    std::max<uint64_t>(1, (a_end - a_begin + FORCE_THREADS - 1) / FORCE_THREADS));
+  if (h->timing && !h->timed.empty() && !h->timed.back().e3) {
+    CU(h, cudaEventCreate(&h->timed.back().e3));
+    CU(h, cudaEventRecord(h->timed.back().e3, s));
+  }
   k_half_sum<<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd, ag_out,
                                                        id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt,
                                                        h->h_bwd, h->h_bcnt, cn);
@@ -870,6 +875,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e0);
     cudaEventDestroy(t.e1);
     cudaEventDestroy(t.e2);
+    if (t.e3) cudaEventDestroy(t.e3);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
@@ -1232,28 +1238,44 @@ int bdm_set_timing(bdm_handle h, int enabled) {
   return BDM_OK;
 }
 
-int bdm_get_timing(bdm_handle h, double* out4) {
-  if (!h || !out4) return fail(h, BDM_EINVAL, "bdm_get_timing: NULL argument");
+int bdm_get_timing_ex(bdm_handle h, double* out6) {
+  if (!h || !out6) return fail(h, BDM_EINVAL, "bdm_get_timing_ex: NULL argument");
   CU(h, cudaSetDevice(h->device));
   CU(h, cudaStreamSynchronize(h->stream));
-  double grid = 0.0, force = 0.0;
+  double grid = 0.0, force = 0.0, search = 0.0, sum = 0.0;
   for (auto& t : h->timed) {
-    float a = 0.f, b = 0.f;
+    float a = 0.f, b = 0.f, c = 0.f;
     CU(h, cudaEventElapsedTime(&a, t.e0, t.e1));
     CU(h, cudaEventElapsedTime(&b, t.e1, t.e2));
     grid += a;
     force += b;
+    if (t.e3) {
+      CU(h, cudaEventElapsedTime(&c, t.e1, t.e3));
+      search += c;
+      sum += b - c;
+      cudaEventDestroy(t.e3);
+    }
     cudaEventDestroy(t.e0);
     cudaEventDestroy(t.e1);
     cudaEventDestroy(t.e2);
   }
-  out4[0] = grid;
-  out4[1] = force;
-  out4[2] = (double)h->timed.size();
-  out4[3] = (double)h->launches;
+  out6[0] = grid;
+  out6[1] = force;
+  out6[2] = (double)h->timed.size();
+  out6[3] = (double)h->launches;
+  out6[4] = search;
+  out6[5] = sum;
   h->timed.clear();
   h->launches = 0;
   return BDM_OK;
+}
+
+int bdm_get_timing(bdm_handle h, double* out4) {
+  if (!out4) return fail(h, BDM_EINVAL, "bdm_get_timing: NULL argument");
+  double o[6];
+  int rc = bdm_get_timing_ex(h, o);
+  for (int k = 0; k < 4; ++k) out4[k] = rc ? 0.0 : o[k];
+  return rc;
 }
 
 int bdm_get_displacements(bdm_handle h, double* out) {

@@ -33,6 +33,8 @@ def launches(path):
 def kernel(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(raw)))
+    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+                         text=True).stdout
     for row in r[2:]:
         d = dict(zip(r[0], row))
         print("kernel:", d.get("Kernel Name", "")[:120])
@@ -50,25 +52,29 @@ def kernel(path):
               for k in d if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("per_issue_active.ratio")]
         st = [x for x in st if x[1] > 0.1]
         print("  stall reasons (warps per issue):", ", ".join(f"{k} {v:.2f}" for k, v in sorted(st, key=lambda x: -x[1])))
-    src = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
-                         text=True).stdout
-    rows = list(csv.reader(io.StringIO(src)))
-    if len(rows) > 2:
-        h = rows[1]
-        si, wi, ei = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-        def num(v):
-            try:
-                return int(float(v.replace(",", "")))
-            except ValueError:
-                return 0
+        # the source page holds one table per captured kernel, each starting with a "Kernel Name" row
+        for part in src.split('"Kernel Name"')[1:]:
+            rows = list(csv.reader(io.StringIO('"Kernel Name"' + part)))
+            base = lambda n: n.split("(")[0].split("<")[0].split("::")[-1].replace("void ", "").strip()
+            if len(rows) <= 2 or base(rows[0][1]) != base(d.get("Kernel Name", "")):
+                continue
+            h = rows[1]
+            si, wi, ei = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
 
-        data = [x for x in rows[2:] if len(x) > max(si, wi, ei)]
-        for x in data:
-            x[wi], x[ei] = num(x[wi]), num(x[ei])
-        tot = sum(x[wi] for x in data) or 1
-        print("  hottest SASS (share of stall samples):")
-        for x in sorted(data, key=lambda x: -x[wi])[:25]:
-            print(f"    {100 * x[wi] / tot:5.1f}%  exec {x[ei] / 1e6:8.2f}M  {x[si].strip()[:70]}")
+            def num(v):
+                try:
+                    return int(float(v.replace(",", "")))
+                except ValueError:
+                    return 0
+
+            data = [x for x in rows[2:] if len(x) > max(si, wi, ei)]
+            for x in data:
+                x[wi], x[ei] = num(x[wi]), num(x[ei])
+            tot = sum(x[wi] for x in data) or 1
+            print(f"  hottest SASS of {rows[0][1].split('(')[0].strip()} (share of its stall samples):")
+            for x in sorted(data, key=lambda x: -x[wi])[:20]:
+                print(f"    {100 * x[wi] / tot:5.1f}%  exec {x[ei] / 1e6:8.2f}M  {x[si].strip()[:70]}")
+            break
 
 
 if __name__ == "__main__":
