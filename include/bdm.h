@@ -196,7 +196,7 @@ int bdm_get_count(bdm_handle h, int64_t* out2);
  * available (no step yet, or the flag is off). */
 int bdm_get_skip_stats(bdm_handle h, int64_t* out3);
 
-/* Force path of the last step (DESIGN.md §6.5): out2[0] = 1 if it ran the half-shell pair path
+/* Force path of the last step (DESIGN.md §6.4): out2[0] = 1 if it ran the half-shell pair path
  * (k_half_search + k_half_sum: each candidate pair tested once, Newton's third law), 0 if the
  * single-pass k_force (BDM_RECORD, BDM_SKIP_STATIONARY, neurites, BDM_HALF=0, or the pair rows
  * could not be allocated); out2[1] = agents of that step whose pair rows overflowed and took the
@@ -220,7 +220,7 @@ int bdm_set_agents(bdm_handle h, const double* pos, const double* diam);
  * launched (counted whether or not timing is enabled); then resets the sums. */
 int bdm_set_timing(bdm_handle h, int enabled);
 int bdm_get_timing(bdm_handle h, double* out4);
-/* As bdm_get_timing, plus the force phase split of the half-shell path (DESIGN.md §6.5):
+/* As bdm_get_timing, plus the force phase split of the half-shell path (DESIGN.md §6.4):
  * out6[4] ms of the search pass (row-counter and fused-column resets + k_half_search), out6[5] ms of
  * the sum pass (k_half_sum); both 0 for steps that ran k_force.  Resets the sums. */
 int bdm_get_timing_ex(bdm_handle h, double* out6);

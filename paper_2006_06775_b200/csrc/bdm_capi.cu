@@ -129,7 +129,7 @@ struct bdm_ctx {
   bool skip_active = false;  // the pending force kernel uses hot flags
   uint32_t last_moved = 0, last_searched = 0;
   bool timing = false;
-  // half-shell force path (k_half_search + k_half_sum, DESIGN.md §6.5): pair rows, sized to cap
+  // half-shell force path (k_half_search + k_half_sum, DESIGN.md §6.4): pair rows, sized to cap
   uint32_t *h_fwd = nullptr, *h_bwd = nullptr, *h_bcnt = nullptr;
   uint8_t* h_fcnt = nullptr;
   int64_t h_cap = 0;

@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
 }
 
 // ------------------------------------------------------------------------------------------ K6h
-// Half-shell force path (DESIGN.md §6.5), used for plain steps (no statistics, no stationary-region
+// Half-shell force path (DESIGN.md §6.4), used for plain steps (no statistics, no stationary-region
 // skip, no neurites).  Newton's third law (R2: F_ji = -F_ij bit-exactly) lets each candidate pair
 // be TESTED once instead of twice:
 //   pass A, k_half_search: agent i walks only the half of its 27-box neighbourhood that follows it in

@@ -1,4 +1,4 @@
-"""Half-shell pair path (k_half_search + k_half_sum, DESIGN.md §6.5) against the CPU oracle.
+"""Half-shell pair path (k_half_search + k_half_sum, DESIGN.md §6.4) against the CPU oracle.
 
 The plain product step tests each candidate pair once (forward half of the 27 boxes) and sums every
 agent's contacts in canonical order from its backward/forward pair rows.  These tests pin:
