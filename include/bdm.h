@@ -274,6 +274,21 @@ int bdm_slab_local_extents(bdm_handle h, int32_t* lohi6);
 int bdm_slab_pack(bdm_handle h, int what, int32_t x_begin, int32_t x_end, double* send_lo, double* send_hi,
                   int64_t cap, int64_t* n_lo, int64_t* n_hi);
 
+/* Single-sync protocol, after a step: split the owned agents without a host round
+ * trip.  Emigrants (box-x left [x_begin, x_end)) go to the FRONT of send_lo / send_hi, the agents
+ * that stay are compacted (committed by bdm_slab_commit), and the stayers of the first / last box-x
+ * layer -- the neighbours' ghosts of the next step -- go to the BACK of send_lo / send_hi (record
+ * cap-1-k).  info (DEVICE int64[12], asynchronous): [0] emigrants lo, [1] halo lo, [2] emigrants hi,
+ * [3] halo hi, [4] stayers, [5..7] box extents lo of the owned agents' positions, [8..10] hi,
+ * [11] 1 if a buffer's cap records did not hold emigrants + halo (then resend with larger buffers
+ * through bdm_slab_pack).  ESTATE if a split is pending. */
+int bdm_slab_split(bdm_handle h, int32_t x_begin, int32_t x_end, double* send_lo, double* send_hi, int64_t cap,
+                   int64_t* info);
+
+/* Commit the pending split: the owned agents become the n_stay stayers (info[4] of the split);
+ * n_stay < 0 cancels it (owned agents unchanged, e.g. to split again with larger buffers). */
+int bdm_slab_commit(bdm_handle h, int64_t n_stay);
+
 /* Append received records (immigrants) to the owned agents.  ERANGE past the capacity. */
 int bdm_slab_add(bdm_handle h, const double* recv_lo, int64_t n_lo, const double* recv_hi, int64_t n_hi);
 

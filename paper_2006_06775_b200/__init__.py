@@ -110,6 +110,8 @@ _SIGS = {
     "bdm_slab_pack": ([_vp, ctypes.c_int, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_int64,
                        ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)], ctypes.c_int),
     "bdm_slab_add": ([_vp, _vp, ctypes.c_int64, _vp, ctypes.c_int64], ctypes.c_int),
+    "bdm_slab_split": ([_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp, ctypes.c_int64, _vp], ctypes.c_int),
+    "bdm_slab_commit": ([_vp, ctypes.c_int64], ctypes.c_int),
     "bdm_slab_step": ([_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                        ctypes.c_int], ctypes.c_int),
     "bdm_slab_get": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, _vp], ctypes.c_int),
@@ -477,6 +479,17 @@ def bdm_slab_pack(h: Handle, what: int, x_begin: int, x_end: int, send_lo, send_
     if rc not in (BDM_OK, BDM_ETRUNC):
         _check(rc, h.raw)
     return rc, nlo.value, nhi.value
+
+
+def bdm_slab_split(h: Handle, x_begin: int, x_end: int, send_lo, send_hi, cap: int, info) -> None:
+    """Asynchronous post-step split (emigrants front, halo back of send_*); counts into the DEVICE
+    int64[12] tensor info."""
+    _check(load_library().bdm_slab_split(h.raw, x_begin, x_end, _ptr(send_lo), _ptr(send_hi), cap, _ptr(info)),
+           h.raw)
+
+
+def bdm_slab_commit(h: Handle, n_stay: int) -> None:
+    _check(load_library().bdm_slab_commit(h.raw, int(n_stay)), h.raw)
 
 
 def bdm_slab_add(h: Handle, recv_lo, n_lo: int, recv_hi, n_hi: int) -> None:

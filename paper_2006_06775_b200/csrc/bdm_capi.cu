@@ -135,6 +135,7 @@ struct bdm_ctx {
   int64_t h_cap = 0;
   bool half_off = false;  // BDM_HALF=0, or the rows could not be allocated: k_force only
   bool last_half = false;  // the last step used the half-shell path
+  bool split_pending = false;  // slab: bdm_slab_split ran, bdm_slab_commit not yet
   int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
   std::vector<TimedStep> timed;
@@ -1533,7 +1534,7 @@ int bdm_slab_init(bdm_handle* out, int64_t n_local, int64_t capacity, const uint
   TRY(dalloc(h, &h->err, 1));
   TRY(dalloc(h, &h->maxd_bits, 1));
   TRY(dalloc(h, &h->scan_ticket, 1));
-  TRY(dalloc(h, &h->cnt, 4));
+  TRY(dalloc(h, &h->cnt, 8));
   if (cudaMallocHost(&h->ext_host, sizeof(Extents)) != cudaSuccess ||
       cudaMallocHost(&h->err_host, sizeof(ErrDev)) != cudaSuccess ||
       cudaMallocHost(&h->cnt_host, 4 * sizeof(uint32_t)) != cudaSuccess) {
@@ -1665,6 +1666,48 @@ int bdm_slab_pack(bdm_handle h, int what, int32_t x_begin, int32_t x_end, double
     h->cur = 1 - h->cur;
     h->n = h->cnt_host[2];
   }
+  return BDM_OK;
+}
+
+int bdm_slab_split(bdm_handle h, int32_t x_begin, int32_t x_end, double* send_lo, double* send_hi, int64_t cap,
+                   int64_t* info) {
+  int rc = slab_check(h, "bdm_slab_split");
+  if (rc) return rc;
+  if (!info || cap < 0 || (cap > 0 && (!send_lo || !send_hi)) || x_begin >= x_end)
+    return fail(h, BDM_EINVAL, "bdm_slab_split: bad arguments");
+  if (h->split_pending) return fail(h, BDM_ESTATE, "bdm_slab_split: the previous split was not committed");
+  CU(h, cudaMemsetAsync(h->cnt, 0, 8 * sizeof(uint32_t), h->stream));
+  const uint32_t n = (uint32_t)h->n;
+  if (n > 0)
+    k_slab_split<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->grid.inv, x_begin, x_end,
+                                                        send_lo, send_hi, (uint64_t)cap, h->cnt, h->ag[1 - h->cur],
+                                                        h->id[1 - h->cur]);
+  if (!h->ext_valid) {  // no step since the last load / add: extents of the owned agents now
+    k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
+    if (n > 0) k_extents<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], n, h->grid.inv, h->ext);
+    h->launches += 1 + (n > 0);
+  }
+  k_split_info<<<1, 32, 0, h->stream>>>(h->cnt, h->ext, (uint64_t)cap, info);
+  CU(h, cudaGetLastError());
+  h->launches += 1 + (n > 0);
+  h->split_pending = true;
+  return BDM_OK;
+}
+
+int bdm_slab_commit(bdm_handle h, int64_t n_stay) {
+  int rc = slab_check(h, "bdm_slab_commit");
+  if (rc) return rc;
+  if (!h->split_pending) return fail(h, BDM_ESTATE, "bdm_slab_commit: no split to commit");
+  if (n_stay < 0) {  // cancel: the owned agents are unchanged (the split only wrote other buffers)
+    h->split_pending = false;
+    return BDM_OK;
+  }
+  if (n_stay > h->n) return fail(h, BDM_EINVAL, "bdm_slab_commit: n_stay = %lld", (long long)n_stay);
+  h->cur = 1 - h->cur;
+  h->n = n_stay;
+  h->split_pending = false;
+  h->ext_valid = false;
+  h->cols_next = false;
   return BDM_OK;
 }
 

@@ -1575,6 +1575,63 @@ __global__ void k_slab_pack(const double4* __restrict__ ag, const uint32_t* __re
   }
 }
 
+// Post-step split of the owned agents (single-sync protocol): emigrants (new box-x
+// outside [x_begin, x_end)) to the front of send_lo / send_hi, stayers compacted into keep_*, and
+// the stayers of the first / last box-x layer (the neighbours' next ghosts) to the BACK of
+// send_lo / send_hi (record cap-1-k).  Counters: cnt[0] emigrants lo, cnt[1] halo lo, cnt[2]
+// emigrants hi, cnt[3] halo hi, cnt[4] stayers; records past a segment's room are dropped (the
+// counts still tell, so the caller detects it).
+__global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
+                             double inv, int32_t x_begin, int32_t x_end, double* __restrict__ send_lo,
+                             double* __restrict__ send_hi, uint64_t cap, uint32_t* __restrict__ cnt,
+                             double4* __restrict__ keep_ag, uint32_t* __restrict__ keep_id) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = i < n;
+  const double4 p = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+  const uint32_t id = valid ? ids[i] : 0u;
+  const int bx = (int)floor(p.x * inv);
+  const bool mlo = valid && bx < x_begin, mhi = valid && bx >= x_end;
+  const bool keep = valid && !mlo && !mhi;
+  const bool hlo = keep && x_begin != INT32_MIN && bx == x_begin;
+  const bool hhi = keep && x_end != INT32_MAX && bx == x_end - 1;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const bool f[5] = {mlo, hlo, mhi, hhi, keep};
+  uint32_t slot[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const unsigned m = __ballot_sync(FULL, f[c]);
+    uint32_t b = 0;
+    if (lane == 0 && m) b = atomicAdd(&cnt[c], (uint32_t)__popc(m));
+    slot[c] = __shfl_sync(FULL, b, 0) + __popc(m & lt);
+  }
+  auto put = [&](double* buf, uint64_t k) {
+    double* r = buf + (size_t)REC * k;
+    r[0] = p.x; r[1] = p.y; r[2] = p.z; r[3] = p.w; r[4] = (double)id;
+  };
+  if (mlo && slot[0] < cap) put(send_lo, slot[0]);
+  if (mhi && slot[2] < cap) put(send_hi, slot[2]);
+  if (hlo && slot[1] < cap) put(send_lo, cap - 1 - slot[1]);
+  if (hhi && slot[3] < cap) put(send_hi, cap - 1 - slot[3]);
+  if (keep) {
+    keep_ag[slot[4]] = p;
+    keep_id[slot[4]] = id;
+  }
+}
+
+// info[0..4] = split counters, info[5..10] = the owned agents' box extents lo[3], hi[3] (from the
+// step that produced these positions), info[11] = 1 if a segment overflowed its room.
+__global__ void k_split_info(const uint32_t* __restrict__ cnt, const Extents* __restrict__ ext, uint64_t cap,
+                             int64_t* __restrict__ info) {
+  const int t = threadIdx.x;
+  if (t < 5) info[t] = cnt[t];
+  if (t < 3) {
+    info[5 + t] = ext->lo[t];
+    info[8 + t] = ext->hi[t];
+  }
+  if (t == 0) info[11] = (uint64_t)cnt[0] + cnt[1] > cap || (uint64_t)cnt[2] + cnt[3] > cap ? 1 : 0;
+}
+
 // Appends records (ghosts or immigrants) at ag[off..off+m).
 __global__ void k_unpack(const double* __restrict__ rec, uint32_t m, double4* __restrict__ ag,
                          uint32_t* __restrict__ ids, uint32_t off) {

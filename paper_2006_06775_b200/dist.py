@@ -5,13 +5,19 @@ exchange of boundary-box agents and migrates agents that cross slab boundaries, 
 send/recv over NVLink."
 
 Rank g owns the agents whose integer box-x lies in [bounds[g], bounds[g+1]) (bounds[0] = INT32_MIN,
-bounds[G] = INT32_MAX).  One step:
-  1. allreduce of the box extents (min lo / max hi of the owned agents' box coordinates, O2);
-  2. halo: every rank sends its first box-x layer to g-1 and its last to g+1 (ghosts);
-  3. bdm_slab_step: slab-local grid over owned + ghosts, force / displacement / update of the owned
-     agents (all in libbdm.so kernels);
-  4. migration: agents whose new box-x left the slab go to g-1 / g+1 and are appended there.
-Counts travel before payloads; records are 5 fp64 (x, y, z, D, id).  The arithmetic is unchanged
+bounds[G] = INT32_MAX).  One step of the single-sync protocol (every slab at least 2 boxes wide):
+  1. bdm_slab_step with the ghosts prepared by the previous step: slab-local grid over owned +
+     ghosts, force / displacement / update of the owned agents (libbdm.so kernels);
+  2. bdm_slab_split (device, no host round trip): emigrants (new box-x outside the slab) and the
+     stayers of the first / last box-x layer (the neighbours' next ghosts) into the send buffers;
+  3. on the device: counts to g-1 / g+1 and an allreduce of the box extents; then ONE host read of
+     all counts and extents;
+  4. payloads to g-1 / g+1; commit the stayers, append the immigrants; the next step's ghosts of a
+     side are the neighbour's boundary stayers plus this rank's own emigrants to that side (they
+     moved less than a box, so they sit exactly in the neighbour's boundary layer).
+The legacy protocol (extents allreduce, halo pack + exchange, step, migration pack + exchange: six
+host round trips) remains for slabs one box wide and for the setup.  Counts travel before payloads;
+records are 5 fp64 (x, y, z, D, id).  The arithmetic is unchanged
 from the single-GPU path and ghosts keep their global ids, so every owned agent's force is summed
 in the same canonical order: results are bit-identical to one GPU.
 
@@ -42,13 +48,17 @@ def choose_bounds(hist: np.ndarray, x0: int, world: int, weights: np.ndarray | N
     if world > 1:
         cum = np.cumsum(w)
         total = cum[-1] if nx else 0.0
+        # inner slabs at least 2 boxes wide when the population spans enough boxes (the single-sync
+        # protocol needs it), else 1
+        wmin = 2 if nx >= 2 * world else 1
         prev = x0
         for g in range(1, world):
             target = total * g / world
             k = int(np.searchsorted(cum, target, side="left")) + 1  # first box of slab g (relative)
             cut = x0 + k
-            cut = max(cut, prev + 1)
-            cut = min(cut, x0 + nx - (world - g)) if nx >= world else max(cut, prev + 1)
+            cut = max(cut, prev + (1 if g == 1 else wmin))
+            if nx >= world:
+                cut = min(cut, x0 + nx - 1 - (world - 1 - g) * wmin)
             bounds.append(int(cut))
             prev = cut
     bounds.append(INT32_MAX)
@@ -136,6 +146,73 @@ class TorchComm:
                 w.wait()
         return [(recv[r - 1], recv[r + 1])]
 
+    def exchange_split(self, splits):
+        return _TorchSplitExchange.run(self, splits)
+
+
+def _split_counts(info):
+    """Host view of one slab's split info (int64[12]) -> dict."""
+    return dict(mig_lo=int(info[0]), halo_lo=int(info[1]), mig_hi=int(info[2]), halo_hi=int(info[3]),
+                n_stay=int(info[4]), lo=np.asarray(info[5:8], np.int64), hi=np.asarray(info[8:11], np.int64),
+                overflow=int(info[11]))
+
+
+class _TorchSplitExchange:
+    """TorchComm.exchange_split (single-sync protocol step 3-4), NCCL or gloo."""
+
+    @staticmethod
+    def run(comm, splits):
+        import torch
+
+        dist = comm.dist
+        (s_lo, s_hi, info), = splits
+        r, G = comm.rank, comm.world
+        dev = info.device
+        cap = s_lo.shape[0]
+        rc_lo = torch.zeros(2, dtype=torch.int64, device=dev)
+        rc_hi = torch.zeros(2, dtype=torch.int64, device=dev)
+        ops = []
+        if r - 1 >= 0:
+            ops += [dist.P2POp(dist.isend, info[0:2].contiguous(), r - 1), dist.P2POp(dist.irecv, rc_lo, r - 1)]
+        if r + 1 < G:
+            ops += [dist.P2POp(dist.isend, info[2:4].contiguous(), r + 1), dist.P2POp(dist.irecv, rc_hi, r + 1)]
+        # extents (min lo, max hi) and any overflow, reduced with one MIN
+        red = torch.cat([info[5:8], -info[8:11], -info[11:12]])
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        dist.all_reduce(red, op=dist.ReduceOp.MIN)
+        host = torch.cat([info, rc_lo, rc_hi, red]).cpu().numpy()  # the step's one host round trip
+        mine = _split_counts(host[:12])
+        in_lo, in_hi = host[12:14], host[14:16]
+        glo, ghi, any_overflow = host[16:19], -host[19:22], -host[22]
+        out = dict(mine, glo=glo.astype(np.int64), ghi=ghi.astype(np.int64), any_overflow=int(any_overflow))
+        if any_overflow:
+            return [out]
+        recv = {}
+        ops = []
+        for side, peer, buf, mig, halo, rin in (("lo", r - 1, s_lo, mine["mig_lo"], mine["halo_lo"], in_lo),
+                                                ("hi", r + 1, s_hi, mine["mig_hi"], mine["halo_hi"], in_hi)):
+            imm = torch.empty((int(rin[0]), REC), dtype=torch.float64, device=dev)
+            hal = torch.empty((int(rin[1]), REC), dtype=torch.float64, device=dev)
+            recv[side] = (imm, hal)
+            if not (0 <= peer < G):
+                assert mig == 0 and halo == 0, "records addressed to a rank outside the job"
+                continue
+            if mig:
+                ops.append(dist.P2POp(dist.isend, buf[:mig], peer))
+            if halo:
+                ops.append(dist.P2POp(dist.isend, buf[cap - halo:], peer))
+            if imm.shape[0]:
+                ops.append(dist.P2POp(dist.irecv, imm, peer))
+            if hal.shape[0]:
+                ops.append(dist.P2POp(dist.irecv, hal, peer))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        out.update(imm_lo=recv["lo"][0], halo_in_lo=recv["lo"][1], imm_hi=recv["hi"][0], halo_in_hi=recv["hi"][1])
+        return [out]
+
 
 class LoopComm:
     """All slabs in one process: exchanges are hand-overs between the local slabs (virtual slabs on
@@ -167,6 +244,29 @@ class LoopComm:
             out.append((frm_lo, frm_hi))
         assert sends[0][0].shape[0] == 0 and sends[G - 1][1].shape[0] == 0
         return out
+
+    def exchange_split(self, splits):
+        G = self.world
+        infos = [_split_counts(np.asarray(info.cpu().numpy())) for _, _, info in splits]
+        glo = np.min(np.stack([c["lo"] for c in infos]), axis=0)
+        ghi = np.max(np.stack([c["hi"] for c in infos]), axis=0)
+        anyo = max(c["overflow"] for c in infos)
+        outs = []
+        for g in range(G):
+            o = dict(infos[g], glo=glo, ghi=ghi, any_overflow=anyo)
+            if not anyo:
+                for side, nb, key_m, key_h in (("lo", g - 1, "mig_hi", "halo_hi"), ("hi", g + 1, "mig_lo", "halo_lo")):
+                    if 0 <= nb < G:
+                        buf = splits[nb][1] if side == "lo" else splits[nb][0]
+                        cap = buf.shape[0]
+                        m, hh = infos[nb][key_m], infos[nb][key_h]
+                        o["imm_" + side], o["halo_in_" + side] = buf[:m], buf[cap - hh:]
+                    else:
+                        empty = splits[g][0][:0]
+                        o["imm_" + side], o["halo_in_" + side] = empty, empty
+            outs.append(o)
+        assert infos[0]["mig_lo"] == infos[0]["halo_lo"] == 0 and infos[G - 1]["mig_hi"] == infos[G - 1]["halo_hi"] == 0
+        return outs
 
 
 # --------------------------------------------------------------------------------- GPU engine
@@ -207,6 +307,19 @@ class GpuSlabEngine:
             self.buf_cap = int(max(nlo, nhi) * 1.25) + 1024
             self._alloc()
 
+    def split(self, xb, xe):
+        if not hasattr(self, "info"):
+            self.info = self.torch.zeros(12, dtype=self.torch.int64, device=self.device)
+        self.bdm.bdm_slab_split(self.h, xb, xe, self.s_lo, self.s_hi, self.buf_cap, self.info)
+        return self.s_lo, self.s_hi, self.info
+
+    def commit(self, n_stay):
+        self.bdm.bdm_slab_commit(self.h, n_stay)
+
+    def grow_buffers(self, need):
+        self.buf_cap = int(need * 1.25) + 1024
+        self._alloc()
+
     def step(self, glo, ghi, xb, xe, recv_lo, recv_hi, want_dp=False):
         self.bdm.bdm_slab_step(self.h, glo, ghi, xb, xe, recv_lo, recv_lo.shape[0], recv_hi, recv_hi.shape[0],
                                want_dp)
@@ -230,11 +343,17 @@ HALO, MIGRANTS = 0, 1
 class SlabDriver:
     """Runs the per-step protocol over the local slabs `engines` (engine k is slab comm.slab_ids()[k])."""
 
-    def __init__(self, engines, comm, bounds):
+    def __init__(self, engines, comm, bounds, fused: bool | None = None):
         self.engines = engines
         self.comm = comm
         self.bounds = bounds
         self.slabs = [(bounds[g], bounds[g + 1]) for g in comm.slab_ids()]
+        # single-sync protocol: needs every inner slab at least 2 boxes wide (so that an emigrant
+        # never lands in a layer that is a third rank's ghost layer) and engines that can split
+        inner = [b - a for a, b in zip(bounds[1:-2], bounds[2:-1])]
+        ok = all(w >= 2 for w in inner) and all(hasattr(e, "split") for e in engines)
+        self.fused = ok if fused is None else (fused and ok)
+        self.next_ghosts = None
         L = comm.allreduce_max([e.local_maxd() for e in engines])  # O1 over all ranks
         for e in engines:
             e.set_box_edge(L)
@@ -260,9 +379,52 @@ class SlabDriver:
             rounds += 1
             if rounds > (max_rounds or len(self.bounds)):
                 raise RuntimeError("agents did not settle in their slabs")
+        self.next_ghosts = None  # the next fused step primes its ghosts and extents
         return rounds
 
+    def prime(self):
+        """Extents and ghosts for the next step of the single-sync protocol (legacy exchanges)."""
+        exts = [e.local_extents() for e in self.engines]
+        self.glo, self.ghi = self.comm.allreduce_extents(exts)
+        halos = [e.pack(HALO, xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]
+        self.next_ghosts = [(gl.clone(), gh.clone()) for gl, gh in self.comm.exchange(halos)]
+
     def step(self, want_dp: bool = False):
+        if not self.fused:
+            return self.step_legacy(want_dp)
+        if self.next_ghosts is None:
+            self.prime()
+        self.ghosts = sum(gl.shape[0] + gh.shape[0] for gl, gh in self.next_ghosts)
+        for e, (xb, xe), (gl, gh) in zip(self.engines, self.slabs, self.next_ghosts):
+            e.step(self.glo, self.ghi, xb, xe, gl, gh, want_dp)
+        while True:
+            splits = [e.split(xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]
+            outs = self.comm.exchange_split(splits)
+            if not outs[0]["any_overflow"]:
+                break
+            for e, o in zip(self.engines, outs):  # some rank's buffers were too small: cancel, grow, redo
+                e.commit(-1)
+                e.grow_buffers(max(o["mig_lo"] + o["halo_lo"], o["mig_hi"] + o["halo_hi"]))
+        ghosts = []
+        for e, (s_lo, s_hi, _), o in zip(self.engines, splits, outs):
+            # this rank's emigrants stay on as ghosts of the next step (they sit in the neighbour's
+            # boundary layer); copied before the buffers are reused
+            gl = self._cat(o["halo_in_lo"], s_lo[: o["mig_lo"]])
+            gh = self._cat(o["halo_in_hi"], s_hi[: o["mig_hi"]])
+            e.commit(o["n_stay"])
+            e.add(o["imm_lo"], o["imm_hi"])
+            self.migrated += o["mig_lo"] + o["mig_hi"]
+            ghosts.append((gl, gh))
+        self.next_ghosts = ghosts
+        self.glo, self.ghi = outs[0]["glo"], outs[0]["ghi"]
+
+    @staticmethod
+    def _cat(a, b):
+        import torch
+
+        return torch.cat([a, b]) if b.shape[0] else a.clone()
+
+    def step_legacy(self, want_dp: bool = False):
         exts = [e.local_extents() for e in self.engines]
         glo, ghi = self.comm.allreduce_extents(exts)
         halos = [e.pack(HALO, xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]

@@ -61,10 +61,45 @@ class CpuSlabEngine:
         self.ids, self.pos, self.diam = self.ids[keep], self.pos[keep], self.diam[keep]
         return out
 
+    def split(self, xb, xe):
+        """Single-sync protocol: emigrants at the front, boundary stayers at the back of each buffer
+        (cap = owned count); counts and extents in info (as bdm_slab_split)."""
+        bx = self._bx()
+        mlo, mhi = bx < xb, bx >= xe
+        keep = ~(mlo | mhi)
+        hlo = keep & (bx == xb) & (xb != INT32_MIN)
+        hhi = keep & (bx == xe - 1) & (xe != INT32_MAX)
+        cap = max(len(self.ids), 1)
+        bufs = []
+        for m, h in ((mlo, hlo), (mhi, hhi)):
+            b = torch.zeros((cap, 5), dtype=torch.float64)
+            nm, nh = int(m.sum()), int(h.sum())
+            b[:nm] = self._rec(m)
+            if nh:
+                b[cap - nh:] = torch.flip(self._rec(h), dims=[0])
+            bufs.append(b)
+        lo, hi = self.local_extents()
+        info = torch.tensor([int(mlo.sum()), int(hlo.sum()), int(mhi.sum()), int(hhi.sum()), int(keep.sum()),
+                             *[int(v) for v in lo], *[int(v) for v in hi], 0], dtype=torch.int64)
+        self.pending = keep
+        return bufs[0], bufs[1], info
+
+    def commit(self, n_stay):
+        keep, self.pending = self.pending, None
+        if n_stay < 0:
+            return
+        assert int(keep.sum()) == n_stay
+        self.ids, self.pos, self.diam = self.ids[keep], self.pos[keep], self.diam[keep]
+        self.ext = None
+
+    def grow_buffers(self, need):
+        pass
+
     def add(self, rl, rh):
         for r in (rl, rh):
             r = r.numpy()
             if len(r):
+                self.ext = None
                 self.pos = np.concatenate([self.pos, r[:, :3]])
                 self.diam = np.concatenate([self.diam, r[:, 3]])
                 self.ids = np.concatenate([self.ids, r[:, 4].astype(np.int64)])

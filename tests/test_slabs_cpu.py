@@ -36,10 +36,39 @@ def test_choose_bounds():
     assert b[1:-1] == [1, 2]
     b = bdist.choose_bounds(np.array([7]), 3, 4)  # more slabs than boxes: strictly increasing
     assert all(x < y for x, y in zip(b, b[1:]))
+    # enough boxes: inner slabs at least 2 wide (single-sync protocol), even for a spike
+    b = bdist.choose_bounds(np.array([0, 0, 1000, 0, 0, 0, 0, 0, 0, 1]), 0, 4)
+    assert all(y - x >= 2 for x, y in zip(b[1:-1], b[2:-1])), b
 
 
+def test_narrow_slab_falls_back_to_legacy_protocol():
+    """A one-box-wide inner slab: an emigrant could land in a third rank's ghost layer, so the driver
+    uses the legacy protocol, which stays exact."""
+    pos, diam = population()
+    _, bx = bdist.initial_bounds(pos, diam, 3)
+    mid = int(np.median(bx))
+    bounds = [bdist.INT32_MIN, mid, mid + 1, bdist.INT32_MAX]
+    engines = []
+    for g in range(3):
+        m = np.flatnonzero((bx >= bounds[g]) & (bx < bounds[g + 1]))
+        engines.append(CpuSlabEngine(m, pos[m], diam[m]))
+    drv = bdist.SlabDriver(engines, bdist.LoopComm(3), bounds)
+    assert not drv.fused
+    for _ in range(2):
+        drv.step()
+    ref, _ = oracle.run(pos, diam, 2)
+    ids = np.concatenate([e.owned()[0] for e in engines])
+    got = np.concatenate([e.owned()[1] for e in engines])
+    out = np.empty_like(got)
+    out[ids] = got
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("fused", [True, False])
 @pytest.mark.parametrize("G", [1, 2, 3, 5])
-def test_loop_slabs_match_single_process(G):
+def test_loop_slabs_match_single_process(G, fused):
+    """Both protocols: the single-sync one (split / one count exchange / ghosts = neighbour's boundary
+    stayers + own emigrants) and the legacy one (six exchanges per step)."""
     pos, diam = population()
     steps = 3
     ref, _ = oracle.run(pos, diam, steps)
@@ -48,7 +77,8 @@ def test_loop_slabs_match_single_process(G):
     for g in range(G):
         m = np.flatnonzero((bx >= bounds[g]) & (bx < bounds[g + 1]))
         engines.append(CpuSlabEngine(m, pos[m], diam[m]))
-    drv = bdist.SlabDriver(engines, bdist.LoopComm(G), bounds)
+    drv = bdist.SlabDriver(engines, bdist.LoopComm(G), bounds, fused=fused)
+    assert drv.fused == fused
     for _ in range(steps):
         drv.step()
     if G > 1:
@@ -88,6 +118,7 @@ def _worker(rank, world, port, steps, q):
         m = np.flatnonzero((bx >= bounds[rank]) & (bx < bounds[rank + 1]))
         eng = CpuSlabEngine(m, pos[m], diam[m])
         drv = bdist.SlabDriver([eng], bdist.TorchComm(torch.device("cpu")), bounds)
+        assert drv.fused
         for _ in range(steps):
             drv.step()
         ids, p = eng.owned()
