@@ -136,6 +136,9 @@ struct bdm_ctx {
   bool half_off = false;  // BDM_HALF=0, or the rows could not be allocated: k_force only
   bool last_half = false;  // the last step used the half-shell path
   bool split_pending = false;  // slab: bdm_slab_split ran, bdm_slab_commit not yet
+  int64_t n_dead = 0;          // slab: committed emigrants still in ag[cur][0..n) (D < 0), dropped by the next sort
+  uint32_t last_n_lo = 0;      // slab: lower ghosts of the last step (sorted first)
+  int32_t split_xb = 0, split_xe = 0;
   int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
   std::vector<TimedStep> timed;
@@ -439,7 +442,8 @@ int compute_extents(bdm_ctx* h) {
 //   key + histogram -> table scan (box starts) -> scatter -> in-box id order + payload gather.
 // The ragged table size T lives on the device (coff[nc]); no host round trip inside the build.
 // cur flips to the sorted buffer.
-int sort_into(bdm_ctx* h, uint32_t n) {
+// n input agents of ag[cur], of which n_dead are marked dead (slab emigrants, D < 0) and dropped.
+int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   GridDev& g = h->grid;
   const uint64_t nc = (uint64_t)(g.hi[0] - g.lo[0] + 1) * (uint64_t)g.ny;
   if (nc >= 0xffffffffull) return fail(h, BDM_ERANGE, "%llu grid columns >= 2^32", (unsigned long long)nc);
@@ -494,7 +498,7 @@ int sort_into(bdm_ctx* h, uint32_t n) {
     k_scatter<<<blocks(n, 256), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
     DBG(h, "k_scatter");
     const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
-    k_place<<<blocks(n, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n, h->ag[dst],
+    k_place<<<blocks(n - n_dead, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n - n_dead, h->ag[dst],
                                            h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
                                            perm_hist ? h->hist[dst] : nullptr);
     DBG(h, "k_place");
@@ -1577,6 +1581,8 @@ int bdm_slab_load(bdm_handle h, int64_t n_local, const uint32_t* ids, const doub
   }
   h->cur = 0;
   h->n = n_local;
+  h->n_dead = 0;
+  h->split_pending = false;
   h->ext_valid = false;
   h->cols_next = false;
   h->have_dp = false;
@@ -1588,6 +1594,7 @@ int bdm_slab_load(bdm_handle h, int64_t n_local, const uint32_t* ids, const doub
 int bdm_slab_local_maxd(bdm_handle h, double* maxd) {
   int rc = slab_check(h, "bdm_slab_local_maxd");
   if (rc) return rc;
+  if (h->n_dead) return fail(h, BDM_ESTATE, "bdm_slab_local_maxd: emigrants of the last split are pending (run a step)");
   if (!maxd) return fail(h, BDM_EINVAL, "bdm_slab_local_maxd: NULL output");
   CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), h->stream));
   if (h->n > 0) k_maxd<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], (uint32_t)h->n, h->maxd_bits);
@@ -1617,6 +1624,7 @@ int bdm_slab_set_box_edge(bdm_handle h, double L) {
 int bdm_slab_local_extents(bdm_handle h, int32_t* lohi6) {
   int rc = slab_check(h, "bdm_slab_local_extents");
   if (rc) return rc;
+  if (h->n_dead) return fail(h, BDM_ESTATE, "bdm_slab_local_extents: emigrants of the last split are pending (run a step)");
   if (!lohi6) return fail(h, BDM_EINVAL, "bdm_slab_local_extents: NULL output");
   if (!(h->grid.inv > 0.0)) return fail(h, BDM_ESTATE, "bdm_slab_local_extents: call bdm_slab_set_box_edge first");
   if (!h->ext_valid) {
@@ -1644,6 +1652,7 @@ int bdm_slab_pack(bdm_handle h, int what, int32_t x_begin, int32_t x_end, double
                   int64_t cap, int64_t* n_lo, int64_t* n_hi) {
   int rc = slab_check(h, "bdm_slab_pack");
   if (rc) return rc;
+  if (h->n_dead) return fail(h, BDM_ESTATE, "bdm_slab_pack: emigrants of the last split are pending (run a step)");
   if ((what != BDM_HALO && what != BDM_MIGRANTS) || !n_lo || !n_hi || cap < 0 || (cap > 0 && (!send_lo || !send_hi)))
     return fail(h, BDM_EINVAL, "bdm_slab_pack: bad arguments");
   if (x_begin >= x_end) return fail(h, BDM_EINVAL, "bdm_slab_pack: empty slab [%d, %d)", x_begin, x_end);
@@ -1676,21 +1685,31 @@ int bdm_slab_split(bdm_handle h, int32_t x_begin, int32_t x_end, double* send_lo
   if (!info || cap < 0 || (cap > 0 && (!send_lo || !send_hi)) || x_begin >= x_end)
     return fail(h, BDM_EINVAL, "bdm_slab_split: bad arguments");
   if (h->split_pending) return fail(h, BDM_ESTATE, "bdm_slab_split: the previous split was not committed");
+  if (h->n_dead) return fail(h, BDM_ESTATE, "bdm_slab_split: run a step after the last commit");
   CU(h, cudaMemsetAsync(h->cnt, 0, 8 * sizeof(uint32_t), h->stream));
   const uint32_t n = (uint32_t)h->n;
-  if (n > 0)
-    k_slab_split<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->grid.inv, x_begin, x_end,
-                                                        send_lo, send_hi, (uint64_t)cap, h->cnt, h->ag[1 - h->cur],
-                                                        h->id[1 - h->cur]);
-  if (!h->ext_valid) {  // no step since the last load / add: extents of the owned agents now
+  init_device_info(h);
+  if (h->state == State::Stepped && h->have_grid) {  // boundary layers of the step's sorted order
+    k_layer_bounds<<<1, 32, 0, h->stream>>>(h->grid, x_begin, x_end, h->last_n_lo, n, h->cnt + 4);
+  } else {  // no step since the last load / add: the whole array
+    const uint32_t r2[2] = {n, n};
+    CU(h, cudaMemcpyAsync(h->cnt + 4, r2, sizeof r2, cudaMemcpyHostToDevice, h->stream));
+  }
+  if (!h->ext_valid) {  // extents of the owned agents now
     k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
     if (n > 0) k_extents<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], n, h->grid.inv, h->ext);
     h->launches += 1 + (n > 0);
+    h->ext_valid = true;
   }
-  k_split_info<<<1, 32, 0, h->stream>>>(h->cnt, h->ext, (uint64_t)cap, info);
+  if (n > 0)
+    k_slab_split<<<h->sm_count * 4, 256, 0, h->stream>>>(h->ag[h->cur], h->id[h->cur], n, h->cnt + 4, h->grid.inv,
+                                                          x_begin, x_end, send_lo, send_hi, (uint64_t)cap, h->cnt);
+  k_split_info<<<1, 32, 0, h->stream>>>(h->cnt, h->ext, (uint64_t)cap, n, info);
   CU(h, cudaGetLastError());
-  h->launches += 1 + (n > 0);
+  h->launches += 2 + (n > 0);
   h->split_pending = true;
+  h->split_xb = x_begin;
+  h->split_xe = x_end;
   return BDM_OK;
 }
 
@@ -1703,8 +1722,13 @@ int bdm_slab_commit(bdm_handle h, int64_t n_stay) {
     return BDM_OK;
   }
   if (n_stay > h->n) return fail(h, BDM_EINVAL, "bdm_slab_commit: n_stay = %lld", (long long)n_stay);
-  h->cur = 1 - h->cur;
-  h->n = n_stay;
+  // mark the emigrants dead in place (boundary ranges only); the next sort drops them
+  if (n_stay < h->n)
+    k_slab_mark_dead<<<h->sm_count * 4, 256, 0, h->stream>>>(h->ag[h->cur], (uint32_t)h->n, h->cnt + 4, h->grid.inv,
+                                                              h->split_xb, h->split_xe);
+  CU(h, cudaGetLastError());
+  h->launches += n_stay < h->n;
+  h->n_dead = h->n - n_stay;
   h->split_pending = false;
   h->ext_valid = false;
   h->cols_next = false;
@@ -1737,7 +1761,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   if (!glo3 || !ghi3 || n_lo < 0 || n_hi < 0 || (n_lo && !recv_lo) || (n_hi && !recv_hi) || x_begin >= x_end)
     return fail(h, BDM_EINVAL, "bdm_slab_step: bad arguments");
   if (!(h->grid.inv > 0.0)) return fail(h, BDM_ESTATE, "bdm_slab_step: call bdm_slab_set_box_edge first");
-  const int64_t n_own = h->n, n_tot = n_own + n_lo + n_hi;
+  const int64_t n_own = h->n, n_tot = n_own + n_lo + n_hi, n_dead = h->n_dead;  // n_own counts dead entries
   if (n_tot > h->cap)
     return fail(h, BDM_ERANGE, "bdm_slab_step: %lld owned + ghost agents exceed the capacity %lld", (long long)n_tot,
                 (long long)h->cap);
@@ -1781,25 +1805,27 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   g.ny = g.hi[1] - g.lo[1] + 1;
   g.nz = g.hi[2] - g.lo[2] + 1;
   g.n_boxes = (uint32_t)nb;
-  rc = sort_into(h, (uint32_t)n_tot);  // cur -> sorted owned + ghosts
+  rc = sort_into(h, (uint32_t)n_tot, (uint32_t)n_dead);  // cur -> sorted live owned + ghosts (dead dropped)
   if (rc) return rc;
   if (h->timing) CU(h, cudaEventRecord(ts.e1, s));
   // ghosts_lo (box-x = x_begin-1) sort first, ghosts_hi (box-x = x_end) last: the owned agents are
-  // the contiguous range [n_lo, n_tot - n_hi) of the sorted array
+  // the contiguous range [n_lo, n_sorted - n_hi) of the sorted array
   const int src = h->cur, dst = 1 - h->cur;
+  const int64_t n_live = n_own - n_dead, n_sorted = n_tot - n_dead;
+  h->last_n_lo = (uint32_t)n_lo;
   RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
   ParamsDev pd = params_dev(h->prm);
-  const unsigned grid = force_grid(h, (uint32_t)n_own);
-  h->last_half = n_own > 0 && ensure_half(h);
+  const unsigned grid = force_grid(h, (uint32_t)n_live);
+  h->last_half = n_live > 0 && ensure_half(h);
   if (h->last_half) {
     // pass A from the first lower ghost (their forward pairs with owned agents are the owned
     // agents' backward pairs); owned agents' forward runs reach into the upper ghosts
-    rc = half_force(h, src, 0u, (uint32_t)n_lo, (uint32_t)(n_tot - n_hi), (uint32_t)n_tot, pd, h->ag[dst], h->id[dst],
+    rc = half_force(h, src, 0u, (uint32_t)n_lo, (uint32_t)(n_sorted - n_hi), (uint32_t)n_sorted, pd, h->ag[dst], h->id[dst],
                     want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr);
     if (rc) return rc;
-  } else if (n_own > 0) {
+  } else if (n_live > 0) {
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
-                                                 (uint32_t)(n_tot - n_hi), g, pd, h->ag[dst], h->id[dst],
+                                                 (uint32_t)(n_sorted - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
                                                  h->err, rec, nullptr, nullptr, nullptr);
     CU(h, cudaGetLastError());
@@ -1807,10 +1833,11 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   }
   if (h->timing) CU(h, cudaEventRecord(ts.e2, s));
   h->cur = dst;
-  h->n = n_own;
+  h->n = n_live;
+  h->n_dead = 0;
   h->ext_valid = true;
   if (want_dp) {
-    h->n_dp = n_own;
+    h->n_dp = n_live;
     h->have_dp = true;
   }
   h->state = State::Stepped;
@@ -1820,6 +1847,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
 int bdm_slab_get(bdm_handle h, int what, int64_t* n, uint32_t* ids, double* vals) {
   int rc = slab_check(h, "bdm_slab_get");
   if (rc) return rc;
+  if (h->n_dead) return fail(h, BDM_ESTATE, "bdm_slab_get: emigrants of the last split are pending (run a step)");
   if (!n || (what != BDM_OWNED_POSITIONS && what != BDM_LAST_DISPLACEMENTS))
     return fail(h, BDM_EINVAL, "bdm_slab_get: bad arguments");
   if (what == BDM_LAST_DISPLACEMENTS && !h->have_dp) return fail(h, BDM_ESTATE, "bdm_slab_get: no displacements yet");

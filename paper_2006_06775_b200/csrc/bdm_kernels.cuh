@@ -255,7 +255,7 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
     const bool valid = ia[u] < n;
     uint32_t c = 0xffffffffu;
     int bz = 0;
-    if (valid) {
+    if (valid && pa[u].w >= 0.0) {  // (slab mode: emigrants are marked dead by D < 0 until the sort)
       const int bx = (int)floor(pa[u].x * g.inv), by = (int)floor(pa[u].y * g.inv);
       bz = (int)floor(pa[u].z * g.inv);
       c = col_of(g, bx, by);
@@ -265,7 +265,7 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
     const unsigned peers = __match_any_sync(FULL, c);
     const int zmin = __reduce_min_sync(peers, bz);
     const int zmax = __reduce_max_sync(peers, bz);
-    if (valid && lane == __ffs(peers) - 1) {
+    if (c != 0xffffffffu && lane == __ffs(peers) - 1) {
       if (zmin < __ldcg(&czlo[c])) atomicMin(&czlo[c], zmin);
       if (zmax > __ldcg(&czhi[c])) atomicMax(&czhi[c], zmax);
     }
@@ -298,7 +298,7 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
   for (int u = 0; u < 2; ++u) {
     const bool valid = ia[u] < n;
     uint32_t k = 0xffffffffu;
-    if (valid) {
+    if (valid && pa[u].w >= 0.0) {  // dead (slab emigrant, D < 0): dropped by the sort
       const double4 p = pa[u];
       const int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv), bz = (int)floor(p.z * g.inv);
       k = box_key(g, bx, by, bz);
@@ -307,7 +307,7 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
     const unsigned peers = __match_any_sync(FULL, k);
     const int leader = __ffs(peers) - 1;
     uint32_t base = 0;
-    if (valid && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
+    if (k != 0xffffffffu && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
     base = __shfl_sync(FULL, base, leader);
     if (valid) {
       key[ia[u]] = k;
@@ -431,6 +431,7 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __re
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   uint32_t k = key[i];
+  if (k == 0xffffffffu) return;  // dead
   uint32_t d = start[k] + slot[i];
   tsrc[d] = i;
   tid[d] = ids[i];
@@ -1575,56 +1576,107 @@ __global__ void k_slab_pack(const double4* __restrict__ ag, const uint32_t* __re
   }
 }
 
-// Post-step split of the owned agents (single-sync protocol): emigrants (new box-x
-// outside [x_begin, x_end)) to the front of send_lo / send_hi, stayers compacted into keep_*, and
-// the stayers of the first / last box-x layer (the neighbours' next ghosts) to the BACK of
-// send_lo / send_hi (record cap-1-k).  Counters: cnt[0] emigrants lo, cnt[1] halo lo, cnt[2]
-// emigrants hi, cnt[3] halo hi, cnt[4] stayers; records past a segment's room are dropped (the
-// counts still tell, so the caller detects it).
+// Post-step split of the owned agents (single-sync protocol).  Only the first two and
+// last two box-x layers of the step's sorted order can hold emigrants (a step moves an agent by less
+// than a box) or the stayers of the first / last layer (the neighbours' next ghosts): ranges
+// [0, r_lo) and [r_hi, n) of the stepped array.  Emigrants (new box-x outside [x_begin, x_end)) go
+// to the FRONT of send_lo / send_hi (bdm_slab_commit then marks them dead in place, D < 0, and the
+// next sort drops them); the stayers of the first / last layer go to the BACK (record cap-1-k).  The middle of the array
+// is not touched.  cnt[0] emigrants lo, [1] halo lo, [2] emigrants hi, [3] halo hi (block-aggregated
+// atomics); records past a segment's room are dropped (the counts still tell).
 __global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
-                             double inv, int32_t x_begin, int32_t x_end, double* __restrict__ send_lo,
-                             double* __restrict__ send_hi, uint64_t cap, uint32_t* __restrict__ cnt,
-                             double4* __restrict__ keep_ag, uint32_t* __restrict__ keep_id) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const bool valid = i < n;
-  const double4 p = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-  const uint32_t id = valid ? ids[i] : 0u;
-  const int bx = (int)floor(p.x * inv);
-  const bool mlo = valid && bx < x_begin, mhi = valid && bx >= x_end;
-  const bool keep = valid && !mlo && !mhi;
-  const bool hlo = keep && x_begin != INT32_MIN && bx == x_begin;
-  const bool hhi = keep && x_end != INT32_MAX && bx == x_end - 1;
+                             const uint32_t* __restrict__ r2, double inv, int32_t x_begin, int32_t x_end,
+                             double* __restrict__ send_lo, double* __restrict__ send_hi, uint64_t cap,
+                             uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t s_cnt[4], s_base[4];
+  const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
+  const uint32_t hi0 = r2[1] > n_lo_part ? r2[1] : n_lo_part;  // ranges do not overlap
+  const uint64_t total = (uint64_t)n_lo_part + (n - hi0);
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const bool f[5] = {mlo, hlo, mhi, hhi, keep};
-  uint32_t slot[5];
+  for (uint64_t t0 = (uint64_t)blockIdx.x * blockDim.x; t0 < total; t0 += (uint64_t)gridDim.x * blockDim.x) {
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0u;
+    __syncthreads();
+    const uint64_t t = t0 + threadIdx.x;
+    const bool valid = t < total;
+    const uint32_t i = !valid ? 0u : (t < n_lo_part ? (uint32_t)t : hi0 + (uint32_t)(t - n_lo_part));
+    double4 p = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const int bx = (int)floor(p.x * inv);
+    const bool mlo = valid && bx < x_begin, mhi = valid && bx >= x_end;
+    const bool keep = valid && !mlo && !mhi;
+    const bool hlo = keep && x_begin != INT32_MIN && bx == x_begin;
+    const bool hhi = keep && x_end != INT32_MAX && bx == x_end - 1;
+    const bool f[4] = {mlo, hlo, mhi, hhi};
+    uint32_t loc[4];
 #pragma unroll
-  for (int c = 0; c < 5; ++c) {
-    const unsigned m = __ballot_sync(FULL, f[c]);
-    uint32_t b = 0;
-    if (lane == 0 && m) b = atomicAdd(&cnt[c], (uint32_t)__popc(m));
-    slot[c] = __shfl_sync(FULL, b, 0) + __popc(m & lt);
-  }
-  auto put = [&](double* buf, uint64_t k) {
-    double* r = buf + (size_t)REC * k;
-    r[0] = p.x; r[1] = p.y; r[2] = p.z; r[3] = p.w; r[4] = (double)id;
-  };
-  if (mlo && slot[0] < cap) put(send_lo, slot[0]);
-  if (mhi && slot[2] < cap) put(send_hi, slot[2]);
-  if (hlo && slot[1] < cap) put(send_lo, cap - 1 - slot[1]);
-  if (hhi && slot[3] < cap) put(send_hi, cap - 1 - slot[3]);
-  if (keep) {
-    keep_ag[slot[4]] = p;
-    keep_id[slot[4]] = id;
+    for (int c = 0; c < 4; ++c) {
+      const unsigned m = __ballot_sync(FULL, f[c]);
+      uint32_t b = 0;
+      if (lane == 0 && m) b = atomicAdd(&s_cnt[c], (uint32_t)__popc(m));
+      loc[c] = __shfl_sync(FULL, b, 0) + __popc(m & lt);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) s_base[threadIdx.x] = s_cnt[threadIdx.x] ? atomicAdd(&cnt[threadIdx.x], s_cnt[threadIdx.x]) : 0u;
+    __syncthreads();
+    if (valid && (mlo || mhi || hlo || hhi)) {
+      const uint32_t id = ids[i];
+      auto put = [&](double* buf, uint64_t k) {
+        double* r = buf + (size_t)REC * k;
+        r[0] = p.x; r[1] = p.y; r[2] = p.z; r[3] = p.w; r[4] = (double)id;
+      };
+      if (mlo && s_base[0] + loc[0] < cap) put(send_lo, s_base[0] + loc[0]);
+      if (mhi && s_base[2] + loc[2] < cap) put(send_hi, s_base[2] + loc[2]);
+      if (hlo && s_base[1] + loc[1] < cap) put(send_lo, cap - 1 - (s_base[1] + loc[1]));
+      if (hhi && s_base[3] + loc[3] < cap) put(send_hi, cap - 1 - (s_base[3] + loc[3]));
+    }
+    __syncthreads();
   }
 }
 
-// info[0..4] = split counters, info[5..10] = the owned agents' box extents lo[3], hi[3] (from the
+// bdm_slab_commit: emigrants of the split (same boundary ranges) are marked dead (D < 0) in place.
+__global__ void k_slab_mark_dead(double4* __restrict__ ag, uint32_t n, const uint32_t* __restrict__ r2, double inv,
+                                 int32_t x_begin, int32_t x_end) {
+  const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
+  const uint32_t hi0 = r2[1] > n_lo_part ? r2[1] : n_lo_part;
+  const uint64_t total = (uint64_t)n_lo_part + (n - hi0);
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = t < n_lo_part ? (uint32_t)t : hi0 + (uint32_t)(t - n_lo_part);
+    const int bx = (int)floor(ag[i].x * inv);
+    if (bx < x_begin || bx >= x_end) ag[i].w = -1.0;
+  }
+}
+
+// First stepped agent of box-x layer X in the slab step's sorted order (owned indexing: the lower
+// ghosts, which sort first, are subtracted); X outside the grid clamps.
+__global__ void k_layer_bounds(GridDev g, int32_t x_begin, int32_t x_end, uint32_t n_lo, uint32_t n,
+                               uint32_t* __restrict__ out2) {
+  if (threadIdx.x >= 2) return;
+  const int64_t X = threadIdx.x == 0 ? (int64_t)x_begin + 2 : (int64_t)x_end - 2;
+  uint32_t r;
+  if (threadIdx.x == 0 && x_begin == INT32_MIN) {
+    r = 0u;
+  } else if (threadIdx.x == 1 && x_end == INT32_MAX) {
+    r = n;
+  } else if (X <= g.lo[0]) {
+    r = 0u;
+  } else if (X > g.hi[0]) {
+    r = n;
+  } else {
+    const uint32_t c = (uint32_t)(X - g.lo[0]) * (uint32_t)g.ny;
+    const uint32_t k = g.table[g.coff[c]];
+    r = k > n_lo ? k - n_lo : 0u;
+    r = r < n ? r : n;
+  }
+  out2[threadIdx.x] = r;
+}
+
+// info[0..3] = split counters, info[4] = stayers, info[5..10] = the owned agents' box extents lo[3], hi[3] (from the
 // step that produced these positions), info[11] = 1 if a segment overflowed its room.
 __global__ void k_split_info(const uint32_t* __restrict__ cnt, const Extents* __restrict__ ext, uint64_t cap,
-                             int64_t* __restrict__ info) {
+                             uint32_t n, int64_t* __restrict__ info) {
   const int t = threadIdx.x;
-  if (t < 5) info[t] = cnt[t];
+  if (t < 4) info[t] = cnt[t];
+  if (t == 4) info[4] = (int64_t)n - cnt[0] - cnt[2];
   if (t < 3) {
     info[5 + t] = ext->lo[t];
     info[8 + t] = ext->hi[t];

@@ -390,13 +390,23 @@ class SlabDriver:
         self.next_ghosts = [(gl.clone(), gh.clone()) for gl, gh in self.comm.exchange(halos)]
 
     def step(self, want_dp: bool = False):
+        """One protocol step.  Single-sync protocol: the exchange of the previous step's results (split,
+        counts + extents, payloads, commit, immigrants, next ghosts) runs first, then the slab step;
+        after it every agent is still owned by the rank that stepped it (an emigrant moves at the next
+        exchange), so the owned sets partition the population between steps."""
         if not self.fused:
             return self.step_legacy(want_dp)
         if self.next_ghosts is None:
             self.prime()
+        else:
+            self.exchange()
         self.ghosts = sum(gl.shape[0] + gh.shape[0] for gl, gh in self.next_ghosts)
         for e, (xb, xe), (gl, gh) in zip(self.engines, self.slabs, self.next_ghosts):
             e.step(self.glo, self.ghi, xb, xe, gl, gh, want_dp)
+        self.stepped = True
+
+    def exchange(self):
+        """Steps 2-4 of the single-sync protocol after a slab step (one host round trip)."""
         while True:
             splits = [e.split(xb, xe) for e, (xb, xe) in zip(self.engines, self.slabs)]
             outs = self.comm.exchange_split(splits)
