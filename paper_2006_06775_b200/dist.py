@@ -577,10 +577,14 @@ def bench_multi(args, metric, unit, config_obj, load_peaks, ClockSampler):
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_obj(args, n, world), "bounds": [int(b) for b in bounds[1:-1]],
                 "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12,
-                             "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None, "kernel": "k_force",
+                             "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                             "kernel": "force phase: k_half_search + k_half_sum" if tm["search_ms"] > 0 else "k_force",
                              "ms_per_launch": force_s * 1e3,
-                             "note": "rank 0's force kernel; its algorithmic fp64 ops taken as the rank's share of "
+                             "passes_ms": {"search": tm["search_ms"] / max(tm["steps"], 1),
+                                           "sum": tm["sum_ms"] / max(tm["steps"], 1)},
+                             "note": "rank 0's force phase; its algorithmic fp64 ops taken as the rank's share of "
                                      "agents x the whole-population per-agent mix (DESIGN.md §6.2)"},
+                "protocol": "single-sync" if drv.fused else "legacy",
                 "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches.item()),
                 "clocks": clk.summary(), "timing": "CUDA events on each rank's stream, max over ranks"}
         print(json.dumps(line), flush=True)
