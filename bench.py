@@ -340,36 +340,54 @@ REBUILD_BYTES_PER_AGENT = 160  # key+hist 40, scatter 24, place 96 (column pass 
 
 
 def run_e2e(bdm, torch, pos_h, diam_h, local, args):
+    """Same metric through the public C ABI with HOST buffers: every batch pays its pinned H2D
+    (bdm_set_agents), one step and the D2H of its displacements (bdm_get_displacements).  Two
+    handles on two streams, each driven by its own host thread (ctypes releases the GIL), process
+    alternate batches, so one batch's upload overlaps the other's step and download (H2D and D2H use
+    separate copy engines) -- a serving pipeline; the timed region is the wall time of all batches."""
+    import threading
+
     n = len(diam_h)
     pin_pos = torch.from_numpy(pos_h).pin_memory()
     pin_diam = torch.from_numpy(diam_h).pin_memory()
-    out = torch.empty((n, 3), dtype=torch.float64).pin_memory()
-    ppos, pdiam, pout = pin_pos.numpy(), pin_diam.numpy(), out.numpy()
-    h = bdm.bdm_init(ppos, pdiam, bdm.bdm_params_default(device=local))
-    stream = torch.cuda.current_stream()
-    bdm.bdm_set_stream(h, stream)
+    ppos, pdiam = pin_pos.numpy(), pin_diam.numpy()
+    lanes = []
+    for _ in range(2):
+        out = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+        st = torch.cuda.Stream(device=local)
+        h = bdm.bdm_init(ppos, pdiam, bdm.bdm_params_default(device=local))
+        bdm.bdm_set_stream(h, st)
+        lanes.append((h, out.numpy(), out))
 
-    def one():
-        bdm.bdm_set_agents(h, ppos, pdiam)  # H2D of this step's inputs
+    def one(h, pout):
+        bdm.bdm_set_agents(h, ppos, pdiam)  # H2D of this batch's inputs
         bdm.bdm_mech_step(h, 1)
-        bdm.bdm_get_displacements(h, pout)  # D2H of the step's result
+        bdm.bdm_get_displacements(h, pout)  # D2H of the batch's result (synchronises its stream)
 
-    one()
+    for h, pout, _ in lanes:
+        one(h, pout)
     torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
+    batches = max(2, 2 * args.e2e_steps)
+
+    def worker(k):
+        h, pout, _ = lanes[k]
+        for _ in range(k, batches, 2):
+            one(h, pout)
+
     w0 = time.perf_counter()
-    t0.record(stream)
-    for _ in range(args.e2e_steps):
-        one()
-    t1.record(stream)
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
     torch.cuda.synchronize()
     wall = time.perf_counter() - w0
-    ms = t0.elapsed_time(t1)
-    h.close()
-    return {"value": n * args.e2e_steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(pos_h.nbytes + diam_h.nbytes),
-            "d2h_bytes_per_step": int(n * 3 * 8), "steps": args.e2e_steps, "wall_s": wall,
-            "path": "bdm_set_agents(host pinned) -> bdm_mech_step(1) -> bdm_get_displacements(host pinned)"}
+    for h, _, _ in lanes:
+        h.close()
+    return {"value": n * batches / wall, "unit": UNIT, "h2d_bytes_per_step": int(pos_h.nbytes + diam_h.nbytes),
+            "d2h_bytes_per_step": int(n * 3 * 8), "steps": batches, "wall_s": wall,
+            "path": "2 host threads x (bdm_set_agents(host pinned) -> bdm_mech_step(1) -> "
+                    "bdm_get_displacements(host pinned)) on 2 streams, alternate batches; wall clock"}
 
 
 def main():
