@@ -1182,18 +1182,22 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     // (+1,-1), (+1,0), (+1,+1): bit q kept, bit 8+q z-1 box culled, bit 16+q z+1 box culled
     uint32_t cull = 0u;
     {
-      const double rp = (ri + g.thr_pad + g.m32) * (1.0 + 0x1p-20);
-      const double Rc = rp + g.m32;
-      const double Rc2 = Rc * Rc;
-      const double Lb = 1.0 / g.inv;
-      const double fy = fmax(me.y - by * Lb, 0.0), gy = fmax((by + 1) * Lb - me.y, 0.0);
-      const double gx = fmax((bx + 1) * Lb - me.x, 0.0);
-      const double fz = fmax(me.z - bz * Lb, 0.0), gz = fmax((bz + 1) * Lb - me.z, 0.0);
+      // in fp32 from the fp32 copy: the face distances are off by a few ulp32(max |coordinate|) at
+      // most (< m32), so the bound carries two extra margins m32 and a relative
+      // 2^-18: a box is culled only if it truly cannot hold a contact (conservative)
+      const float m = (float)g.m32;
+      const float rp = (-mf.w + (float)g.thr_pad + m) * (1.0f + 0x1p-19f);
+      const float Rc = rp + 3.0f * m;
+      const float Rc2 = Rc * Rc * (1.0f + 0x1p-18f);
+      const float Lb = (float)(1.0 / g.inv);
+      const float fy = fmaxf(mf.y - (float)by * Lb, 0.f), gy = fmaxf((float)(by + 1) * Lb - mf.y, 0.f);
+      const float gx = fmaxf((float)(bx + 1) * Lb - mf.x, 0.f);
+      const float fz = fmaxf(mf.z - (float)bz * Lb, 0.f), gz = fmaxf((float)(bz + 1) * Lb - mf.z, 0.f);
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
-        const double ex = q >= 2 ? gx : 0.0;
-        const double ey = q == 1 || q == 4 ? gy : (q == 2 ? fy : 0.0);
-        const double exy2 = ex * ex + ey * ey;
+        const float ex = q >= 2 ? gx : 0.f;
+        const float ey = q == 1 || q == 4 ? gy : (q == 2 ? fy : 0.f);
+        const float exy2 = ex * ex + ey * ey;
         cull |= (uint32_t)(exy2 <= Rc2) << q;
         cull |= (uint32_t)(exy2 + fz * fz > Rc2) << (8 + q);
         cull |= (uint32_t)(exy2 + gz * gz > Rc2) << (16 + q);
@@ -1219,15 +1223,12 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
           cze = czh >= czl ? czh - czl + 1 : 0;
         }
       }
-      const int total = 5 * span;
-      for (int t0 = 0; t0 < total; t0 += 32) {
-        const int t = t0 + lane;
-        const int c = t / span < 4 ? t / span : 4;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {  // box starts of column c, z in [zf-1, zl+2], one lane per z
         const int zlo_c = __shfl_sync(FULL, czl, c), ext_c = __shfl_sync(FULL, cze, c);
         const uint32_t off_c = __shfl_sync(FULL, cof, c);
-        if (t < total) {
+        for (int tt = lane; tt < span; tt += 32) {
           uint32_t v = 0u;
-          const int tt = t - c * span;
           if (off_c != 0xffffffffu) {
             int k = zf - 1 + tt - zlo_c;
             k = k < 0 ? 0 : (k > ext_c ? ext_c : k);
