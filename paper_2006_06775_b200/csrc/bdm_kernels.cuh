@@ -1011,6 +1011,9 @@ constexpr int HA_THREADS = 256;
 constexpr int HA_MIN_BLOCKS = BDM_HA_MIN_BLOCKS;  // pass A: 4 x 8 resident warps per SM
 constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 
+#ifndef BDM_HMAP
+#define BDM_HMAP 1  // pass A: closed-form cursor (0: shared-memory run list with predicated refills)
+#endif
 #ifndef BDM_HSTAGE
 #define BDM_HSTAGE 0  // 1: pass A single-column chunks read candidates from a TMA-staged shared copy (measured slower)
 #endif
@@ -1153,6 +1156,55 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
   }
 }
 
+// BDM_HMAP: the candidate loop with the closed-form cursor -- no shared-memory run refills and no
+// serial dependency between the slots of an iteration.
+__device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __restrict__ agf, const uint32_t S[5],
+                                              const uint32_t A[5], uint32_t wmax, uint32_t w, uint32_t i,
+                                              unsigned long long mxy, unsigned long long mzr, int& cnt,
+                                              uint32_t& extra, uint32_t* __restrict__ bwd,
+                                              uint32_t* __restrict__ bcnt) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
+    uint32_t qs[NSLOT];
+    bool ok[NSLOT];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+      const uint32_t k = s0 + t;
+      uint32_t a = A[0];
+#pragma unroll
+      for (int q = 1; q < 5; ++q) a = k >= S[q] ? A[q] : a;
+      ok[t] = k < w;
+      qs[t] = ok[t] ? k + a : 0u;
+    }
+    float4 o[NSLOT];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) o[t] = __ldg(&agf[qs[t]]);
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+      float2 dxy, dzs;
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
+          : "l"(mxy), "l"(pack2(o[t].x, o[t].y)));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dzs))
+          : "l"(mzr), "l"(pack2(o[t].z, o[t].w)));
+      float2 sq, qz;
+      asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&sq))
+          : "l"(*reinterpret_cast<unsigned long long*>(&dxy)));
+      asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&qz))
+          : "l"(*reinterpret_cast<unsigned long long*>(&dzs)));
+      const float d2 = (sq.x + sq.y) + qz.x;
+      if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) {
+        if (cnt < HLA) {
+          sm.list[cnt++][lane] = qs[t];
+        } else {  // rare: the partner still gets its backward entry
+          const uint32_t sl = atomicAdd(&bcnt[qs[t]], 1u);
+          if (sl < (uint32_t)HBC) bwd[(size_t)qs[t] * HBC + sl] = i;
+          ++extra;
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     k_half_search(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin, uint32_t s_end,
                   GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
@@ -1278,7 +1330,34 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     // this lane's forward z-runs in canonical (= ascending sorted) order
     int nr = 0;
     uint32_t w = 0;
+#if BDM_HMAP
+    // closed-form cursor (BDM_HMAP): run q occupies flattened positions [S[q], S[q+1]); position k
+    // maps to k + A[q] (empty runs are skipped by the compare chain)
+    uint32_t S[5], A[5];
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      uint32_t b = 0, e = 0;
+      if (valid && ((cull >> q) & 1u)) {
+        const int z0 = q == 0 ? bz : bz - 1 + (int)((cull >> (8 + q)) & 1u);
+        const int z1 = bz + 1 - (int)((cull >> (16 + q)) & 1u);
+        if (coop) {
+          b = sm.tab[q][z0 - zf + 1];
+          e = sm.tab[q][z1 - zf + 2];
+        } else {
+          const int cx = bx + (q >= 2 ? 1 : 0), cy = by + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
+          zrun(g, cx, cy, z0, z1, b, e);
+        }
+        if (q == 0) b = i + 1;  // own box: only the agents after i
+        if (b >= e) b = e = 0;
+      }
+      S[q] = w;
+      A[q] = b - w;
+      w += e - b;
+    }
+    if (false) {
+#else
     if (valid) {
+#endif
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
         if (!((cull >> q) & 1u)) continue;
@@ -1330,7 +1409,11 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
       __syncwarp();  // every lane is done with buf before the next chunk's copies overwrite it
     } else
 #endif
+#if BDM_HMAP
+      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+#else
       half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+#endif
     if (valid) {
       half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
       const uint32_t nf = (uint32_t)cnt + extra;
