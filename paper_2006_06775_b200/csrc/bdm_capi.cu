@@ -279,6 +279,19 @@ void init_device_info(bdm_ctx* h) {
   h->scan_blocks_per_sm = per_sm > 0 ? per_sm : 1;
   cudaFuncSetAttribute(k_half_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HA_SMEM_BYTES);
   cudaFuncSetAttribute(k_half_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
+#ifndef BDM_NO_CARVEOUT
+  {  // shared memory only as large as the resident blocks need: the rest stays L1 for the gathers
+    int smem_sm = 0;
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, h->device);
+    auto pct = [&](size_t per_block, int blocks_per_sm) {
+      const double need = (double)blocks_per_sm * (per_block + 1024);
+      return smem_sm > 0 ? std::min(100, (int)std::ceil(100.0 * need / smem_sm) + 1) : -1;
+    };
+    cudaFuncSetAttribute(k_half_search, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HA_SMEM_BYTES, HA_MIN_BLOCKS));
+    cudaFuncSetAttribute(k_half_sum, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
+    (void)cudaGetLastError();
+  }
+#endif
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_search, HA_THREADS, HA_SMEM_BYTES);
   h->half_a_blocks_per_sm = per_sm > 0 ? per_sm : 1;

@@ -1022,6 +1022,7 @@ constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 #endif
 constexpr int HPCAP = BDM_HPCAP;  // staged candidates (float4) per warp
 
+#define HA_RR (!BDM_HMAP || BDM_HSTAGE)  // the shared-memory run list (cursor with refills)
 struct HalfASmem {
 #if BDM_HSTAGE
   float4 buf[HPCAP];        // fp32 candidates of the 5 forward columns' union z-runs (staged chunks)
@@ -1031,7 +1032,9 @@ struct HalfASmem {
   uint32_t pad_;
 #endif
   uint32_t list[HLA][32];  // survivors (sorted index j, or staged buffer index) of this lane, ascending
+#if HA_RR
   uint2 rr[7][32];         // this lane's non-empty forward z-runs [b, e), then the sentinel (0, 0)
+#endif
   uint32_t tab[5][TSPAN];  // box starts of the 5 forward columns (single-column chunks)
 };
 
@@ -1085,6 +1088,7 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
 // Candidate loop of pass A over this lane's runs rr[] (flattened, branch-free run switch): fp32
 // conservative filter of k_force; survivors to the lane's list (STAGED: runs and survivors are
 // buffer indices of sm.buf).  A survivor beyond the list (rare) gets its backward entry at once.
+#if HA_RR
 template <bool STAGED>
 __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restrict__ agf, uint32_t rr_base,
                                           uint32_t wmax, uint32_t w, uint32_t i, unsigned long long mxy,
@@ -1156,6 +1160,8 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
   }
 }
 
+#endif
+
 // BDM_HMAP: the candidate loop with the closed-form cursor -- no shared-memory run refills and no
 // serial dependency between the slots of an iteration.
 __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __restrict__ agf, const uint32_t S[5],
@@ -1212,7 +1218,9 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
+#if HA_RR
   const uint32_t rr_base = (uint32_t)__cvta_generic_to_shared(&sm.rr[0][lane]);
+#endif
 #if BDM_HSTAGE
   uint32_t phase = 0;  // parity of this warp's staging mbarrier
   if (lane == 0) mbar_init(&sm.bar);
@@ -1354,10 +1362,10 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
       A[q] = b - w;
       w += e - b;
     }
-    if (false) {
-#else
-    if (valid) {
 #endif
+#if HA_RR
+    uint32_t wr = 0;  // total length of the run list (staged path, or BDM_HMAP=0)
+    if (valid) {
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
         if (!((cull >> q) & 1u)) continue;
@@ -1381,12 +1389,16 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
           }
 #endif
           sm.rr[nr][lane] = make_uint2(b, e);
-          w += e - b;
+          wr += e - b;
           ++nr;
         }
       }
     }
     sm.rr[nr][lane] = make_uint2(0u, 0u);  // sentinel: after the last run q never meets e again
+#if !BDM_HMAP
+    w = wr;
+#endif
+#endif
     __syncwarp();
     const uint32_t wmax = __reduce_max_sync(FULL, w);
     const float ri32 = __double2float_ru(ri + g.m32);
