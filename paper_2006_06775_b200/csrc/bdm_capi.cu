@@ -137,6 +137,7 @@ struct bdm_ctx {
   bool last_half = false;  // the last step used the half-shell path
   bool split_pending = false;  // slab: bdm_slab_split ran, bdm_slab_commit not yet
   int64_t n_dead = 0;          // slab: committed emigrants still in ag[cur][0..n) (D < 0), dropped by the next sort
+  int64_t fused_n0 = 0;        // slab: agents whose next columns the last step accumulated (ag[cur][0..fused_n0))
   uint32_t last_n_lo = 0;      // slab: lower ghosts of the last step (sorted first)
   int32_t split_xb = 0, split_xe = 0;
   int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
@@ -328,17 +329,18 @@ bool ensure_half(bdm_ctx* h) {
 // Half-shell force step over the owned sorted range [a_begin, a_end) of ag[src]; pass A searches
 // from s_begin (slab mode: the lower ghost layer searches too, its pairs with owned agents are
 // forward pairs of the ghost).
+// frame4 (x lo, y lo, nx, ny) of the fused column pass; nullptr: this step's tight extents +- 1 box.
 int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t a_end, uint32_t n_all,
                const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids,
-               bool fuse_cols = false) {
+               bool fuse_cols = false, const int32_t* frame4 = nullptr) {
   cudaStream_t s = h->stream;
   ColNext cn{0, 0, 0, 0, nullptr, nullptr};
   h->cols_next = false;
   if (fuse_cols) {  // next build's frame: this step's tight extents +- 1 box (|dp| < L)
-    cn.lo0 = h->tlo[0] - 1;
-    cn.lo1 = h->tlo[1] - 1;
-    cn.nx = h->thi[0] - h->tlo[0] + 3;
-    cn.ny = h->thi[1] - h->tlo[1] + 3;
+    cn.lo0 = frame4 ? frame4[0] : h->tlo[0] - 1;
+    cn.lo1 = frame4 ? frame4[1] : h->tlo[1] - 1;
+    cn.nx = frame4 ? frame4[2] : h->thi[0] - h->tlo[0] + 3;
+    cn.ny = frame4 ? frame4[3] : h->thi[1] - h->tlo[1] + 3;
     const size_t nc2 = (size_t)cn.nx * (size_t)cn.ny;
     int rc = ensure_columns(h, nc2 + 1, true);
     if (rc) return rc;
@@ -1687,6 +1689,7 @@ int bdm_slab_pack(bdm_handle h, int what, int32_t x_begin, int32_t x_end, double
   if (what == BDM_MIGRANTS) {  // commit the compaction of the agents that stay
     h->cur = 1 - h->cur;
     h->n = h->cnt_host[2];
+    h->fused_n0 = std::min<int64_t>(h->fused_n0, h->n);  // agents appended from here on need their columns
   }
   return BDM_OK;
 }
@@ -1741,10 +1744,9 @@ int bdm_slab_commit(bdm_handle h, int64_t n_stay) {
                                                               h->split_xb, h->split_xe);
   CU(h, cudaGetLastError());
   h->launches += n_stay < h->n;
-  h->n_dead = h->n - n_stay;
+  h->n_dead = h->n - n_stay;  // (the fused next columns stay valid: they cover a superset)
   h->split_pending = false;
   h->ext_valid = false;
-  h->cols_next = false;
   return BDM_OK;
 }
 
@@ -1813,7 +1815,25 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
     g.lo[a] = glo3[a];
     g.hi[a] = ghi3[a];
   }
-  const int64_t nb = (hix - lox + 1) * ((int64_t)g.hi[1] - g.lo[1] + 1) * ((int64_t)g.hi[2] - g.lo[2] + 1);
+  // fused column pass of the last step: its frame becomes this grid's x/y frame if it contains this
+  // step's (it does when every agent moved less than a box); the agents appended since (immigrants,
+  // ghosts) add their columns first
+  if (h->cols_next && g.lo[0] >= h->nlo[0] && g.hi[0] < h->nlo[0] + h->nnx && g.lo[1] >= h->nlo[1] &&
+      g.hi[1] < h->nlo[1] + h->nny && h->fused_n0 <= n_own) {
+    g.lo[0] = h->nlo[0];
+    g.lo[1] = h->nlo[1];
+    g.hi[0] = h->nlo[0] + h->nnx - 1;
+    g.hi[1] = h->nlo[1] + h->nny - 1;
+    g.ny = h->nny;
+    const int64_t m = n_tot - h->fused_n0;
+    if (m > 0) {
+      k_col_ext<<<blocks(m, 512), 256, 0, s>>>(h->ag[h->cur] + h->fused_n0, (uint32_t)m, g, h->czlo2, h->czhi2);
+      h->launches += 1;
+    }
+  } else {
+    h->cols_next = false;
+  }
+  const int64_t nb = ((int64_t)g.hi[0] - g.lo[0] + 1) * ((int64_t)g.hi[1] - g.lo[1] + 1) * ((int64_t)g.hi[2] - g.lo[2] + 1);
   if (nb >= (int64_t)0xffffffffll) return fail(h, BDM_ERANGE, "bdm_slab_step: n_boxes = %lld >= 2^32", (long long)nb);
   g.ny = g.hi[1] - g.lo[1] + 1;
   g.nz = g.hi[2] - g.lo[2] + 1;
@@ -1832,9 +1852,15 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   h->last_half = n_live > 0 && ensure_half(h);
   if (h->last_half) {
     // pass A from the first lower ghost (their forward pairs with owned agents are the owned
-    // agents' backward pairs); owned agents' forward runs reach into the upper ghosts
+    // agents' backward pairs); owned agents' forward runs reach into the upper ghosts.  The sum
+    // pass accumulates the next step's columns in the frame [x_begin-1, x_end] x [ylo-1, yhi+1]
+    // (clipped to the extents +- 1): every agent of the next step lies in it (|dp| < L)
+    const bool fuse = h->prm.max_disp < h->grid.L * (1.0 - 0x1p-20);
+    const int64_t fx0 = std::max<int64_t>((int64_t)x_begin - 1, (int64_t)glo3[0] - 1);
+    const int64_t fx1 = std::min<int64_t>((int64_t)x_end, (int64_t)ghi3[0] + 1);
+    const int32_t frame4[4] = {(int32_t)fx0, glo3[1] - 1, (int32_t)(fx1 - fx0 + 1), ghi3[1] - glo3[1] + 3};
     rc = half_force(h, src, 0u, (uint32_t)n_lo, (uint32_t)(n_sorted - n_hi), (uint32_t)n_sorted, pd, h->ag[dst], h->id[dst],
-                    want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr);
+                    want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, fuse, frame4);
     if (rc) return rc;
   } else if (n_live > 0) {
     k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], (uint32_t)n_lo,
@@ -1848,6 +1874,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
   h->cur = dst;
   h->n = n_live;
   h->n_dead = 0;
+  h->fused_n0 = n_live;
   h->ext_valid = true;
   if (want_dp) {
     h->n_dp = n_live;
