@@ -487,7 +487,7 @@ __device__ __forceinline__ void unpack_box(unsigned long long v, int& bx, int& b
 // one box, is marked hot (conservative superset of every mover's two 3x3x3 neighbourhoods).
 // Only boxes inside their column's occupied z-range exist (and only they can hold agents).
 __global__ void k_mark_hot(const double4* __restrict__ ag, const unsigned long long* __restrict__ hist, uint32_t n,
-                           GridDev g, uint8_t* __restrict__ bflag) {
+                           GridDev g, uint8_t* __restrict__ bflag, int radius = 1, uint8_t value = 1) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const unsigned long long h = i < n ? hist[i] : 0ull;
@@ -501,8 +501,8 @@ __global__ void k_mark_hot(const double4* __restrict__ ag, const unsigned long l
     unpack_box(h & ~(1ull << 63), ob[0], ob[1], ob[2]);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      lo[a] = min(nb[a], ob[a]) - 1;
-      hi[a] = max(nb[a], ob[a]) + 1;
+      lo[a] = min(nb[a], ob[a]) - radius;
+      hi[a] = max(nb[a], ob[a]) + radius;
     }
   }
 #pragma unroll
@@ -521,7 +521,7 @@ __global__ void k_mark_hot(const double4* __restrict__ ag, const unsigned long l
       const int a = max(lo[2], zl), d = min(hi[2], zh);
       if (a > d) continue;
       const uint32_t o = __ldg(&g.coff[c]) + (uint32_t)(a - zl);
-      for (int t = lane; t <= d - a; t += 32) bflag[o + t] = 1;
+      for (int t = lane; t <= d - a; t += 32) bflag[o + t] = value;
     }
 }
 
@@ -1214,7 +1214,7 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
 __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     k_half_search(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin, uint32_t s_end,
                   GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
-                  uint32_t* __restrict__ bcnt, Extents* ext) {
+                  uint32_t* __restrict__ bcnt, Extents* ext, const uint8_t* __restrict__ hot, bool count_searched) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1233,11 +1233,18 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
     if (base >= s_end) break;
     const uint32_t i = (uint32_t)base + lane;
-    const bool valid = i < s_end;
-    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool in_range = i < s_end;
+    const double4 me = in_range ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const float4 mf = in_range ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
     const double ri = 0.5 * me.w;
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+    // stationary-region skip (NEXT-1): only agents of warm boxes (within 2 boxes of a mover) search;
+    // their forward pairs give the hot agents (within 1 box) their backward pairs
+    const bool valid = in_range && (hot == nullptr || hot[box_key(g, bx, by, bz)] != 0);
+    if (count_searched) {  // skip statistics (bdm_get_skip_stats)
+      const unsigned se = __ballot_sync(FULL, valid);
+      if (se && lane == 0) atomicAdd(&ext->searched, (uint32_t)__popc(se));
+    }
     // box culling of k_force, for the 5 forward columns q = 0..4 <-> (dx, dy) = (0,0), (0,+1),
     // (+1,-1), (+1,0), (+1,+1): bit q kept, bit 8+q z-1 box culled, bit 16+q z+1 box culled
     uint32_t cull = 0u;
@@ -1430,6 +1437,8 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
       half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
       const uint32_t nf = (uint32_t)cnt + extra;
       fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+    } else if (in_range) {
+      fcnt[i] = 0;  // quiet (skip mode): no forward pairs
     }
     __syncwarp();
   }
@@ -1471,7 +1480,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
                const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
-               const uint32_t* __restrict__ bcnt, ColNext cn) {
+               const uint32_t* __restrict__ bcnt, ColNext cn, const uint8_t* __restrict__ hot,
+               unsigned long long* __restrict__ hist_out) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1490,8 +1500,12 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const uint4* brow = reinterpret_cast<const uint4*>(bwd + (size_t)i * HBC);
     const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
     const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const uint32_t nf = valid ? fcnt[i] : 0u;
-    const uint32_t nb = valid ? bcnt[i] : 0u;
+    // stationary-region skip: an agent outside the hot boxes had no moving agent within a box, so
+    // its force is unchanged and its displacement stays exactly 0 (NEXT-1, as k_force)
+    const bool active = valid && (hot == nullptr || hot[box_key(g, (int)floor(me.x * g.inv), (int)floor(me.y * g.inv),
+                                                                 (int)floor(me.z * g.inv))] == 2);
+    const uint32_t nf = active ? fcnt[i] : 0u;
+    const uint32_t nb = active ? bcnt[i] : 0u;
     // (rows are read only where the count says so: a speculative read of every row costs more DRAM
     // traffic than the round trip it saves)
     const uint4 b4 = nb ? __ldg(brow) : make_uint4(0u, 0u, 0u, 0u);
@@ -1548,6 +1562,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       const unsigned sm_ = __ballot_sync(FULL, slow);
       if (sm_ && lane == 0) atomicAdd(&ext_next->slow, (uint32_t)__popc(sm_));
     }
+
     // O6 displacement, O7 update (as k_force)
     double dpx = 0.0, dpy = 0.0, dpz = 0.0;
     const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
@@ -1568,6 +1583,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
       ag_out[o] = np;
+      if (hist_out) {
+        const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
+        hist_out[o] = ((unsigned long long)moved << 63) |
+                      pack_box((int)floor(me.x * g.inv), (int)floor(me.y * g.inv), (int)floor(me.z * g.inv));
+      }
       if (id_out) id_out[o] = ids[i];
       if (dp_out) {
         dp_out[3 * (size_t)o] = dpx;
@@ -1583,6 +1603,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
         elo[a] = min(elo[a], nb3[a]);
         ehi[a] = max(ehi[a], nb3[a]);
       }
+    }
+    if (hist_out) {  // movers of this step (the skip heuristic of the next build)
+      const unsigned mv = __ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0));
+      if (mv && lane == 0) atomicAdd(&ext_next->moved, (uint32_t)__popc(mv));
     }
     if (cn.czlo) {  // fused column pass (warp-aggregated: a chunk touches one or two columns)
       uint32_t c = 0xffffffffu;
