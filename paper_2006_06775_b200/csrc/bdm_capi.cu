@@ -332,8 +332,7 @@ bool ensure_half(bdm_ctx* h) {
 // frame4 (x lo, y lo, nx, ny) of the fused column pass; nullptr: this step's tight extents +- 1 box.
 int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t a_end, uint32_t n_all,
                const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids,
-               bool fuse_cols = false, const int32_t* frame4 = nullptr, const uint8_t* hot = nullptr,
-               unsigned long long* hist_out = nullptr) {
+               bool fuse_cols = false, const int32_t* frame4 = nullptr, unsigned long long* hist_out = nullptr) {
   cudaStream_t s = h->stream;
   ColNext cn{0, 0, 0, 0, nullptr, nullptr};
   h->cols_next = false;
@@ -359,7 +358,7 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
                                                    std::max<uint64_t>(1, (a_end - s_begin + HA_THREADS - 1) / HA_THREADS));
   k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, s>>>(h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
-                                                       h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext, hot, hist_out != nullptr);
+                                                       h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr);
   DBG(h, "k_half_search");
   const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
                                                    std::max<uint64_t>(1, (a_end - a_begin + FORCE_THREADS - 1) / FORCE_THREADS));
@@ -369,7 +368,7 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   }
   k_half_sum<<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd, ag_out,
                                                        id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt,
-                                                       h->h_bwd, h->h_bcnt, cn, hot, hist_out);
+                                                       h->h_bwd, h->h_bcnt, cn, hist_out);
   DBG(h, "k_half_sum");
   CU(h, cudaGetLastError());
   h->launches += 2;
@@ -548,14 +547,8 @@ int grid_build(bdm_ctx* h) {
       h->hot_cap = h->table_cap + 4;
     }
     k_flag_zero<<<h->sm_count * 4, 256, 0, h->stream>>>(h->hot, h->coff, h->grid.n_cols);
-    if (!h->half_off && !g_no_half) {
-      // half-shell path: warm (1) = within 2 boxes of a mover, searches; hot (2) = within 1 box, sums
-      k_mark_hot<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->hist[h->cur], (uint32_t)h->n, h->grid,
-                                                           h->hot, 2, (uint8_t)1);
-      h->launches += 1;
-    }
     k_mark_hot<<<blocks(h->n, 256), 256, 0, h->stream>>>(h->ag[h->cur], h->hist[h->cur], (uint32_t)h->n, h->grid,
-                                                         h->hot, 1, (uint8_t)2);
+                                                         h->hot);
     DBG(h, "k_mark_hot");
     CU(h, cudaGetLastError());
     h->launches += 2;
@@ -583,7 +576,9 @@ int force_step(bdm_ctx* h, bool want_dp) {
   ParamsDev pd = params_dev(h->prm);
   double* dp = want_dp ? h->dp : nullptr;
   const unsigned grid = force_grid(h, n);
-  h->last_half = !(h->prm.flags & BDM_RECORD) && n > 0 && ensure_half(h);
+  // the single-pass k_force serves the stationary-region skip (it skips the whole search of quiet
+  // agents); otherwise the half-shell path, which also keeps the skip statistics (hist) current
+  h->last_half = !(h->prm.flags & BDM_RECORD) && !h->skip_active && n > 0 && ensure_half(h);
   h->cols_next = false;
   if (h->last_half) {
     // fuse the next build's column pass when nothing moves agents between this step and that build
@@ -591,7 +586,7 @@ int force_step(bdm_ctx* h, bool want_dp) {
     const bool fuse = !h->growth_on && !h->fields_on && h->n_el == 0 && !h->slab &&
                       h->prm.max_disp < h->grid.L * (1.0 - 0x1p-20);
     int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr, fuse, nullptr,
-                        h->skip_active ? h->hot : nullptr, h->hist[0] ? h->hist[dst] : nullptr);
+                        h->hist[0] ? h->hist[dst] : nullptr);
     if (rc) return rc;
   } else if (h->prm.flags & BDM_RECORD)
     k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],

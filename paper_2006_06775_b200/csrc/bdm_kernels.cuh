@@ -673,6 +673,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
   ForceSmem& sm = s_all[threadIdx.x >> 5];
   int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
   bool ebad = false;
+  uint32_t n_moved = 0, n_searched = 0;  // skip statistics of this warp
 
   while (true) {
     uint32_t chunk = 0;
@@ -961,14 +962,14 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
         rec.ct_hash[o] = ct_hash;
       }
     }
-    if (hist_out) {
-      const unsigned mv = __ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0));
-      const unsigned se = __ballot_sync(FULL, search);
-      if (lane == 0) {
-        if (mv) atomicAdd(&ext_next->moved, (uint32_t)__popc(mv));
-        if (se) atomicAdd(&ext_next->searched, (uint32_t)__popc(se));
-      }
+    if (hist_out) {  // counted per warp, added once at the end (a same-address atomic per chunk serialises)
+      n_moved += __popc(__ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0)));
+      n_searched += __popc(__ballot_sync(FULL, search));
     }
+  }
+  if (hist_out && lane == 0) {
+    if (n_moved) atomicAdd(&ext_next->moved, n_moved);
+    if (n_searched) atomicAdd(&ext_next->searched, n_searched);
   }
   // next step's extents: one guarded atomic set per warp (a few thousand warps per launch)
   if (__any_sync(FULL, ebad) && lane == 0) ext_next->range_err = 1;
@@ -1214,13 +1215,15 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
 __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     k_half_search(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin, uint32_t s_end,
                   GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
-                  uint32_t* __restrict__ bcnt, Extents* ext, const uint8_t* __restrict__ hot, bool count_searched) {
+                  uint32_t* __restrict__ bcnt, Extents* ext, bool count_searched) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
 #if HA_RR
   const uint32_t rr_base = (uint32_t)__cvta_generic_to_shared(&sm.rr[0][lane]);
 #endif
+  // statistics of the stationary-region skip mode (bdm_get_skip_stats): this path searches everyone
+  if (count_searched && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ext->searched, s_end - s_begin);
 #if BDM_HSTAGE
   uint32_t phase = 0;  // parity of this warp's staging mbarrier
   if (lane == 0) mbar_init(&sm.bar);
@@ -1233,18 +1236,11 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
     if (base >= s_end) break;
     const uint32_t i = (uint32_t)base + lane;
-    const bool in_range = i < s_end;
-    const double4 me = in_range ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-    const float4 mf = in_range ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool valid = i < s_end;
+    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
     const double ri = 0.5 * me.w;
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
-    // stationary-region skip (NEXT-1): only agents of warm boxes (within 2 boxes of a mover) search;
-    // their forward pairs give the hot agents (within 1 box) their backward pairs
-    const bool valid = in_range && (hot == nullptr || hot[box_key(g, bx, by, bz)] != 0);
-    if (count_searched) {  // skip statistics (bdm_get_skip_stats)
-      const unsigned se = __ballot_sync(FULL, valid);
-      if (se && lane == 0) atomicAdd(&ext->searched, (uint32_t)__popc(se));
-    }
     // box culling of k_force, for the 5 forward columns q = 0..4 <-> (dx, dy) = (0,0), (0,+1),
     // (+1,-1), (+1,0), (+1,+1): bit q kept, bit 8+q z-1 box culled, bit 16+q z+1 box culled
     uint32_t cull = 0u;
@@ -1437,8 +1433,6 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
       half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
       const uint32_t nf = (uint32_t)cnt + extra;
       fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
-    } else if (in_range) {
-      fcnt[i] = 0;  // quiet (skip mode): no forward pairs
     }
     __syncwarp();
   }
@@ -1480,13 +1474,13 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
                const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
-               const uint32_t* __restrict__ bcnt, ColNext cn, const uint8_t* __restrict__ hot,
-               unsigned long long* __restrict__ hist_out) {
+               const uint32_t* __restrict__ bcnt, ColNext cn, unsigned long long* __restrict__ hist_out) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
   bool ebad = false;
+  uint32_t n_moved = 0;
   while (true) {
     uint32_t chunk = 0;
     if (lane == 0) chunk = atomicAdd(&ext_next->work, 1u);
@@ -1500,12 +1494,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const uint4* brow = reinterpret_cast<const uint4*>(bwd + (size_t)i * HBC);
     const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
     const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
-    // stationary-region skip: an agent outside the hot boxes had no moving agent within a box, so
-    // its force is unchanged and its displacement stays exactly 0 (NEXT-1, as k_force)
-    const bool active = valid && (hot == nullptr || hot[box_key(g, (int)floor(me.x * g.inv), (int)floor(me.y * g.inv),
-                                                                 (int)floor(me.z * g.inv))] == 2);
-    const uint32_t nf = active ? fcnt[i] : 0u;
-    const uint32_t nb = active ? bcnt[i] : 0u;
+    const uint32_t nf = valid ? fcnt[i] : 0u;
+    const uint32_t nb = valid ? bcnt[i] : 0u;
     // (rows are read only where the count says so: a speculative read of every row costs more DRAM
     // traffic than the round trip it saves)
     const uint4 b4 = nb ? __ldg(brow) : make_uint4(0u, 0u, 0u, 0u);
@@ -1604,10 +1594,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
         ehi[a] = max(ehi[a], nb3[a]);
       }
     }
-    if (hist_out) {  // movers of this step (the skip heuristic of the next build)
-      const unsigned mv = __ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0));
-      if (mv && lane == 0) atomicAdd(&ext_next->moved, (uint32_t)__popc(mv));
-    }
+    if (hist_out)  // movers of this step (the skip heuristic of the next build), added once per warp
+      n_moved += __popc(__ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0)));
     if (cn.czlo) {  // fused column pass (warp-aggregated: a chunk touches one or two columns)
       uint32_t c = 0xffffffffu;
       bool out = false;
@@ -1628,6 +1616,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       if (__any_sync(FULL, out) && lane == 0) ext_next->col_bad = 1u;
     }
   }
+  if (hist_out && lane == 0 && n_moved) atomicAdd(&ext_next->moved, n_moved);
   if (__any_sync(FULL, ebad) && lane == 0) ext_next->range_err = 1;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {

@@ -47,4 +47,6 @@ for s in range(0, a.steps, a.every):
     print(f"steps {s + a.every:4d}: moved {st['moved'] / st['n']:.3f} searched {st['searched'] / st['n']:.3f} "
           f"ms/step skip {(ts['grid_ms'] + ts['force_ms']) / ts['steps']:.3f} "
           f"(force {ts['force_ms'] / ts['steps']:.3f}) no-skip {(tn['grid_ms'] + tn['force_ms']) / tn['steps']:.3f} "
-          f"(force {tn['force_ms'] / tn['steps']:.3f}) identical={same}", flush=True)
+          f"(force {tn['force_ms'] / tn['steps']:.3f}) identical={same}; skip passes search "
+          f"{ts['search_ms'] / ts['steps']:.3f} sum {ts['sum_ms'] / ts['steps']:.3f}, no-skip "
+          f"{tn['search_ms'] / tn['steps']:.3f} / {tn['sum_ms'] / tn['steps']:.3f}", flush=True)
