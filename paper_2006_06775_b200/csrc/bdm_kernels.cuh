@@ -533,6 +533,25 @@ __global__ void k_flag_zero(uint8_t* __restrict__ bflag, const uint32_t* __restr
 }
 
 // ------------------------------------------------------------------------------------------ K6
+#ifndef BDM_TICKET
+#define BDM_TICKET 4
+#endif
+// Chunk tickets of the persistent kernels: a warp takes BDM_TICKET consecutive 32-agent chunks per
+// atomic on the (single, same-address) work counter -- one atomic per chunk serialises in L2.
+struct Tickets {
+  uint32_t next = 0, left = 0;
+  __device__ __forceinline__ uint32_t take(uint32_t* work, int lane) {
+    if (left == 0) {
+      uint32_t t = 0;
+      if (lane == 0) t = atomicAdd(work, 1u);
+      next = __shfl_sync(0xffffffffu, t, 0) * (uint32_t)BDM_TICKET;
+      left = BDM_TICKET;
+    }
+    --left;
+    return next++;
+  }
+};
+
 constexpr int FORCE_THREADS = 256;
 constexpr int FORCE_WARPS = FORCE_THREADS / 32;
 #ifndef BDM_FORCE_MIN_BLOCKS
@@ -675,10 +694,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
   bool ebad = false;
   uint32_t n_moved = 0, n_searched = 0;  // skip statistics of this warp
 
+  Tickets tk;
   while (true) {
-    uint32_t chunk = 0;
-    if (lane == 0) chunk = atomicAdd(&ext_next->work, 1u);
-    chunk = __shfl_sync(FULL, chunk, 0);
+    const uint32_t chunk = tk.take(&ext_next->work, lane);
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
     if (base >= a_end) break;
     const uint32_t i = (uint32_t)base + lane;
@@ -1229,10 +1247,9 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   if (lane == 0) mbar_init(&sm.bar);
   __syncwarp();
 #endif
+  Tickets tk;
   while (true) {
-    uint32_t chunk = 0;
-    if (lane == 0) chunk = atomicAdd(&ext->work_a, 1u);
-    chunk = __shfl_sync(FULL, chunk, 0);
+    const uint32_t chunk = tk.take(&ext->work_a, lane);
     const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
     if (base >= s_end) break;
     const uint32_t i = (uint32_t)base + lane;
@@ -1481,10 +1498,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
   bool ebad = false;
   uint32_t n_moved = 0;
+  Tickets tk;
   while (true) {
-    uint32_t chunk = 0;
-    if (lane == 0) chunk = atomicAdd(&ext_next->work, 1u);
-    chunk = __shfl_sync(FULL, chunk, 0);
+    const uint32_t chunk = tk.take(&ext_next->work, lane);
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
     if (base >= a_end) break;
     const uint32_t i = (uint32_t)base + lane;
