@@ -1031,7 +1031,7 @@ constexpr int HA_MIN_BLOCKS = BDM_HA_MIN_BLOCKS;  // pass A: 4 x 8 resident warp
 constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 
 #ifndef BDM_HMAP
-#define BDM_HMAP 1  // pass A: closed-form cursor (0: shared-memory run list with predicated refills)
+#define BDM_HMAP 0  // pass A cursor: 0 shared-memory run list with predicated refills, 1 closed-form map
 #endif
 #ifndef BDM_HSTAGE
 #define BDM_HSTAGE 0  // 1: pass A single-column chunks read candidates from a TMA-staged shared copy (measured slower)
