@@ -538,14 +538,20 @@ __global__ void k_flag_zero(uint8_t* __restrict__ bflag, const uint32_t* __restr
 #endif
 // Chunk tickets of the persistent kernels: a warp takes BDM_TICKET consecutive 32-agent chunks per
 // atomic on the (single, same-address) work counter -- one atomic per chunk serialises in L2.
+// Small populations keep one chunk per ticket while a warp would get fewer than 8 tickets (tail balance).
 struct Tickets {
-  uint32_t next = 0, left = 0;
+  uint32_t next = 0, left = 0, per = 1;
+  __device__ __forceinline__ explicit Tickets(uint64_t n_agents) {
+    const uint64_t chunks = (n_agents + 31) / 32, warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    const uint64_t k = chunks / (warps * 8 + 1);
+    per = k < 1 ? 1u : (k > (uint64_t)BDM_TICKET ? (uint32_t)BDM_TICKET : (uint32_t)k);
+  }
   __device__ __forceinline__ uint32_t take(uint32_t* work, int lane) {
     if (left == 0) {
       uint32_t t = 0;
       if (lane == 0) t = atomicAdd(work, 1u);
-      next = __shfl_sync(0xffffffffu, t, 0) * (uint32_t)BDM_TICKET;
-      left = BDM_TICKET;
+      next = __shfl_sync(0xffffffffu, t, 0) * per;
+      left = per;
     }
     --left;
     return next++;
@@ -694,7 +700,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
   bool ebad = false;
   uint32_t n_moved = 0, n_searched = 0;  // skip statistics of this warp
 
-  Tickets tk;
+  Tickets tk(a_end - a_begin);
   while (true) {
     const uint32_t chunk = tk.take(&ext_next->work, lane);
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
@@ -1247,7 +1253,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   if (lane == 0) mbar_init(&sm.bar);
   __syncwarp();
 #endif
-  Tickets tk;
+  Tickets tk(s_end - s_begin);
   while (true) {
     const uint32_t chunk = tk.take(&ext->work_a, lane);
     const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
@@ -1498,7 +1504,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
   bool ebad = false;
   uint32_t n_moved = 0;
-  Tickets tk;
+  Tickets tk(a_end - a_begin);
   while (true) {
     const uint32_t chunk = tk.take(&ext_next->work, lane);
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
