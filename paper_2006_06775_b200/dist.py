@@ -445,15 +445,36 @@ class SlabDriver:
         self.migrated += self.migrate()
 
 
-def initial_bounds(pos: np.ndarray, diam: np.ndarray, world: int, box_edge_min: float = 0.0):
-    """Setup helper (outside the hot path): global L and count-balanced bounds from the full population
-    known to every rank (the bench generates the whole seeded population on every rank)."""
+def layer_work(pos: np.ndarray, inv: float, x0: int, nx: int) -> np.ndarray:
+    """Estimated work per box-x layer (cut by work, not by count).  An agent costs a
+    fixed part (sort, displacement) plus a part proportional to its 27-box candidates, which scale
+    with the occupancy n_b of its box: cost_i ~ 1 + c_i / c_mean with c_i ~ n_b(i).  Per layer:
+    sum_b n_b + sum_b n_b^2 / (sum_all n_b^2 / N)."""
+    b = np.floor(pos * inv).astype(np.int64)
+    b -= b.min(axis=0)
+    dims = b.max(axis=0) + 1
+    key = (b[:, 0] * dims[1] + b[:, 1]) * dims[2] + b[:, 2]
+    uk, cnt = np.unique(key, return_counts=True)
+    layer = (uk // (dims[1] * dims[2])).astype(np.int64)
+    cnt = cnt.astype(np.float64)
+    n = np.bincount(layer, weights=cnt, minlength=nx)[:nx]
+    sq = np.bincount(layer, weights=cnt * cnt, minlength=nx)[:nx]
+    mean_sq = sq.sum() / max(len(pos), 1)
+    return n + (sq / mean_sq if mean_sq > 0 else 0.0)
+
+
+def initial_bounds(pos: np.ndarray, diam: np.ndarray, world: int, box_edge_min: float = 0.0,
+                   weighted: bool = True):
+    """Setup helper (outside the hot path): global L and work-balanced (weighted, default) or
+    count-balanced bounds from the full population known to every rank (the bench generates the
+    whole seeded population on every rank)."""
     L = max(float(diam.max()), box_edge_min)
     inv = 1.0 / (L * (1.0 + 2.0 ** -30))
     bx = np.floor(pos[:, 0] * inv).astype(np.int64)
     x0 = int(bx.min())
     hist = np.bincount(bx - x0)
-    return choose_bounds(hist, x0, world), bx
+    w = layer_work(pos, inv, x0, len(hist)) if weighted and world > 1 and len(pos) else None
+    return choose_bounds(hist, x0, world, w), bx
 
 
 # --------------------------------------------------------------------------------- bench (N > 1)

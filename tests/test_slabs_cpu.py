@@ -41,6 +41,34 @@ def test_choose_bounds():
     assert all(y - x >= 2 for x, y in zip(b[1:-1], b[2:-1])), b
 
 
+def _slab_work(b, bx, w, x0):
+    cuts = [x0 - 1] + list(b[1:-1]) + [int(bx.max()) + 1]
+    return np.array([w[max(a - x0, 0):c - x0].sum() for a, c in zip(cuts, cuts[1:])])
+
+
+def test_work_weighted_bounds_balance_a_spheroid():
+    """count-balanced cuts leave the core slabs of the Gaussian spheroid with more
+    candidate work; cuts by estimated work (layer_work) balance it better, and a uniform population
+    keeps count-like cuts."""
+    rng = np.random.default_rng(3)
+    n = 400_000
+    sig = 992.2 * (n / 2e7) ** (1 / 3)
+    pos = rng.normal(0.0, sig, (n, 3))
+    diam = np.clip(np.exp(np.log(10.0) + 0.15 * rng.standard_normal(n)), 6.0, 16.0)
+    inv = 1.0 / (16.0 * (1.0 + 2.0 ** -30))
+    bc, bx = bdist.initial_bounds(pos, diam, 4, weighted=False)
+    bw, _ = bdist.initial_bounds(pos, diam, 4, weighted=True)
+    x0 = int(bx.min())
+    w = bdist.layer_work(pos, inv, x0, int(bx.max()) - x0 + 1)
+    imb = lambda b: (lambda v: v.max() / v.mean())(_slab_work(b, bx, w, x0))
+    assert imb(bw) < imb(bc)
+    # uniform density: the work estimate is proportional to the count, the cuts barely move
+    pos_u = rng.uniform(0, 400, (n, 3))
+    bu_c, _ = bdist.initial_bounds(pos_u, diam, 4, weighted=False)
+    bu_w, _ = bdist.initial_bounds(pos_u, diam, 4, weighted=True)
+    assert max(abs(a - c) for a, c in zip(bu_c[1:-1], bu_w[1:-1])) <= 1
+
+
 def test_narrow_slab_falls_back_to_legacy_protocol():
     """A one-box-wide inner slab: an emigrant could land in a third rank's ghost layer, so the driver
     uses the legacy protocol, which stays exact."""
