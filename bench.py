@@ -341,10 +341,11 @@ REBUILD_BYTES_PER_AGENT = 160  # key+hist 40, scatter 24, place 96 (column pass 
 
 def run_e2e(bdm, torch, pos_h, diam_h, local, args):
     """Same metric through the public C ABI with HOST buffers: every batch pays its pinned H2D
-    (bdm_set_agents), one step and the D2H of its displacements (bdm_get_displacements).  Two
-    handles on two streams, each driven by its own host thread (ctypes releases the GIL), process
-    alternate batches, so one batch's upload overlaps the other's step and download (H2D and D2H use
-    separate copy engines) -- a serving pipeline; the timed region is the wall time of all batches."""
+    (bdm_set_agents), one step and the D2H of its displacements (bdm_get_displacements).  Three
+    handles on three streams (BDM_E2E_LANES), each driven by its own host thread (ctypes releases the
+    GIL), take batches round-robin, so one batch's upload overlaps the others' steps and downloads
+    (H2D and D2H use separate copy engines) -- a serving pipeline; the timed region is the wall time
+    of all batches."""
     import threading
 
     n = len(diam_h)
@@ -352,7 +353,8 @@ def run_e2e(bdm, torch, pos_h, diam_h, local, args):
     pin_diam = torch.from_numpy(diam_h).pin_memory()
     ppos, pdiam = pin_pos.numpy(), pin_diam.numpy()
     lanes = []
-    for _ in range(2):
+    lanes_n = int(os.environ.get("BDM_E2E_LANES", "3"))
+    for _ in range(lanes_n):
         out = torch.empty((n, 3), dtype=torch.float64).pin_memory()
         st = torch.cuda.Stream(device=local)
         h = bdm.bdm_init(ppos, pdiam, bdm.bdm_params_default(device=local))
@@ -367,15 +369,15 @@ def run_e2e(bdm, torch, pos_h, diam_h, local, args):
     for h, pout, _ in lanes:
         one(h, pout)
     torch.cuda.synchronize()
-    batches = max(2, 2 * args.e2e_steps)
+    batches = max(lanes_n, lanes_n * args.e2e_steps)
 
     def worker(k):
         h, pout, _ = lanes[k]
-        for _ in range(k, batches, 2):
+        for _ in range(k, batches, lanes_n):
             one(h, pout)
 
     w0 = time.perf_counter()
-    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(lanes_n)]
     for t in th:
         t.start()
     for t in th:
@@ -386,7 +388,7 @@ def run_e2e(bdm, torch, pos_h, diam_h, local, args):
         h.close()
     return {"value": n * batches / wall, "unit": UNIT, "h2d_bytes_per_step": int(pos_h.nbytes + diam_h.nbytes),
             "d2h_bytes_per_step": int(n * 3 * 8), "steps": batches, "wall_s": wall,
-            "path": "2 host threads x (bdm_set_agents(host pinned) -> bdm_mech_step(1) -> "
+            "path": f"{lanes_n} host threads x (bdm_set_agents(host pinned) -> bdm_mech_step(1) -> "
                     "bdm_get_displacements(host pinned)) on 2 streams, alternate batches; wall clock"}
 
 
