@@ -1031,7 +1031,7 @@ constexpr int HA_THREADS = 256;
 #define BDM_HA_MIN_BLOCKS 4
 #endif
 #ifndef BDM_HB_MIN_BLOCKS
-#define BDM_HB_MIN_BLOCKS 3
+#define BDM_HB_MIN_BLOCKS 4
 #endif
 constexpr int HA_MIN_BLOCKS = BDM_HA_MIN_BLOCKS;  // pass A: 4 x 8 resident warps per SM
 constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
@@ -1469,14 +1469,12 @@ struct HalfBSmem {
 constexpr size_t HB_SMEM_BYTES = sizeof(HalfBSmem) * FORCE_WARPS;
 
 // Full canonical 27-box sum of agent i (O3-O5 as written): the overflow path of pass B.
-__device__ __noinline__ void full_force(const GridDev& g, const double4* __restrict__ ag, const uint32_t* __restrict__ ids,
-                                        const ParamsDev& p, uint32_t i, double4 me, double& Fx,
-                                        double& Fy, double& Fz) {
+__device__ __noinline__ double3 full_force(const GridDev& g, const double4* __restrict__ ag,
+                                           const uint32_t* __restrict__ ids, const ParamsDev& p, uint32_t i,
+                                           double4 me) {
   const double ri = 0.5 * me.w;
   const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
-  Fx = 0.0;
-  Fy = 0.0;
-  Fz = 0.0;
+  double Fx = 0.0, Fy = 0.0, Fz = 0.0;
   for (int c = 0; c < 9; ++c) {
     uint32_t b = 0, e = 0;
     if (!zrun(g, bx + c / 3 - 1, by + c % 3 - 1, bz - 1, bz + 1, b, e)) continue;
@@ -1490,6 +1488,7 @@ __device__ __noinline__ void full_force(const GridDev& g, const double4* __restr
       }
     }
   }
+  return make_double3(Fx, Fy, Fz);
 }
 
 __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
@@ -1569,7 +1568,12 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     if (__any_sync(FULL, cnt > 0))
       flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct,
                                        ct_hash);
-    if (slow) full_force(g, ag, ids, p, i, me, Fx, Fy, Fz);
+    if (slow) {  // (returned by value: the sums stay in registers)
+      const double3 f = full_force(g, ag, ids, p, i, me);
+      Fx = f.x;
+      Fy = f.y;
+      Fz = f.z;
+    }
     {
       const unsigned sm_ = __ballot_sync(FULL, slow);
       if (sm_ && lane == 0) atomicAdd(&ext_next->slow, (uint32_t)__popc(sm_));
