@@ -1465,6 +1465,7 @@ struct HalfBSmem {
   uint32_t list[HFC + HBC][32];  // all contact candidates of this lane, ascending sorted index
   double term[3][32];
   uint32_t cidx[32];
+  int ext[8];  // this warp's running next-step extents lo[3], hi[3] and range flag (lane 0)
 };
 constexpr size_t HB_SMEM_BYTES = sizeof(HalfBSmem) * FORCE_WARPS;
 
@@ -1500,8 +1501,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
-  int elo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, ehi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
-  bool ebad = false;
+  // next-step extents: reduced per chunk, kept per warp in shared memory (not in registers across
+  // the chunk loop), one guarded atomic set per warp at the end
+  if (lane < 8) sm.ext[lane] = lane < 3 ? INT32_MAX : (lane < 6 ? INT32_MIN : 0);
+  __syncwarp();
   uint32_t n_moved = 0;
   Tickets tk(a_end - a_begin);
   while (true) {
@@ -1594,6 +1597,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       dpz = Fz * p.c;
     }
     int nb3[3] = {INT32_MAX, INT32_MAX, INT32_MAX};  // box of p'
+    bool ebad = false;
     if (valid) {
       if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
@@ -1614,10 +1618,22 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       nb3[0] = box_coord(np.x, g.inv, ebad);
       nb3[1] = box_coord(np.y, g.inv, ebad);
       nb3[2] = box_coord(np.z, g.inv, ebad);
+    }
+    {
+      int lo3[3], hi3[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
-        elo[a] = min(elo[a], nb3[a]);
-        ehi[a] = max(ehi[a], nb3[a]);
+        lo3[a] = __reduce_min_sync(FULL, nb3[a]);
+        hi3[a] = __reduce_max_sync(FULL, valid ? nb3[a] : INT32_MIN);
+      }
+      const bool anybad = __any_sync(FULL, ebad);
+      if (lane == 0) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          sm.ext[a] = min(sm.ext[a], lo3[a]);
+          sm.ext[3 + a] = max(sm.ext[3 + a], hi3[a]);
+        }
+        if (anybad) sm.ext[6] = 1;
       }
     }
     if (hist_out)  // movers of this step (the skip heuristic of the next build), added once per warp
@@ -1643,12 +1659,12 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     }
   }
   if (hist_out && lane == 0 && n_moved) atomicAdd(&ext_next->moved, n_moved);
-  if (__any_sync(FULL, ebad) && lane == 0) ext_next->range_err = 1;
+  __syncwarp();
+  if (lane == 0) {
+    if (sm.ext[6]) ext_next->range_err = 1;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const int lo = __reduce_min_sync(FULL, elo[a]);
-    const int hi = __reduce_max_sync(FULL, ehi[a]);
-    if (lane == 0) {
+    for (int a = 0; a < 3; ++a) {
+      const int lo = sm.ext[a], hi = sm.ext[3 + a];
       if (lo != INT32_MAX && lo < __ldcg(&ext_next->lo[a])) atomicMin(&ext_next->lo[a], lo);
       if (hi != INT32_MIN && hi > __ldcg(&ext_next->hi[a])) atomicMax(&ext_next->hi[a], hi);
     }
