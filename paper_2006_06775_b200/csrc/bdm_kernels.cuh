@@ -281,7 +281,13 @@ __global__ void k_col_len(const int32_t* __restrict__ czlo, const int32_t* __res
 // zero table[0 .. T] with T = coff[nc] read on the device (no host round trip)
 __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __restrict__ coff, uint32_t nc) {
   const uint32_t T = coff[nc];
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= T; k += gridDim.x * blockDim.x) table[k] = 0u;
+  // 16-byte stores (the table is 256-byte aligned), then the last T+1 mod 4 entries
+  const uint32_t n4 = (T + 1) / 4;
+  uint4* t4 = reinterpret_cast<uint4*>(table);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += gridDim.x * blockDim.x)
+    t4[k] = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t k = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (k <= T) table[k] = 0u;
 }
 
 // ------------------------------------------------------------------------------------------ K2
@@ -318,7 +324,10 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
 
 // ------------------------------------------------------------------------------------------ K3
 constexpr int SCAN_THREADS = 256;
-constexpr int SCAN_ITEMS = 16;  // per thread
+#ifndef BDM_SCAN_ITEMS
+#define BDM_SCAN_ITEMS 16
+#endif
+constexpr int SCAN_ITEMS = BDM_SCAN_ITEMS;  // per thread
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v) {
