@@ -1302,7 +1302,11 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     const int bx0 = __shfl_sync(FULL, bx, 0), by0 = __shfl_sync(FULL, by, 0);
     const int zf = __reduce_min_sync(FULL, valid ? bz : INT32_MAX);
     const int zl = __reduce_max_sync(FULL, valid ? bz : INT32_MIN);
-    const bool coop = __all_sync(FULL, !valid || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
+#ifndef BDM_HCOOP
+#define BDM_HCOOP BDM_HSTAGE  // single-column chunks stage their box starts cooperatively (needed by BDM_HSTAGE;
+                              // per-lane lookups are slightly faster otherwise)
+#endif
+    const bool coop = BDM_HCOOP && __all_sync(FULL, !valid || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
     const int span = zl - zf + 4;
     if (coop) {
       int czl = 0, cze = 0;
