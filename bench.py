@@ -389,7 +389,7 @@ def run_e2e(bdm, torch, pos_h, diam_h, local, args):
     return {"value": n * batches / wall, "unit": UNIT, "h2d_bytes_per_step": int(pos_h.nbytes + diam_h.nbytes),
             "d2h_bytes_per_step": int(n * 3 * 8), "steps": batches, "wall_s": wall,
             "path": f"{lanes_n} host threads x (bdm_set_agents(host pinned) -> bdm_mech_step(1) -> "
-                    "bdm_get_displacements(host pinned)) on 2 streams, alternate batches; wall clock"}
+                    "bdm_get_displacements(host pinned)) on as many streams, batches round-robin; wall clock"}
 
 
 def main():
