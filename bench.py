@@ -386,8 +386,28 @@ def run_e2e(bdm, torch, pos_h, diam_h, local, args):
     wall = time.perf_counter() - w0
     for h, _, _ in lanes:
         h.close()
+    # the link's own bound for this traffic: plain pinned copies of the same sizes, both directions
+    # at once (separate copy engines), timed the same way
+    dev_in = torch.empty(pos_h.nbytes + diam_h.nbytes, dtype=torch.uint8, device=local)
+    dev_out = torch.empty(n * 3 * 8, dtype=torch.uint8, device=local)
+    host_in = torch.empty(dev_in.numel(), dtype=torch.uint8).pin_memory()
+    host_out = lanes[0][2].view(torch.uint8).view(-1)
+    s_in, s_out = torch.cuda.Stream(device=local), torch.cuda.Stream(device=local)
+    reps = 4
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    for _ in range(reps):
+        with torch.cuda.stream(s_in):
+            dev_in.copy_(host_in, non_blocking=True)
+        with torch.cuda.stream(s_out):
+            host_out.copy_(dev_out, non_blocking=True)
+    torch.cuda.synchronize()
+    link = (time.perf_counter() - c0) / reps
     return {"value": n * batches / wall, "unit": UNIT, "h2d_bytes_per_step": int(pos_h.nbytes + diam_h.nbytes),
             "d2h_bytes_per_step": int(n * 3 * 8), "steps": batches, "wall_s": wall,
+            "copy_bound": {"value": n / link, "unit": UNIT,
+                           "note": "pinned H2D of the inputs and D2H of the result alone (concurrent, no step): "
+                                   "the PCIe ceiling of this e2e path"},
             "path": f"{lanes_n} host threads x (bdm_set_agents(host pinned) -> bdm_mech_step(1) -> "
                     "bdm_get_displacements(host pinned)) on as many streams, batches round-robin; wall clock"}
 
@@ -401,7 +421,7 @@ def main():
     ap.add_argument("--n", type=int, default=None, help="override N (testing only)")
     ap.add_argument("--impl", default="bdm", choices=["bdm", "reference"])
     ap.add_argument("--cpu-stride", type=int, default=10)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", action="store_true", help="use the x-slab driver even at one rank (testing)")
     args = ap.parse_args()
