@@ -115,8 +115,12 @@ struct bdm_ctx {
   int4* et = nullptr;                   // mother, daughter1, daughter2
   double* edq = nullptr;                // distal displacements of the last step
   double* cpos = nullptr;               // element centres (3E) and extents len + d (E)
+  ElGeo* geo = nullptr;                 // element geometry of the current step (E)
   double* cdiam = nullptr;
   double* fss = nullptr;                // sphere-sphere forces of the force-only pass (3 cap)
+  uint32_t* scnt = nullptr;             // sphere-element contact rows (neurites): counts ...
+  uint32_t* srow = nullptr;             // ... and SCAP element sorted indices per sphere
+  size_t sc_cap = 0;
   int eqc = 0;
   double k_spring = 0.0;
   double sphere_L = 0.0;  // O1 box edge of the spheres alone
@@ -743,7 +747,7 @@ int neurite_step(bdm_ctx* h, bool want_dp) {
   const uint32_t n = (uint32_t)h->n, E = (uint32_t)h->n_el;
   cudaStream_t s = h->stream;
   const int ec = h->eqc;
-  k_el_geom<<<blocks(E, 256), 256, 0, s>>>(h->eq[ec], h->ea, h->et, E, h->cpos, h->cdiam);
+  k_el_geom<<<blocks(E, 256), 256, 0, s>>>(h->eq[ec], h->ea, h->et, E, h->cpos, h->cdiam, h->geo, h->k_spring);
   CU(h, cudaGetLastError());
   DBG(h, "k_el_geom");
   bdm_ctx* el = h->el;
@@ -768,17 +772,30 @@ int neurite_step(bdm_ctx* h, bool want_dp) {
         h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst], nullptr, nullptr, nullptr, h->ext, h->err, rec,
         nullptr, nullptr, h->fss);
     DBG(h, "k_force (force-only)");
-    k_sc_sphere<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], h->fss, n, h->grid, el->grid, el->id[el->cur],
-                                               h->eq[ec], h->ea, h->et, pd, h->ag[dst], want_dp ? h->dp : nullptr,
-                                               h->ext);
-    DBG(h, "k_sc_sphere");
   }
+  if (n > 0 && (size_t)n > h->sc_cap) {  // sphere-element contact rows (k_el_update -> k_sc_rows)
+    if (h->scnt) CU(h, cudaFree(h->scnt));
+    if (h->srow) CU(h, cudaFree(h->srow));
+    h->scnt = nullptr;
+    h->srow = nullptr;
+    h->sc_cap = (size_t)n + (size_t)n / 4;
+    CU(h, cudaMalloc(&h->scnt, h->sc_cap * sizeof(uint32_t)));
+    CU(h, cudaMalloc(&h->srow, h->sc_cap * SCAP * sizeof(uint32_t)));
+  }
+  if (n > 0) CU(h, cudaMemsetAsync(h->scnt, 0, (size_t)n * sizeof(uint32_t), s));
   GridDev gs = h->grid;
   if (n == 0) gs.table = nullptr;
-  k_el_update<<<blocks(E, 256), 256, 0, s>>>(h->eq[ec], h->ea, h->et, E, h->k_spring, h->ag[src], gs, pd,
-                                             h->eq[1 - ec], h->edq);
+  k_el_update<<<blocks(E, 256), 256, 0, s>>>(h->eq[ec], h->geo, h->et, E, el->id[el->cur], h->ag[src], h->agf, gs,
+                                             el->grid.m32, pd, h->eq[1 - ec], h->edq, h->scnt, h->srow);
   CU(h, cudaGetLastError());
   DBG(h, "k_el_update");
+  if (n > 0) {
+    k_sc_rows<<<blocks(n, 256), 256, 0, s>>>(h->ag[src], h->agf, h->fss, n, h->grid, el->grid, el->agf,
+                                             el->id[el->cur], h->geo, h->scnt, h->srow, pd,
+                                             h->ag[dst], want_dp ? h->dp : nullptr, h->ext);
+    CU(h, cudaGetLastError());
+    DBG(h, "k_sc_rows");
+  }
   h->launches += 5;
   h->eqc = 1 - ec;
   h->out_ids = h->id[src];
@@ -901,7 +918,7 @@ void bdm_destroy(bdm_handle h) {
     if (t.e3) cudaEventDestroy(t.e3);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->czlo2, h->czhi2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -1181,7 +1198,8 @@ int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const dou
   auto fr = [](void* p) {
     if (p) cudaFree(p);
   };
-  fr(h->eq[0]); fr(h->eq[1]); fr(h->ea); fr(h->et); fr(h->edq); fr(h->cpos); fr(h->cdiam); fr(h->fss);
+  fr(h->eq[0]); fr(h->eq[1]); fr(h->ea); fr(h->et); fr(h->edq); fr(h->cpos); fr(h->cdiam); fr(h->fss); fr(h->geo);
+  h->geo = nullptr;
   h->eq[0] = h->eq[1] = h->ea = nullptr;
   h->et = nullptr;
   h->edq = h->cpos = h->cdiam = h->fss = nullptr;
@@ -1194,7 +1212,8 @@ int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const dou
   int rc;
   if ((rc = dalloc(h, &h->eq[0], E)) || (rc = dalloc(h, &h->eq[1], E)) || (rc = dalloc(h, &h->ea, E)) ||
       (rc = dalloc(h, &h->et, E)) || (rc = dalloc(h, &h->edq, 3 * E)) || (rc = dalloc(h, &h->cpos, 3 * E)) ||
-      (rc = dalloc(h, &h->cdiam, E)) || (rc = dalloc(h, &h->fss, 3 * (size_t)std::max<int64_t>(h->cap, 1))))
+      (rc = dalloc(h, &h->cdiam, E)) || (rc = dalloc(h, &h->fss, 3 * (size_t)std::max<int64_t>(h->cap, 1))) ||
+      (rc = dalloc(h, &h->geo, E)))
     return rc;
   CU(h, cudaMemcpy(h->eq[0], q.data(), E * sizeof(double4), cudaMemcpyHostToDevice));
   CU(h, cudaMemcpy(h->ea, a.data(), E * sizeof(double4), cudaMemcpyHostToDevice));
@@ -1202,7 +1221,8 @@ int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const dou
   CU(h, cudaMemset(h->edq, 0, 3 * E * sizeof(double)));
   h->eqc = 0;
   h->k_spring = k_spring;
-  k_el_geom<<<blocks(E, 256), 256, 0, h->stream>>>(h->eq[0], h->ea, h->et, (uint32_t)E, h->cpos, h->cdiam);
+  k_el_geom<<<blocks(E, 256), 256, 0, h->stream>>>(h->eq[0], h->ea, h->et, (uint32_t)E, h->cpos, h->cdiam, nullptr,
+                                                    0.0);
   CU(h, cudaGetLastError());
   CU(h, cudaStreamSynchronize(h->stream));
   bdm_params ep = h->prm;

@@ -234,6 +234,31 @@ __device__ __forceinline__ bool zrun(const GridDev& g, int cx, int cy, int z0, i
   return true;
 }
 
+// The 9 z-runs (z in [bz-1, bz+1]) of the columns around (bx, by), in canonical column order; empty
+// runs as b = e.  All table loads of one level are issued together (two dependent levels instead of
+// 9 x 3 for successive zrun calls).
+__device__ __forceinline__ void zrun9(const GridDev& g, int bx, int by, int bz, uint32_t rb[9], uint32_t re[9]) {
+  int zl[9], zh[9];
+  uint32_t o[9];
+  bool ok[9];
+#pragma unroll
+  for (int col = 0; col < 9; ++col) {
+    const int cx = bx + col / 3 - 1, cy = by + col % 3 - 1;
+    ok[col] = cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1];
+    const uint32_t c = ok[col] ? col_of(g, cx, cy) : 0u;
+    zl[col] = ok[col] ? __ldg(&g.czlo[c]) : 1;
+    zh[col] = ok[col] ? __ldg(&g.czhi[c]) : 0;
+    o[col] = ok[col] ? __ldg(&g.coff[c]) : 0u;
+  }
+#pragma unroll
+  for (int col = 0; col < 9; ++col) {
+    const int a = bz - 1 > zl[col] ? bz - 1 : zl[col], d = bz + 1 < zh[col] ? bz + 1 : zh[col];
+    const bool live = ok[col] && a <= d;
+    rb[col] = live ? __ldg(&g.table[o[col] + (uint32_t)(a - zl[col])]) : 0u;
+    re[col] = live ? __ldg(&g.table[o[col] + (uint32_t)(d - zl[col]) + 1u]) : 0u;
+  }
+}
+
 // ---- column pass: occupied z-range of every column, then lengths for the offset scan
 __global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ czhi, uint32_t nc) {
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
@@ -2065,17 +2090,33 @@ __device__ __forceinline__ void el_geom(uint32_t e, const double4* __restrict__ 
   len = sqrt((v[0] * v[0] + v[1] * v[1]) + v[2] * v[2]);
 }
 
-// N1/N2: element centres (for the element grid) and their extent len + d
+// Per-element geometry of a step, computed once (id order) and gathered by the contact kernels:
+// a = (P, r_e), b = (v, len), c = (T, 1/len) with T = k_s ((len - l0)/l0) (N1, N3)
+struct ElGeo {
+  double4 a, b, c;
+};
+
+// N1/N2: element centres (for the element grid) and their extent len + d; the geometry records
 __global__ void k_el_geom(const double4* __restrict__ eq, const double4* __restrict__ ea, const int4* __restrict__ et,
-                          uint32_t E, double* __restrict__ cpos, double* __restrict__ cdiam) {
+                          uint32_t E, double* __restrict__ cpos, double* __restrict__ cdiam, ElGeo* __restrict__ geo,
+                          double k_spring) {
   const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   double P[3], v[3], len;
   el_geom(e, eq, ea, et, P, v, len);
+  const double de = eq[e].w;
   cpos[3 * (size_t)e] = P[0] + 0.5 * v[0];
   cpos[3 * (size_t)e + 1] = P[1] + 0.5 * v[1];
   cpos[3 * (size_t)e + 2] = P[2] + 0.5 * v[2];
-  cdiam[e] = len + eq[e].w;
+  cdiam[e] = len + de;
+  if (geo) {
+    const double l0 = ea[e].w;
+    ElGeo g;
+    g.a = make_double4(P[0], P[1], P[2], 0.5 * de);
+    g.b = make_double4(v[0], v[1], v[2], len);
+    g.c = make_double4(k_spring * ((len - l0) / l0), 1.0 / len, 0.0, 0.0);
+    geo[e] = g;
+  }
 }
 
 // N4: force on the sphere at c (radius rs) from the element (P, v, re); false without contact
@@ -2124,36 +2165,101 @@ __device__ __forceinline__ int disp_rule(double Fx, double Fy, double Fz, const 
 
 // N5 (spheres) + O6/O7: sphere-sphere sum from the force-only pass, then the element terms over the
 // 27 element boxes (canonical order, ascending element id inside a box).
-__global__ void k_sc_sphere(const double4* __restrict__ ag, const double* __restrict__ fss, uint32_t n, GridDev gs,
-                            GridDev ge, const uint32_t* __restrict__ el_ids, const double4* __restrict__ eq,
-                            const double4* __restrict__ ea, const int4* __restrict__ et, ParamsDev p,
-                            double4* __restrict__ ag_out, double* __restrict__ dp_out, Extents* ext_next) {
+// Conservative fp32 sphere-element prefilter.  A contact needs d < r_s + r_e with d the distance
+// to the segment, and d >= |c - C| - len/2 for the midpoint C, so |c - C| < r_s + h with h = len/2 +
+// r_e = 0.5 * (len + d_e), the element grid's half extent (the element agf holds (C, -h) in fp32).
+// Both fp32 centres are within their grid's m32 of the fp64 values, the bound is
+// rounded up and carries a relative 2^-20 for the fp32 sum of squares: only pairs that can be
+// contacts reach the exact fp64 evaluation (sc_term), so the sums are unchanged.
+__device__ __forceinline__ bool sc_near(float4 a, float4 b, float rsm, float h) {
+  const float dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+  const float d2 = (dx * dx + dy * dy) + dz * dz;
+  const float R = __fadd_ru(rsm, h);
+  return d2 <= __fmul_ru(__fmul_ru(R, R), 1.0f + 0x1p-20f);
+}
+
+// Sphere-element contact rows: k_el_update finds every contact (it searches the 27 sphere boxes of
+// each element anyway) and appends the element's sorted index to the sphere's row; the sphere pass
+// evaluates its row's terms in ascending element sorted index, which is N5's canonical order (boxes
+// in (dx,dy,dz) lexicographic order = ascending key, ascending id inside a box), with the same
+// sc_term arguments as a sphere-side search: the sums are bit-identical to one.
+constexpr int SCAP = 16;  // entries per sphere row; more contacts -> the sphere searches itself
+
+// N4 + N5 (one sphere): element terms over the 27 element boxes in canonical order (overflow path)
+__device__ __noinline__ double3 sc_full(const double4 me, const float4 mf, double3 F, const GridDev gs,
+                                        const GridDev ge, const float4* __restrict__ elf,
+                                        const uint32_t* __restrict__ el_ids, const ElGeo* __restrict__ geo,
+                                        const ParamsDev p) {
+  const double c[3] = {me.x, me.y, me.z};
+  const double rs = 0.5 * me.w;
+  const float rsm = __double2float_ru(rs + gs.m32 + ge.m32);
+  const int bx = (int)floor(me.x * ge.inv), by = (int)floor(me.y * ge.inv), bz = (int)floor(me.z * ge.inv);
+  for (int col = 0; col < 9; ++col) {
+    uint32_t b, e;
+    if (!zrun(ge, bx + col / 3 - 1, by + col % 3 - 1, bz - 1, bz + 1, b, e)) continue;
+    for (uint32_t q = b; q < e; ++q) {
+      const float4 ef = __ldg(&elf[q]);
+      if (!sc_near(mf, ef, rsm, -ef.w)) continue;
+      const uint32_t el = el_ids[q];
+      const double4 ga = geo[el].a, gb = geo[el].b;
+      const double P[3] = {ga.x, ga.y, ga.z}, v[3] = {gb.x, gb.y, gb.z};
+      double t3[3];
+      if (sc_term(c, rs, P, v, ga.w, p, t3)) {
+        F.x = F.x + t3[0];
+        F.y = F.y + t3[1];
+        F.z = F.z + t3[2];
+      }
+    }
+  }
+  return F;
+}
+
+// N5 (spheres) + O6/O7: sphere-sphere sums fss plus the element terms of the sphere's contact row
+// (sorted by element index; overflowing rows take sc_full), then the displacement rule and update.
+__global__ void k_sc_rows(const double4* __restrict__ ag, const float4* __restrict__ agf,
+                          const double* __restrict__ fss, uint32_t n, GridDev gs, GridDev ge,
+                          const float4* __restrict__ elf, const uint32_t* __restrict__ el_ids,
+                          const ElGeo* __restrict__ geo, const uint32_t* __restrict__ scnt,
+                          const uint32_t* __restrict__ srow, ParamsDev p,
+                          double4* __restrict__ ag_out, double* __restrict__ dp_out, Extents* ext_next) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const bool valid = i < n;
   int nb3[3] = {0, 0, 0};
   bool bad = false;
   if (valid) {
     const double4 me = ag[i];
-    const double c[3] = {me.x, me.y, me.z};
-    const double rs = 0.5 * me.w;
-    double Fx = fss[3 * (size_t)i], Fy = fss[3 * (size_t)i + 1], Fz = fss[3 * (size_t)i + 2];
-    const int bx = (int)floor(me.x * ge.inv), by = (int)floor(me.y * ge.inv), bz = (int)floor(me.z * ge.inv);
-    for (int col = 0; col < 9; ++col) {
-      uint32_t b, e;
-      if (!zrun(ge, bx + col / 3 - 1, by + col % 3 - 1, bz - 1, bz + 1, b, e)) continue;
-      for (uint32_t q = b; q < e; ++q) {
-        const uint32_t el = el_ids[q];
-        double P[3], v[3], len, t3[3];
-        el_geom(el, eq, ea, et, P, v, len);
-        if (sc_term(c, rs, P, v, 0.5 * eq[el].w, p, t3)) {
-          Fx = Fx + t3[0];
-          Fy = Fy + t3[1];
-          Fz = Fz + t3[2];
+    double3 F = make_double3(fss[3 * (size_t)i], fss[3 * (size_t)i + 1], fss[3 * (size_t)i + 2]);
+    const uint32_t c = scnt[i];
+    if (c > (uint32_t)SCAP) {
+      F = sc_full(me, agf[i], F, gs, ge, elf, el_ids, geo, p);
+    } else if (c > 0) {
+      uint32_t r[SCAP];
+      const uint32_t* row = srow + (size_t)i * SCAP;
+      for (uint32_t k = 0; k < c; ++k) {  // insertion sort (a handful of entries)
+        const uint32_t v = row[k];
+        uint32_t x = k;
+        while (x > 0 && r[x - 1] > v) {
+          r[x] = r[x - 1];
+          --x;
+        }
+        r[x] = v;
+      }
+      const double cc[3] = {me.x, me.y, me.z};
+      const double rs = 0.5 * me.w;
+      for (uint32_t k = 0; k < c; ++k) {
+        const uint32_t el = el_ids[r[k]];
+        const double4 ga = geo[el].a, gb = geo[el].b;
+        const double P[3] = {ga.x, ga.y, ga.z}, v[3] = {gb.x, gb.y, gb.z};
+        double t3[3];
+        if (sc_term(cc, rs, P, v, ga.w, p, t3)) {  // (always: the row holds contacts)
+          F.x = F.x + t3[0];
+          F.y = F.y + t3[1];
+          F.z = F.z + t3[2];
         }
       }
     }
     double dx, dy, dz;
-    disp_rule(Fx, Fy, Fz, p, dx, dy, dz);
+    disp_rule(F.x, F.y, F.z, p, dx, dy, dz);
     const double4 np = make_double4(me.x + dx, me.y + dy, me.z + dz, me.w);
     ag_out[i] = np;
     if (dp_out) {
@@ -2171,16 +2277,34 @@ __global__ void k_sc_sphere(const double4* __restrict__ ag, const double* __rest
 
 // N3 + N5 (distal points) + O6: own spring, daughters' springs (ascending id), sphere reactions over
 // the 27 sphere boxes around box(C_e) (canonical order, ascending sphere id).
-__global__ void k_el_update(const double4* __restrict__ eq, const double4* __restrict__ ea,
-                            const int4* __restrict__ et, uint32_t E, double k_spring, const double4* __restrict__ ag,
-                            GridDev gs, ParamsDev p, double4* __restrict__ eq_out, double* __restrict__ dq_out) {
-  const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  double P[3], v[3], len;
-  el_geom(e, eq, ea, et, P, v, len);
-  const double4 a = ea[e];
-  const double T = k_spring * ((len - a.w) / a.w);
-  const double inv = 1.0 / len;
+// One thread per element in the element grid's sorted order (el_ids: sorted -> id), so the lanes of a
+// warp search neighbouring sphere boxes.  Each contact also goes to the sphere's contact row for
+// k_sc_rows (the element's sorted index); the row slots are taken after the search, a few atomics in
+// flight at once (an atomic whose result feeds a store inside the divergent search loop stalls the
+// whole warp for an L2 round trip per contact).
+constexpr int EL_PEND = 8;
+__device__ __forceinline__ void sc_flush(uint32_t* __restrict__ scnt, uint32_t* __restrict__ srow, const uint32_t* cs,
+                                         int nc, uint32_t qe) {
+  uint32_t slot[EL_PEND];
+#pragma unroll
+  for (int k = 0; k < EL_PEND; ++k)
+    if (k < nc) slot[k] = atomicAdd(&scnt[cs[k]], 1u);
+#pragma unroll
+  for (int k = 0; k < EL_PEND; ++k)
+    if (k < nc && slot[k] < (uint32_t)SCAP) srow[(size_t)cs[k] * SCAP + slot[k]] = qe;
+}
+
+__global__ void k_el_update(const double4* __restrict__ eq, const ElGeo* __restrict__ geo,
+                            const int4* __restrict__ et, uint32_t E, const uint32_t* __restrict__ el_ids,
+                            const double4* __restrict__ ag, const float4* __restrict__ agf, GridDev gs,
+                            double m_el, ParamsDev p, double4* __restrict__ eq_out, double* __restrict__ dq_out,
+                            uint32_t* __restrict__ scnt, uint32_t* __restrict__ srow) {
+  const uint32_t qe = blockIdx.x * blockDim.x + threadIdx.x;
+  if (qe >= E) return;
+  const uint32_t e = el_ids[qe];
+  const ElGeo ge = geo[e];
+  const double P[3] = {ge.a.x, ge.a.y, ge.a.z}, v[3] = {ge.b.x, ge.b.y, ge.b.z};
+  const double len = ge.b.w, T = ge.c.x, inv = ge.c.y;
   double F[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int k = 0; k < 3; ++k) F[k] = F[k] + (-T) * (v[k] * inv);
@@ -2188,21 +2312,28 @@ __global__ void k_el_update(const double4* __restrict__ eq, const double4* __res
   const int ch[2] = {tp.y, tp.z};
   for (int k = 0; k < 2; ++k) {
     if (ch[k] < 0) continue;
-    double Pc[3], vc[3], lc;
-    el_geom((uint32_t)ch[k], eq, ea, et, Pc, vc, lc);
-    const double Tc = k_spring * ((lc - ea[ch[k]].w) / ea[ch[k]].w);
-    const double ic = 1.0 / lc;
+    const double4 cb = geo[ch[k]].b, cc = geo[ch[k]].c;
+    const double vc[3] = {cb.x, cb.y, cb.z};
+    const double Tc = cc.x, ic = cc.y;
 #pragma unroll
     for (int j = 0; j < 3; ++j) F[j] = F[j] + Tc * (vc[j] * ic);
   }
-  const double re = 0.5 * eq[e].w;
+  const double re = ge.a.w;
   const double C[3] = {P[0] + 0.5 * v[0], P[1] + 0.5 * v[1], P[2] + 0.5 * v[2]};
   if (gs.table) {
     const int bx = (int)floor(C[0] * gs.inv), by = (int)floor(C[1] * gs.inv), bz = (int)floor(C[2] * gs.inv);
+    // fp32 prefilter (sc_near): this element's centre and half extent against each sphere's agf
+    const float4 cf = make_float4(__double2float_rn(C[0]), __double2float_rn(C[1]), __double2float_rn(C[2]), 0.f);
+    const float hm = __double2float_ru(0.5 * (len + 2.0 * re) + gs.m32 + m_el);
+    uint32_t cs[EL_PEND];
+    int nc = 0;
+    uint32_t rb[9], rn[9];
+    zrun9(gs, bx, by, bz, rb, rn);
     for (int col = 0; col < 9; ++col) {
-      uint32_t b, en;
-      if (!zrun(gs, bx + col / 3 - 1, by + col % 3 - 1, bz - 1, bz + 1, b, en)) continue;
+      const uint32_t b = rb[col], en = rn[col];
       for (uint32_t q = b; q < en; ++q) {
+        const float4 sf = __ldg(&agf[q]);
+        if (!sc_near(cf, sf, hm, -sf.w)) continue;
         const double4 sp = ag[q];
         const double c[3] = {sp.x, sp.y, sp.z};
         double t3[3];
@@ -2210,9 +2341,15 @@ __global__ void k_el_update(const double4* __restrict__ eq, const double4* __res
           F[0] = F[0] - t3[0];
           F[1] = F[1] - t3[1];
           F[2] = F[2] - t3[2];
+          if (nc == EL_PEND) {
+            sc_flush(scnt, srow, cs, nc, qe);
+            nc = 0;
+          }
+          cs[nc++] = q;
         }
       }
     }
+    sc_flush(scnt, srow, cs, nc, qe);
   }
   double dx, dy, dz;
   disp_rule(F[0], F[1], F[2], p, dx, dy, dz);

@@ -76,3 +76,49 @@ def test_sphere_pushed_by_neurite(bdm):
     assert abs(dp[0, 1] - 0.001 * f) < 1e-15 and dp[0, 0] == 0.0
     _, dq = bdm.bdm_get_neurites(h)
     assert np.array_equal(dq[0], -dp[0])
+
+
+def test_grazing_and_crowded_contacts(bdm):
+    """Pins the sphere-element contact rows and their fp32 prefilter: spheres grazing a segment's side
+    or its distal cap at distance r_s + r_e -+ 1e-9 (contact / none), and hub spheres touched by 8
+    radiating elements (more than a contact row holds -> the sphere's own exact search)."""
+    pos, diam, Q, d, l0, A, mother = [], [], [], [], [], [], []
+    rng = np.random.default_rng(5)
+    for k in range(40):
+        x0 = np.array([60.0 * k, 0.0, 0.0])
+        e = len(Q)
+        Q.append(x0 + [20.0, 0.0, 0.0])
+        d.append(2.0)
+        l0.append(20.0)
+        A.append(x0)
+        mother.append(-1)
+        eps = 1e-9 * (1 if k % 2 else -1)
+        pos += [x0 + [10.0, 6.0 + eps, 0.0], x0 + [26.0 + eps, 0.0, 0.0], x0 + [-6.0 - eps, 0.0, 0.0]]
+        diam += [10.0, 10.0, 10.0]
+        hub = x0 + [0.0, 40.0, 0.0]
+        pos.append(hub)
+        diam.append(10.0)
+        for _ in range(8):
+            u = rng.normal(size=3)
+            u /= np.linalg.norm(u)
+            A.append(hub + 3.0 * u)
+            Q.append(hub + 15.0 * u)
+            d.append(2.0)
+            l0.append(12.0)
+            mother.append(-1)
+        assert e >= 0
+    pos, diam, Q, A = map(np.array, (pos, diam, Q, A))
+    d, l0, mother = np.array(d), np.array(l0), np.array(mother)
+    dau = np.full((len(Q), 2), -1)
+    prm = dict(dt=0.01, adherence=0.0, max_disp=100.0)
+    h = bdm.bdm_init(pos, diam, bdm.bdm_params_default(**prm))
+    bdm.bdm_set_neurites(h, Q, d, l0, A, mother, dau, 10.0)
+    bdm.bdm_mech_step(h, 1)
+    dp = bdm.bdm_get_displacements(h)
+    q, dq = bdm.bdm_get_neurites(h)
+    po, qo, dpo, dqo = oracle.neurite_step(pos, diam, Q, d, l0, A, mother, dau[:, 0], dau[:, 1], 10.0,
+                                           oracle.params(**prm), steps=1)
+    assert np.array_equal(dp, dpo) and np.array_equal(dq, dqo) and np.array_equal(q, qo)
+    touched = np.any(dpo != 0.0, axis=1).reshape(40, 4)
+    assert touched[1::2, :3].sum() == 0 and touched[0::2, :3].all()  # +1e-9: none, -1e-9: contact
+    assert touched[:, 3].all()
