@@ -53,13 +53,8 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1)
 tm = bdm.bdm_get_timing(h)
 n_end = bdm.bdm_get_count(h)[0]
-slow = []  # agents whose pair rows overflowed (exact full-search path), two untimed steps more
-for _ in range(2):
-    bdm.bdm_mech_step(h, 1)
-    slow.append(bdm.bdm_get_path_stats(h)["slow"])
 print(json.dumps({"workload": f"cgd: {a.n} agents at 1e-3/um^3, D~U[8,12), growth {a.growth} um/step, division at {a.div} um",
                   "value": updates / (ms / 1e3), "unit": "agent-updates/s", "steps": a.steps,
                   "ms_per_step": ms / a.steps, "population": [n_start, n_end],
                   "grid_ms_per_step": tm["grid_ms"] / tm["steps"], "force_ms_per_step": tm["force_ms"] / tm["steps"],
-                  "overflow_agents_per_step": slow,
                   "note": "force_ms includes the growth + division kernels (they run after the force kernel)"}))
