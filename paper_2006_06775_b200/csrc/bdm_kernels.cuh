@@ -1060,6 +1060,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
 constexpr int HFC = 16;  // forward row capacity (entries per agent)
 constexpr int HBC = 16;  // backward row capacity
 constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
+#ifndef BDM_HA32
+#define BDM_HA32 1  // pass A takes boxes and radii from the fp32 copy (fp64 position only near box faces)
+#endif
 constexpr int HA_THREADS = 256;
 #ifndef BDM_HA_MIN_BLOCKS
 #define BDM_HA_MIN_BLOCKS 4
@@ -1294,10 +1297,41 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     if (base >= s_end) break;
     const uint32_t i = (uint32_t)base + lane;
     const bool valid = i < s_end;
-    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
     const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#if BDM_HA32
+    // O2's box from the fp32 copy: t = x32 * inv32 is within 3 * 2^-24 |t| of x * inv, so floor(t)
+    // is O2's box unless t lies within |t| 2^-21 + 2^-30 of an integer; such lanes (about 1e-3 of
+    // the agents) load the fp64 position.  r_i from the fp32 copy too, rounded up with a relative
+    // 2^-20 (the filter bound only has to be an upper bound)
+    int bx, by, bz;
+    {
+      const float inv32 = (float)g.inv;
+      const float t[3] = {mf.x * inv32, mf.y * inv32, mf.z * inv32};
+      int b3[3];
+      bool amb = false;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float fl = floorf(t[a]);
+        const float tol = fabsf(t[a]) * 0x1p-21f + 0x1p-30f;
+        amb |= t[a] - fl <= tol || fl + 1.0f - t[a] <= tol;
+        b3[a] = (int)fl;
+      }
+      if (valid && amb) {
+        const double4 me = ag[i];
+        b3[0] = (int)floor(me.x * g.inv);
+        b3[1] = (int)floor(me.y * g.inv);
+        b3[2] = (int)floor(me.z * g.inv);
+      }
+      bx = b3[0];
+      by = b3[1];
+      bz = b3[2];
+    }
+    const double ri = (double)__fmul_ru(-mf.w, 1.0f + 0x1p-20f);
+#else
+    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
     const double ri = 0.5 * me.w;
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+#endif
     // box culling of k_force, for the 5 forward columns q = 0..4 <-> (dx, dy) = (0,0), (0,+1),
     // (+1,-1), (+1,0), (+1,+1): bit q kept, bit 8+q z-1 box culled, bit 16+q z+1 box culled
     uint32_t cull = 0u;

@@ -276,6 +276,28 @@ def test_prefilter_boundary_contacts(bdm):
     assert np.array_equal(g["dp"], o["dp"])
 
 
+def test_agents_on_box_faces(bdm):
+    """Agents placed on, just below and just above box faces on every axis (x * inv within 1e-12 of an
+    integer, also far from the origin): box coordinates, pair sets and displacements equal the
+    oracle's (pins the product kernels' box assignment from the fp32 copy, which defers such
+    agents to their fp64 position)."""
+    rng = np.random.default_rng(9)
+    D = 10.0
+    edge = D * (1.0 + 2.0 ** -30)
+    k = rng.integers(-200, 200, size=(3000, 3)).astype(float)
+    k[::2, 0] += 700.0  # half of them far from the origin along x (larger fp32 rounding)
+    # relative offsets from exactly on a face to beyond the fp32 decision margin (|t| 2^-21 ~ 4.8e-7 |t|)
+    off = rng.choice([-2e-6, -1e-6, -5e-7, -4e-7, -1e-9, -1e-12, 0.0, 1e-12, 1e-9, 4e-7, 5e-7, 1e-6, 2e-6],
+                     size=(3000, 3))
+    pos = k * edge + off * np.maximum(1.0, np.abs(k * edge))
+    # a partner in contact across a face for each
+    u = rng.normal(size=(3000, 3))
+    u /= np.linalg.norm(u, axis=1)[:, None]
+    pos = np.concatenate([pos, pos + 9.0 * u])
+    diam = np.full(len(pos), D)
+    compare_full(bdm, pos, diam, pairs=True)
+
+
 @pytest.mark.slow
 def test_cfg3_full_size_sampled(bdm):
     """configs[2] at full size (2e7 agents) in the launch configuration bench.py times: every
