@@ -5,4 +5,4 @@ timeout 300 python tools/profile_step.py --steps 2 > gpurun_out/prof_plain.log 2
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file gpurun_out/launches.csv python tools/profile_step.py --steps 2 > gpurun_out/ncu_launch.log 2>&1; echo launch rc=$?
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_half -c 2 \
-  -o gpurun_out/half -f python tools/profile_step.py --steps 1 > gpurun_out/ncu_half.log 2>&1; echo half rc=$?
+  -o gpurun_out/half -f python tools/profile_step.py --steps 2 > gpurun_out/ncu_half.log 2>&1; echo half rc=$?
