@@ -29,6 +29,8 @@ thread_local std::string g_tls_error;
 const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after every launch
 // BDM_HALF=0 selects the single-pass k_force for plain steps (A/B measurements of the half-shell path)
 const bool g_no_half = std::getenv("BDM_HALF") != nullptr && std::getenv("BDM_HALF")[0] == '0';
+// BDM_DEFER=k: at most k consecutive deferred builds (no host round trip); 0 = off
+const int g_defer = std::getenv("BDM_DEFER") ? std::atoi(std::getenv("BDM_DEFER")) : 8;
 
 enum class State { NoGrid, Fresh, Stepped };
 
@@ -87,6 +89,8 @@ struct bdm_ctx {
   bool cols_next = false;
   int32_t nlo[2] = {0, 0}, nnx = 0, nny = 0;
   int32_t tlo[3] = {0, 0, 0}, thi[3] = {0, 0, 0};  // tight extents of the last build (reported)
+  bool defer_ok = false;  // this build may be deferred (not the last step of a bdm_mech_step call)
+  int deferred = 0;       // consecutive deferred builds
   int scan_blocks_per_sm = 0;
   // x-slab mode (multi-GPU)
   bool slab = false;
@@ -223,6 +227,8 @@ int check_async(bdm_ctx* h) {
                   h->err_host->first_bad);
     if (h->err_host->code == 6u)
       return fail(h, BDM_ENONFINITE, "non-finite force on agent %u", h->err_host->first_bad);
+    if (h->err_host->code == 7u)
+      return fail(h, BDM_ERANGE, "agent at input position %u left the grid of a deferred build", h->err_host->first_bad);
     return fail(h, BDM_ECUDA, "device error code %u", h->err_host->code);
   }
   return BDM_OK;
@@ -410,8 +416,34 @@ int scan(bdm_ctx* h, uint32_t* data, uint64_t items, const uint32_t* n_dev) {
 // Grid parameters from the (already reduced) extents of ag[cur]; one small D2H per build.
 int compute_extents(bdm_ctx* h) {
   uint32_t n = (uint32_t)h->n;
+  GridDev& g = h->grid;
+  // Deferred build (no host round trip): the last step fused this build's columns over its frame,
+  // which holds every agent by construction (|dp| < L), so the grid is that frame in x/y and the
+  // last grid's z-range +- 1 box, no tighter than needed for correctness.  Its flags (range,
+  // frame) stay on the device and are checked at the next synchronised build: at least every
+  // BDM_DEFER builds and for the last step of every bdm_mech_step call (whose grid info is tight).
+  if (h->defer_ok && h->cols_next && h->deferred < g_defer && h->ext_valid && !h->slab && !h->hist[0] &&
+      !(h->prm.flags & BDM_RECORD)) {
+    g.lo[0] = h->tlo[0] = h->nlo[0];
+    g.lo[1] = h->tlo[1] = h->nlo[1];
+    g.hi[0] = h->thi[0] = h->nlo[0] + h->nnx - 1;
+    g.hi[1] = h->thi[1] = h->nlo[1] + h->nny - 1;
+    g.lo[2] = h->tlo[2] = g.lo[2] - 1;
+    g.hi[2] = h->thi[2] = g.hi[2] + 1;
+    int64_t nb = 1;
+    for (int a = 0; a < 3; ++a) nb *= (int64_t)g.hi[a] - g.lo[a] + 1;
+    if (nb < (int64_t)0xffffffffll && g.hi[2] < (1 << 20) && g.lo[2] > -(1 << 20)) {
+      g.ny = g.hi[1] - g.lo[1] + 1;
+      g.nz = g.hi[2] - g.lo[2] + 1;
+      g.n_boxes = (uint32_t)nb;
+      ++h->deferred;
+      return BDM_OK;
+    }
+    h->cols_next = false;  // (frame grown too large: synchronise and start tight again)
+  }
+  h->deferred = 0;
   if (!h->ext_valid) {
-    k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext);
+    k_ext_reset<<<1, 32, 0, h->stream>>>(h->ext, 0);
     k_extents<<<blocks(n, 256), 256, 0, h->stream>>>(h->ag[h->cur], n, h->grid.inv, h->ext);
     DBG(h, "k_extents");
     CU(h, cudaGetLastError());
@@ -420,13 +452,16 @@ int compute_extents(bdm_ctx* h) {
   CU(h, cudaMemcpyAsync(h->ext_host, h->ext, sizeof(Extents), cudaMemcpyDeviceToHost, h->stream));
   int rc = check_async(h);  // synchronises
   if (rc) return rc;
-  if (h->ext_host->range_err) {
+  if (h->ext_host->range_err || (h->ext_host->sticky & 1u)) {
     h->poisoned = true;
     return fail(h, BDM_ERANGE, "an agent lies >= 2^20 boxes from the origin (|p*inv| >= 2^20, DESIGN.md R9)");
   }
+  if (h->ext_host->sticky & 2u) {  // a deferred build's frame missed an agent: cannot happen (|dp| < L)
+    h->poisoned = true;
+    return fail(h, BDM_ERANGE, "an agent left the frame of a deferred build");
+  }
   h->last_moved = h->ext_host->moved;
   h->last_searched = h->ext_host->searched;
-  GridDev& g = h->grid;
   int64_t dims[3];
   for (int a = 0; a < 3; ++a) {
     g.lo[a] = h->tlo[a] = h->ext_host->lo[a];
@@ -509,7 +544,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   if (rc) return rc;
   k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
   DBG(h, "k_table_zero");
-  if (n > 0) k_key_hist<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table);
+  if (n > 0) k_key_hist<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
   DBG(h, "k_key_hist");
   rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
   if (rc) return rc;
@@ -575,7 +610,7 @@ int force_step(bdm_ctx* h, bool want_dp) {
   const uint32_t n = (uint32_t)h->n;
   cudaStream_t s = h->stream;
   const int src = h->cur, dst = 1 - h->cur;
-  k_ext_reset<<<1, 32, 0, s>>>(h->ext);
+  k_ext_reset<<<1, 32, 0, s>>>(h->ext, h->deferred > 0 ? 2 : 1);
   RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
   ParamsDev pd = params_dev(h->prm);
   double* dp = want_dp ? h->dp : nullptr;
@@ -1077,7 +1112,9 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
       continue;
     }
     if (h->state != State::Fresh) {
+      h->defer_ok = s < n_steps - 1;
       int rc = grid_build(h);
+      h->defer_ok = false;
       if (rc) return rc;
     }
     if (h->timing) CU(h, cudaEventRecord(ts.e1, h->stream));

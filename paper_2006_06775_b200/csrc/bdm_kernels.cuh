@@ -60,6 +60,7 @@ struct Extents {
   uint32_t work_a;    // chunk counter of the half-shell search pass (k_half_search)
   uint32_t slow;      // agents of the half-shell sum pass whose pair rows overflowed (full search)
   uint32_t col_bad;   // fused column pass: some agent's new box left its frame (columns invalid)
+  uint32_t sticky;    // range_err (bit 0) / col_bad (bit 1) of earlier steps (deferred builds)
 };
 
 // Fused column pass (k_half_sum): occupied z-range of every column (bx, by) of the NEXT build's
@@ -197,7 +198,13 @@ __global__ void k_extents(const double4* __restrict__ ag, uint32_t n, double inv
   block_minmax_atomic(ext, b, valid);
 }
 
-__global__ void k_ext_reset(Extents* ext) {
+// mode 0: also clear the sticky flags; 1: the range flag of the last step becomes sticky first; 2: so
+// does its frame flag (the build just made was deferred: its frame had to hold every agent)
+__global__ void k_ext_reset(Extents* ext, int mode = 1) {
+  if (threadIdx.x == 0)
+    ext->sticky = mode == 0 ? 0u
+                            : ext->sticky | (ext->range_err ? 1u : 0u) | (mode == 2 && ext->col_bad ? 2u : 0u);
+  __syncwarp();
   if (threadIdx.x < 3) {
     ext->lo[threadIdx.x] = INT32_MAX;
     ext->hi[threadIdx.x] = INT32_MIN;
@@ -317,8 +324,10 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
 
 // ------------------------------------------------------------------------------------------ K2
 // Two agents per thread (block-strided, both loads coalesced and in flight together).
+// An agent whose box lies outside the grid (only possible after a deferred build saw a non-finite
+// or out-of-range position) is counted in box 0 and reported (code 7): no out-of-bounds access.
 __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g, uint32_t* __restrict__ key,
-                           uint32_t* __restrict__ slot, uint32_t* __restrict__ count) {
+                           uint32_t* __restrict__ slot, uint32_t* __restrict__ count, ErrDev* err) {
   const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const uint32_t ia[2] = {i0, i0 + blockDim.x};
   double4 pa[2];
@@ -332,7 +341,16 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
     if (valid && pa[u].w >= 0.0) {  // dead (slab emigrant, D < 0): dropped by the sort
       const double4 p = pa[u];
       const int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv), bz = (int)floor(p.z * g.inv);
-      k = box_key(g, bx, by, bz);
+      bool ok = bx >= g.lo[0] && bx <= g.hi[0] && by >= g.lo[1] && by <= g.hi[1];
+      const uint32_t c = ok ? col_of(g, bx, by) : 0u;
+      const int zl = __ldg(&g.czlo[c]);
+      ok = ok && bz >= zl && bz <= __ldg(&g.czhi[c]);
+      if (ok) {
+        k = __ldg(&g.coff[c]) + (uint32_t)(bz - zl);
+      } else {
+        k = 0u;
+        report(err, 7u, ia[u], 0u);
+      }
     }
     // warp-aggregated histogram: one atomic per distinct key in the warp
     const unsigned peers = __match_any_sync(FULL, k);
