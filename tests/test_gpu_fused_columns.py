@@ -64,3 +64,26 @@ def test_set_agents_after_fused_steps(bdm):
     bdm.bdm_mech_step(h, 2)
     ref, _ = oracle.run(pos2, diam, 2)
     assert np.array_equal(bdm.bdm_get_positions(h), ref)
+
+
+@pytest.mark.parametrize("max_disp", [3.0, 11.0])
+def test_deferred_builds_bit_exact(bdm, max_disp):
+    """One bdm_mech_step(12) call defers the builds of steps 0..10 (no host round trip: the grid is
+    the fused frame, growing one box per axis per step, re-tightened after 8) -- positions equal the
+    oracle's and those of 12 single-step calls (every build synchronised); grid info stays tight."""
+    rng = np.random.default_rng(8)
+    n = 6000
+    pos = rng.normal(0.0, 40.0, (n, 3))
+    diam = np.clip(rng.lognormal(np.log(10.0), 0.15, n), 6.0, 16.0)
+    h = bdm.bdm_init(pos, diam, bdm.bdm_params_default(max_disp=max_disp))
+    bdm.bdm_mech_step(h, 12)
+    p = bdm.bdm_get_positions(h)
+    _, p1 = trajectory(bdm, pos, diam, 12, max_disp=max_disp)
+    assert np.array_equal(p, p1)
+    ref, _ = oracle.run(pos, diam, 12, oracle.params(max_disp=max_disp))
+    assert np.array_equal(p, ref)
+    # grid info describes the last step's build: the tight extents of its start positions
+    start11, _ = oracle.run(pos, diam, 11, oracle.params(max_disp=max_disp))
+    gp = oracle.grid_params(start11, diam)
+    info = bdm.bdm_get_grid_info(h)
+    assert info["lo"] == gp["lo"] and info["hi"] == gp["hi"]
