@@ -215,6 +215,9 @@ def run_bdm(args):
         bdm.bdm_sync(h)
         bdm.bdm_get_timing(h)  # reset sums
         torch.cuda.synchronize()
+        prof = os.environ.get("BDM_PROFILE_TIMED") == "1"  # ncu --profile-from-start off: the timed steps only
+        if prof:
+            torch.cuda.profiler.start()
         if flush is None:  # state larger than L2: time the K steps as one bdm_mech_step(K) call
             evs[0][0].record(stream)
             bdm.bdm_mech_step(h, args.steps)
@@ -227,6 +230,8 @@ def run_bdm(args):
                 bdm.bdm_mech_step(h, 1)
                 evs[k][1].record(stream)
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
     bdm.bdm_sync(h)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tm = bdm.bdm_get_timing(h)

@@ -31,6 +31,8 @@ from __future__ import annotations
 import json
 import time
 
+import os
+
 import numpy as np
 
 INT32_MIN = -(2 ** 31)
@@ -534,11 +536,16 @@ def bench_multi(args, metric, unit, config_obj, load_peaks, ClockSampler):
         bdm.bdm_get_timing(eng.h)  # reset
         dist.barrier()
         torch.cuda.synchronize()
+        prof = os.environ.get("BDM_PROFILE_TIMED") == "1"  # ncu --profile-from-start off: the timed steps only
+        if prof:
+            torch.cuda.profiler.start()
         e0.record(stream)
         for _ in range(args.steps):
             drv.step()
         e1.record(stream)
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.profiler.stop()
         dist.barrier()
     tm = bdm.bdm_get_timing(eng.h)
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
