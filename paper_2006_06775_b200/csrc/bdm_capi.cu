@@ -544,7 +544,12 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   if (rc) return rc;
   k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
   DBG(h, "k_table_zero");
-  if (n > 0) k_key_hist<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
+  if (n > 0) {
+    if (h->deferred > 0)
+      k_key_hist<true><<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
+    else
+      k_key_hist<false><<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
+  }
   DBG(h, "k_key_hist");
   rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
   if (rc) return rc;

@@ -324,8 +324,10 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
 
 // ------------------------------------------------------------------------------------------ K2
 // Two agents per thread (block-strided, both loads coalesced and in flight together).
-// An agent whose box lies outside the grid (only possible after a deferred build saw a non-finite
-// or out-of-range position) is counted in box 0 and reported (code 7): no out-of-bounds access.
+// GUARD (deferred builds, whose extents were not checked on the host): an agent whose box lies
+// outside the grid (a non-finite or out-of-range position) is counted in box 0 and reported (code 7)
+// instead of indexing outside the table.
+template <bool GUARD>
 __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g, uint32_t* __restrict__ key,
                            uint32_t* __restrict__ slot, uint32_t* __restrict__ count, ErrDev* err) {
   const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
@@ -341,15 +343,16 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
     if (valid && pa[u].w >= 0.0) {  // dead (slab emigrant, D < 0): dropped by the sort
       const double4 p = pa[u];
       const int bx = (int)floor(p.x * g.inv), by = (int)floor(p.y * g.inv), bz = (int)floor(p.z * g.inv);
-      bool ok = bx >= g.lo[0] && bx <= g.hi[0] && by >= g.lo[1] && by <= g.hi[1];
-      const uint32_t c = ok ? col_of(g, bx, by) : 0u;
-      const int zl = __ldg(&g.czlo[c]);
-      ok = ok && bz >= zl && bz <= __ldg(&g.czhi[c]);
-      if (ok) {
-        k = __ldg(&g.coff[c]) + (uint32_t)(bz - zl);
+      if (GUARD) {  // column inside the frame and key inside the table (T = coff[n_cols])
+        const bool okxy = bx >= g.lo[0] && bx <= g.hi[0] && by >= g.lo[1] && by <= g.hi[1];
+        const uint32_t c = okxy ? col_of(g, bx, by) : 0u;
+        k = __ldg(&g.coff[c]) + (uint32_t)(bz - __ldg(&g.czlo[c]));
+        if (!okxy || k >= __ldg(&g.coff[g.n_cols])) {
+          k = 0u;
+          report(err, 7u, ia[u], 0u);
+        }
       } else {
-        k = 0u;
-        report(err, 7u, ia[u], 0u);
+        k = box_key(g, bx, by, bz);
       }
     }
     // warp-aggregated histogram: one atomic per distinct key in the warp
