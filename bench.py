@@ -341,7 +341,9 @@ def device_inputs(bdm, torch, cfg, n, dev, stream, scale_from=None):
 # rebuild kernels, algorithmic bytes per agent: column pass 32 | key + histogram
 # 32 + 8 | scatter 12 + 12 | place 12 + 32 gather + 32 + 4 + 16 (fp32 copy) = 192 B/agent (the
 # ragged box table adds ~12 B per box, not counted)
-REBUILD_BYTES_PER_AGENT = 160  # key+hist 40, scatter 24, place 96 (column pass fused into the sum pass)
+# key+hist 12 (packed new box written by the last sum pass) or 40 (BDM_PBOX=0: the state), scatter 24,
+# place 96 (column pass fused into the sum pass)
+REBUILD_BYTES_PER_AGENT = 132 if os.environ.get("BDM_PBOX", "1") != "0" else 160
 
 
 def run_e2e(bdm, torch, pos_h, diam_h, local, args):

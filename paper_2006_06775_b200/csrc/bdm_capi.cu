@@ -31,6 +31,8 @@ const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after
 const bool g_no_half = std::getenv("BDM_HALF") != nullptr && std::getenv("BDM_HALF")[0] == '0';
 // BDM_DEFER=k: at most k consecutive deferred builds (no host round trip); 0 = off
 const int g_defer = std::getenv("BDM_DEFER") ? std::atoi(std::getenv("BDM_DEFER")) : 8;
+// BDM_PBOX=0: the key pass re-reads the state instead of the sum pass's packed boxes
+const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
 
 enum class State { NoGrid, Fresh, Stepped };
 
@@ -89,6 +91,10 @@ struct bdm_ctx {
   bool cols_next = false;
   int32_t nlo[2] = {0, 0}, nnx = 0, nny = 0;
   int32_t tlo[3] = {0, 0, 0}, thi[3] = {0, 0, 0};  // tight extents of the last build (reported)
+  uint32_t* pbox = nullptr;  // packed new boxes of the last step (sum pass), read by the next key pass
+  size_t pbox_cap = 0;
+  bool pbox_next = false;
+  int32_t pb_z0 = 0, pb_zbits = 0;
   bool defer_ok = false;  // this build may be deferred (not the last step of a bdm_mech_step call)
   int deferred = 0;       // consecutive deferred builds
   int scan_blocks_per_sm = 0;
@@ -344,7 +350,7 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
                const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids,
                bool fuse_cols = false, const int32_t* frame4 = nullptr, unsigned long long* hist_out = nullptr) {
   cudaStream_t s = h->stream;
-  ColNext cn{0, 0, 0, 0, nullptr, nullptr};
+  ColNext cn{0, 0, 0, 0, nullptr, nullptr, nullptr, 0, 0};
   h->cols_next = false;
   if (fuse_cols) {  // next build's frame: this step's tight extents +- 1 box (|dp| < L)
     cn.lo0 = frame4 ? frame4[0] : h->tlo[0] - 1;
@@ -363,6 +369,28 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     h->nlo[1] = cn.lo1;
     h->nnx = cn.nx;
     h->nny = cn.ny;
+    // single handle: the new boxes packed as (frame column << zbits | z - z0), z in this grid's
+    // z-range +- 1 box, when that fits 32 bits
+    h->pbox_next = false;
+    if (!frame4 && !h->slab && g_pbox) {
+      const int32_t z0 = h->grid.lo[2] - 1, zspan = h->grid.hi[2] - h->grid.lo[2] + 3;
+      int zbits = 1;
+      while ((1 << zbits) < zspan) ++zbits;
+      if (zbits < 31 && (uint64_t)nc2 <= (0xffffffffull >> zbits)) {
+        if ((size_t)a_end > h->pbox_cap) {
+          if (h->pbox) CU(h, cudaFree(h->pbox));
+          h->pbox = nullptr;
+          h->pbox_cap = (size_t)a_end + a_end / 4 + 1024;
+          CU(h, cudaMalloc(&h->pbox, h->pbox_cap * sizeof(uint32_t)));
+        }
+        cn.pbox = h->pbox;
+        cn.z0 = z0;
+        cn.zbits = zbits;
+        h->pbox_next = true;
+        h->pb_z0 = z0;
+        h->pb_zbits = zbits;
+      }
+    }
   }
   CU(h, cudaMemsetAsync(h->h_bcnt, 0, (size_t)std::max<uint32_t>(n_all, 1) * sizeof(uint32_t), s));
   const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
@@ -521,6 +549,8 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   const int src = h->cur, dst = 1 - h->cur;
   init_device_info(h);
   const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
+  const bool packed = h->cols_next && h->pbox_next && n_dead == 0;
+  h->pbox_next = false;
   if (h->cols_next) {  // z-ranges already accumulated by the last step's sum pass
     std::swap(h->czlo, h->czlo2);
     std::swap(h->czhi, h->czhi2);
@@ -544,7 +574,14 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   if (rc) return rc;
   k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
   DBG(h, "k_table_zero");
-  if (n > 0) {
+  if (n > 0 && packed) {  // boxes from the last sum pass (4 B/agent instead of the state)
+    if (h->deferred > 0)
+      k_key_hist_packed<true><<<blocks(n, 1024), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key, h->slot,
+                                                              h->table, h->err);
+    else
+      k_key_hist_packed<false><<<blocks(n, 1024), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key,
+                                                               h->slot, h->table, h->err);
+  } else if (n > 0) {
     if (h->deferred > 0)
       k_key_hist<true><<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
     else
@@ -958,7 +995,7 @@ void bdm_destroy(bdm_handle h) {
     if (t.e3) cudaEventDestroy(t.e3);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->pbox, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->czlo2, h->czhi2};
   for (void* p : ptrs)
     if (p) cudaFree(p);

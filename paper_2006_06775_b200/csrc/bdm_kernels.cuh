@@ -69,6 +69,8 @@ struct ColNext {
   int32_t lo0, lo1, nx, ny;
   int32_t* czlo;
   int32_t* czhi;
+  uint32_t* pbox;  // (optional) per stepped agent: its new column in the frame << zbits | (bz - z0)
+  int32_t z0, zbits;
 };
 
 struct ErrDev {
@@ -364,6 +366,46 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
     if (valid) {
       key[ia[u]] = k;
       slot[ia[u]] = base + __popc(peers & ((1u << lane) - 1u));
+    }
+  }
+}
+
+// K2 from the packed boxes the last step's sum pass wrote (column << zbits | z - z0): 4 bytes per
+// agent instead of the 32-byte state.  GUARD as in k_key_hist.
+template <bool GUARD>
+__global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n, GridDev g, int32_t z0, int32_t zbits,
+                                  uint32_t* __restrict__ key, uint32_t* __restrict__ slot,
+                                  uint32_t* __restrict__ count, ErrDev* err) {
+  const uint32_t i0 = blockIdx.x * (4 * blockDim.x) + threadIdx.x;
+  uint32_t pa[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) pa[u] = i0 + u * blockDim.x < n ? __ldg(&pbox[i0 + u * blockDim.x]) : 0u;
+  const int lane = threadIdx.x & 31;
+  const uint32_t T = GUARD ? __ldg(&g.coff[g.n_cols]) : 0u;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t i = i0 + u * blockDim.x;
+    const bool valid = i < n;
+    uint32_t k = 0xffffffffu;
+    if (valid) {
+      uint32_t c = pa[u] >> zbits;
+      const int bz = z0 + (int)(pa[u] & ((1u << zbits) - 1u));
+      const bool okc = !GUARD || c < g.n_cols;
+      c = okc ? c : 0u;
+      k = __ldg(&g.coff[c]) + (uint32_t)(bz - __ldg(&g.czlo[c]));
+      if (GUARD && (!okc || k >= T)) {
+        k = 0u;
+        report(err, 7u, i, 0u);
+      }
+    }
+    const unsigned peers = __match_any_sync(FULL, k);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (k != 0xffffffffu && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
+    base = __shfl_sync(FULL, base, leader);
+    if (valid) {
+      key[i] = k;
+      slot[i] = base + __popc(peers & ((1u << lane) - 1u));
     }
   }
 }
@@ -1740,6 +1782,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
           c = (uint32_t)ux * (uint32_t)cn.ny + (uint32_t)uy;
         else
           out = true;
+        if (cn.pbox) {  // the next build's column and z, so its key pass need not re-read the state
+          const uint32_t uz = (uint32_t)(nb3[2] - cn.z0);
+          out |= uz >> cn.zbits != 0u;
+          cn.pbox[i - a_begin] = (c << cn.zbits) | uz;
+        }
       }
       const unsigned peers = __match_any_sync(FULL, c);
       const int zmin = __reduce_min_sync(peers, valid ? nb3[2] : INT32_MAX);
