@@ -200,6 +200,27 @@ __global__ void k_extents(const double4* __restrict__ ag, uint32_t n, double inv
   block_minmax_atomic(ext, b, valid);
 }
 
+#ifndef BDM_V256
+#define BDM_V256 1  // 256-bit loads/stores of the 32-byte state (one LSU instruction and one request per sector)
+#endif
+// The state is double4 in 32-byte aligned arrays (cudaMalloc'd): one 256-bit access per lane.
+__device__ __forceinline__ double4 ld_state(const double4* p) {
+#if BDM_V256
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+  return v;
+#else
+  return *p;
+#endif
+}
+__device__ __forceinline__ void st_state(double4* p, double4 v) {
+#if BDM_V256
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w) : "memory");
+#else
+  *p = v;
+#endif
+}
+
 // mode 0: also clear the sticky flags; 1: the range flag of the last step becomes sticky first; 2: so
 // does its frame flag (the build just made was deferred: its frame had to hold every agent)
 __global__ void k_ext_reset(Extents* ext, int mode = 1) {
@@ -549,8 +570,8 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
   for (uint32_t t = b; t < e; ++t) rank += tid[t] < id;
   uint32_t dst = b + rank;
   const uint32_t src = tsrc[q];
-  const double4 p = ag_in[src];
-  ag_out[dst] = p;
+  const double4 p = ld_state(&ag_in[src]);
+  st_state(&ag_out[dst], p);
   ids_out[dst] = id;
   if (hist_out) hist_out[dst] = hist_in[src];
   // fp32 copy of the position for the force kernel's conservative candidate filter
@@ -743,7 +764,7 @@ __device__ __forceinline__ void flush_contacts(Smem& sm, int lane, int& cnt, dou
     uint32_t flag = 0xffffffffu;
     if (e < total) {
       const uint32_t j = sm.list[e - oexcl][owner];
-      const double4 o = ag[j];
+      const double4 o = ld_state(&ag[j]);
       double tx, ty, tz, fa;
       if (pair_term(ox, oy, oz, orr, oidx, o, ids, j, p, tx, ty, tz, fa)) {
         sm.term[0][lane] = tx;
@@ -1652,7 +1673,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     // entries past a count are stale and ignored)
     const uint4* brow = reinterpret_cast<const uint4*>(bwd + (size_t)i * HBC);
     const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
-    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const double4 me = valid ? ld_state(&ag[i]) : make_double4(0.0, 0.0, 0.0, 0.0);
     const uint32_t nf = valid ? fcnt[i] : 0u;
     const uint32_t nb = valid ? bcnt[i] : 0u;
     // (rows are read only where the count says so: a speculative read of every row costs more DRAM
@@ -1737,7 +1758,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
-      ag_out[o] = np;
+      st_state(&ag_out[o], np);
       if (hist_out) {
         const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
         hist_out[o] = ((unsigned long long)moved << 63) |
