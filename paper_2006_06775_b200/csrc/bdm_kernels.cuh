@@ -1212,12 +1212,24 @@ constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 // entry per pair through an atomic slot of the partner.
 __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint32_t i, uint32_t* __restrict__ fwd,
                                           uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
+#if BDM_V256
+  uint32_t* frow = fwd + (size_t)i * HFC;  // 64-byte rows: one 256-bit store per used sector
+#pragma unroll
+  for (int v = 0; v < HFC / 8; ++v)
+    if (cnt > 8 * v) {
+      const uint32_t* l = &sm.list[8 * v][lane];
+      asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(frow + 8 * v), "r"(l[0]),
+                   "r"(l[32]), "r"(l[64]), "r"(l[96]), "r"(l[128]), "r"(l[160]), "r"(l[192]), "r"(l[224])
+                   : "memory");
+    }
+#else
   uint4* frow = reinterpret_cast<uint4*>(fwd + (size_t)i * HFC);
 #pragma unroll
   for (int v = 0; v < HFC / 4; ++v)
     if (cnt > 8 * (v / 2))
       frow[v] = make_uint4(sm.list[4 * v][lane], sm.list[4 * v + 1][lane], sm.list[4 * v + 2][lane],
                            sm.list[4 * v + 3][lane]);
+#endif
   for (int x0 = 0; x0 < cnt; x0 += 4) {
     uint32_t j[4], slot[4];
 #pragma unroll
