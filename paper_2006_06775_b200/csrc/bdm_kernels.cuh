@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
     if (base >= a_end) break;
     const uint32_t i = (uint32_t)base + lane;
     const bool valid = i < a_end;
-    const double4 me = valid ? ag[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const double4 me = valid ? ld_state(&ag[i]) : make_double4(0.0, 0.0, 0.0, 0.0);
     const uint32_t myid = valid ? ids[i] : 0u;
     const double ri = 0.5 * me.w;
     const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, myid);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
-      ag_out[o] = np;
+      st_state(&ag_out[o], np);
       if (hist_out) {
         const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
         hist_out[o] = ((unsigned long long)moved << 63) | pack_box(bx, by, bz);
