@@ -725,7 +725,7 @@ int grow_capacity(bdm_ctx* h, int64_t new_cap) {
       (rc = regrow(h, &h->r_cand, nd, N)) || (rc = regrow(h, &h->r_nb, nd, N)) || (rc = regrow(h, &h->r_ct, nd, N)) ||
       (rc = regrow(h, &h->r_branch, nd, N)) || (rc = regrow(h, &h->r_nbh, nd, N)) ||
       (rc = regrow(h, &h->r_cth, nd, N)) || (rc = regrow(h, &h->hist[0], 0, N)) ||
-      (rc = regrow(h, &h->hist[1], 0, N)) || (rc = regrow(h, &h->gflag, 0, N + 1)))
+      (rc = regrow(h, &h->hist[1], 0, N)) || (rc = regrow(h, &h->gflag, n + 1, N + 1)))
     return rc;
   if (oi >= 0) h->out_ids = h->id[oi];
   if (h->stage) {
@@ -769,29 +769,30 @@ int fields_step(bdm_ctx* h) {
 // NEXT-2: growth + division after the mechanics of a step (G1-G3).
 int grow_divide_step(bdm_ctx* h) {
   const uint32_t n = (uint32_t)h->n;
-  if (h->cap < 2 * h->n) {
-    int rc = grow_capacity(h, std::max<int64_t>(2 * h->n, h->cap + h->cap / 2));
-    if (rc) return rc;
-  }
   if (!h->gflag) CU(h, cudaMalloc(&h->gflag, ((size_t)h->cap + 1) * sizeof(uint32_t)));
   cudaStream_t s = h->stream;
   const int cur = h->cur;  // stepped buffer, sorted order of the step, ids in id[cur]
-  k_grow<<<blocks(n, 256), 256, 0, s>>>(h->ag[cur], h->id[cur], n, h->growth, h->div_diam, h->gflag);
+  // G1 + division flags + the new max D (k_grow knows every final diameter), then the ranks; one
+  // round trip reads the births and max D, and the capacity grows only if the births need it
+  CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), s));
+  k_grow<<<blocks(n, 256), 256, 0, s>>>(h->ag[cur], h->id[cur], n, h->growth, h->div_diam, h->gflag, h->maxd_bits);
   DBG(h, "k_grow");
   CU(h, cudaMemsetAsync(h->gflag + n, 0, sizeof(uint32_t), s));
   int rc = scan(h, h->gflag, (uint64_t)n + 1, nullptr);
   if (rc) return rc;
-  CU(h, cudaMemsetAsync(h->maxd_bits, 0, sizeof(unsigned long long), s));
-  k_divide<<<blocks(n, 256), 256, 0, s>>>(h->ag[cur], h->id[cur], n, h->div_diam, h->gseed, h->step_count, h->gflag,
-                                          h->maxd_bits);
-  DBG(h, "k_divide");
-  CU(h, cudaGetLastError());
-  h->launches += 3;
   uint32_t* hostbuf = reinterpret_cast<uint32_t*>(h->ext_host);  // pinned scratch: total, then max D
   CU(h, cudaMemcpyAsync(hostbuf, h->gflag + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   CU(h, cudaMemcpyAsync(hostbuf + 2, h->maxd_bits, sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
   rc = check_async(h);
   if (rc) return rc;
+  if ((uint64_t)h->cap < (uint64_t)n + hostbuf[0]) {  // (keeps the agents and the ranks)
+    rc = grow_capacity(h, std::max<int64_t>((int64_t)n + hostbuf[0], h->cap + h->cap / 2));
+    if (rc) return rc;
+  }
+  k_divide<<<blocks(n, 256), 256, 0, s>>>(h->ag[cur], h->id[cur], n, h->div_diam, h->gseed, h->step_count, h->gflag);
+  DBG(h, "k_divide");
+  CU(h, cudaGetLastError());
+  h->launches += 3;
   const uint32_t born = hostbuf[0];
   double maxd;
   std::memcpy(&maxd, hostbuf + 2, sizeof maxd);

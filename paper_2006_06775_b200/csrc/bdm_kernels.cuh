@@ -2034,12 +2034,22 @@ __global__ void k_maxd(const double4* __restrict__ ag, uint32_t n, unsigned long
 // buffer (sorted order of that step, ids alongside).  Daughters are appended behind the n agents
 // (unsorted; the next build sorts them).
 __global__ void k_grow(double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n, double growth,
-                       double div_diam, uint32_t* __restrict__ flag_by_id) {
+                       double div_diam, uint32_t* __restrict__ flag_by_id, unsigned long long* maxd_bits) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const double D = ag[i].w + growth;  // G1
-  ag[i].w = D;
-  flag_by_id[ids[i]] = D >= div_diam ? 1u : 0u;
+  double Dfin = 0.0;  // the diameter this agent has after G2 (the new max D of O1 is over these)
+  if (i < n) {
+    const double D = ag[i].w + growth;  // G1
+    ag[i].w = D;
+    const bool divides = D >= div_diam;
+    flag_by_id[ids[i]] = divides ? 1u : 0u;
+    Dfin = divides ? D * 0.79370052598409973737585281963615 : D;  // (k_divide's D', bit for bit)
+  }
+  unsigned long long b = __double_as_longlong(Dfin);
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long v = __shfl_xor_sync(FULL, b, o);
+    b = v > b ? v : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b && b > __ldcg(maxd_bits)) atomicMax(maxd_bits, b);
 }
 
 __device__ __forceinline__ double div_u01(uint64_t seed, uint64_t step, uint64_t id, uint64_t a) {
@@ -2047,15 +2057,12 @@ __device__ __forceinline__ double div_u01(uint64_t seed, uint64_t step, uint64_t
 }
 
 // G2.  rank_by_id = exclusive scan of the division flags in id order, so the k-th divider in
-// ascending id order creates daughter id n + k at position n + k.  Also reduces the new max D (O1).
+// ascending id order creates daughter id n + k at position n + k.
 __global__ void k_divide(double4* __restrict__ ag, uint32_t* __restrict__ ids, uint32_t n, double div_diam,
-                         uint64_t seed, uint64_t step, const uint32_t* __restrict__ rank_by_id,
-                         unsigned long long* maxd_bits) {
+                         uint64_t seed, uint64_t step, const uint32_t* __restrict__ rank_by_id) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  double Dfin = 0.0;
   if (i < n) {
     double4 p = ag[i];
-    Dfin = p.w;
     if (p.w >= div_diam) {
       const uint32_t id = ids[i];
       const uint32_t d = n + rank_by_id[id];
@@ -2077,15 +2084,8 @@ __global__ void k_divide(double4* __restrict__ ag, uint32_t* __restrict__ ids, u
       ag[i] = make_double4(p.x - ox, p.y - oy, p.z - oz, Dd);
       ag[d] = make_double4(p.x + ox, p.y + oy, p.z + oz, Dd);
       ids[d] = d;
-      Dfin = Dd;
     }
   }
-  unsigned long long b = __double_as_longlong(Dfin);
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long v = __shfl_xor_sync(FULL, b, o);
-    b = v > b ? v : b;
-  }
-  if ((threadIdx.x & 31) == 0 && b && b > __ldcg(maxd_bits)) atomicMax(maxd_bits, b);
 }
 
 // ------------------------------------------------------------------------------------------ NEXT-3

@@ -57,4 +57,5 @@ print(json.dumps({"workload": f"cgd: {a.n} agents at 1e-3/um^3, D~U[8,12), growt
                   "value": updates / (ms / 1e3), "unit": "agent-updates/s", "steps": a.steps,
                   "ms_per_step": ms / a.steps, "population": [n_start, n_end],
                   "grid_ms_per_step": tm["grid_ms"] / tm["steps"], "force_ms_per_step": tm["force_ms"] / tm["steps"],
+                  "search_ms_per_step": tm.get("search_ms", 0.0) / tm["steps"],
                   "note": "force_ms includes the growth + division kernels (they run after the force kernel)"}))
