@@ -295,7 +295,8 @@ void init_device_info(bdm_ctx* h) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan, SCAN_THREADS, 0);
   h->scan_blocks_per_sm = per_sm > 0 ? per_sm : 1;
   cudaFuncSetAttribute(k_half_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HA_SMEM_BYTES);
-  cudaFuncSetAttribute(k_half_sum, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
+  cudaFuncSetAttribute(k_half_sum<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
+  cudaFuncSetAttribute(k_half_sum<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
 #ifndef BDM_NO_CARVEOUT
   {  // shared memory only as large as the resident blocks need: the rest stays L1 for the gathers
     int smem_sm = 0;
@@ -305,7 +306,8 @@ void init_device_info(bdm_ctx* h) {
       return smem_sm > 0 ? std::min(100, (int)std::ceil(100.0 * need / smem_sm) + 1) : -1;
     };
     cudaFuncSetAttribute(k_half_search, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HA_SMEM_BYTES, HA_MIN_BLOCKS));
-    cudaFuncSetAttribute(k_half_sum, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
+    cudaFuncSetAttribute(k_half_sum<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
+    cudaFuncSetAttribute(k_half_sum<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
     (void)cudaGetLastError();
   }
 #endif
@@ -313,7 +315,7 @@ void init_device_info(bdm_ctx* h) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_search, HA_THREADS, HA_SMEM_BYTES);
   h->half_a_blocks_per_sm = per_sm > 0 ? per_sm : 1;
   per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_sum, FORCE_THREADS, HB_SMEM_BYTES);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_sum<false>, FORCE_THREADS, HB_SMEM_BYTES);
   h->half_b_blocks_per_sm = per_sm > 0 ? per_sm : 1;
 }
 
@@ -348,7 +350,8 @@ bool ensure_half(bdm_ctx* h) {
 // frame4 (x lo, y lo, nx, ny) of the fused column pass; nullptr: this step's tight extents +- 1 box.
 int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t a_end, uint32_t n_all,
                const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids,
-               bool fuse_cols = false, const int32_t* frame4 = nullptr, unsigned long long* hist_out = nullptr) {
+               bool fuse_cols = false, const int32_t* frame4 = nullptr, unsigned long long* hist_out = nullptr,
+               double* force_only = nullptr) {
   cudaStream_t s = h->stream;
   ColNext cn{0, 0, 0, 0, nullptr, nullptr, nullptr, 0, 0};
   h->cols_next = false;
@@ -404,9 +407,14 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     CU(h, cudaEventCreate(&h->timed.back().e3));
     CU(h, cudaEventRecord(h->timed.back().e3, s));
   }
-  k_half_sum<<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd, ag_out,
-                                                       id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt,
-                                                       h->h_bwd, h->h_bcnt, cn, hist_out);
+  if (force_only)  // (sphere-sphere sums only: the neurite step adds the element terms, O6 and O7)
+    k_half_sum<true><<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd,
+                                                               nullptr, nullptr, force_only, nullptr, h->ext, h->err,
+                                                               h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, nullptr);
+  else
+    k_half_sum<false><<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd,
+                                                                ag_out, id_out, dp, dp_ids, h->ext, h->err, h->h_fwd,
+                                                                h->h_fcnt, h->h_bwd, h->h_bcnt, cn, hist_out);
   DBG(h, "k_half_sum");
   CU(h, cudaGetLastError());
   h->launches += 2;
@@ -845,11 +853,16 @@ int neurite_step(bdm_ctx* h, bool want_dp) {
   k_ext_reset<<<1, 32, 0, s>>>(h->ext);
   RecordDev rec{};
   ParamsDev pd = params_dev(h->prm);
-  if (n > 0) {
-    k_force<false><<<force_grid(h, n), FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(
-        h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst], nullptr, nullptr, nullptr, h->ext, h->err, rec,
-        nullptr, nullptr, h->fss);
-    DBG(h, "k_force (force-only)");
+  if (n > 0) {  // sphere-sphere sums (half-shell passes when the pair rows fit, else k_force)
+    if (!(h->prm.flags & BDM_RECORD) && ensure_half(h)) {
+      rc = half_force(h, src, 0u, 0u, n, n, pd, nullptr, nullptr, nullptr, nullptr, false, nullptr, nullptr, h->fss);
+      if (rc) return rc;
+    } else {
+      k_force<false><<<force_grid(h, n), FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(
+          h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst], nullptr, nullptr, nullptr, h->ext, h->err,
+          rec, nullptr, nullptr, h->fss);
+      DBG(h, "k_force (force-only)");
+    }
   }
   if (n > 0 && (size_t)n > h->sc_cap) {  // sphere-element contact rows (k_el_update -> k_sc_rows)
     if (h->scnt) CU(h, cudaFree(h->scnt));

@@ -1660,6 +1660,9 @@ __device__ __noinline__ double3 full_force(const GridDev& g, const double4* __re
   return make_double3(Fx, Fy, Fz);
 }
 
+// FONLY (neurite steps): the sphere-sphere sums F go to dp_out (3 per agent, the force-only output
+// fss of k_force), the displacement rule and everything after it are left to k_sc_rows.
+template <bool FONLY>
 __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     k_half_sum(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t a_begin, uint32_t a_end,
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
@@ -1748,6 +1751,16 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     {
       const unsigned sm_ = __ballot_sync(FULL, slow);
       if (sm_ && lane == 0) atomicAdd(&ext_next->slow, (uint32_t)__popc(sm_));
+    }
+    if (FONLY) {
+      if (valid) {
+        if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+        const size_t o = 3 * (size_t)(i - a_begin);
+        dp_out[o] = Fx;
+        dp_out[o + 1] = Fy;
+        dp_out[o + 2] = Fz;
+      }
+      continue;
     }
 
     // O6 displacement, O7 update (as k_force)
