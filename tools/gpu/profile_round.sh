@@ -10,3 +10,7 @@ timeout 900 ncu --set full --clock-control none --import-source on --profile-fro
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
   -k "regex:k_key_hist|k_scatter|k_place|k_scan|k_table_zero" -c 6 \
   -o gpurun_out/rebuild -f python tools/profile_step.py --steps 2 > gpurun_out/ncu_rebuild.log 2>&1; echo rebuild rc=$?
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/nb_launches.csv \
+  python tools/neurite_bench.py --steps 2 --warmup 1 > gpurun_out/ncu_nb.log 2>&1; echo neurite launches rc=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k "regex:k_el_update|k_sc_rows" -s 2 -c 2 \
+  -o gpurun_out/elu -f python tools/neurite_bench.py --steps 2 --warmup 1 > gpurun_out/ncu_elu.log 2>&1; echo neurite kernels rc=$?
