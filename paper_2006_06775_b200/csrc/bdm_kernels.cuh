@@ -2200,16 +2200,23 @@ __global__ void k_chemotaxis(double4* __restrict__ ag, const uint32_t* __restric
     b[a] = i0;
     w[a] = t;
   }
+  // the 8 corner weights are the same for the three axes (computed once, the same expressions)
+  double wk[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
+    const double wxy = (dx ? w[0] : 1.0 - w[0]) * (dy ? w[1] : 1.0 - w[1]);
+    wk[k] = wxy * (dz ? w[2] : 1.0 - w[2]);
+  }
   double g[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
     double acc = 0.0;
+#pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int dx = (k >> 2) & 1, dy = (k >> 1) & 1, dz = k & 1;
       const int x = min(b[0] + dx, f.nx - 1), y = min(b[1] + dy, f.ny - 1), z = min(b[2] + dz, f.nz - 1);
-      double wk = (dx ? w[0] : 1.0 - w[0]) * (dy ? w[1] : 1.0 - w[1]);
-      wk = wk * (dz ? w[2] : 1.0 - w[2]);
-      acc = acc + wk * node_grad(c, f, x, y, z, a);
+      acc = acc + wk[k] * node_grad(c, f, x, y, z, a);
     }
     g[a] = acc;
   }
