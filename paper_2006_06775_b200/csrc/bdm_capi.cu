@@ -84,6 +84,7 @@ struct bdm_ctx {
   int32_t *czlo = nullptr, *czhi = nullptr;
   uint32_t* coff = nullptr;
   size_t col_cap = 0, coff_cap = 0;
+  int4* colrec = nullptr;  // packed column records (czlo, czhi, coff) of the current grid (coff_cap)
   // next build's column z-ranges, accumulated by the half-shell sum pass (fused column pass):
   // frame [nlo[0], nlo[0]+nnx) x [nlo[1], nlo[1]+nny) = tight extents of the step start +- 1 box
   int32_t *czlo2 = nullptr, *czhi2 = nullptr;
@@ -276,8 +277,11 @@ int ensure_columns(bdm_ctx* h, size_t entries, bool second = false) {
   }
   if (!second && entries > h->coff_cap) {
     if (h->coff) CU(h, cudaFree(h->coff));
+    if (h->colrec) CU(h, cudaFree(h->colrec));
     h->coff = nullptr;
+    h->colrec = nullptr;
     CU(h, cudaMalloc(&h->coff, cap * sizeof(uint32_t)));
+    CU(h, cudaMalloc(&h->colrec, cap * sizeof(int4)));
     h->coff_cap = cap;
   }
   return BDM_OK;
@@ -546,6 +550,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   g.czhi = h->czhi;
   g.coff = h->coff;
   g.table = h->table;
+  g.col = h->colrec;
   {  // fp32 prefilter margin from the largest coordinate magnitude of this grid
     double P = 0.0;
     for (int a = 0; a < 3; ++a)
@@ -580,7 +585,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   DBG(h, "k_col_len");
   rc = scan(h, h->coff, nc + 1, nullptr);  // exclusive: coff[c] = table offset, coff[nc] = T
   if (rc) return rc;
-  k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols);
+  k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec);
   DBG(h, "k_table_zero");
   if (n > 0 && packed) {  // boxes from the last sum pass (4 B/agent instead of the state)
     if (h->deferred > 0)
@@ -1009,7 +1014,7 @@ void bdm_destroy(bdm_handle h) {
     if (t.e3) cudaEventDestroy(t.e3);
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
-                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->pbox, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
+                  h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->pbox, h->colrec, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->czlo2, h->czhi2};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -44,6 +44,7 @@ struct GridDev {
   const int32_t* czhi;
   const uint32_t* coff;  // n_cols + 1
   const uint32_t* table;
+  const int4* col;       // per column (czlo, czhi, coff, 0): one 16-byte load per column lookup
 };
 
 struct ParamsDev {
@@ -248,17 +249,19 @@ __device__ __forceinline__ uint32_t col_of(const GridDev& g, int bx, int by) {
 // key of an occupied box (the agent's own box)
 __device__ __forceinline__ uint32_t box_key(const GridDev& g, int bx, int by, int bz) {
   const uint32_t c = col_of(g, bx, by);
-  return __ldg(&g.coff[c]) + (uint32_t)(bz - __ldg(&g.czlo[c]));
+  const int4 ci = __ldg(&g.col[c]);
+  return (uint32_t)ci.z + (uint32_t)(bz - ci.x);
 }
 
 // Sorted-agent range [b, e) of the boxes (cx, cy, z0..z1) (O3's z-run of one column); false if empty.
 __device__ __forceinline__ bool zrun(const GridDev& g, int cx, int cy, int z0, int z1, uint32_t& b, uint32_t& e) {
   if (cx < g.lo[0] || cx > g.hi[0] || cy < g.lo[1] || cy > g.hi[1]) return false;
   const uint32_t c = col_of(g, cx, cy);
-  const int zl = __ldg(&g.czlo[c]), zh = __ldg(&g.czhi[c]);
+  const int4 ci = __ldg(&g.col[c]);
+  const int zl = ci.x, zh = ci.y;
   const int a = z0 > zl ? z0 : zl, d = z1 < zh ? z1 : zh;
   if (a > d) return false;
-  const uint32_t o = __ldg(&g.coff[c]);
+  const uint32_t o = (uint32_t)ci.z;
   b = __ldg(&g.table[o + (uint32_t)(a - zl)]);
   e = __ldg(&g.table[o + (uint32_t)(d - zl) + 1u]);
   return true;
@@ -276,9 +279,10 @@ __device__ __forceinline__ void zrun9(const GridDev& g, int bx, int by, int bz, 
     const int cx = bx + col / 3 - 1, cy = by + col % 3 - 1;
     ok[col] = cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1];
     const uint32_t c = ok[col] ? col_of(g, cx, cy) : 0u;
-    zl[col] = ok[col] ? __ldg(&g.czlo[c]) : 1;
-    zh[col] = ok[col] ? __ldg(&g.czhi[c]) : 0;
-    o[col] = ok[col] ? __ldg(&g.coff[c]) : 0u;
+    const int4 ci = ok[col] ? __ldg(&g.col[c]) : make_int4(1, 0, 0, 0);
+    zl[col] = ci.x;
+    zh[col] = ci.y;
+    o[col] = (uint32_t)ci.z;
   }
 #pragma unroll
   for (int col = 0; col < 9; ++col) {
@@ -333,8 +337,13 @@ __global__ void k_col_len(const int32_t* __restrict__ czlo, const int32_t* __res
     len[c] = c < nc && czhi[c] >= czlo[c] ? (uint32_t)(czhi[c] - czlo[c] + 1) : 0u;
 }
 
-// zero table[0 .. T] with T = coff[nc] read on the device (no host round trip)
-__global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __restrict__ coff, uint32_t nc) {
+// zero table[0 .. T] with T = coff[nc] read on the device (no host round trip); also packs the
+// column records (czlo, czhi, coff) for the lookups
+__global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __restrict__ coff, uint32_t nc,
+                             const int32_t* __restrict__ czlo, const int32_t* __restrict__ czhi,
+                             int4* __restrict__ col) {
+  for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
+    col[c] = make_int4(czlo[c], czhi[c], (int)coff[c], 0);
   const uint32_t T = coff[nc];
   // 16-byte stores (the table is 256-byte aligned), then the last T+1 mod 4 entries
   const uint32_t n4 = (T + 1) / 4;
@@ -369,7 +378,8 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
       if (GUARD) {  // column inside the frame and key inside the table (T = coff[n_cols])
         const bool okxy = bx >= g.lo[0] && bx <= g.hi[0] && by >= g.lo[1] && by <= g.hi[1];
         const uint32_t c = okxy ? col_of(g, bx, by) : 0u;
-        k = __ldg(&g.coff[c]) + (uint32_t)(bz - __ldg(&g.czlo[c]));
+        const int4 ci = __ldg(&g.col[c]);
+        k = (uint32_t)ci.z + (uint32_t)(bz - ci.x);
         if (!okxy || k >= __ldg(&g.coff[g.n_cols])) {
           k = 0u;
           report(err, 7u, ia[u], 0u);
@@ -413,7 +423,8 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
       const int bz = z0 + (int)(pa[u] & ((1u << zbits) - 1u));
       const bool okc = !GUARD || c < g.n_cols;
       c = okc ? c : 0u;
-      k = __ldg(&g.coff[c]) + (uint32_t)(bz - __ldg(&g.czlo[c]));
+      const int4 ci = __ldg(&g.col[c]);
+      k = (uint32_t)ci.z + (uint32_t)(bz - ci.x);
       if (GUARD && (!okc || k >= T)) {
         k = 0u;
         report(err, 7u, i, 0u);
