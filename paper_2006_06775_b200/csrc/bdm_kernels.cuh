@@ -368,6 +368,7 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
 #pragma unroll
   for (int u = 0; u < 2; ++u) pa[u] = ia[u] < n ? ag[ia[u]] : make_double4(0.0, 0.0, 0.0, 0.0);
   const int lane = threadIdx.x & 31;
+  uint32_t kk[2], peers[2], base[2];
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
     const bool valid = ia[u] < n;
@@ -388,15 +389,22 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
         k = box_key(g, bx, by, bz);
       }
     }
-    // warp-aggregated histogram: one atomic per distinct key in the warp
-    const unsigned peers = __match_any_sync(FULL, k);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (k != 0xffffffffu && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
-    base = __shfl_sync(FULL, base, leader);
-    if (valid) {
-      key[ia[u]] = k;
-      slot[ia[u]] = base + __popc(peers & ((1u << lane) - 1u));
+    kk[u] = k;
+  }
+  // warp-aggregated histogram (one atomic per distinct key in the warp), both atomics in flight
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    peers[u] = __match_any_sync(FULL, kk[u]);
+    base[u] = 0u;
+    if (kk[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1)
+      base[u] = atomicAdd(&count[kk[u]], (uint32_t)__popc(peers[u]));
+  }
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t b = __shfl_sync(FULL, base[u], __ffs(peers[u]) - 1);
+    if (ia[u] < n) {
+      key[ia[u]] = kk[u];
+      slot[ia[u]] = b + __popc(peers[u] & ((1u << lane) - 1u));
     }
   }
 }
@@ -413,31 +421,38 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
   for (int u = 0; u < 4; ++u) pa[u] = i0 + u * blockDim.x < n ? __ldg(&pbox[i0 + u * blockDim.x]) : 0u;
   const int lane = threadIdx.x & 31;
   const uint32_t T = GUARD ? __ldg(&g.coff[g.n_cols]) : 0u;
+  uint32_t k[4], peers[4], base[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
-    const bool valid = i < n;
-    uint32_t k = 0xffffffffu;
-    if (valid) {
+    k[u] = 0xffffffffu;
+    if (i < n) {
       uint32_t c = pa[u] >> zbits;
       const int bz = z0 + (int)(pa[u] & ((1u << zbits) - 1u));
       const bool okc = !GUARD || c < g.n_cols;
       c = okc ? c : 0u;
       const int4 ci = __ldg(&g.col[c]);
-      k = (uint32_t)ci.z + (uint32_t)(bz - ci.x);
-      if (GUARD && (!okc || k >= T)) {
-        k = 0u;
+      k[u] = (uint32_t)ci.z + (uint32_t)(bz - ci.x);
+      if (GUARD && (!okc || k[u] >= T)) {
+        k[u] = 0u;
         report(err, 7u, i, 0u);
       }
     }
-    const unsigned peers = __match_any_sync(FULL, k);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (k != 0xffffffffu && lane == leader) base = atomicAdd(&count[k], (uint32_t)__popc(peers));
-    base = __shfl_sync(FULL, base, leader);
-    if (valid) {
-      key[i] = k;
-      slot[i] = base + __popc(peers & ((1u << lane) - 1u));
+  }
+  // the four warp-aggregated atomics in flight together, then their bases broadcast
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    peers[u] = __match_any_sync(FULL, k[u]);
+    base[u] = 0u;
+    if (k[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1) base[u] = atomicAdd(&count[k[u]], (uint32_t)__popc(peers[u]));
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t i = i0 + u * blockDim.x;
+    const uint32_t b = __shfl_sync(FULL, base[u], __ffs(peers[u]) - 1);
+    if (i < n) {
+      key[i] = k[u];
+      slot[i] = b + __popc(peers[u] & ((1u << lane) - 1u));
     }
   }
 }
