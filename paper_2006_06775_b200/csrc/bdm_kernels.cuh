@@ -602,13 +602,13 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
                         const unsigned long long* __restrict__ hist_in, unsigned long long* __restrict__ hist_out) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= n) return;
-  uint32_t k = tkey[q], id = tid[q];
-  uint32_t b = start[k], e = start[k + 1];
+  const uint32_t k = tkey[q], id = tid[q], src = tsrc[q];
+  const double4 p = ld_state(&ag_in[src]);  // (the gather is in flight during the rank loop)
+  const uint32_t b = start[k], e = start[k + 1];
   uint32_t rank = 0;
+#pragma unroll 4
   for (uint32_t t = b; t < e; ++t) rank += tid[t] < id;
-  uint32_t dst = b + rank;
-  const uint32_t src = tsrc[q];
-  const double4 p = ld_state(&ag_in[src]);
+  const uint32_t dst = b + rank;
   st_state(&ag_out[dst], p);
   ids_out[dst] = id;
   if (hist_out) hist_out[dst] = hist_in[src];
