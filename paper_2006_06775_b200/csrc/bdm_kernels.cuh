@@ -1182,6 +1182,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
 constexpr int HFC = 16;  // forward row capacity (entries per agent)
 constexpr int HBC = 16;  // backward row capacity
 constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
+#ifndef BDM_HAPF
+#define BDM_HAPF 1  // pass A loads the next chunk's fp32 agents one chunk ahead
+#endif
 #ifndef BDM_HA32
 #define BDM_HA32 1  // pass A takes boxes and radii from the fp32 copy (fp64 position only near box faces)
 #endif
@@ -1425,13 +1428,33 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   __syncwarp();
 #endif
   Tickets tk(s_end - s_begin);
+#if BDM_HAPF
+  // the next chunk's fp32 agents are loaded one chunk ahead (four registers)
+  uint32_t chunk = tk.take(&ext->work_a, lane);
+  float4 mf_next = make_float4(0.f, 0.f, 0.f, 0.f);
+  {
+    const uint64_t i1 = (uint64_t)s_begin + 32ull * chunk + lane;
+    if (i1 < s_end) mf_next = __ldg(&agf[i1]);
+  }
+#endif
   while (true) {
+#if !BDM_HAPF
     const uint32_t chunk = tk.take(&ext->work_a, lane);
+#endif
     const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
     if (base >= s_end) break;
     const uint32_t i = (uint32_t)base + lane;
     const bool valid = i < s_end;
+#if BDM_HAPF
+    const float4 mf = mf_next;
+    chunk = tk.take(&ext->work_a, lane);
+    {
+      const uint64_t i1 = (uint64_t)s_begin + 32ull * chunk + lane;
+      mf_next = i1 < s_end ? __ldg(&agf[i1]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#else
     const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#endif
 #if BDM_HA32
     // O2's box from the fp32 copy: t = x32 * inv32 is within 3 * 2^-24 |t| of x * inv, so floor(t)
     // is O2's box unless t lies within |t| 2^-21 + 2^-30 of an integer; such lanes (about 1e-3 of
