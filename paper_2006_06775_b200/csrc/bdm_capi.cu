@@ -589,10 +589,10 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   DBG(h, "k_table_zero");
   if (n > 0 && packed) {  // boxes from the last sum pass (4 B/agent instead of the state)
     if (h->deferred > 0)
-      k_key_hist_packed<true><<<blocks(n, 1024), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key, h->slot,
+      k_key_hist_packed<true><<<blocks(n, 256 * KHP), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key, h->slot,
                                                               h->table, h->err);
     else
-      k_key_hist_packed<false><<<blocks(n, 1024), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key,
+      k_key_hist_packed<false><<<blocks(n, 256 * KHP), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key,
                                                                h->slot, h->table, h->err);
   } else if (n > 0) {
     if (h->deferred > 0)

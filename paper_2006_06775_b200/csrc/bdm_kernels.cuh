@@ -409,21 +409,25 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
   }
 }
 
+#ifndef BDM_KHP
+#define BDM_KHP 4  // agents per thread in k_key_hist_packed (all loads and atomics of a level in flight)
+#endif
+constexpr int KHP = BDM_KHP;
 // K2 from the packed boxes the last step's sum pass wrote (column << zbits | z - z0): 4 bytes per
 // agent instead of the 32-byte state.  GUARD as in k_key_hist.
 template <bool GUARD>
 __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n, GridDev g, int32_t z0, int32_t zbits,
                                   uint32_t* __restrict__ key, uint32_t* __restrict__ slot,
                                   uint32_t* __restrict__ count, ErrDev* err) {
-  const uint32_t i0 = blockIdx.x * (4 * blockDim.x) + threadIdx.x;
-  uint32_t pa[4];
+  const uint32_t i0 = blockIdx.x * (KHP * blockDim.x) + threadIdx.x;
+  uint32_t pa[KHP];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) pa[u] = i0 + u * blockDim.x < n ? __ldg(&pbox[i0 + u * blockDim.x]) : 0u;
+  for (int u = 0; u < KHP; ++u) pa[u] = i0 + u * blockDim.x < n ? __ldg(&pbox[i0 + u * blockDim.x]) : 0u;
   const int lane = threadIdx.x & 31;
   const uint32_t T = GUARD ? __ldg(&g.coff[g.n_cols]) : 0u;
-  uint32_t k[4], peers[4], base[4];
+  uint32_t k[KHP], peers[KHP], base[KHP];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < KHP; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
     k[u] = 0xffffffffu;
     if (i < n) {
@@ -441,13 +445,13 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
   }
   // the four warp-aggregated atomics in flight together, then their bases broadcast
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < KHP; ++u) {
     peers[u] = __match_any_sync(FULL, k[u]);
     base[u] = 0u;
     if (k[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1) base[u] = atomicAdd(&count[k[u]], (uint32_t)__popc(peers[u]));
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < KHP; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
     const uint32_t b = __shfl_sync(FULL, base[u], __ffs(peers[u]) - 1);
     if (i < n) {
