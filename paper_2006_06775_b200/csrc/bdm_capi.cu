@@ -146,6 +146,7 @@ struct bdm_ctx {
   bool timing = false;
   // half-shell force path (k_half_search + k_half_sum): pair rows, sized to cap
   uint32_t *h_fwd = nullptr, *h_bwd = nullptr, *h_bcnt = nullptr;
+  uint32_t* h_slow = nullptr;  // sum pass: agents whose pair rows overflowed (k_half_slow)
   uint8_t* h_fcnt = nullptr;
   int64_t h_cap = 0;
   bool half_off = false;  // BDM_HALF=0, or the rows could not be allocated: k_force only
@@ -328,18 +329,19 @@ void init_device_info(bdm_ctx* h) {
 bool ensure_half(bdm_ctx* h) {
   if (h->half_off || g_no_half) return false;
   if (h->h_cap >= h->cap && h->h_fwd) return true;
-  for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt})
+  for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt, (void*)h->h_slow})
     if (q) cudaFree(q);
-  h->h_fwd = h->h_bwd = h->h_bcnt = nullptr;
+  h->h_fwd = h->h_bwd = h->h_bcnt = h->h_slow = nullptr;
   h->h_fcnt = nullptr;
   const size_t N = (size_t)std::max<int64_t>(h->cap, 1);
   if (cudaMalloc(&h->h_fwd, N * HFC * sizeof(uint32_t)) != cudaSuccess ||
       cudaMalloc(&h->h_bwd, N * HBC * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMalloc(&h->h_bcnt, N * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->h_fcnt, N) != cudaSuccess) {
+      cudaMalloc(&h->h_bcnt, N * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->h_fcnt, N) != cudaSuccess ||
+      cudaMalloc(&h->h_slow, N * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
-    for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt})
+    for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt, (void*)h->h_slow})
       if (q) cudaFree(q);
-    h->h_fwd = h->h_bwd = h->h_bcnt = nullptr;
+    h->h_fwd = h->h_bwd = h->h_bcnt = h->h_slow = nullptr;
     h->h_fcnt = nullptr;
     h->half_off = true;
     return false;
@@ -411,14 +413,23 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     CU(h, cudaEventCreate(&h->timed.back().e3));
     CU(h, cudaEventRecord(h->timed.back().e3, s));
   }
-  if (force_only)  // (sphere-sphere sums only: the neurite step adds the element terms, O6 and O7)
+  const unsigned gs = (unsigned)h->sm_count * 4;  // the overflow list is short: a small persistent grid
+  if (force_only) {  // (sphere-sphere sums only: the neurite step adds the element terms, O6 and O7)
     k_half_sum<true><<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd,
                                                                nullptr, nullptr, force_only, nullptr, h->ext, h->err,
-                                                               h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, nullptr);
-  else
+                                                               h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, nullptr,
+                                                               h->h_slow);
+    k_half_slow<true><<<gs, 128, 0, s>>>(h->ag[src], h->id[src], a_begin, h->grid, pd, nullptr, nullptr, force_only,
+                                         nullptr, h->ext, h->err, cn, nullptr, h->h_slow);
+  } else {
     k_half_sum<false><<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd,
                                                                 ag_out, id_out, dp, dp_ids, h->ext, h->err, h->h_fwd,
-                                                                h->h_fcnt, h->h_bwd, h->h_bcnt, cn, hist_out);
+                                                                h->h_fcnt, h->h_bwd, h->h_bcnt, cn, hist_out,
+                                                                h->h_slow);
+    k_half_slow<false><<<gs, 128, 0, s>>>(h->ag[src], h->id[src], a_begin, h->grid, pd, ag_out, id_out, dp, dp_ids,
+                                          h->ext, h->err, cn, hist_out, h->h_slow);
+  }
+  DBG(h, "k_half_slow");
   DBG(h, "k_half_sum");
   CU(h, cudaGetLastError());
   h->launches += 2;
@@ -1015,7 +1026,7 @@ void bdm_destroy(bdm_handle h) {
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->pbox, h->colrec, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
-                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->czlo2, h->czhi2};
+                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->h_slow, h->czlo2, h->czhi2};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->ext_host) cudaFreeHost(h->ext_host);

@@ -1733,7 +1733,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
                const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
-               const uint32_t* __restrict__ bcnt, ColNext cn, unsigned long long* __restrict__ hist_out) {
+               const uint32_t* __restrict__ bcnt, ColNext cn, unsigned long long* __restrict__ hist_out,
+               uint32_t* __restrict__ slow_list) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1807,18 +1808,19 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     if (__any_sync(FULL, cnt > 0))
       flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct,
                                        ct_hash);
-    if (slow) {  // (returned by value: the sums stay in registers)
-      const double3 f = full_force(g, ag, ids, p, i, me);
-      Fx = f.x;
-      Fy = f.y;
-      Fz = f.z;
-    }
-    {
+    {  // overflowing agents go to the slow list: k_half_slow sums and steps them (keeping the full
+       // search out of this kernel keeps its registers and stack small)
       const unsigned sm_ = __ballot_sync(FULL, slow);
-      if (sm_ && lane == 0) atomicAdd(&ext_next->slow, (uint32_t)__popc(sm_));
+      if (sm_) {
+        uint32_t b0 = 0;
+        if (lane == 0) b0 = atomicAdd(&ext_next->slow, (uint32_t)__popc(sm_));
+        b0 = __shfl_sync(FULL, b0, 0);
+        if (slow) slow_list[b0 + __popc(sm_ & ((1u << lane) - 1u))] = i;
+      }
     }
+    const bool live = valid && !slow;
     if (FONLY) {
-      if (valid) {
+      if (live) {
         if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
         const size_t o = 3 * (size_t)(i - a_begin);
         dp_out[o] = Fx;
@@ -1844,7 +1846,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     }
     int nb3[3] = {INT32_MAX, INT32_MAX, INT32_MAX};  // box of p'
     bool ebad = false;
-    if (valid) {
+    if (live) {
       if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
@@ -1870,7 +1872,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         lo3[a] = __reduce_min_sync(FULL, nb3[a]);
-        hi3[a] = __reduce_max_sync(FULL, valid ? nb3[a] : INT32_MIN);
+        hi3[a] = __reduce_max_sync(FULL, live ? nb3[a] : INT32_MIN);
       }
       const bool anybad = __any_sync(FULL, ebad);
       if (lane == 0) {
@@ -1883,11 +1885,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       }
     }
     if (hist_out)  // movers of this step (the skip heuristic of the next build), added once per warp
-      n_moved += __popc(__ballot_sync(FULL, valid && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0)));
+      n_moved += __popc(__ballot_sync(FULL, live && (dpx != 0.0 || dpy != 0.0 || dpz != 0.0)));
     if (cn.czlo) {  // fused column pass (warp-aggregated: a chunk touches one or two columns)
       uint32_t c = 0xffffffffu;
       bool out = false;
-      if (valid) {
+      if (live) {
         const int ux = nb3[0] - cn.lo0, uy = nb3[1] - cn.lo1;
         if (ux >= 0 && ux < cn.nx && uy >= 0 && uy < cn.ny)
           c = (uint32_t)ux * (uint32_t)cn.ny + (uint32_t)uy;
@@ -1900,8 +1902,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
         }
       }
       const unsigned peers = __match_any_sync(FULL, c);
-      const int zmin = __reduce_min_sync(peers, valid ? nb3[2] : INT32_MAX);
-      const int zmax = __reduce_max_sync(peers, valid ? nb3[2] : INT32_MIN);
+      const int zmin = __reduce_min_sync(peers, live ? nb3[2] : INT32_MAX);
+      const int zmax = __reduce_max_sync(peers, live ? nb3[2] : INT32_MIN);
       if (c != 0xffffffffu && lane == __ffs(peers) - 1) {  // fire-and-forget reductions (RED)
         atomicMin(&cn.czlo[c], zmin);
         atomicMax(&cn.czhi[c], zmax);
@@ -1922,6 +1924,86 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   }
 }
 
+
+// The agents of the sum pass whose pair rows overflowed (slow_list[0 .. ext->slow)): the full
+// canonical 27-box sum (full_force, O3-O5 as written), then exactly the sum pass's per-agent
+// epilogue with global atomics in place of the warp reductions.  Grid-stride over the list.
+template <bool FONLY>
+__global__ void __launch_bounds__(128) k_half_slow(const double4* __restrict__ ag, const uint32_t* __restrict__ ids,
+                                                   uint32_t a_begin, GridDev g, ParamsDev p,
+                                                   double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
+                                                   double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
+                                                   Extents* ext_next, ErrDev* err, ColNext cn,
+                                                   unsigned long long* __restrict__ hist_out,
+                                                   const uint32_t* __restrict__ slow_list) {
+  const uint32_t n_slow = __ldcg(&ext_next->slow);
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_slow; k += gridDim.x * blockDim.x) {
+    const uint32_t i = slow_list[k];
+    const double4 me = ag[i];
+    const double3 f = full_force(g, ag, ids, p, i, me);
+    const double Fx = f.x, Fy = f.y, Fz = f.z;
+    const uint32_t o = i - a_begin;
+    if (FONLY) {
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+      dp_out[3 * (size_t)o] = Fx;
+      dp_out[3 * (size_t)o + 1] = Fy;
+      dp_out[3 * (size_t)o + 2] = Fz;
+      continue;
+    }
+    double dpx = 0.0, dpy = 0.0, dpz = 0.0;
+    const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
+    if (fn <= p.adherence) {
+    } else if (fn * p.c > p.max_disp) {
+      const double scale = p.max_disp / fn;
+      dpx = Fx * scale;
+      dpy = Fy * scale;
+      dpz = Fz * scale;
+    } else {
+      dpx = Fx * p.c;
+      dpy = Fy * p.c;
+      dpz = Fz * p.c;
+    }
+    if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+    const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
+    ag_out[o] = np;
+    const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
+    if (hist_out) {
+      hist_out[o] = ((unsigned long long)moved << 63) |
+                    pack_box((int)floor(me.x * g.inv), (int)floor(me.y * g.inv), (int)floor(me.z * g.inv));
+      if (moved) atomicAdd(&ext_next->moved, 1u);
+    }
+    if (id_out) id_out[o] = ids[i];
+    if (dp_out) {
+      dp_out[3 * (size_t)o] = dpx;
+      dp_out[3 * (size_t)o + 1] = dpy;
+      dp_out[3 * (size_t)o + 2] = dpz;
+      if (dp_id_out) dp_id_out[o] = ids[i];
+    }
+    bool ebad = false;
+    const int nb3[3] = {box_coord(np.x, g.inv, ebad), box_coord(np.y, g.inv, ebad), box_coord(np.z, g.inv, ebad)};
+    if (ebad) ext_next->range_err = 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&ext_next->lo[a], nb3[a]);
+      atomicMax(&ext_next->hi[a], nb3[a]);
+    }
+    if (cn.czlo) {
+      const int ux = nb3[0] - cn.lo0, uy = nb3[1] - cn.lo1;
+      if (ux >= 0 && ux < cn.nx && uy >= 0 && uy < cn.ny) {
+        const uint32_t c = (uint32_t)ux * (uint32_t)cn.ny + (uint32_t)uy;
+        atomicMin(&cn.czlo[c], nb3[2]);
+        atomicMax(&cn.czhi[c], nb3[2]);
+        if (cn.pbox) {
+          const uint32_t uz = (uint32_t)(nb3[2] - cn.z0);
+          if (uz >> cn.zbits != 0u) ext_next->col_bad = 1u;
+          cn.pbox[o] = (c << cn.zbits) | uz;
+        }
+      } else {
+        ext_next->col_bad = 1u;
+      }
+    }
+  }
+}
 
 // ------------------------------------------------------------------------------------------ K5/K9
 // x-slab exchange records: 5 fp64 per agent (x, y, z, D, id) -- ids < 2^32 are exact in fp64.
