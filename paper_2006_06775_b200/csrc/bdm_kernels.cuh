@@ -1214,6 +1214,10 @@ constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 constexpr int HPCAP = BDM_HPCAP;  // staged candidates (float4) per warp
 
 #define HA_RR (!BDM_HMAP || BDM_HSTAGE)  // the shared-memory run list (cursor with refills)
+#ifndef BDM_HCOOP
+#define BDM_HCOOP BDM_HSTAGE  // single-column chunks stage their box starts cooperatively (needed by BDM_HSTAGE;
+                              // per-lane lookups are slightly faster otherwise)
+#endif
 struct HalfASmem {
 #if BDM_HSTAGE
   float4 buf[HPCAP];        // fp32 candidates of the 5 forward columns' union z-runs (staged chunks)
@@ -1226,7 +1230,8 @@ struct HalfASmem {
 #if HA_RR
   uint2 rr[7][32];         // this lane's non-empty forward z-runs [b, e), then the sentinel (0, 0)
 #endif
-  uint32_t tab[5][TSPAN];  // box starts of the 5 forward columns (single-column chunks)
+  uint32_t tab[5][BDM_HCOOP ? TSPAN : 1];  // box starts of the 5 forward columns (cooperative lookups only:
+                                           // otherwise the shared memory goes to L1)
 };
 
 // ---- TMA bulk copies (cp.async.bulk, async proxy) completing on a per-warp mbarrier
@@ -1522,10 +1527,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     const int bx0 = __shfl_sync(FULL, bx, 0), by0 = __shfl_sync(FULL, by, 0);
     const int zf = __reduce_min_sync(FULL, valid ? bz : INT32_MAX);
     const int zl = __reduce_max_sync(FULL, valid ? bz : INT32_MIN);
-#ifndef BDM_HCOOP
-#define BDM_HCOOP BDM_HSTAGE  // single-column chunks stage their box starts cooperatively (needed by BDM_HSTAGE;
-                              // per-lane lookups are slightly faster otherwise)
-#endif
+
     const bool coop = BDM_HCOOP && __all_sync(FULL, !valid || (bx == bx0 && by == by0)) && zl - zf + 4 <= TSPAN;
     const int span = zl - zf + 4;
     if (coop) {
