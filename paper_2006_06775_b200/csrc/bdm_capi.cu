@@ -615,7 +615,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
   if (rc) return rc;
   if (n > 0) {
-    k_scatter<<<blocks(n, 1024), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
+    k_scatter<<<blocks(n, 256 * KSC), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
     DBG(h, "k_scatter");
     const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
     k_place<<<blocks(n - n_dead, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n - n_dead, h->ag[dst],

@@ -573,23 +573,27 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(uint32_t* __restrict__ da
 }
 
 // ------------------------------------------------------------------------------------------ K4
-// (four agents per thread, all loads of a level in flight together: the pass is latency-bound)
+// (KSC agents per thread, all loads of a level in flight together: the pass is latency-bound)
+#ifndef BDM_KSC
+#define BDM_KSC 4  // agents per thread in k_scatter
+#endif
+constexpr int KSC = BDM_KSC;
 __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
                           const uint32_t* __restrict__ ids, const uint32_t* __restrict__ start, uint32_t n,
                           uint32_t* __restrict__ tsrc, uint32_t* __restrict__ tid, uint32_t* __restrict__ tkey) {
-  const uint32_t i0 = blockIdx.x * (4 * blockDim.x) + threadIdx.x;
-  uint32_t k[4], sl[4], id[4], st[4];
+  const uint32_t i0 = blockIdx.x * (KSC * blockDim.x) + threadIdx.x;
+  uint32_t k[KSC], sl[KSC], id[KSC], st[KSC];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < KSC; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
     k[u] = i < n ? __ldg(&key[i]) : 0xffffffffu;
     sl[u] = i < n ? __ldg(&slot[i]) : 0u;
     id[u] = i < n ? __ldg(&ids[i]) : 0u;
   }
 #pragma unroll
-  for (int u = 0; u < 4; ++u) st[u] = k[u] != 0xffffffffu ? __ldg(&start[k[u]]) : 0u;  // (dead: dropped)
+  for (int u = 0; u < KSC; ++u) st[u] = k[u] != 0xffffffffu ? __ldg(&start[k[u]]) : 0u;  // (dead: dropped)
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
+  for (int u = 0; u < KSC; ++u) {
     if (k[u] == 0xffffffffu) continue;
     const uint32_t d = st[u] + sl[u];
     tsrc[d] = i0 + u * blockDim.x;
