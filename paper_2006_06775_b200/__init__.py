@@ -97,6 +97,7 @@ _SIGS = {
     "bdm_set_stream": ([_vp, _vp], ctypes.c_int),
     "bdm_sync": ([_vp], ctypes.c_int),
     "bdm_set_timing": ([_vp, ctypes.c_int], ctypes.c_int),
+    "bdm_set_defer": ([_vp, ctypes.c_int], ctypes.c_int),
     "bdm_get_timing": ([_vp, _vp], ctypes.c_int),
     "bdm_get_timing_ex": ([_vp, _vp], ctypes.c_int),
     "bdm_generate_uniform": ([ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, ctypes.c_double,
@@ -398,6 +399,11 @@ def bdm_get_path_stats(h: Handle) -> dict:
     out = np.zeros(2, np.int64)
     _check(load_library().bdm_get_path_stats(h.raw, _ptr(out)), h.raw)
     return dict(half=int(out[0]), slow=int(out[1]))
+
+
+def bdm_set_defer(h: Handle, max_deferred: int) -> None:
+    """At most max_deferred consecutive deferred builds inside one bdm_mech_step call (0 = off)."""
+    _check(load_library().bdm_set_defer(h.raw, int(max_deferred)), h.raw)
 
 
 def bdm_set_timing(h: Handle, enabled: bool = True) -> None:

@@ -30,7 +30,9 @@ const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after
 // BDM_HALF=0 selects the single-pass k_force for plain steps (A/B measurements of the half-shell path)
 const bool g_no_half = std::getenv("BDM_HALF") != nullptr && std::getenv("BDM_HALF")[0] == '0';
 // BDM_DEFER=k: at most k consecutive deferred builds (no host round trip); 0 = off
-const int g_defer = std::getenv("BDM_DEFER") ? std::atoi(std::getenv("BDM_DEFER")) : 8;
+// (default 0: with the current kernels the wider frames of deferred builds cost more than the round
+// trip they save; bdm_set_defer sets it per handle)
+const int g_defer = std::getenv("BDM_DEFER") ? std::atoi(std::getenv("BDM_DEFER")) : 0;
 // BDM_PBOX=0: the key pass re-reads the state instead of the sum pass's packed boxes
 const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
 
@@ -97,6 +99,7 @@ struct bdm_ctx {
   bool pbox_next = false;
   int32_t pb_z0 = 0, pb_zbits = 0;
   bool defer_ok = false;  // this build may be deferred (not the last step of a bdm_mech_step call)
+  int defer_max = g_defer;  // at most this many consecutive deferred builds (bdm_set_defer)
   int deferred = 0;       // consecutive deferred builds
   int scan_blocks_per_sm = 0;
   // x-slab mode (multi-GPU)
@@ -473,7 +476,7 @@ int compute_extents(bdm_ctx* h) {
   // last grid's z-range +- 1 box, no tighter than needed for correctness.  Its flags (range,
   // frame) stay on the device and are checked at the next synchronised build: at least every
   // BDM_DEFER builds and for the last step of every bdm_mech_step call (whose grid info is tight).
-  if (h->defer_ok && h->cols_next && h->deferred < g_defer && h->ext_valid && !h->slab && !h->hist[0] &&
+  if (h->defer_ok && h->cols_next && h->deferred < h->defer_max && h->ext_valid && !h->slab && !h->hist[0] &&
       !(h->prm.flags & BDM_RECORD)) {
     g.lo[0] = h->tlo[0] = h->nlo[0];
     g.lo[1] = h->tlo[1] = h->nlo[1];
@@ -1381,6 +1384,12 @@ int bdm_get_count(bdm_handle h, int64_t* out2) {
   if (!h || !out2) return fail(h, BDM_EINVAL, "bdm_get_count: NULL argument");
   out2[0] = h->n;
   out2[1] = h->n_dp;
+  return BDM_OK;
+}
+
+int bdm_set_defer(bdm_handle h, int max_deferred) {
+  if (!h || max_deferred < 0) return fail(h, BDM_EINVAL, "bdm_set_defer: NULL handle or negative count");
+  h->defer_max = max_deferred;
   return BDM_OK;
 }
 

@@ -1190,6 +1190,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
 constexpr int HFC = 16;  // forward row capacity (entries per agent)
 constexpr int HBC = 16;  // backward row capacity
 constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
+#ifndef BDM_HBCNT
+#define BDM_HBCNT 1  // pass B loads the next chunk's pair counts one chunk ahead
+#endif
 #ifndef BDM_HAPF
 #define BDM_HAPF 1  // pass A loads the next chunk's fp32 agents one chunk ahead
 #endif
@@ -1750,8 +1753,23 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   __syncwarp();
   uint32_t n_moved = 0;
   Tickets tk(a_end - a_begin);
+#if BDM_HBCNT
+  // the next chunk's pair counts are loaded one chunk ahead (two registers): a chunk's dependent
+  // chain then starts at its rows
+  uint32_t chunk = tk.take(&ext_next->work, lane);
+  uint32_t nf_n = 0u, nb_n = 0u;
+  {
+    const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
+    if (i1 < a_end) {
+      nf_n = fcnt[i1];
+      nb_n = bcnt[i1];
+    }
+  }
+#endif
   while (true) {
+#if !BDM_HBCNT
     const uint32_t chunk = tk.take(&ext_next->work, lane);
+#endif
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
     if (base >= a_end) break;
     const uint32_t i = (uint32_t)base + lane;
@@ -1761,8 +1779,18 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const uint4* brow = reinterpret_cast<const uint4*>(bwd + (size_t)i * HBC);
     const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
     const double4 me = valid ? ld_state(&ag[i]) : make_double4(0.0, 0.0, 0.0, 0.0);
+#if BDM_HBCNT
+    const uint32_t nf = nf_n, nb = nb_n;
+    chunk = tk.take(&ext_next->work, lane);
+    {
+      const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
+      nf_n = i1 < a_end ? fcnt[i1] : 0u;
+      nb_n = i1 < a_end ? bcnt[i1] : 0u;
+    }
+#else
     const uint32_t nf = valid ? fcnt[i] : 0u;
     const uint32_t nb = valid ? bcnt[i] : 0u;
+#endif
     // (rows are read only where the count says so: a speculative read of every row costs more DRAM
     // traffic than the round trip it saves)
     const uint4 b4 = nb ? __ldg(brow) : make_uint4(0u, 0u, 0u, 0u);

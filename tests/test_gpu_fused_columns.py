@@ -76,6 +76,7 @@ def test_deferred_builds_bit_exact(bdm, max_disp):
     pos = rng.normal(0.0, 40.0, (n, 3))
     diam = np.clip(rng.lognormal(np.log(10.0), 0.15, n), 6.0, 16.0)
     h = bdm.bdm_init(pos, diam, bdm.bdm_params_default(max_disp=max_disp))
+    bdm.bdm_set_defer(h, 8)
     bdm.bdm_mech_step(h, 12)
     p = bdm.bdm_get_positions(h)
     _, p1 = trajectory(bdm, pos, diam, 12, max_disp=max_disp)
