@@ -118,16 +118,62 @@ def make_inputs(cfg: int, n: int | None):
 
 
 # ------------------------------------------------------------------------------------ oracle arm
-def oracle_sample_run(pos, diam, stride: int):
+def oracle_sample_run(pos, diam, stride: int, nthreads: int = 0):
     """The CPU oracle as it stands on a bounded sample: the whole population is the environment
     (the oracle rebuilds its grid over all N agents) and every stride-th agent id is updated."""
     import oracle
 
     sample = np.arange(0, len(diam), stride, dtype=np.int64)
     t0 = time.perf_counter()
-    oracle.step(pos, diam, sample=sample, record=False)
+    oracle.step(pos, diam, sample=sample, record=False, nthreads=nthreads)
     dt = time.perf_counter() - t0
-    return len(sample), dt, oracle.threads()
+    return len(sample), dt, (nthreads or oracle.threads())
+
+
+def host_info():
+    """nproc, CPU model and RAM of the host the oracle runs on."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    ram = None
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    ram = round(int(ln.split()[1]) / 2 ** 20, 1)
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "ram_gib": ram}
+
+
+def cpu_baseline(pos, diam, what, stride_1t):
+    """The CPU oracle as it stands: ONE full step of the whole population (every
+    agent updated, grid rebuilt) with OpenMP on all host cores, and a single-threaded run on a
+    bounded sample (every stride-th agent updated; the grid over all agents is still built, so that
+    figure includes the whole index build)."""
+    import oracle
+
+    t0 = time.perf_counter()
+    oracle.step(pos, diam, record=False)
+    t_all = time.perf_counter() - t0
+    threads = oracle.threads()
+    m, t_1, _ = oracle_sample_run(pos, diam, stride_1t, nthreads=1)
+    n = len(diam)
+    return {"value": n / t_all, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"one full oracle step of {what} (all {n} agents updated, grid rebuilt), OpenMP on "
+                      f"{threads} threads, {t_all:.1f} s wall",
+            "single_thread": {"value": m / t_1, "unit": UNIT, "cores": 1,
+                              "sample": f"every {stride_1t}th agent id updated ({m} agents) with {what} as "
+                                        f"environment, 1 thread; includes the oracle's full grid build; "
+                                        f"{t_1:.1f} s wall"},
+            **host_info()}
 
 
 def run_reference(args):
@@ -151,7 +197,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_obj(args, n, world),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                             **host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -272,14 +319,11 @@ def run_bdm(args):
     if not args.no_cpu_baseline:
         if big:  # the oracle on a 2e7-agent sub-volume of the same density
             ps, ds = sub_volume(args.config, n)
-            m, dt, threads = oracle_sample_run(ps, ds, args.cpu_stride)
-            what = f"a {SUB_N}-agent sub-volume at the same density"
+            what = f"a {SUB_N}-agent sub-volume of the workload at the same density"
         else:
-            m, dt, threads = oracle_sample_run(pos_h, diam_h, args.cpu_stride)
-            what = f"the full {n}-agent population"
-        cpu = {"value": m / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"every {args.cpu_stride}th agent id updated ({m} agents) with {what} as environment; "
-                         f"oracle grid rebuilt over all of them; {dt:.1f} s wall"}
+            ps, ds = pos_h, diam_h
+            what = f"the whole {n}-agent workload"
+        cpu = cpu_baseline(ps, ds, what, args.cpu_stride_1t)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
@@ -437,7 +481,8 @@ def main():
     ap.add_argument("--config", type=int, default=3, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--n", type=int, default=None, help="override N (testing only)")
     ap.add_argument("--impl", default="bdm", choices=["bdm", "reference"])
-    ap.add_argument("--cpu-stride", type=int, default=10)
+    ap.add_argument("--cpu-stride", type=int, default=10, help="reference arm: every k-th agent updated per step")
+    ap.add_argument("--cpu-stride-1t", type=int, default=200, help="single-threaded oracle sample stride")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--slabs", action="store_true", help="use the x-slab driver even at one rank (testing)")

@@ -45,7 +45,10 @@ extern "C" {
                                by an earlier asynchronous error) */
 #define BDM_ENOMEM (-3)     /* device or host allocation failed */
 #define BDM_ECUDA (-4)      /* CUDA runtime error (no device, launch failure, ...) */
-#define BDM_ENONFINITE (-6) /* a summed force or displacement was not finite */
+#define BDM_ENONFINITE (-6) /* a summed force or displacement was not finite; the message
+                               names the agent and the offending pair (id, partner id): the first
+                               partner, in O5's canonical order, whose term or partial sum is not
+                               finite */
 #define BDM_ERANGE (-7)     /* n >= 2^32, n_boxes >= 2^32, or |p * inv| >= 2^20 boxes (R9) */
 #define BDM_ETRUNC (-8)     /* output buffer too small; the required size was written back */
 
@@ -208,10 +211,20 @@ int bdm_get_skip_stats(bdm_handle h, int64_t* out3);
 
 /* Force path of the last step: out2[0] = 1 if it ran the half-shell pair path
  * (k_half_search + k_half_sum: each candidate pair tested once, Newton's third law), 0 if the
- * single-pass k_force (BDM_RECORD, BDM_SKIP_STATIONARY, neurites, BDM_HALF=0, or the pair rows
- * could not be allocated); out2[1] = agents of that step whose pair rows overflowed and took the
- * exact full-search path (results are identical either way).  -1 entries before the first step. */
+ * single-pass k_force (BDM_RECORD, BDM_SKIP_STATIONARY, bdm_set_force_path(BDM_PATH_SINGLE), or the
+ * pair rows could not be allocated); out2[1] = agents of that step whose pair rows overflowed and
+ * took the exact full-search path (results are identical either way).  -1 entries before the first
+ * step. */
 int bdm_get_path_stats(bdm_handle h, int64_t* out2);
+
+/* Force-path selection for plain steps of this handle: BDM_PATH_AUTO (default)
+ * runs the half-shell passes whenever their pair rows (133 B/agent) can be allocated and falls back
+ * to the single-pass k_force otherwise (e.g. 10^9 agents on one GPU); BDM_PATH_SINGLE always runs
+ * k_force.  Both compute O3-O7 in the canonical order: results are bit-identical.  EINVAL for any
+ * other value. */
+#define BDM_PATH_AUTO 0
+#define BDM_PATH_SINGLE 1
+int bdm_set_force_path(bdm_handle h, int path);
 
 /* Issue all later work on this CUDA stream (cudaStream_t; NULL = legacy default stream). */
 int bdm_set_stream(bdm_handle h, void* cuda_stream);

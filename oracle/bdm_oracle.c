@@ -542,7 +542,8 @@ int64_t orc_run_growth(int64_t n, double* pos, double* diam, const orc_params* p
  *                 node_a = clamp(floor((p_a - origin_a) * (1/h) + 0.5), 0, dims_a - 1);
  *                 c[node] += count(node) * secretion  (one multiply per node)
  *   S2 diffusion  c' = c + dt * (D * lap - mu * c), lap = (((xm + xp) + (ym + yp)) + (zm + zp) - 6c) * (1/h^2),
- *                 closed boundary: a missing neighbour is the node itself; both fields
+ *                 closed boundary: a missing neighbour is the node itself; both fields; a negative c' is
+ *                 clamped to 0 ("Concentrations remain >= 0 (clamped)")
  *   S3 chemotaxis g = grad c_t(p): central differences (g_a = (c[+1] - c[-1]) * (0.5/h), one-sided
  *                 (c[+1]-c[0])/h or (c[0]-c[-1])/h on the boundary layers) at the 8 nodes of the cell
  *                 containing p, trilinearly interpolated (weights clamped to the lattice);
@@ -588,7 +589,8 @@ void orc_diffuse(const orc_fields* f, const double* c, double* out) {
         double ym = c[fidx(f, x, y > 0 ? y - 1 : y, z)], yp = c[fidx(f, x, y + 1 < f->dims[1] ? y + 1 : y, z)];
         double zm = c[fidx(f, x, y, z > 0 ? z - 1 : z)], zp = c[fidx(f, x, y, z + 1 < f->dims[2] ? z + 1 : z)];
         double lap = ((((xm + xp) + (ym + yp)) + (zm + zp)) - 6.0 * c0) * ih2;
-        out[fidx(f, x, y, z)] = c0 + f->dt * (f->diff * lap - f->decay * c0);
+        double v = c0 + f->dt * (f->diff * lap - f->decay * c0);
+        out[fidx(f, x, y, z)] = v < 0.0 ? 0.0 : v; /* negative results clamped to 0 */
       }
 }
 

@@ -38,6 +38,8 @@ BDM_HALO = 0
 BDM_MIGRANTS = 1
 BDM_OWNED_POSITIONS = 0
 BDM_LAST_DISPLACEMENTS = 1
+BDM_PATH_AUTO = 0
+BDM_PATH_SINGLE = 1
 
 ERRNAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -6: "ENONFINITE", -7: "ERANGE", -8: "ETRUNC"}
 
@@ -98,6 +100,7 @@ _SIGS = {
     "bdm_sync": ([_vp], ctypes.c_int),
     "bdm_set_timing": ([_vp, ctypes.c_int], ctypes.c_int),
     "bdm_set_defer": ([_vp, ctypes.c_int], ctypes.c_int),
+    "bdm_set_force_path": ([_vp, ctypes.c_int], ctypes.c_int),
     "bdm_get_timing": ([_vp, _vp], ctypes.c_int),
     "bdm_get_timing_ex": ([_vp, _vp], ctypes.c_int),
     "bdm_generate_uniform": ([ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, _vp, _vp, ctypes.c_double,
@@ -399,6 +402,11 @@ def bdm_get_path_stats(h: Handle) -> dict:
     out = np.zeros(2, np.int64)
     _check(load_library().bdm_get_path_stats(h.raw, _ptr(out)), h.raw)
     return dict(half=int(out[0]), slow=int(out[1]))
+
+
+def bdm_set_force_path(h: Handle, path: int) -> None:
+    """BDM_PATH_AUTO (half-shell passes when their rows fit, else k_force) or BDM_PATH_SINGLE."""
+    _check(load_library().bdm_set_force_path(h.raw, int(path)), h.raw)
 
 
 def bdm_set_defer(h: Handle, max_deferred: int) -> None:

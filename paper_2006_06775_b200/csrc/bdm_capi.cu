@@ -27,8 +27,6 @@ namespace {
 
 thread_local std::string g_tls_error;
 const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after every launch
-// BDM_HALF=0 selects the single-pass k_force for plain steps (A/B measurements of the half-shell path)
-const bool g_no_half = std::getenv("BDM_HALF") != nullptr && std::getenv("BDM_HALF")[0] == '0';
 // BDM_DEFER=k: at most k consecutive deferred builds (no host round trip); 0 = off
 // (default 0: with the current kernels the wider frames of deferred builds cost more than the round
 // trip they save; bdm_set_defer sets it per handle)
@@ -152,7 +150,8 @@ struct bdm_ctx {
   uint32_t* h_slow = nullptr;  // sum pass: agents whose pair rows overflowed (k_half_slow)
   uint8_t* h_fcnt = nullptr;
   int64_t h_cap = 0;
-  bool half_off = false;  // BDM_HALF=0, or the rows could not be allocated: k_force only
+  bool half_off = false;  // the rows could not be allocated: k_force only
+  int force_path = BDM_PATH_AUTO;  // bdm_set_force_path
   bool last_half = false;  // the last step used the half-shell path
   bool split_pending = false;  // slab: bdm_slab_split ran, bdm_slab_commit not yet
   int64_t n_dead = 0;          // slab: committed emigrants still in ag[cur][0..n) (D < 0), dropped by the next sort
@@ -233,13 +232,18 @@ int check_async(bdm_ctx* h) {
   CU(h, cudaStreamSynchronize(h->stream));
   if (h->err_host->code) {
     h->poisoned = true;
+    const uint32_t first = (uint32_t)(h->err_host->bad >> 32);
     if (h->err_host->code == 1u)
-      return fail(h, BDM_EINVAL, "invalid agent %u: diameter must be > 0 and finite, positions finite",
-                  h->err_host->first_bad);
-    if (h->err_host->code == 6u)
-      return fail(h, BDM_ENONFINITE, "non-finite force on agent %u", h->err_host->first_bad);
+      return fail(h, BDM_EINVAL, "invalid agent %u: diameter must be > 0 and finite, positions finite", first);
+    if (h->err_host->code == 6u) {  // the offending pair (partner located by k_locate_nonfinite)
+      const uint32_t j = h->err_host->second;
+      if (j < 0xfffffffeu)
+        return fail(h, BDM_ENONFINITE, "non-finite force or displacement on agent %u from its pair (%u, %u)", first,
+                    first, j);
+      return fail(h, BDM_ENONFINITE, "non-finite force or displacement on agent %u", first);
+    }
     if (h->err_host->code == 7u)
-      return fail(h, BDM_ERANGE, "agent at input position %u left the grid of a deferred build", h->err_host->first_bad);
+      return fail(h, BDM_ERANGE, "agent at input position %u left the grid of a deferred build", first);
     return fail(h, BDM_ECUDA, "device error code %u", h->err_host->code);
   }
   return BDM_OK;
@@ -330,7 +334,7 @@ void init_device_info(bdm_ctx* h) {
 // Pair rows of the half-shell path for cap agents (16 + 16 u32 + counters: 133 B/agent).  An
 // allocation failure is not an error: the handle falls back to k_force (no rows needed).
 bool ensure_half(bdm_ctx* h) {
-  if (h->half_off || g_no_half) return false;
+  if (h->half_off || h->force_path == BDM_PATH_SINGLE) return false;
   if (h->h_cap >= h->cap && h->h_fwd) return true;
   for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt, (void*)h->h_slow})
     if (q) cudaFree(q);
@@ -434,8 +438,9 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   }
   DBG(h, "k_half_slow");
   DBG(h, "k_half_sum");
+  k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
   CU(h, cudaGetLastError());
-  h->launches += 2;
+  h->launches += 4;
   h->cols_next = fuse_cols;
   return BDM_OK;
 }
@@ -705,9 +710,10 @@ int force_step(bdm_ctx* h, bool want_dp) {
                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
                                                  h->skip_active ? h->hot : nullptr,
                                                  h->hist[0] ? h->hist[dst] : nullptr, nullptr);
+  k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
   CU(h, cudaGetLastError());
   DBG(h, "k_force");
-  h->launches += 2;
+  h->launches += 3;
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
   // pointers (the kernel already captured its arguments) instead of copying.
   h->out_ids = h->id[src];
@@ -1109,7 +1115,7 @@ int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, 
     (void)cudaGetLastError();
     TRY(fail(h, BDM_ENOMEM, "bdm_init: pinned host allocation"));
   }
-  ErrDev e0{0u, 0xffffffffu, 0u, 0u};
+  ErrDev e0{0u, 0xffffffffu, ERR_NONE};
   if (cudaMemcpy(h->err, &e0, sizeof e0, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemset(h->maxd_bits, 0, sizeof(unsigned long long)) != cudaSuccess) {
     (void)cudaGetLastError();
@@ -1128,7 +1134,7 @@ int bdm_set_agents(bdm_handle h, const double* pos, const double* diam) {
   if (h->n > 0 && (!pos || !diam)) return fail(h, BDM_EINVAL, "bdm_set_agents: NULL array with n > 0");
   CU(h, cudaSetDevice(h->device));
   if (h->poisoned) {  // a fresh population clears an earlier data error
-    ErrDev e0{0u, 0xffffffffu, 0u, 0u};
+    ErrDev e0{0u, 0xffffffffu, ERR_NONE};
     CU(h, cudaMemcpyAsync(h->err, &e0, sizeof e0, cudaMemcpyHostToDevice, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
     h->poisoned = false;
@@ -1384,6 +1390,13 @@ int bdm_get_count(bdm_handle h, int64_t* out2) {
   if (!h || !out2) return fail(h, BDM_EINVAL, "bdm_get_count: NULL argument");
   out2[0] = h->n;
   out2[1] = h->n_dp;
+  return BDM_OK;
+}
+
+int bdm_set_force_path(bdm_handle h, int path) {
+  if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_force_path: NULL handle");
+  if (path != BDM_PATH_AUTO && path != BDM_PATH_SINGLE) return fail(h, BDM_EINVAL, "bdm_set_force_path: bad path %d", path);
+  h->force_path = path;
   return BDM_OK;
 }
 
@@ -1701,7 +1714,7 @@ int bdm_slab_init(bdm_handle* out, int64_t n_local, int64_t capacity, const uint
     (void)cudaGetLastError();
     TRY(fail(h, BDM_ENOMEM, "bdm_slab_init: pinned host allocation"));
   }
-  ErrDev e0{0u, 0xffffffffu, 0u, 0u};
+  ErrDev e0{0u, 0xffffffffu, ERR_NONE};
   if (cudaMemcpy(h->err, &e0, sizeof e0, cudaMemcpyHostToDevice) != cudaSuccess) {
     (void)cudaGetLastError();
     TRY(fail(h, BDM_ECUDA, "bdm_slab_init: device initialisation"));
@@ -2008,8 +2021,9 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
                                                  (uint32_t)(n_sorted - n_hi), g, pd, h->ag[dst], h->id[dst],
                                                  want_dp ? h->dp : nullptr, want_dp ? h->dp_ids : nullptr, h->ext,
                                                  h->err, rec, nullptr, nullptr, nullptr);
+    k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], g, pd, h->err);
     CU(h, cudaGetLastError());
-    h->launches += 1;
+    h->launches += 2;
   }
   if (h->timing) CU(h, cudaEventRecord(ts.e2, s));
   h->cur = dst;

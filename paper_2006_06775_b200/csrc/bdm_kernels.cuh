@@ -75,11 +75,12 @@ struct ColNext {
 };
 
 struct ErrDev {
-  uint32_t code;       // 0 ok, else |BDM_E*|
-  uint32_t first_bad;  // id of the first offending agent (min over reports)
-  uint32_t second;     // partner id for ENONFINITE
-  uint32_t pad;
+  uint32_t code;            // 0 ok, else |BDM_E*|
+  uint32_t second;          // ENONFINITE: partner id located by k_locate_nonfinite (0xffffffff = not yet)
+  unsigned long long bad;   // (id of the first offending agent << 32) | aux, min over reports; aux =
+                            // the agent's sorted index in the force phase's state (ENONFINITE)
 };
+constexpr unsigned long long ERR_NONE = ~0ull;
 
 struct RecordDev {
   int32_t *n_cand, *n_nb, *n_ct;
@@ -99,10 +100,11 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   return z ^ (z >> 31);
 }
 
-__device__ __forceinline__ void report(ErrDev* e, uint32_t code, uint32_t id, uint32_t other) {
+// First error wins the code; the reported (id, aux) pair is the one with the smallest id (one 64-bit
+// atomicMin keeps id and aux consistent).
+__device__ __forceinline__ void report(ErrDev* e, uint32_t code, uint32_t id, uint32_t aux) {
   atomicCAS(&e->code, 0u, code);
-  uint32_t prev = atomicMin(&e->first_bad, id);
-  if (id < prev) e->second = other;  // best effort partner id
+  atomicMin(&e->bad, ((unsigned long long)id << 32) | aux);
 }
 
 // ------------------------------------------------------------------------------------------ K0
@@ -1120,7 +1122,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
       branch = 2;
     }
     if (valid) {
-      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, myid);
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, myid, i);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
       st_state(&ag_out[o], np);
@@ -1734,6 +1736,38 @@ __device__ __noinline__ double3 full_force(const GridDev& g, const double4* __re
   return make_double3(Fx, Fy, Fz);
 }
 
+// ENONFINITE diagnosis ("abort ... with the offending pair"): after a force phase that
+// reported a non-finite sum, one thread re-walks the reported agent's 27 boxes in canonical order
+// (O3-O5 as written) and names the first partner whose term, or the partial sum / its norm after
+// adding it, is not finite.  Returns at once when nothing was reported (one load).
+__global__ void k_locate_nonfinite(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, GridDev g,
+                                   ParamsDev p, ErrDev* err) {
+  if (threadIdx.x != 0 || __ldcg(&err->code) != 6u || __ldcg(&err->second) != 0xffffffffu) return;
+  const uint32_t i = (uint32_t)(__ldcg(&err->bad) & 0xffffffffull);
+  const double4 me = ag[i];
+  const double ri = 0.5 * me.w;
+  const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
+  double Fx = 0.0, Fy = 0.0, Fz = 0.0;
+  for (int c = 0; c < 9; ++c) {
+    uint32_t b = 0, e = 0;
+    if (!zrun(g, bx + c / 3 - 1, by + c % 3 - 1, bz - 1, bz + 1, b, e)) continue;
+    for (uint32_t j = b; j < e; ++j) {
+      if (j == i) continue;
+      double tx, ty, tz, fa;
+      if (!pair_term(me.x, me.y, me.z, ri, i, ag[j], ids, j, p, tx, ty, tz, fa)) continue;
+      Fx = Fx + tx;
+      Fy = Fy + ty;
+      Fz = Fz + tz;
+      const double fn = sqrt((Fx * Fx + Fy * Fy) + Fz * Fz);
+      if (!(isfinite(tx) && isfinite(ty) && isfinite(tz) && isfinite(fn))) {
+        err->second = ids[j];
+        return;
+      }
+    }
+  }
+  err->second = 0xfffffffeu;  // (no single pair: cannot happen for a sum that the force phase found non-finite)
+}
+
 // FONLY (neurite steps): the sphere-sphere sums F go to dp_out (3 per agent, the force-only output
 // fss of k_force), the displacement rule and everything after it are left to k_sc_rows.
 template <bool FONLY>
@@ -1855,7 +1889,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const bool live = valid && !slow;
     if (FONLY) {
       if (live) {
-        if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+        if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], i);
         const size_t o = 3 * (size_t)(i - a_begin);
         dp_out[o] = Fx;
         dp_out[o + 1] = Fy;
@@ -1881,7 +1915,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     int nb3[3] = {INT32_MAX, INT32_MAX, INT32_MAX};  // box of p'
     bool ebad = false;
     if (live) {
-      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], i);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
       const uint32_t o = i - a_begin;
       st_state(&ag_out[o], np);
@@ -1978,7 +2012,7 @@ __global__ void __launch_bounds__(128) k_half_slow(const double4* __restrict__ a
     const double Fx = f.x, Fy = f.y, Fz = f.z;
     const uint32_t o = i - a_begin;
     if (FONLY) {
-      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+      if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], i);
       dp_out[3 * (size_t)o] = Fx;
       dp_out[3 * (size_t)o + 1] = Fy;
       dp_out[3 * (size_t)o + 2] = Fz;
@@ -1997,7 +2031,7 @@ __global__ void __launch_bounds__(128) k_half_slow(const double4* __restrict__ a
       dpy = Fy * p.c;
       dpz = Fz * p.c;
     }
-    if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], ids[i]);
+    if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], i);
     const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
     ag_out[o] = np;
     const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
@@ -2335,7 +2369,8 @@ __global__ void k_diffuse(const double* __restrict__ c, const uint32_t* __restri
   const double ym = secreted(c, cnt, y > 0 ? k - sy : k, s), yp = secreted(c, cnt, y + 1 < f.ny ? k + sy : k, s);
   const double zm = secreted(c, cnt, z > 0 ? k - 1 : k, s), zp = secreted(c, cnt, z + 1 < f.nz ? k + 1 : k, s);
   const double lap = ((((xm + xp) + (ym + yp)) + (zm + zp)) - 6.0 * c0) * f.ih2;
-  out[k] = c0 + f.dt * (f.diff * lap - f.decay * c0);
+  const double v = c0 + f.dt * (f.diff * lap - f.decay * c0);
+  out[k] = v < 0.0 ? 0.0 : v;  // negative results clamped to 0 (reachable when 6 D dt/h^2 + mu dt > 1)
 }
 
 __device__ __forceinline__ double node_grad(const double* __restrict__ c, const FieldDev& f, int x, int y, int z,

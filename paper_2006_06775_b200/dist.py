@@ -283,7 +283,8 @@ class GpuSlabEngine:
         self.bdm = bdm
         self.torch = torch
         self.device = device if device is not None else pos.device
-        self.h = bdm.bdm_slab_init(ids, pos, diam, capacity, params, stream=stream)
+        self.params = params if params is not None else bdm.bdm_params_default()
+        self.h = bdm.bdm_slab_init(ids, pos, diam, capacity, self.params, stream=stream)
         self.buf_cap = max(1024, capacity // 16)
         self._alloc()
 
@@ -294,6 +295,12 @@ class GpuSlabEngine:
 
     def local_maxd(self):
         return self.bdm.bdm_slab_local_maxd(self.h)
+
+    def max_disp(self):
+        return float(self.params.max_disp)
+
+    def box_edge_min(self):
+        return float(self.params.box_edge_min)
 
     def set_box_edge(self, L):
         self.bdm.bdm_slab_set_box_edge(self.h, L)
@@ -353,13 +360,18 @@ class SlabDriver:
         # single-sync protocol: needs every inner slab at least 2 boxes wide (so that an emigrant
         # never lands in a layer that is a third rank's ghost layer) and engines that can split
         inner = [b - a for a, b in zip(bounds[1:-2], bounds[2:-1])]
-        ok = all(w >= 2 for w in inner) and all(hasattr(e, "split") for e in engines)
-        self.fused = ok if fused is None else (fused and ok)
-        self.next_ghosts = None
         L = comm.allreduce_max([e.local_maxd() for e in engines])  # O1 over all ranks
+        L = max([L] + [e.box_edge_min() for e in engines if hasattr(e, "box_edge_min")])
         for e in engines:
             e.set_box_edge(L)
         self.L = L
+        # the single-sync protocol also needs every step to move an agent by less than one box
+        # (|dp| <= max_disp (1 + 4u) < L): only then are emigrants and next ghosts confined to the
+        # two boundary layers k_slab_split scans
+        small_moves = all(e.max_disp() < L * (1.0 - 2.0 ** -20) for e in engines if hasattr(e, "max_disp"))
+        ok = all(w >= 2 for w in inner) and all(hasattr(e, "split") for e in engines) and small_moves
+        self.fused = ok if fused is None else (fused and ok)
+        self.next_ghosts = None
         self.migrated = 0  # agents moved between slabs by step() (diagnostics)
         self.settle()
 
@@ -470,7 +482,7 @@ def initial_bounds(pos: np.ndarray, diam: np.ndarray, world: int, box_edge_min: 
     """Setup helper (outside the hot path): global L and work-balanced (weighted, default) or
     count-balanced bounds from the full population known to every rank (the bench generates the
     whole seeded population on every rank)."""
-    L = max(float(diam.max()), box_edge_min)
+    L = max(float(diam.max()), box_edge_min)  # the engines' box edge (set_box_edge applies box_edge_min too)
     inv = 1.0 / (L * (1.0 + 2.0 ** -30))
     bx = np.floor(pos[:, 0] * inv).astype(np.int64)
     x0 = int(bx.min())

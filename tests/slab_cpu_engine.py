@@ -28,6 +28,12 @@ class CpuSlabEngine:
     def local_maxd(self):
         return float(self.diam.max()) if len(self.diam) else 0.0
 
+    def max_disp(self):
+        return float(self.prm["max_disp"])
+
+    def box_edge_min(self):
+        return float(self.prm["box_edge_min"])
+
     def set_box_edge(self, L):
         self.L = max(L, self.prm["box_edge_min"])
         self.inv = 1.0 / (self.L * (1.0 + 2.0 ** -30))

@@ -102,3 +102,50 @@ def test_chemotaxis_moves_speed_along_gradient(orc):
     out, _, _, _ = orc.run_soma(pos, np.array([1.0, 1.0]), np.array([0, 1], np.int8), f, 1, c0, c1)
     assert abs(out[0, 0] - (7.3 + 0.5)) < 1e-14 and out[0, 1] == 8.1 and out[0, 2] == 9.9
     assert np.array_equal(out[1], pos[1])  # type 1 sees a flat field
+
+
+def test_negative_results_clamped(orc):
+    """SPEC.md:270 / :286: "negative results clamped to 0".  Closed forms: (a) pure decay with
+    mu dt = 1.5 gives c (1 - 1.5) < 0 at every node -> the field is exactly 0 after one step;
+    (b) a unit spike with D dt/h^2 = 1/6 and mu dt = 0.5: the spike node would be
+    1 + 1 (1/6 (0 - 6) - 0.5) = -0.5 -> 0, its six face neighbours get exactly 1/6 (positive,
+    unclamped), everything else stays 0."""
+    f = fp(orc, diff=0.0, decay=1.5)
+    c = np.random.default_rng(4).uniform(0.1, 5, (20, 20, 20))
+    out = orc.diffuse(f, c)
+    assert np.array_equal(out, np.zeros_like(c)) and not np.signbit(out).any()
+    f = fp(orc, dims=(9, 9, 9), h=3.0, diff=1.5, decay=0.5)  # D dt / h^2 = 1.5 / 9 = 1/6
+    c = np.zeros((9, 9, 9))
+    c[4, 4, 4] = 1.0
+    out = orc.diffuse(f, c)
+    assert out[4, 4, 4] == 0.0 and out.min() == 0.0
+    expect = 1.0 * (1.5 * (1.0 * (1.0 / 9.0)))  # dt * (D * lap) at a face neighbour, lap = 1/h^2
+    for d in [(3, 4, 4), (5, 4, 4), (4, 3, 4), (4, 5, 4), (4, 4, 3), (4, 4, 5)]:
+        assert abs(out[d] - 1.0 / 6.0) <= 1e-16 and out[d] == expect
+    assert np.count_nonzero(out) == 6
+
+
+def test_gradient_boundary_cells_one_sided(orc):
+    """S3 / SPEC.md:304 "one-sided differences at boundary layers", pinned with closed forms.
+    (a) A linear field c = 2x - y + 3z is reproduced exactly by one-sided and central differences
+    alike, so the gradient is (2, -1, 3) in the boundary cells and for positions outside the
+    lattice (clamped sampling) -- a central-difference factor on a boundary node (0.5/h
+    instead of 1/h) would give half the slope there.  (b) c = z^2 (h = 2, 6 nodes): on node 0 the
+    one-sided difference is (c1 - c0)/h = h = 2 (central would be undefined, the exact derivative 0);
+    on the last node (z = 10) it is (100 - 64)/2 = 18; at the cell midpoint z = 1 the gradient
+    interpolates nodes 0 and 1: 0.5 * 2 + 0.5 * (16 - 0)/4 = 3."""
+    n, h = 6, 2.0
+    f = fp(orc, dims=(n, n, n), h=h)
+    x = np.arange(n) * h
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    c = 2.0 * X - Y + 3.0 * Z
+    pts = [(0.3, 0.7, 9.9), (9.5, 0.1, 0.0), (0.0, 0.0, 0.0), (10.0, 10.0, 10.0), (1.0, 9.0, 5.0),
+           (-3.0, 4.0, 12.5), (15.0, -2.0, 3.3)]
+    for p in pts:
+        g = orc.gradient_at(f, c, np.array(p))
+        assert np.abs(g - np.array([2.0, -1.0, 3.0])).max() <= 1e-13, (p, g)
+    c = Z ** 2
+    assert orc.gradient_at(f, c, np.array([5.0, 5.0, 0.0]))[2] == 2.0
+    assert orc.gradient_at(f, c, np.array([5.0, 5.0, 10.0]))[2] == 18.0
+    assert orc.gradient_at(f, c, np.array([5.0, 5.0, 1.0]))[2] == 3.0
+    assert orc.gradient_at(f, c, np.array([5.0, 5.0, -4.0]))[2] == 2.0  # clamped below the lattice
