@@ -45,6 +45,7 @@ extern "C" {
                                by an earlier asynchronous error) */
 #define BDM_ENOMEM (-3)     /* device or host allocation failed */
 #define BDM_ECUDA (-4)      /* CUDA runtime error (no device, launch failure, ...) */
+#define BDM_ENCCL (-5)      /* NCCL error, or libnccl.so.2 could not be loaded (distributed handles) */
 #define BDM_ENONFINITE (-6) /* a summed force or displacement was not finite; the message
                                names the agent and the offending pair (id, partner id): the first
                                partner, in O5's canonical order, whose term or partial sum is not
@@ -326,6 +327,82 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
  * step with want_dp (BDM_LAST_DISPLACEMENTS: ids + n x 3), in the handle's internal order; *n gets
  * the count.  ids / vals may be NULL to query the count. */
 int bdm_slab_get(bdm_handle h, int what, int64_t* n, uint32_t* ids, double* vals);
+
+/* ---------------------------------------------------------------------------------------------
+ * Distributed handles (multi-GPU).  north_star: "Across the 8
+ * GPUs of one box the domain is split into x-slabs.  Each step does a halo exchange of boundary-box
+ * agents and migrates agents that cross slab boundaries, using NCCL send/recv over NVLink."
+ * PAPER.md:436-453 (§2.3 (i)-(iii): the parallel runtime this replaces); SPEC.md:118 (one
+ * controlling caller per instance: here one per rank).
+ *
+ * One process (rank) per GPU.  The library owns the exchange's data plane: an NCCL communicator
+ * (libnccl.so.2 loaded at the first distributed call), the partition, the halo exchange and the
+ * migration.  A rank owns the agents whose integer box-x lies in its slab [cut[r], cut[r+1]);
+ * the cuts are chosen at init from a global per-layer histogram and then from each rank's own
+ * per-layer work (sum n_b + sum n_b^2 / mean), all on the device.  bdm_mech_step runs
+ * chunks of up to 16 steps with no host synchronisation inside a chunk (device-resident counts,
+ * fixed-capacity messages whose headers carry the counts, a fixed grid frame per chunk); a chunk
+ * in which a message overflowed is re-run from a device checkpoint with larger buffers.  Results
+ * are bit-identical to a single handle (ghosts keep their global ids and canonical order).
+ * Errors: NCCL failures -> BDM_ENCCL; the others as for bdm_init / bdm_mech_step.
+ * --------------------------------------------------------------------------------------------- */
+
+/* Rank 0 creates the communicator id (128 bytes into out128) and broadcasts it to the other ranks
+ * (e.g. over torch.distributed); ENCCL if NCCL cannot be loaded. */
+int bdm_nccl_unique_id(void* out128);
+
+/* Collective over the `world` ranks (every rank calls it with the same uid).  This rank contributes
+ * n_local agents with global ids (int64, unique over all ranks, 0 <= id < 2^32 - 1), positions
+ * (n x 3) and diameters (n); any initial distribution is allowed (agents are redistributed to
+ * their owners).  Arrays are host pointers, or device pointers with p->flags & BDM_DEVICE_PTRS.
+ * device: CUDA ordinal of this rank; cuda_stream: the stream all work of the handle runs on (also
+ * NCCL's).  Validates as bdm_init (EINVAL names the first bad agent).  The returned handle accepts
+ * bdm_mech_step, bdm_set_timing / bdm_get_timing(_ex), bdm_get_stats, bdm_get_local,
+ * bdm_get_cuts, bdm_sync and bdm_destroy. */
+int bdm_init_dist(bdm_handle* h, int64_t n_local, const int64_t* ids, const double* pos, const double* diam,
+                  const bdm_params* p, int rank, int world, const void* nccl_uid, int device, void* cuda_stream);
+
+/* Virtual ranks (tests of the data plane on one GPU): all `world` ranks live in this process on
+ * p->device over a 1-rank NCCL communicator (every message a self send/recv); counts[r] agents
+ * start on rank r, the arrays hold them concatenated in rank order.  Same protocol and kernels as
+ * bdm_init_dist; getters return all ranks' owned agents. */
+int bdm_init_dist_local(bdm_handle* h, int world, const int64_t* counts, const int64_t* ids, const double* pos,
+                        const double* diam, const bdm_params* p, void* cuda_stream);
+
+/* Owned agents of a distributed handle (all local ranks): what = BDM_OWNED_POSITIONS (ids + n x 3
+ * positions) or BDM_LAST_DISPLACEMENTS (ids + n x 3 displacements of the last step; ESTATE before
+ * one).  *n receives the count; ids / vals may be NULL (count only).  Host or device pointers per
+ * BDM_DEVICE_PTRS at init.  Synchronises. */
+int bdm_get_local(bdm_handle h, int what, int64_t* n, int64_t* ids, double* vals);
+
+/* The partition of a distributed handle: world + 1 box-x cuts (cut[0] = INT32_MIN, cut[world] =
+ * INT32_MAX) into out[cap]; ETRUNC if cap is too small. */
+int bdm_get_cuts(bdm_handle h, int32_t* out, int32_t cap);
+
+/* Order-free pair digest of the current positions (SURVEY §8(c) outputs, used for large configs):
+ * for every agent (id order) the number of partners of kind BDM_NEIGHBOR (d2 <= L2, O3) or
+ * BDM_CONTACT (delta > 0, O4) and the sum over them of mix64(partner id) mod 2^64 (mix64 = the
+ * SplitMix64 finaliser).  Builds the grid if needed.  count: n uint32, hash: n uint64, host or
+ * device per BDM_DEVICE_PTRS.  Single handles only (ESTATE otherwise). */
+int bdm_get_pair_digest(bdm_handle h, int kind, uint32_t* count, uint64_t* hash);
+
+/* Counters of a handle since init (SURVEY §8(b) bdm_get_stats). */
+typedef struct {
+  int64_t n_agents;       /* agents (distributed: owned by this process's ranks) */
+  int64_t steps;          /* mechanical steps run */
+  int64_t launches;       /* kernels of this library launched */
+  int64_t host_syncs;     /* host synchronisations with the device (distributed: set-up, one per chunk
+                             of up to 16 steps, getters) */
+  int64_t half_path;      /* 1: the last step ran the half-shell passes, 0: k_force, -1: no step */
+  int64_t migrated;       /* distributed: agents that changed owner during steps */
+  int64_t ghosts;         /* distributed: ghost agents of the last step (all local ranks) */
+  int64_t exchange_bytes; /* distributed: bytes sent by this process's ranks */
+  int64_t chunks;         /* distributed: synchronised chunks of steps */
+  int64_t redo_chunks;    /* distributed: chunks re-run after a message overflow */
+  int64_t world;          /* ranks (1 for single handles) */
+  int64_t local_ranks;    /* ranks in this process */
+} bdm_stats;
+int bdm_get_stats(bdm_handle h, bdm_stats* out);
 
 /* Human-readable message of the last failure on h (or of the calling thread when h is NULL). */
 const char* bdm_last_error(bdm_handle h);

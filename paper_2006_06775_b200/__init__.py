@@ -26,6 +26,7 @@ BDM_EINVAL = -1
 BDM_ESTATE = -2
 BDM_ENOMEM = -3
 BDM_ECUDA = -4
+BDM_ENCCL = -5
 BDM_ENONFINITE = -6
 BDM_ERANGE = -7
 BDM_ETRUNC = -8
@@ -41,7 +42,8 @@ BDM_LAST_DISPLACEMENTS = 1
 BDM_PATH_AUTO = 0
 BDM_PATH_SINGLE = 1
 
-ERRNAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -6: "ENONFINITE", -7: "ERANGE", -8: "ETRUNC"}
+ERRNAMES = {-1: "EINVAL", -2: "ESTATE", -3: "ENOMEM", -4: "ECUDA", -5: "ENCCL", -6: "ENONFINITE", -7: "ERANGE",
+            -8: "ETRUNC"}
 
 
 class BdmError(RuntimeError):
@@ -66,6 +68,12 @@ class bdm_field_params(ctypes.Structure):
     _fields_ = [("h", ctypes.c_double), ("origin", ctypes.c_double * 3), ("dims", ctypes.c_int32 * 3),
                 ("diff", ctypes.c_double), ("decay", ctypes.c_double), ("dt", ctypes.c_double),
                 ("secretion", ctypes.c_double), ("speed", ctypes.c_double)]
+
+
+class bdm_stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("n_agents", "steps", "launches", "host_syncs", "half_path", "migrated",
+                                               "ghosts", "exchange_bytes", "chunks", "redo_chunks", "world",
+                                               "local_ranks")]
 
 
 class bdm_agent_stats(ctypes.Structure):
@@ -119,6 +127,15 @@ _SIGS = {
     "bdm_slab_step": ([_vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32, _vp, ctypes.c_int64, _vp, ctypes.c_int64,
                        ctypes.c_int], ctypes.c_int),
     "bdm_slab_get": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, _vp], ctypes.c_int),
+    "bdm_nccl_unique_id": ([_vp], ctypes.c_int),
+    "bdm_init_dist": ([ctypes.POINTER(_vp), ctypes.c_int64, _vp, _vp, _vp, ctypes.POINTER(bdm_params), ctypes.c_int,
+                       ctypes.c_int, _vp, ctypes.c_int, _vp], ctypes.c_int),
+    "bdm_init_dist_local": ([ctypes.POINTER(_vp), ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.POINTER(bdm_params), _vp],
+                            ctypes.c_int),
+    "bdm_get_local": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, _vp], ctypes.c_int),
+    "bdm_get_cuts": ([_vp, _vp, ctypes.c_int32], ctypes.c_int),
+    "bdm_get_pair_digest": ([_vp, ctypes.c_int, _vp, _vp], ctypes.c_int),
+    "bdm_get_stats": ([_vp, ctypes.POINTER(bdm_stats)], ctypes.c_int),
     "bdm_last_error": ([_vp], ctypes.c_char_p),
     "bdm_destroy": ([_vp], None),
 }
@@ -531,3 +548,121 @@ def bdm_slab_get(h: Handle, what: int):
     vals = torch.empty((n.value, 3), dtype=torch.float64, device="cuda")
     _check(lib.bdm_slab_get(h.raw, what, ctypes.byref(n), _ptr(ids), _ptr(vals)), h.raw)
     return ids.to(torch.int64) & 0xFFFFFFFF, vals
+
+
+# ------------------------------------------------------------------------------ distributed handles
+def bdm_nccl_unique_id() -> bytes:
+    """128-byte NCCL communicator id (rank 0 creates it and broadcasts it to the other ranks)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().bdm_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _dist_arrays(ids, pos, diam, p):
+    dev = _is_torch(pos) and pos.is_cuda
+    if dev:
+        import torch
+
+        assert pos.dtype == torch.float64 and diam.dtype == torch.float64 and ids.dtype == torch.int64
+        assert pos.is_contiguous() and diam.is_contiguous() and ids.is_contiguous()
+        p.flags |= BDM_DEVICE_PTRS
+    else:
+        p.flags &= ~BDM_DEVICE_PTRS
+        pos = np.ascontiguousarray(pos, dtype=np.float64).reshape(-1, 3)
+        diam = np.ascontiguousarray(diam, dtype=np.float64).reshape(-1)
+        ids = np.ascontiguousarray(ids, dtype=np.int64).reshape(-1)
+    if not (len(ids) == len(diam) == pos.shape[0]):
+        raise ValueError("ids, pos and diam lengths differ")
+    return ids, pos, diam, dev
+
+
+def bdm_init_dist(ids, pos, diam, params: bdm_params | None = None, rank: int = 0, world: int = 1,
+                  uid: bytes | None = None, device: int = 0, stream=None) -> Handle:
+    """Collective: this rank's agents (global int64 ids, [n,3] positions, [n] diameters; NumPy or
+    CUDA tensors) -> a distributed handle over `world` ranks (one process per GPU)."""
+    p = params if params is not None else bdm_params_default()
+    ids, pos, diam, dev = _dist_arrays(ids, pos, diam, p)
+    p.device = device
+    raw = ctypes.c_void_p()
+    sp = getattr(stream, "cuda_stream", stream)
+    if dev:
+        import torch
+
+        torch.cuda.synchronize(device)
+    ubuf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(load_library().bdm_init_dist(ctypes.byref(raw), len(diam), _ptr(ids), _ptr(pos), _ptr(diam),
+                                        ctypes.byref(p), rank, world, ubuf, device, ctypes.c_void_p(sp or 0)))
+    h = Handle(raw, 0, dev)
+    h.world = world
+    bdm_get_count(h)
+    return h
+
+
+def bdm_init_dist_local(world: int, counts, ids, pos, diam, params: bdm_params | None = None,
+                        stream=None) -> Handle:
+    """Virtual ranks (one GPU, one process): counts[r] agents of the concatenated arrays start on
+    rank r; every exchange is a self send/recv of a 1-rank NCCL communicator."""
+    p = params if params is not None else bdm_params_default()
+    ids, pos, diam, dev = _dist_arrays(ids, pos, diam, p)
+    c = np.ascontiguousarray(counts, dtype=np.int64)
+    assert len(c) == world and int(c.sum()) == len(diam)
+    if dev:
+        import torch
+
+        if p.device < 0:
+            p.device = pos.device.index
+        torch.cuda.synchronize()
+    raw = ctypes.c_void_p()
+    sp = getattr(stream, "cuda_stream", stream)
+    _check(load_library().bdm_init_dist_local(ctypes.byref(raw), world, _ptr(c), _ptr(ids), _ptr(pos), _ptr(diam),
+                                              ctypes.byref(p), ctypes.c_void_p(sp or 0)))
+    h = Handle(raw, 0, dev)
+    h.world = world
+    bdm_get_count(h)
+    return h
+
+
+def bdm_get_local(h: Handle, what: int = BDM_OWNED_POSITIONS):
+    """(ids [n] int64, values [n,3]) of the owned agents of a distributed handle: positions or the
+    displacements of the last step."""
+    lib = load_library()
+    n = ctypes.c_int64(0)
+    _check(lib.bdm_get_local(h.raw, what, ctypes.byref(n), None, None), h.raw)
+    m = int(n.value)
+    if h.device_ptrs:
+        import torch
+
+        ids = torch.empty(m, dtype=torch.int64, device="cuda")
+        vals = torch.empty((m, 3), dtype=torch.float64, device="cuda")
+    else:
+        ids = np.empty(m, np.int64)
+        vals = np.empty((m, 3), np.float64)
+    _check(lib.bdm_get_local(h.raw, what, ctypes.byref(n), _ptr(ids), _ptr(vals)), h.raw)
+    return ids, vals
+
+
+def bdm_get_cuts(h: Handle) -> list:
+    out = np.zeros(h.world + 1, np.int32)
+    _check(load_library().bdm_get_cuts(h.raw, _ptr(out), len(out)), h.raw)
+    return [int(v) for v in out]
+
+
+def bdm_get_pair_digest(h: Handle, kind: int):
+    """(count [n] uint32, hash [n] uint64) of the neighbour (0) or contact (1) partners, id order."""
+    n, _ = bdm_get_count(h)
+    if h.device_ptrs:
+        import torch
+
+        cnt = torch.empty(n, dtype=torch.int32, device="cuda")
+        hs = torch.empty(n, dtype=torch.int64, device="cuda")
+    else:
+        cnt = np.empty(n, np.uint32)
+        hs = np.empty(n, np.uint64)
+    _check(load_library().bdm_get_pair_digest(h.raw, kind, _ptr(cnt), _ptr(hs)), h.raw)
+    return cnt, hs
+
+
+def bdm_get_stats(h: Handle) -> dict:
+    st = bdm_stats()
+    _check(load_library().bdm_get_stats(h.raw, ctypes.byref(st)), h.raw)
+    return {k: int(getattr(st, k)) for k, _ in bdm_stats._fields_}

@@ -41,6 +41,8 @@ struct TimedStep {
   cudaEvent_t e3 = nullptr;  // half-shell path: between the search and the sum pass
 };
 
+struct DistGroup;  // distributed x-slab runtime (bdm_dist.cuh)
+
 }  // namespace
 
 struct bdm_ctx {
@@ -159,12 +161,21 @@ struct bdm_ctx {
   uint32_t last_n_lo = 0;      // slab: lower ghosts of the last step (sorted first)
   int32_t split_xb = 0, split_xe = 0;
   int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
-  int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build
+  int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build (since bdm_get_timing)
+  int64_t launches_total = 0;  // launches before the last bdm_get_timing reset
+  int64_t host_syncs = 0;      // host synchronisations with the device (bdm_get_stats)
+  uint64_t steps_total = 0;    // mechanical steps since init
+  DistGroup* dist = nullptr;   // distributed handle (bdm_init_dist): the local slabs, communicator
   std::vector<TimedStep> timed;
   std::string error;
 };
 
 namespace {
+
+void dist_destroy(DistGroup* G);
+int dist_mech_step(bdm_ctx* H, int32_t n_steps);
+void dist_set_timing(DistGroup* G, bool on);
+int dist_get_timing(bdm_ctx* H, double* out6);
 
 int fail(bdm_ctx* h, int code, const char* fmt, ...) {
   char buf[512];
@@ -230,6 +241,7 @@ ParamsDev params_dev(const bdm_params& p) {
 int check_async(bdm_ctx* h) {
   CU(h, cudaMemcpyAsync(h->err_host, h->err, sizeof(ErrDev), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
+  ++h->host_syncs;
   if (h->err_host->code) {
     h->poisoned = true;
     const uint32_t first = (uint32_t)(h->err_host->bad >> 32);
@@ -1022,6 +1034,10 @@ const char* bdm_last_error(bdm_handle h) { return h ? h->error.c_str() : g_tls_e
 
 void bdm_destroy(bdm_handle h) {
   if (!h) return;
+  if (h->dist) {
+    dist_destroy(h->dist);
+    h->dist = nullptr;
+  }
   if (h->el) bdm_destroy(h->el);
   int prev = 0;
   cudaGetDevice(&prev);
@@ -1167,6 +1183,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
   if (n_steps < 0) return fail(h, BDM_EINVAL, "bdm_mech_step: n_steps = %d < 0", n_steps);
   if (h->poisoned) return fail(h, BDM_ESTATE, "handle poisoned by an earlier error: %s", h->error.c_str());
   CU(h, cudaSetDevice(h->device));
+  if (h->dist) return dist_mech_step(h, n_steps);
   if (h->n == 0 && h->n_el == 0) {
     if (n_steps > 0) h->have_dp = true;
     return BDM_OK;
@@ -1189,6 +1206,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
       int rc = neurite_step(h, s == n_steps - 1);
       if (rc) return rc;
       ++h->step_count;
+      ++h->steps_total;
       if (h->timing) CU(h, cudaEventRecord(ts.e2, h->stream));
       continue;
     }
@@ -1206,6 +1224,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
       if (rc) return rc;
     }
     ++h->step_count;
+    ++h->steps_total;
     if (h->timing) CU(h, cudaEventRecord(ts.e2, h->stream));
   }
   return BDM_OK;
@@ -1409,12 +1428,14 @@ int bdm_set_defer(bdm_handle h, int max_deferred) {
 int bdm_set_timing(bdm_handle h, int enabled) {
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_timing: NULL handle");
   h->timing = enabled != 0;
+  if (h->dist) dist_set_timing(h->dist, h->timing);
   return BDM_OK;
 }
 
 int bdm_get_timing_ex(bdm_handle h, double* out6) {
   if (!h || !out6) return fail(h, BDM_EINVAL, "bdm_get_timing_ex: NULL argument");
   CU(h, cudaSetDevice(h->device));
+  if (h->dist) return dist_get_timing(h, out6);
   CU(h, cudaStreamSynchronize(h->stream));
   double grid = 0.0, force = 0.0, search = 0.0, sum = 0.0;
   for (auto& t : h->timed) {
@@ -1440,6 +1461,7 @@ int bdm_get_timing_ex(bdm_handle h, double* out6) {
   out6[4] = search;
   out6[5] = sum;
   h->timed.clear();
+  h->launches_total += h->launches;
   h->launches = 0;
   return BDM_OK;
 }
@@ -2107,3 +2129,5 @@ int bdm_generate_uniform(uint64_t seed, int64_t id0, int64_t n, const double* lo
 }
 
 }  // extern "C"
+
+#include "bdm_dist.cuh"

@@ -303,8 +303,16 @@ __global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ cz
   }
 }
 
+// rng (distributed steps, device counts): the agents [rng[0], rng[1]) of ag instead of [0, n) (n = bound)
 __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g, int32_t* __restrict__ czlo,
-                          int32_t* __restrict__ czhi) {
+                          int32_t* __restrict__ czhi, const uint32_t* __restrict__ rng = nullptr) {
+  uint32_t b0 = 0u;
+  if (rng) {
+    b0 = __ldg(&rng[0]);
+    n = __ldg(&rng[1]) - b0;
+    ag += b0;
+  }
+  if (blockIdx.x * (2 * blockDim.x) >= n) return;  // (whole blocks only: the warps reduce below)
   const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const uint32_t ia[2] = {i0, i0 + blockDim.x};
   double4 pa[2];
@@ -361,9 +369,13 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
 // GUARD (deferred builds, whose extents were not checked on the host): an agent whose box lies
 // outside the grid (a non-finite or out-of-range position) is counted in box 0 and reported (code 7)
 // instead of indexing outside the table.
+// n_dev (distributed steps): the agent count is read on the device (n is the launch bound)
 template <bool GUARD>
 __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g, uint32_t* __restrict__ key,
-                           uint32_t* __restrict__ slot, uint32_t* __restrict__ count, ErrDev* err) {
+                           uint32_t* __restrict__ slot, uint32_t* __restrict__ count, ErrDev* err,
+                           const uint32_t* __restrict__ n_dev = nullptr) {
+  if (n_dev) n = __ldg(n_dev);
+  if (blockIdx.x * (2 * blockDim.x) >= n) return;  // (whole blocks only: the warps aggregate below)
   const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const uint32_t ia[2] = {i0, i0 + blockDim.x};
   double4 pa[2];
@@ -582,7 +594,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(uint32_t* __restrict__ da
 constexpr int KSC = BDM_KSC;
 __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
                           const uint32_t* __restrict__ ids, const uint32_t* __restrict__ start, uint32_t n,
-                          uint32_t* __restrict__ tsrc, uint32_t* __restrict__ tid, uint32_t* __restrict__ tkey) {
+                          uint32_t* __restrict__ tsrc, uint32_t* __restrict__ tid, uint32_t* __restrict__ tkey,
+                          const uint32_t* __restrict__ n_dev = nullptr) {
+  if (n_dev) n = __ldg(n_dev);
+  if (blockIdx.x * (KSC * blockDim.x) >= n) return;
   const uint32_t i0 = blockIdx.x * (KSC * blockDim.x) + threadIdx.x;
   uint32_t k[KSC], sl[KSC], id[KSC], st[KSC];
 #pragma unroll
@@ -609,8 +624,10 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
                         const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ start,
                         const double4* __restrict__ ag_in, uint32_t n, double4* __restrict__ ag_out,
                         uint32_t* __restrict__ ids_out, float4* __restrict__ agf_out,
-                        const unsigned long long* __restrict__ hist_in, unsigned long long* __restrict__ hist_out) {
+                        const unsigned long long* __restrict__ hist_in, unsigned long long* __restrict__ hist_out,
+                        const uint32_t* __restrict__ n_dev = nullptr) {
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev) n = __ldg(n_dev);
   if (q >= n) return;
   const uint32_t k = tkey[q], id = tid[q], src = tsrc[q];
   const double4 p = ld_state(&ag_in[src]);  // (the gather is in flight during the rank loop)
@@ -1431,7 +1448,9 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
 __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     k_half_search(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin, uint32_t s_end,
                   GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
-                  uint32_t* __restrict__ bcnt, Extents* ext, bool count_searched) {
+                  uint32_t* __restrict__ bcnt, Extents* ext, bool count_searched,
+                  const uint32_t* __restrict__ s_end_dev = nullptr) {
+  if (s_end_dev) s_end = __ldg(s_end_dev);
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1777,7 +1796,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
                const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
                const uint32_t* __restrict__ bcnt, ColNext cn, unsigned long long* __restrict__ hist_out,
-               uint32_t* __restrict__ slow_list) {
+               uint32_t* __restrict__ slow_list, const uint32_t* __restrict__ ab_dev = nullptr) {
+  if (ab_dev) {  // distributed steps: the owned range [a_begin, a_end) read on the device
+    a_begin = __ldg(&ab_dev[0]);
+    a_end = __ldg(&ab_dev[1]);
+  }
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -2003,7 +2026,9 @@ __global__ void __launch_bounds__(128) k_half_slow(const double4* __restrict__ a
                                                    double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out,
                                                    Extents* ext_next, ErrDev* err, ColNext cn,
                                                    unsigned long long* __restrict__ hist_out,
-                                                   const uint32_t* __restrict__ slow_list) {
+                                                   const uint32_t* __restrict__ slow_list,
+                                                   const uint32_t* __restrict__ ab_dev = nullptr) {
+  if (ab_dev) a_begin = __ldg(&ab_dev[0]);
   const uint32_t n_slow = __ldcg(&ext_next->slow);
   for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_slow; k += gridDim.x * blockDim.x) {
     const uint32_t i = slow_list[k];
@@ -2139,8 +2164,9 @@ __global__ void k_slab_pack(const double4* __restrict__ ag, const uint32_t* __re
 __global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t n,
                              const uint32_t* __restrict__ r2, double inv, int32_t x_begin, int32_t x_end,
                              double* __restrict__ send_lo, double* __restrict__ send_hi, uint64_t cap,
-                             uint32_t* __restrict__ cnt) {
+                             uint32_t* __restrict__ cnt, const uint32_t* __restrict__ n_dev = nullptr) {
   __shared__ uint32_t s_cnt[4], s_base[4];
+  if (n_dev) n = __ldg(n_dev);
   const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
   const uint32_t hi0 = r2[1] > n_lo_part ? r2[1] : n_lo_part;  // ranges do not overlap
   const uint64_t total = (uint64_t)n_lo_part + (n - hi0);
@@ -2187,7 +2213,8 @@ __global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __r
 
 // bdm_slab_commit: emigrants of the split (same boundary ranges) are marked dead (D < 0) in place.
 __global__ void k_slab_mark_dead(double4* __restrict__ ag, uint32_t n, const uint32_t* __restrict__ r2, double inv,
-                                 int32_t x_begin, int32_t x_end) {
+                                 int32_t x_begin, int32_t x_end, const uint32_t* __restrict__ n_dev = nullptr) {
+  if (n_dev) n = __ldg(n_dev);
   const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
   const uint32_t hi0 = r2[1] > n_lo_part ? r2[1] : n_lo_part;
   const uint64_t total = (uint64_t)n_lo_part + (n - hi0);

@@ -1,0 +1,160 @@
+"""The distributed runtime of libbdm.so (bdm_init_dist / bdm_init_dist_local, DESIGN.md §7;
+north_star: x-slabs, halo exchange and migration with NCCL send/recv) against the CPU oracle.
+
+Only one GPU is available to the tests, so the multi-rank data plane runs as virtual ranks
+(bdm_init_dist_local): G ranks in one process over a 1-rank NCCL communicator, every message a
+self send/recv -- the same kernels, protocol, fixed-capacity messages and device counts as G
+processes.  Positions and displacements must equal oracle.run's bit for bit (ghosts keep their
+global ids and canonical in-box order)."""
+import os
+
+import numpy as np
+import pytest
+
+import bdm_inputs
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def bdm():
+    import torch
+
+    assert torch.cuda.is_available()
+    import paper_2006_06775_b200 as b
+
+    b.load_library()
+    return b
+
+
+def split_counts(n, G, rng):
+    """An arbitrary initial distribution: random counts, agents in id order (not by slab)."""
+    cuts = np.sort(rng.choice(np.arange(1, n), G - 1, replace=False)) if G > 1 else np.array([], int)
+    return np.diff(np.concatenate([[0], cuts, [n]]))
+
+
+def gather(bdm, h, what, n):
+    ids, vals = bdm.bdm_get_local(h, what)
+    out = np.full((n, 3), np.nan)
+    seen = np.zeros(n, int)
+    np.add.at(seen, ids, 1)
+    out[ids] = vals
+    assert np.all(seen == 1), "agents lost or duplicated"
+    return out
+
+
+def run_dist(bdm, pos, diam, G, steps, seed=0, device=True, **kw):
+    import torch
+
+    n = len(diam)
+    counts = split_counts(n, G, np.random.default_rng(seed))
+    ids = np.arange(n, dtype=np.int64)
+    prm = bdm.bdm_params_default(device=0, **kw)
+    if device:
+        h = bdm.bdm_init_dist_local(G, counts, torch.from_numpy(ids).cuda(), torch.from_numpy(pos).cuda(),
+                                    torch.from_numpy(diam).cuda(), prm)
+    else:
+        h = bdm.bdm_init_dist_local(G, counts, ids, pos, diam, prm)
+    bdm.bdm_mech_step(h, steps)
+    p = gather(bdm, h, bdm.BDM_OWNED_POSITIONS, n)
+    d = gather(bdm, h, bdm.BDM_LAST_DISPLACEMENTS, n)
+    if device:
+        torch.cuda.synchronize()
+    return h, p, d
+
+
+def to_np(a):
+    return a.cpu().numpy() if hasattr(a, "cpu") else a
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 7])
+def test_dist_virtual_ranks_equal_oracle(bdm, G):
+    """cfg2 window (40^3 lattice), 5 steps: the C-ABI distributed path equals oracle.run."""
+    pos, diam = bdm_inputs.make_config(2, n=40 ** 3)
+    h, p, d = run_dist(bdm, pos, diam, G, 5)
+    o_p, o_dp = oracle.run(pos, diam, 5)
+    assert np.array_equal(p, o_p) and np.array_equal(d, o_dp)
+    st = bdm.bdm_get_stats(h)
+    assert st["world"] == G and st["steps"] == 5 and st["n_agents"] == len(diam)
+    if G > 1:
+        assert st["migrated"] > 0 and st["ghosts"] > 0
+        cuts = bdm.bdm_get_cuts(h)
+        assert cuts[0] == -(2 ** 31) and cuts[-1] == 2 ** 31 - 1 and all(a < b for a, b in zip(cuts, cuts[1:]))
+
+
+def test_dist_gaussian_host_inputs_across_chunks(bdm):
+    """Gaussian cfg3 subset (work-balanced cuts differ from count cuts), host input arrays, 20 steps
+    = two chunks (one host round trip each): equals oracle.run; the steps inside a chunk issue no
+    host synchronisation (bdm_get_stats.host_syncs grows by exactly 1 per chunk)."""
+    pos, diam = bdm_inputs.make_config(3, n=200_000)
+    n = len(diam)
+    counts = split_counts(n, 3, np.random.default_rng(4))
+    h = bdm.bdm_init_dist_local(3, counts, np.arange(n, dtype=np.int64), pos, diam)
+    s0 = bdm.bdm_get_stats(h)
+    bdm.bdm_mech_step(h, 20)
+    s1 = bdm.bdm_get_stats(h)
+    assert s1["chunks"] - s0["chunks"] == 2 and s1["host_syncs"] - s0["host_syncs"] == 2
+    p = gather(bdm, h, bdm.BDM_OWNED_POSITIONS, n)
+    d = gather(bdm, h, bdm.BDM_LAST_DISPLACEMENTS, n)
+    o_p, o_dp = oracle.run(pos, diam, 20)
+    assert np.array_equal(p, o_p) and np.array_equal(d, o_dp)
+
+
+def test_dist_overflow_rerun_is_exact(bdm, monkeypatch):
+    """Messages of 16 records overflow at once: the chunk is re-run from its device checkpoint with
+    larger buffers (stats.redo_chunks > 0) and the result is still oracle.run's."""
+    monkeypatch.setenv("BDM_DIST_CAP0", "16")
+    # (the variable is read at init)
+    pos, diam = bdm_inputs.make_config(2, n=30 ** 3)
+    h, p, d = run_dist(bdm, pos, diam, 4, 6, seed=2)
+    assert bdm.bdm_get_stats(h)["redo_chunks"] > 0
+    o_p, o_dp = oracle.run(pos, diam, 6)
+    assert np.array_equal(p, o_p) and np.array_equal(d, o_dp)
+
+
+def test_dist_small_diameters_single_rank_path(bdm):
+    """Empty ranks and a rank count larger than the occupied layers do not break the protocol."""
+    rng = np.random.default_rng(3)
+    pos = rng.uniform(0.0, 40.0, (2000, 3))
+    diam = rng.uniform(8.0, 12.0, 2000)
+    h, p, d = run_dist(bdm, pos, diam, 8, 3, seed=5)
+    o_p, o_dp = oracle.run(pos, diam, 3)
+    assert np.array_equal(p, o_p) and np.array_equal(d, o_dp)
+
+
+def test_dist_real_communicator_one_rank(bdm):
+    """bdm_nccl_unique_id + bdm_init_dist with a real 1-rank NCCL communicator (the path bench.py's
+    ranks take): equals oracle.run."""
+    import torch
+
+    pos, diam = bdm_inputs.make_config(1)
+    n = len(diam)
+    uid = bdm.bdm_nccl_unique_id()
+    assert len(uid) == 128
+    h = bdm.bdm_init_dist(torch.arange(n, dtype=torch.int64, device="cuda"), torch.from_numpy(pos).cuda(),
+                          torch.from_numpy(diam).cuda(), rank=0, world=1, uid=uid, device=0)
+    bdm.bdm_mech_step(h, 3)
+    p = gather(bdm, h, bdm.BDM_OWNED_POSITIONS, n)
+    o_p, _ = oracle.run(pos, diam, 3)
+    assert np.array_equal(p, o_p)
+
+
+def test_dist_rejects_bad_input(bdm):
+    pos = np.zeros((3, 3))
+    pos[1, 0] = np.nan
+    with pytest.raises(bdm.BdmError) as e:
+        bdm.bdm_init_dist_local(2, [2, 1], np.arange(3, dtype=np.int64), pos, np.full(3, 10.0))
+    assert e.value.code == bdm.BDM_EINVAL
+
+
+def test_pair_digest_matches_oracle(bdm):
+    """bdm_get_pair_digest (product handle, no BDM_RECORD) equals the oracle's per-agent neighbour /
+    contact counts and order-free hashes (SURVEY §8(c) digest)."""
+    pos, diam = bdm_inputs.make_config(1)
+    h = bdm.bdm_init(pos, diam)
+    o = oracle.step(pos, diam)
+    for kind, kc, kh in ((0, "n_nb", "nb_hash"), (1, "n_ct", "ct_hash")):
+        c, hs = bdm.bdm_get_pair_digest(h, kind)
+        assert np.array_equal(c.astype(np.int64), o[kc].astype(np.int64))
+        assert np.array_equal(hs, o[kh])
