@@ -219,9 +219,7 @@ def run_bdm(args):
 
     world, rank, local = dist_env()
     if world > 1 or args.slabs:
-        from paper_2006_06775_b200 import dist as bdist
-
-        return bdist.bench_multi(args, METRIC, UNIT, config_obj, load_peaks, ClockSampler)
+        return run_dist(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream()
@@ -345,6 +343,191 @@ def run_bdm(args):
             "clocks": clk.summary(), "step_ms": [round(x, 4) for x in step_ms]}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def run_dist(args):
+    """N ranks (one per GPU) of libbdm's distributed runtime (bdm_init_dist): every rank
+    generates its id share, the library redistributes the agents by x-slab (work-balanced cuts) and
+    steps them with NCCL halo exchange + migration.  Timed: K steps after W warm-up steps, barrier +
+    synchronize on both sides, CUDA events on each rank's stream, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2006_06775_b200 as bdm
+    from paper_2006_06775_b200 import dist as bdist
+
+    world, rank, local = dist_env()
+    os.environ.setdefault("NCCL_DEBUG", "INFO")  # (init logging: the rank count of each communicator)
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        if world > 1:
+            dist.init_process_group("nccl", device_id=dev)
+        else:  # (--slabs at N = 1: a 1-rank group for the barriers)
+            dist.init_process_group("gloo", rank=0, world_size=1, init_method="tcp://127.0.0.1:%d" % free_port())
+    stream = torch.cuda.Stream(device=dev)
+    n = config_size(args.config, args.n)
+    big = n > BIG_N
+    # algorithmic work units per agent (candidates, contacts) from one recorded single-GPU step on
+    # rank 0: the whole population when it fits, else a 2e7-agent sub-volume of the same density
+    units = torch.zeros(2, dtype=torch.float64, device=dev)
+    if rank == 0:
+        prm = bdm.bdm_params_default(device=local)
+        prm.flags |= bdm.BDM_RECORD
+        m = SUB_N if big else n
+        sp, sd, _, _ = device_inputs(bdm, torch, args.config, m, dev, torch.cuda.current_stream(),
+                                     scale_from=n if big else None)
+        hr = bdm.bdm_init(sp, sd, prm)
+        bdm.bdm_mech_step(hr, 1)
+        st = bdm.bdm_get_agent_stats(hr)
+        units[0] = float(st["n_cand"].sum().item()) / m
+        units[1] = float(st["n_ct"].sum().item()) / m
+        hr.close()
+        del st, sp, sd
+        torch.cuda.empty_cache()
+    dist.broadcast(units, 0) if world > 1 else None
+    uid = bdist.broadcast_uid(dist, bdm, dev) if world > 1 else bdm.bdm_nccl_unique_id()
+    ids, pos, diam = bdist.rank_inputs(bdm, torch, bdm_inputs, args.config, n, rank, world, dev, stream)
+    t0 = time.perf_counter()
+    h = bdm.bdm_init_dist(ids, pos, diam, bdm.bdm_params_default(), rank=rank, world=world, uid=uid, device=local,
+                          stream=stream)
+    setup_s = time.perf_counter() - t0
+    del ids, pos, diam
+    torch.cuda.empty_cache()
+    bdm.bdm_set_timing(h, True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        bdm.bdm_mech_step(h, args.warmup)
+        bdm.bdm_sync(h)
+        bdm.bdm_get_timing(h)  # reset the sums
+        s0 = bdm.bdm_get_stats(h)
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        prof = os.environ.get("BDM_PROFILE_TIMED") == "1"
+        if prof:
+            torch.cuda.profiler.start()
+        e0.record(stream)
+        bdm.bdm_mech_step(h, args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if prof:
+            torch.cuda.profiler.stop()
+        dist.barrier()
+    tm = bdm.bdm_get_timing(h)
+    s1 = bdm.bdm_get_stats(h)
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = n * args.steps / (ms / 1e3)
+    agg = torch.tensor([s1["launches"] - s0["launches"], s1["host_syncs"] - s0["host_syncs"],
+                        s1["exchange_bytes"] - s0["exchange_bytes"], s1["migrated"] - s0["migrated"]],
+                       dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(agg, op=dist.ReduceOp.SUM)
+    own = s1["n_agents"]
+    cuts = bdm.bdm_get_cuts(h)
+    # end to end through the public API with HOST buffers: per batch every rank uploads its id share
+    # from pinned memory (bdm_init_dist: validation, cuts, redistribution), runs one step and reads its
+    # owned agents' displacements back (bdm_get_local into pinned memory)
+    h.close()
+    torch.cuda.empty_cache()
+    ids_d, pos_d, diam_d = bdist.rank_inputs(bdm, torch, bdm_inputs, args.config, n, rank, world, dev, stream)
+    pin_ids = ids_d.cpu().pin_memory()
+    pin_pos = pos_d.cpu().pin_memory()
+    pin_diam = diam_d.cpu().pin_memory()
+    del ids_d, pos_d, diam_d
+    torch.cuda.empty_cache()
+    e2e_s, h2d, d2h = 0.0, 0, 0
+    uid = bdist.broadcast_uid(dist, bdm, dev) if world > 1 else bdm.bdm_nccl_unique_id()
+    he = bdm.bdm_init_dist(pin_ids.numpy(), pin_pos.numpy(), pin_diam.numpy(), bdm.bdm_params_default(), rank=rank,
+                           world=world, uid=uid, device=local, stream=stream)
+    for rep in range(args.e2e_steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize(dev)
+        w0 = time.perf_counter()
+        if rep > 0:
+            bdm.bdm_set_agents_dist(he, pin_ids.numpy(), pin_pos.numpy(), pin_diam.numpy())
+        bdm.bdm_mech_step(he, 1)
+        ids_o, dp_o = bdm.bdm_get_local(he, bdm.BDM_LAST_DISPLACEMENTS)
+        wall = time.perf_counter() - w0
+        if rep > 0:  # (the first batch, loaded by bdm_init_dist, is a warm-up)
+            e2e_s += wall
+            h2d += pin_ids.numel() * 8 + pin_pos.numel() * 8 + pin_diam.numel() * 8
+            d2h += ids_o.size * 8 + dp_o.size * 8
+    he.close()
+    et = torch.tensor([e2e_s, h2d, d2h], dtype=torch.float64, device=dev)
+    mx = et.clone()
+    if world > 1:
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(et, op=dist.ReduceOp.SUM)
+    steps_e2e = max(args.e2e_steps, 1)
+    e2e = {"value": n * steps_e2e / float(mx[0].item()), "unit": UNIT,
+           "h2d_bytes_per_step": int(et[1].item() / steps_e2e), "d2h_bytes_per_step": int(et[2].item() / steps_e2e),
+           "steps": steps_e2e,
+           "path": "per rank: host id share (pinned) -> bdm_set_agents_dist (validation, cuts, redistribution) "
+                   "-> bdm_mech_step(1) -> bdm_get_local(displacements, host); wall clock, max over ranks"}
+    if rank == 0:
+        peaks, peak_kind = load_peaks()
+        sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+        fp64_peak = 148 * 64 * sm_max * 1e6
+        ops = (FP64_PER_CANDIDATE * units[0].item() + FP64_PER_CONTACT * units[1].item() + FP64_PER_AGENT) * own
+        steps_t = max(tm["steps"], 1)
+        force_s = tm["force_ms"] / 1e3 / steps_t
+        achieved = ops / force_s if force_s > 0 else 0.0
+        traffic = None
+        tf = os.path.join(ROOT, "profiles", "r02_force_traffic.json")
+        if not os.path.exists(tf):
+            tf = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
+        if args.config == 3 and os.path.exists(tf):
+            with open(tf) as f:
+                tr = json.load(f)
+            traffic = int((tr["dram_bytes_read"] + tr["dram_bytes_write"]) * own / tr.get("n_agents", 20_000_000))
+        cpu = None
+        if not args.no_cpu_baseline:
+            if big:
+                ps, ds = sub_volume(args.config, n)
+                what = f"a {SUB_N}-agent sub-volume of the workload at the same density"
+            else:
+                ps, ds = bdm_inputs.make_config(args.config, n if n != bdm_inputs.CFG_N[args.config] else None)
+                what = f"the whole {n}-agent workload"
+            cpu = cpu_baseline(ps, ds, what, args.cpu_stride_1t)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": dict(config_obj(args, n, world), cuts=[int(c) for c in cuts[1:-1]]),
+                "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
+                             "frac": achieved / fp64_peak, "traffic": traffic,
+                             "traffic_source": (os.path.relpath(tf, ROOT) + " scaled to rank 0's owned agents")
+                             if traffic else None,
+                             "kernel": "rank 0 force phase: k_half_search + k_half_sum",
+                             "ms_per_launch": force_s * 1e3,
+                             "passes_ms": {"search": tm["search_ms"] / steps_t, "sum": tm["sum_ms"] / steps_t},
+                             "note": "rank 0's owned agents x the per-agent fp64-pipe ops of the recorded step "
+                                     "(9 per candidate + 44 per contact + 40 per agent, DESIGN.md §6.2) over its "
+                                     "force-phase event time; peak = 148 SM x 64 fp64 lanes x sm_max_mhz"},
+                "dist": {"host_syncs": int(agg[1].item()), "launches": int(agg[0].item()),
+                         "exchange_bytes": int(agg[2].item()), "migrated": int(agg[3].item()),
+                         "setup_s": setup_s, "rank0_agents": own,
+                         "note": "libbdm distributed runtime: NCCL send/recv of fixed-capacity messages, "
+                                 "device-resident counts, one host round trip per chunk of <= 16 steps"},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(agg[0].item()),
+                "clocks": clk.summary(), "timing": "CUDA events on each rank's stream, max over ranks"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
 
 
 BIG_N = 50_000_000  # above this: device generation, statistics and CPU baseline on a sub-volume
@@ -492,6 +675,11 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    world, _, _ = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:  # not under torchrun: launch the N ranks ourselves
+        from paper_2006_06775_b200 import dist as bdist
+
+        return bdist.relaunch(os.path.abspath(__file__), sys.argv[1:], args.gpus)
     return run_bdm(args)
 
 

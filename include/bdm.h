@@ -362,6 +362,11 @@ int bdm_nccl_unique_id(void* out128);
 int bdm_init_dist(bdm_handle* h, int64_t n_local, const int64_t* ids, const double* pos, const double* diam,
                   const bdm_params* p, int rank, int world, const void* nccl_uid, int device, void* cuda_stream);
 
+/* A new batch for a distributed handle (collective, same rules as bdm_init_dist): the agents are
+ * validated, the cuts recomputed and every agent sent to its owner; the communicator and the device
+ * buffers are reused (bdm_set_agents for distributed handles). */
+int bdm_set_agents_dist(bdm_handle h, int64_t n_local, const int64_t* ids, const double* pos, const double* diam);
+
 /* Virtual ranks (tests of the data plane on one GPU): all `world` ranks live in this process on
  * p->device over a 1-rank NCCL communicator (every message a self send/recv); counts[r] agents
  * start on rank r, the arrays hold them concatenated in rank order.  Same protocol and kernels as

@@ -133,6 +133,7 @@ _SIGS = {
     "bdm_init_dist_local": ([ctypes.POINTER(_vp), ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.POINTER(bdm_params), _vp],
                             ctypes.c_int),
     "bdm_get_local": ([_vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int64), _vp, _vp], ctypes.c_int),
+    "bdm_set_agents_dist": ([_vp, ctypes.c_int64, _vp, _vp, _vp], ctypes.c_int),
     "bdm_get_cuts": ([_vp, _vp, ctypes.c_int32], ctypes.c_int),
     "bdm_get_pair_digest": ([_vp, ctypes.c_int, _vp, _vp], ctypes.c_int),
     "bdm_get_stats": ([_vp, ctypes.POINTER(bdm_stats)], ctypes.c_int),
@@ -620,6 +621,22 @@ def bdm_init_dist_local(world: int, counts, ids, pos, diam, params: bdm_params |
     h.world = world
     bdm_get_count(h)
     return h
+
+
+def bdm_set_agents_dist(h: Handle, ids, pos, diam) -> None:
+    """Collective: a new batch for a distributed handle (redistributed; communicator and buffers reused)."""
+    p = bdm_params()
+    if h.device_ptrs:
+        p.flags |= BDM_DEVICE_PTRS
+    ids, pos, diam, dev = _dist_arrays(ids, pos, diam, p)
+    if dev != h.device_ptrs:
+        raise ValueError("host / device arrays must match the handle's mode")
+    if dev:
+        import torch
+
+        torch.cuda.synchronize()
+    _check(load_library().bdm_set_agents_dist(h.raw, len(diam), _ptr(ids), _ptr(pos), _ptr(diam)), h.raw)
+    bdm_get_count(h)
 
 
 def bdm_get_local(h: Handle, what: int = BDM_OWNED_POSITIONS):

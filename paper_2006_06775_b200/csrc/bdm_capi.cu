@@ -175,6 +175,7 @@ namespace {
 void dist_destroy(DistGroup* G);
 int dist_mech_step(bdm_ctx* H, int32_t n_steps);
 void dist_set_timing(DistGroup* G, bool on);
+int dist_sync(bdm_ctx* H);
 int dist_get_timing(bdm_ctx* H, double* out6);
 
 int fail(bdm_ctx* h, int code, const char* fmt, ...) {
@@ -1169,6 +1170,7 @@ int bdm_set_stream(bdm_handle h, void* stream) {
 int bdm_sync(bdm_handle h) {
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_sync: NULL handle");
   CU(h, cudaSetDevice(h->device));
+  if (h->dist) return dist_sync(h);
   return check_async(h);
 }
 

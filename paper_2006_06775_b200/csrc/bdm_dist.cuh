@@ -484,9 +484,11 @@ int dist_allreduce(bdm_ctx* H, DistGroup* G, std::vector<std::vector<double>>& p
   return BDM_OK;
 }
 
-// Count-balanced (weights null) or weighted cuts on integer box-x from per-layer values over
-// [x0, x0 + nx): every slab at least one box wide, inner slabs at least 2 when the population spans
-// >= 2 * world layers (same rule as dist.choose_bounds).
+// Balanced cuts on integer box-x from per-layer values w over [x0, x0 + nx) (counts, or the work
+// model): cut g is the first layer after the g/world quantile of w.  Every inner slab is at least 2
+// boxes wide -- the protocol relies on it: an emigrant moves less than one box, so it always lands in
+// the neighbour's boundary layer, which no third rank holds as a ghost layer.  When the population
+// spans fewer than 2 * world layers, the last ranks get empty 2-box slabs beyond it.
 std::vector<int32_t> choose_cuts(const std::vector<double>& w, int32_t x0, int world) {
   const int64_t nx = (int64_t)w.size();
   std::vector<int32_t> b{INT32_MIN};
@@ -495,14 +497,14 @@ std::vector<int32_t> choose_cuts(const std::vector<double>& w, int32_t x0, int w
     double t = 0.0;
     for (int64_t k = 0; k < nx; ++k) cum[k] = (t += w[k]);
     const double total = nx ? cum[nx - 1] : 0.0;
-    const int64_t wmin = nx >= 2 * world ? 2 : 1;
     int64_t prev = x0;
     for (int g = 1; g < world; ++g) {
       const double target = total * g / world;
       const int64_t k = (int64_t)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin()) + 1;
-      int64_t cut = x0 + k;
-      cut = std::max<int64_t>(cut, prev + (g == 1 ? 1 : wmin));
-      if (nx >= world) cut = std::min<int64_t>(cut, x0 + nx - 1 - (int64_t)(world - 1 - g) * wmin);
+      const int64_t lo = prev + (g == 1 ? 1 : 2);
+      int64_t cut = std::max<int64_t>(x0 + k, lo);
+      const int64_t hi = x0 + nx - 1 - (int64_t)(world - 1 - g) * 2;  // room for the later slabs
+      if (hi >= lo) cut = std::min<int64_t>(cut, hi);
       b.push_back((int32_t)cut);
       prev = cut;
     }
@@ -734,11 +736,14 @@ int dist_split_all(bdm_ctx* H, DistGroup* G) {
   for (auto& D : G->sl) {
     bdm_ctx* h = D.h;
     k_dist_prep<<<1, 32, 0, st>>>(h->grid, D.stepped ? 1 : 0, D.xb, D.xe, D.dc, h->cnt + 4);
+    DBG(h, "k_dist_prep");
     CU(H, cudaMemsetAsync(h->cnt, 0, 4 * sizeof(uint32_t), st));
     k_slab_split<<<h->sm_count * 4, 256, 0, st>>>(h->ag[h->cur], h->id[h->cur], (uint32_t)D.room, h->cnt + 4,
                                                    h->grid.inv, D.xb, D.xe, D.msg[0] + HDR, D.msg[1] + HDR,
                                                    (uint64_t)G->cap, h->cnt, D.dc + DC_LIVE);
+    DBG(h, "k_slab_split");
     k_dist_header<<<1, 32, 0, st>>>(h->cnt, (uint64_t)G->cap, D.msg[0], D.msg[1], D.dc);
+    DBG(h, "k_dist_header");
     CU(H, cudaGetLastError());
     h->launches += 3;
   }
@@ -760,7 +765,11 @@ int dist_split_all(bdm_ctx* H, DistGroup* G) {
       msgs.push_back(Msg{r, to, a ? a->msg[side] : nullptr, b ? b->msg[side == 0 ? 3 : 2] : nullptr, cnt});
     }
   }
-  return dist_p2p(H, G, msgs);
+  static const int dsync = std::getenv("BDM_DIST_SYNC") ? std::atoi(std::getenv("BDM_DIST_SYNC")) : 0;
+  if (dsync & 2) CU(H, cudaStreamSynchronize(G->stream));
+  int rc = dist_p2p(H, G, msgs);
+  if (!rc && (dsync & 1)) CU(H, cudaStreamSynchronize(G->stream));
+  return rc;
 }
 
 int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp) {
@@ -770,10 +779,12 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   // emigrants of the split are marked dead in place (the sort drops them)
   k_slab_mark_dead<<<h->sm_count * 4, 256, 0, st>>>(h->ag[h->cur], room, h->cnt + 4, h->grid.inv, D.xb, D.xe,
                                                     D.dc + DC_LIVE);
+  DBG(h, "k_slab_mark_dead");
   const bool fused = h->cols_next;
   k_dist_ingest<<<h->sm_count * 2, 256, 0, st>>>(h->ag[h->cur], h->id[h->cur], D.dc, h->cnt, D.msg[0], D.msg[1],
                                                  D.msg[2], D.msg[3], (uint32_t)G->cap, D.rank > 0,
                                                  D.rank + 1 < G->world, room, fused ? 1 : 0);
+  DBG(h, "k_dist_ingest");
   CU(H, cudaGetLastError());
   h->launches += 2;
   TimedStep ts{};
@@ -820,19 +831,25 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     g.table = h->table;
     g.col = h->colrec;
     k_col_ext<<<blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->czlo, h->czhi, D.dc + DC_CE0);
+    DBG(h, "k_col_ext(dist)");
     const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
     k_col_len<<<gs, 256, 0, st>>>(h->czlo, h->czhi, g.n_cols, h->coff);
+    DBG(h, "k_col_len(dist)");
     rc = scan(h, h->coff, nc + 1, nullptr);
     if (rc) return fail(H, rc, "%s", h->error.c_str());
     k_table_zero<<<h->sm_count * 8, 256, 0, st>>>(h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec);
+    DBG(h, "k_table_zero(dist)");
     k_key_hist<true><<<blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
                                                         D.dc + DC_TOT);
+    DBG(h, "k_key_hist(dist)");
     rc = scan(h, h->table, 0, h->coff + nc);
     if (rc) return fail(H, rc, "%s", h->error.c_str());
     k_scatter<<<blocks(room, 256 * KSC), 256, 0, st>>>(h->key, h->slot, h->id[src0], h->table, room, h->tsrc, h->tid,
                                                        h->tkey, D.dc + DC_TOT);
+    DBG(h, "k_scatter(dist)");
     k_place<<<blocks(room, 256), 256, 0, st>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src0], room, h->ag[1 - src0],
                                               h->id[1 - src0], h->agf, nullptr, nullptr, D.dc + DC_SORTED);
+    DBG(h, "k_place(dist)");
     CU(H, cudaGetLastError());
     h->launches += 7;
     h->cur = 1 - src0;
@@ -860,6 +877,7 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   const unsigned ga = (unsigned)h->sm_count * h->half_a_blocks_per_sm;
   k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, st>>>(h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt, h->h_bwd,
                                                        h->h_bcnt, h->ext, false, D.dc + DC_AEND);
+  DBG(h, "k_half_search(dist)");
   if (h->timing && !h->timed.empty() && !h->timed.back().e3) {
     CU(H, cudaEventCreate(&h->timed.back().e3));
     CU(H, cudaEventRecord(h->timed.back().e3, st));
@@ -871,9 +889,11 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
                                                               h->id[dst], dp, dpi, h->ext, h->err, h->h_fwd, h->h_fcnt,
                                                               h->h_bwd, h->h_bcnt, cn, nullptr, h->h_slow,
                                                               D.dc + DC_ABEGIN);
+  DBG(h, "k_half_sum(dist)");
   k_half_slow<false><<<(unsigned)h->sm_count * 4, 128, 0, st>>>(h->ag[src], h->id[src], 0u, g, pd, h->ag[dst],
                                                                h->id[dst], dp, dpi, h->ext, h->err, cn, nullptr,
                                                                h->h_slow, D.dc + DC_ABEGIN);
+  DBG(h, "k_half_slow(dist)");
   k_locate_nonfinite<<<1, 32, 0, st>>>(h->ag[src], h->id[src], g, pd, h->err);
   CU(H, cudaGetLastError());
   h->launches += 7;
@@ -999,6 +1019,23 @@ int dist_chunk_end(bdm_ctx* H, DistGroup* G, int* redo) {
   }
   CU(H, cudaStreamSynchronize(G->stream));
   ++G->syncs;
+  double mx[SUMN];
+  for (int k = 0; k < SUMN; ++k) {
+    mx[k] = G->sl[0].sum_host[k];
+    for (size_t s = 1; s < G->sl.size(); ++s) mx[k] = std::max(mx[k], G->sl[s].sum_host[k]);
+  }
+  *redo = mx[0] != 0.0;
+  const double need = mx[1];
+  if (*redo) {  // results of this chunk are void: clear its error state, grow the messages, re-run it
+    ErrDev e0{0u, 0xffffffffu, ERR_NONE};
+    for (auto& D : G->sl) {
+      CU(H, cudaMemcpyAsync(D.h->err, &e0, sizeof e0, cudaMemcpyHostToDevice, G->stream));
+      k_ext_reset<<<1, 32, 0, G->stream>>>(D.h->ext, 0);
+    }
+    G->cap = std::max<int64_t>(G->cap * 2, (int64_t)(need * 1.5) + 4096);
+    ++G->redo;
+    return BDM_OK;
+  }
   for (auto& D : G->sl) {
     bdm_ctx* h = D.h;
     if (h->err_host->code) {  // asynchronous data errors (non-finite force, agent outside the frame)
@@ -1007,21 +1044,9 @@ int dist_chunk_end(bdm_ctx* H, DistGroup* G, int* redo) {
       return fail(H, rc ? rc : BDM_ECUDA, "rank %d: %s", D.rank, h->error.c_str());
     }
   }
-  double mx[SUMN];
-  for (int k = 0; k < SUMN; ++k) {
-    mx[k] = G->sl[0].sum_host[k];
-    for (size_t s = 1; s < G->sl.size(); ++s) mx[k] = std::max(mx[k], G->sl[s].sum_host[k]);
-  }
-  *redo = mx[0] != 0.0;
-  const double need = mx[1];
-  if (mx[2] != 0.0 && !*redo) {
+  if (mx[2] != 0.0) {
     H->poisoned = true;
     return fail(H, BDM_ERANGE, "an agent left the grid frame of a chunk (|p*inv| >= 2^20 or a non-finite position)");
-  }
-  if (*redo) {
-    G->cap = std::max<int64_t>(G->cap * 2, (int64_t)(need * 1.5) + 4096);
-    ++G->redo;
-    return BDM_OK;
   }
   for (int a = 0; a < 3; ++a) {
     G->glo[a] = (int32_t)(-mx[3 + a]);
@@ -1061,7 +1086,14 @@ int dist_restore(bdm_ctx* H, DistGroup* G) {
   return BDM_OK;
 }
 
+int dist_mech_step_(bdm_ctx* H, int32_t n_steps);
 int dist_mech_step(bdm_ctx* H, int32_t n_steps) {
+  const int rc = dist_mech_step_(H, n_steps);
+  if (rc && H->error.empty()) H->error = g_tls_error;  // (a slab's failure message)
+  return rc;
+}
+
+int dist_mech_step_(bdm_ctx* H, int32_t n_steps) {
   DistGroup* G = H->dist;
   int done = 0;
   while (done < n_steps) {
@@ -1086,6 +1118,17 @@ int dist_mech_step(bdm_ctx* H, int32_t n_steps) {
   }
   H->n = 0;
   for (auto& D : G->sl) H->n += D.live;
+  return BDM_OK;
+}
+
+int dist_sync(bdm_ctx* H) {
+  DistGroup* G = H->dist;
+  CU(H, cudaStreamSynchronize(G->stream));
+  ++G->syncs;
+  for (auto& D : G->sl) {
+    int rc = check_async(D.h);
+    if (rc) return fail(H, rc, "rank %d: %s", D.rank, D.h->error.c_str());
+  }
   return BDM_OK;
 }
 
@@ -1167,6 +1210,9 @@ int dist_setup(bdm_ctx* H, DistGroup* G, std::vector<double*>& recs, std::vector
   G->L = std::max(r[0], H->prm.box_edge_min);
   if (!(G->L > 0.0)) G->L = 1.0;  // (no agents anywhere)
   G->inv = 1.0 / (G->L * (1.0 + 0x1p-30));
+  if (!(H->prm.max_disp < G->L * (1.0 - 0x1p-20)))  // |dp| <= max_disp (1 + 4u) < L: boundary-layer exchange
+    return fail(H, BDM_EINVAL, "distributed steps need max_disp (%g) < the box edge L (%g): a step must move an agent "
+                "by less than one box (DESIGN.md §7)", H->prm.max_disp, G->L);
   // O2 extents
   for (int s = 0; s < S; ++s) {
     k_ext_reset<<<1, 32, 0, G->stream>>>(ext, 0);
@@ -1283,8 +1329,73 @@ __global__ void k_local_out(const double4* __restrict__ ag, const double* __rest
   }
 }
 
-// Group handle shared by bdm_init_dist and bdm_init_dist_local: validates and stages the inputs,
-// creates the communicator, runs the set-up.
+// Validates and stages a batch of agents (counts[s] for local slot s, concatenated), then runs the
+// set-up (box edge, extents, cuts, redistribution) over the group's communicator.
+int dist_load(bdm_ctx* H, const std::vector<int64_t>& counts, const int64_t* ids, const double* pos,
+              const double* diam) {
+  DistGroup* G = H->dist;
+  const bool dev = H->prm.flags & BDM_DEVICE_PTRS;
+  const size_t S = G->sl.size();
+  std::vector<double*> recs(S, nullptr);
+  std::vector<int64_t> n(counts);
+  struct Free {
+    std::vector<double*>& r;
+    ~Free() {
+      for (double* q : r)
+        if (q) cudaFree(q);
+    }
+  } free_recs{recs};
+  ErrDev* err = nullptr;
+  unsigned long long* mb = nullptr;
+  if (cudaMalloc(&err, sizeof(ErrDev)) != cudaSuccess || cudaMalloc(&mb, sizeof(unsigned long long)) != cudaSuccess)
+    return fail(H, BDM_ENOMEM, "distributed load: device allocation");
+  Scratch sce, scm;
+  sce.p = err;
+  scm.p = mb;
+  ErrDev e0{0u, 0xffffffffu, ERR_NONE};
+  int64_t off = 0;
+  for (size_t s = 0; s < S; ++s) {
+    const int64_t m = n[s];
+    CU(H, cudaMalloc(&recs[s], std::max<int64_t>(m, 1) * REC * sizeof(double)));
+    if (m) {
+      const double *dpos = pos + 3 * off, *ddiam = diam + off;
+      const int64_t* dids = ids + off;
+      Scratch stage;
+      if (!dev) {  // host inputs: staged
+        const size_t bytes = (size_t)m * (4 * sizeof(double) + sizeof(int64_t));
+        CU(H, cudaMalloc(&stage.p, bytes));
+        double* sp = static_cast<double*>(stage.p);
+        CU(H, cudaMemcpyAsync(sp, dpos, 3 * m * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+        CU(H, cudaMemcpyAsync(sp + 3 * m, ddiam, m * sizeof(double), cudaMemcpyHostToDevice, G->stream));
+        CU(H, cudaMemcpyAsync(sp + 4 * m, dids, m * sizeof(int64_t), cudaMemcpyHostToDevice, G->stream));
+        dpos = sp;
+        ddiam = sp + 3 * m;
+        dids = reinterpret_cast<const int64_t*>(sp + 4 * m);
+      }
+      CU(H, cudaMemcpyAsync(err, &e0, sizeof e0, cudaMemcpyHostToDevice, G->stream));
+      k_dist_pack_in<<<blocks(m, 256), 256, 0, G->stream>>>(dpos, ddiam, dids, (uint32_t)m, recs[s], mb, err);
+      CU(H, cudaGetLastError());
+      ErrDev he;
+      CU(H, cudaMemcpyAsync(&he, err, sizeof he, cudaMemcpyDeviceToHost, G->stream));
+      CU(H, cudaStreamSynchronize(G->stream));
+      ++G->syncs;
+      if (he.code)
+        return fail(H, BDM_EINVAL, "distributed load: invalid agent %llu of rank %d (D > 0 and finite, finite "
+                    "positions, 0 <= id < 2^32 - 1)", (unsigned long long)(he.bad >> 32), G->sl[s].rank);
+    }
+    off += m;
+  }
+  int rc = dist_setup(H, G, recs, n);
+  if (rc) return rc;
+  H->n = 0;
+  for (auto& D : G->sl) H->n += D.live;
+  H->have_grid = true;
+  H->poisoned = false;
+  return BDM_OK;
+}
+
+// Group handle shared by bdm_init_dist and bdm_init_dist_local: creates the communicator, then loads
+// the first batch.
 int dist_create(bdm_handle* out, int world, const std::vector<int>& ranks, const std::vector<int64_t>& counts,
                 const int64_t* ids, const double* pos, const double* diam, const bdm_params* p, const void* uid,
                 bool virt, int device, void* stream) {
@@ -1328,65 +1439,8 @@ int dist_create(bdm_handle* out, int world, const std::vector<int>& ranks, const
     D.rank = r;
     G->sl.push_back(D);
   }
-  // inputs -> validated records per local slot
-  const bool dev = p->flags & BDM_DEVICE_PTRS;
-  std::vector<double*> recs(ranks.size(), nullptr);
-  std::vector<int64_t> n(counts);
-  ErrDev* err = nullptr;
-  unsigned long long* mb = nullptr;
-  if (cudaMalloc(&err, sizeof(ErrDev)) != cudaSuccess || cudaMalloc(&mb, sizeof(unsigned long long)) != cudaSuccess)
-    return bail(fail(H, BDM_ENOMEM, "bdm_init_dist: device allocation"));
-  Scratch sce, scm;
-  sce.p = err;
-  scm.p = mb;
-  ErrDev e0{0u, 0xffffffffu, ERR_NONE};
-  int64_t off = 0;
-  for (size_t s = 0; s < ranks.size(); ++s) {
-    const int64_t m = n[s];
-    if (cudaMalloc(&recs[s], std::max<int64_t>(m, 1) * REC * sizeof(double)) != cudaSuccess) {
-      for (double* q : recs) if (q) cudaFree(q);
-      return bail(fail(H, BDM_ENOMEM, "bdm_init_dist: %lld input records", (long long)m));
-    }
-    if (m) {
-      const double *dpos = pos + 3 * off, *ddiam = diam + off;
-      const int64_t* dids = ids + off;
-      Scratch stage;
-      if (!dev) {  // host inputs: staged
-        const size_t bytes = (size_t)m * (4 * sizeof(double) + sizeof(int64_t));
-        if (cudaMalloc(&stage.p, bytes) != cudaSuccess) return bail(fail(H, BDM_ENOMEM, "bdm_init_dist: staging"));
-        double* sp = static_cast<double*>(stage.p);
-        cudaMemcpyAsync(sp, dpos, 3 * m * sizeof(double), cudaMemcpyHostToDevice, G->stream);
-        cudaMemcpyAsync(sp + 3 * m, ddiam, m * sizeof(double), cudaMemcpyHostToDevice, G->stream);
-        cudaMemcpyAsync(sp + 4 * m, dids, m * sizeof(int64_t), cudaMemcpyHostToDevice, G->stream);
-        dpos = sp;
-        ddiam = sp + 3 * m;
-        dids = reinterpret_cast<const int64_t*>(sp + 4 * m);
-      }
-      cudaMemcpyAsync(err, &e0, sizeof e0, cudaMemcpyHostToDevice, G->stream);
-      k_dist_pack_in<<<blocks(m, 256), 256, 0, G->stream>>>(dpos, ddiam, dids, (uint32_t)m, recs[s], mb, err);
-      ErrDev he;
-      cudaMemcpyAsync(&he, err, sizeof he, cudaMemcpyDeviceToHost, G->stream);
-      if (cudaStreamSynchronize(G->stream) != cudaSuccess) {
-        (void)cudaGetLastError();
-        for (double* q : recs) if (q) cudaFree(q);
-        return bail(fail(H, BDM_ECUDA, "bdm_init_dist: input staging"));
-      }
-      ++G->syncs;
-      if (he.code) {
-        for (double* q : recs) if (q) cudaFree(q);
-        return bail(fail(H, BDM_EINVAL, "bdm_init_dist: invalid agent %llu of rank %d (D > 0 and finite, finite "
-                         "positions, 0 <= id < 2^32 - 1)", (unsigned long long)(he.bad >> 32), ranks[s]));
-      }
-    }
-    off += m;
-  }
-  int rc = dist_setup(H, G, recs, n);
-  for (double* q : recs)
-    if (q) cudaFree(q);
+  int rc = dist_load(H, counts, ids, pos, diam);
   if (rc) return bail(rc);
-  H->n = 0;
-  for (auto& D : G->sl) H->n += D.live;
-  H->have_grid = true;
   *out = H;
   return BDM_OK;
 }
@@ -1441,6 +1495,15 @@ int bdm_init_dist_local(bdm_handle* h, int world, const int64_t* counts, const i
     return fail(nullptr, BDM_ECUDA, "bdm_init_dist_local: no CUDA device");
   }
   return dist_create(h, world, ranks, cnt, ids, pos, diam, p, nullptr, true, dev, cuda_stream);
+}
+
+int bdm_set_agents_dist(bdm_handle h, int64_t n_local, const int64_t* ids, const double* pos, const double* diam) {
+  if (!h || !h->dist) return fail(h, BDM_EINVAL, "bdm_set_agents_dist: needs a distributed handle");
+  if (h->dist->sl.size() != 1) return fail(h, BDM_EINVAL, "bdm_set_agents_dist: one local rank per handle");
+  if (n_local < 0 || n_local >= (int64_t)0xffffffffll || (n_local > 0 && (!ids || !pos || !diam)))
+    return fail(h, BDM_EINVAL, "bdm_set_agents_dist: need 0 <= n_local < 2^32 - 1 and non-NULL arrays");
+  CU(h, cudaSetDevice(h->dist->device));
+  return dist_load(h, {n_local}, ids, pos, diam);
 }
 
 int bdm_get_local(bdm_handle h, int what, int64_t* n, int64_t* ids, double* vals) {

@@ -327,7 +327,9 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
     if (valid && pa[u].w >= 0.0) {  // (slab mode: emigrants are marked dead by D < 0 until the sort)
       const int bx = (int)floor(pa[u].x * g.inv), by = (int)floor(pa[u].y * g.inv);
       bz = (int)floor(pa[u].z * g.inv);
-      c = col_of(g, bx, by);
+      // distributed steps (rng): the frame is fixed for a chunk; an agent outside it is left to the
+      // guarded key pass (which reports it) instead of indexing outside the column arrays
+      if (!rng || (bx >= g.lo[0] && bx <= g.hi[0] && by >= g.lo[1] && by <= g.hi[1])) c = col_of(g, bx, by);
     }
     // warp-aggregated: agents arrive mostly in box order, so a warp touches few columns; each group
     // of lanes with the same column reduces with redux.sync over its own member mask

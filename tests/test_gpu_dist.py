@@ -36,6 +36,7 @@ def split_counts(n, G, rng):
 
 def gather(bdm, h, what, n):
     ids, vals = bdm.bdm_get_local(h, what)
+    ids, vals = to_np(ids), to_np(vals)
     out = np.full((n, 3), np.nan)
     seen = np.zeros(n, int)
     np.add.at(seen, ids, 1)
@@ -158,3 +159,13 @@ def test_pair_digest_matches_oracle(bdm):
         c, hs = bdm.bdm_get_pair_digest(h, kind)
         assert np.array_equal(c.astype(np.int64), o[kc].astype(np.int64))
         assert np.array_equal(hs, o[kh])
+
+
+def test_dist_requires_small_moves(bdm):
+    """The boundary-layer exchange needs |dp| < L (max_disp < box edge): rejected otherwise."""
+    rng = np.random.default_rng(8)
+    pos = rng.uniform(0.0, 100.0, (500, 3))
+    diam = rng.uniform(1.0, 2.0, 500)  # L = 2 < max_disp = 3
+    with pytest.raises(bdm.BdmError) as e:
+        bdm.bdm_init_dist_local(2, [250, 250], np.arange(500, dtype=np.int64), pos, diam)
+    assert e.value.code == bdm.BDM_EINVAL and "max_disp" in str(e.value)

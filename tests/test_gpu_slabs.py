@@ -18,7 +18,7 @@ def mods():
 
     assert torch.cuda.is_available()
     import paper_2006_06775_b200 as bdm
-    from paper_2006_06775_b200 import dist as bdist
+    import slab_protocol as bdist
 
     return torch, bdm, bdist
 

@@ -15,7 +15,7 @@ import torch.multiprocessing as mp
 
 import bdm_inputs
 import oracle
-from paper_2006_06775_b200 import dist as bdist
+import slab_protocol as bdist
 from slab_cpu_engine import CpuSlabEngine
 
 

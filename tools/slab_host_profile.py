@@ -15,7 +15,8 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import bdm_inputs  # noqa: E402
-from paper_2006_06775_b200 import dist as bdist  # noqa: E402
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+import slab_protocol as bdist  # noqa: E402
 
 local = int(os.environ.get("LOCAL_RANK", "0"))
 torch.cuda.set_device(local)
