@@ -31,6 +31,9 @@ const bool g_debug = std::getenv("BDM_DEBUG") != nullptr;  // sync + check after
 // (default 0: with the current kernels the wider frames of deferred builds cost more than the round
 // trip they save; bdm_set_defer sets it per handle)
 const int g_defer = std::getenv("BDM_DEFER") ? std::atoi(std::getenv("BDM_DEFER")) : 0;
+// BDM_HTILE=1: pass A with the TMA-staged neighbourhood (k_half_search_tile, warp-specialised producer);
+// measured slower than k_half_search on cfg3, so off by default
+const bool g_htile = std::getenv("BDM_HTILE") && std::getenv("BDM_HTILE")[0] == '1';
 // BDM_PBOX=0: the key pass re-reads the state instead of the sum pass's packed boxes
 const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
 
@@ -160,7 +163,7 @@ struct bdm_ctx {
   int64_t fused_n0 = 0;        // slab: agents whose next columns the last step accumulated (ag[cur][0..fused_n0))
   uint32_t last_n_lo = 0;      // slab: lower ghosts of the last step (sorted first)
   int32_t split_xb = 0, split_xe = 0;
-  int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0;
+  int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0, tile_blocks_per_sm = 0;
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build (since bdm_get_timing)
   int64_t launches_total = 0;  // launches before the last bdm_get_timing reset
   int64_t host_syncs = 0;      // host synchronisations with the device (bdm_get_stats)
@@ -339,6 +342,12 @@ void init_device_info(bdm_ctx* h) {
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_search, HA_THREADS, HA_SMEM_BYTES);
   h->half_a_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  cudaFuncSetAttribute(k_half_search_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TILE_SMEM_BYTES);
+  cudaFuncSetAttribute(k_half_search_tile, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_search_tile, TILE_THREADS, TILE_SMEM_BYTES);
+  h->tile_blocks_per_sm = per_sm > 0 ? per_sm : 1;
+  (void)cudaGetLastError();
   per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_half_sum<false>, FORCE_THREADS, HB_SMEM_BYTES);
   h->half_b_blocks_per_sm = per_sm > 0 ? per_sm : 1;
@@ -422,10 +431,18 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     }
   }
   CU(h, cudaMemsetAsync(h->h_bcnt, 0, (size_t)std::max<uint32_t>(n_all, 1) * sizeof(uint32_t), s));
-  const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
-                                                   std::max<uint64_t>(1, (a_end - s_begin + HA_THREADS - 1) / HA_THREADS));
-  k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, s>>>(h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
-                                                       h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr);
+  if (g_htile) {  // staged neighbourhood
+    const unsigned gt = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->tile_blocks_per_sm,
+                                                     std::max<uint64_t>(1, (a_end - s_begin + TILE_AG - 1) / TILE_AG));
+    k_half_search_tile<<<gt, TILE_THREADS, TILE_SMEM_BYTES, s>>>(h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
+                                                             h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext,
+                                                             hist_out != nullptr);
+  } else {
+    const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
+                                                     std::max<uint64_t>(1, (a_end - s_begin + HA_THREADS - 1) / HA_THREADS));
+    k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, s>>>(h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
+                                                         h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr);
+  }
   DBG(h, "k_half_search");
   const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
                                                    std::max<uint64_t>(1, (a_end - a_begin + FORCE_THREADS - 1) / FORCE_THREADS));

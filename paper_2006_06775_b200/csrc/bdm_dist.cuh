@@ -874,9 +874,15 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   }
   k_ext_reset<<<1, 32, 0, st>>>(h->ext, 1);
   CU(H, cudaMemsetAsync(h->h_bcnt, 0, (size_t)room * sizeof(uint32_t), st));
-  const unsigned ga = (unsigned)h->sm_count * h->half_a_blocks_per_sm;
-  k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, st>>>(h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt, h->h_bwd,
-                                                       h->h_bcnt, h->ext, false, D.dc + DC_AEND);
+  if (g_htile) {
+    const unsigned gt = (unsigned)h->sm_count * h->tile_blocks_per_sm;
+    k_half_search_tile<<<gt, TILE_THREADS, TILE_SMEM_BYTES, st>>>(h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt,
+                                                              h->h_bwd, h->h_bcnt, h->ext, false, D.dc + DC_AEND);
+  } else {
+    const unsigned ga = (unsigned)h->sm_count * h->half_a_blocks_per_sm;
+    k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, st>>>(h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt,
+                                                         h->h_bwd, h->h_bcnt, h->ext, false, D.dc + DC_AEND);
+  }
   DBG(h, "k_half_search(dist)");
   if (h->timing && !h->timed.empty() && !h->timed.back().e3) {
     CU(H, cudaEventCreate(&h->timed.back().e3));

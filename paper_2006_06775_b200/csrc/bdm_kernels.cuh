@@ -1726,6 +1726,438 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   }
 }
 
+// ---- Pass A with the neighbourhood staged in shared memory (north_star: "a force kernel that stages
+// each 3x3x3 neighbourhood of sorted agents in shared memory (or uses TMA bulk copies)").
+// Warp-specialised, persistent CTAs: one producer warp and TILE_W consumer warps.  The producer takes
+// tiles of TILE_AG = 32 TILE_W consecutive sorted agents; for a tile whose agents lie in at most TMAXC
+// columns it stages the forward half of their 3x3x3 neighbourhood -- for every own column c and
+// forward column q (0,0), (0,+1), (+1,-1), (+1,0), (+1,+1) the agents of the boxes
+// [zmin_c - 1, zmax_c + 1] (own column: from zmin_c), each one contiguous run of the sorted fp32
+// copy -- into shared memory with TMA bulk copies (cp.async.bulk completing on the slot's "full"
+// mbarrier), two slots deep: it prepares tile k+1 (columns, box starts of every run, copies) while
+// the consumers search tile k and releases nothing until they arrive on the slot's "empty"
+// mbarrier.  Consumers (one 32-agent chunk per warp) read candidates with LDS instead of L1/L2
+// gathers; culling, flattened cursor, fp32 filter and rows are pass A's.  Tiles spanning more
+// columns (sparse regions) or whose neighbourhood exceeds the buffer are searched from global memory.
+#ifndef BDM_TILE_NOSTAGE
+#define BDM_TILE_NOSTAGE 0  // experiment: the producer never stages (the pipeline without the shared copies)
+#endif
+#ifndef BDM_TILE_W
+#define BDM_TILE_W 4
+#endif
+constexpr int TILE_W = BDM_TILE_W;          // consumer warps (one chunk each)
+constexpr int TILE_AG = 32 * TILE_W;        // agents per tile
+constexpr int TILE_THREADS = 32 * (TILE_W + 1);
+constexpr int TMAXC = 3;                    // own columns of a staged tile
+constexpr int TRUNS = 5 * TMAXC;
+constexpr int TZS = 48;                     // box starts per staged run (z-span + 4)
+#ifndef BDM_TCAP
+#define BDM_TCAP (TILE_W == 4 ? 768 : 1152)
+#endif
+constexpr int TCAP = BDM_TCAP;              // staged candidates (float4) per slot
+#ifndef BDM_TILE_MIN_BLOCKS
+#define BDM_TILE_MIN_BLOCKS (TILE_W == 4 ? 4 : 2)
+#endif
+constexpr int TILE_MIN_BLOCKS = BDM_TILE_MIN_BLOCKS;
+
+struct TileMeta {
+  uint32_t t0;        // first sorted agent of the tile (>= s_end: no more tiles)
+  int32_t staged;     // 1 if the runs below are in the buffer
+  int32_t ncol;       // own columns (staged tiles)
+  int32_t cx[TMAXC], cy[TMAXC], zb[TMAXC];  // own column (bx, by) and its first staged box z (zmin - 1)
+  uint32_t ub[TRUNS + 1];                   // global sorted index of each staged run's first agent
+  uint32_t off[TRUNS + 1];                  // buffer offset of each run (off[5 ncol] = total)
+};
+
+struct TileSmem {
+  float4 buf[2][TCAP];
+  uint32_t tab[2][TRUNS][TZS];  // box starts of each (own column, forward column) run
+  TileMeta meta[2];
+  unsigned long long full[2], empty[2];
+};
+constexpr size_t TILE_SMEM_BYTES = sizeof(TileSmem) + sizeof(HalfASmem) * TILE_W;
+
+__device__ __forceinline__ void mbar_init_n(unsigned long long* bar, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Producer (one warp): the tile at t0 -> meta[slot], tab[slot], bulk copies into buf[slot]; arrives on
+// full[slot] (with the copies' byte count when staged).  Boxes as pass A computes them (fp32 copy,
+// fp64 position near box faces).  Loads of one level are issued together (latency-bound warp).
+__device__ void tile_produce(TileSmem& ts, int slot, uint32_t t0, uint32_t s_end, const double4* __restrict__ ag,
+                             const float4* __restrict__ agf, const GridDev& g) {
+  const int lane = threadIdx.x & 31;
+  TileMeta& m = ts.meta[slot];
+  bool staged = false;
+  int ncol = 0;
+  uint32_t total = 0;
+  if (t0 < s_end) {
+    const float inv32 = (float)g.inv;
+    float4 mf[TILE_W];
+#pragma unroll
+    for (int w = 0; w < TILE_W; ++w) {
+      const uint32_t i = t0 + 32u * w + lane;
+      mf[w] = i < s_end ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    int cxs[TMAXC], cys[TMAXC], zlo[TMAXC], zhi[TMAXC];
+    bool ok = true;
+#pragma unroll
+    for (int w = 0; w < TILE_W; ++w) {
+      const uint32_t i = t0 + 32u * w + lane;
+      const bool valid = i < s_end;
+      int b3[3];
+      const float t[3] = {mf[w].x * inv32, mf[w].y * inv32, mf[w].z * inv32};
+      bool amb = false;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float fl = floorf(t[a]);
+        const float tol = fabsf(t[a]) * 0x1p-21f + 0x1p-30f;
+        amb |= t[a] - fl <= tol || fl + 1.0f - t[a] <= tol;
+        b3[a] = (int)fl;
+      }
+      if (valid && amb) {
+        const double4 me = ag[i];
+        b3[0] = (int)floor(me.x * g.inv);
+        b3[1] = (int)floor(me.y * g.inv);
+        b3[2] = (int)floor(me.z * g.inv);
+      }
+      // distinct columns in order (the agents are sorted by column, then z)
+      unsigned left = __ballot_sync(FULL, valid);
+      while (left && ok) {
+        const int src = __ffs(left) - 1;
+        const int cx = __shfl_sync(FULL, b3[0], src), cy = __shfl_sync(FULL, b3[1], src);
+        const bool same = valid && b3[0] == cx && b3[1] == cy;
+        left &= ~__ballot_sync(FULL, same);
+        const int zl = __reduce_min_sync(FULL, same ? b3[2] : INT32_MAX);
+        const int zh = __reduce_max_sync(FULL, same ? b3[2] : INT32_MIN);
+        if (ncol > 0 && cxs[ncol - 1] == cx && cys[ncol - 1] == cy) {
+          zlo[ncol - 1] = min(zlo[ncol - 1], zl);
+          zhi[ncol - 1] = max(zhi[ncol - 1], zh);
+        } else if (ncol < TMAXC) {
+          cxs[ncol] = cx;
+          cys[ncol] = cy;
+          zlo[ncol] = zl;
+          zhi[ncol] = zh;
+          ++ncol;
+        } else {
+          ok = false;
+        }
+      }
+    }
+    for (int c = 0; c < ncol; ++c) ok &= zhi[c] - zlo[c] + 4 <= TZS;
+    if (ok && ncol > 0) {
+      // lane r < 5 ncol: run r = 5 c + q -> its neighbour column's record (one load level)
+      const int nrun = 5 * ncol;
+      int czl = 1, czh = 0, zb = 0, span = 0;
+      uint32_t cof = 0;
+      bool inside = false;
+      if (lane < nrun) {
+        const int c = lane / 5, q = lane % 5;
+        int cxv = cxs[0], cyv = cys[0], zlv = zlo[0], zhv = zhi[0];
+#pragma unroll
+        for (int u = 1; u < TMAXC; ++u)
+          if (c == u) {
+            cxv = cxs[u];
+            cyv = cys[u];
+            zlv = zlo[u];
+            zhv = zhi[u];
+          }
+        const int nx = cxv + (q >= 2 ? 1 : 0), ny = cyv + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
+        zb = zlv - 1;
+        span = zhv - zlv + 3;  // entries 0..span: starts of boxes zb .. zhi + 2
+        inside = nx >= g.lo[0] && nx <= g.hi[0] && ny >= g.lo[1] && ny <= g.hi[1];
+        if (inside) {
+          const int4 ci = __ldg(&g.col[col_of(g, nx, ny)]);
+          czl = ci.x;
+          czh = ci.y;
+          cof = (uint32_t)ci.z;
+        }
+      }
+      // every box start of every run (second load level: all loads issued, then stored)
+      constexpr int PER = (TRUNS * TZS + 31) / 32;
+      uint32_t v[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = lane + 32 * k;
+        const int r = e / TZS, tt = e % TZS;
+        const int rs = r < nrun ? r : 0;
+        const int zl_r = __shfl_sync(FULL, czl, rs), zh_r = __shfl_sync(FULL, czh, rs);
+        const int zb_r = __shfl_sync(FULL, zb, rs), sp_r = __shfl_sync(FULL, span, rs);
+        const uint32_t of_r = __shfl_sync(FULL, cof, rs);
+        const bool in_r = __shfl_sync(FULL, inside, rs);
+        v[k] = 0u;
+        const int ext = zh_r >= zl_r ? zh_r - zl_r + 1 : 0;
+        if (r < nrun && tt <= sp_r && in_r && ext > 0) {
+          int kk = zb_r + tt - zl_r;
+          kk = kk < 0 ? 0 : (kk > ext ? ext : kk);
+          v[k] = __ldg(&g.table[of_r + (uint32_t)kk]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = lane + 32 * k;
+        if (e < TRUNS * TZS) (&ts.tab[slot][0][0])[e] = v[k];
+      }
+      __syncwarp();
+      // run lengths -> buffer offsets (warp scan over the runs)
+      uint32_t ub = 0, len = 0;
+      if (lane < nrun) {
+        ub = ts.tab[slot][lane][lane % 5 == 0 ? 1 : 0];
+        const uint32_t ue = ts.tab[slot][lane][span];
+        len = ue > ub ? ue - ub : 0u;
+      }
+      const uint32_t incl = warp_incl_scan(len);
+      total = __shfl_sync(FULL, incl, 31);
+      if (lane < nrun) {
+        m.ub[lane] = ub;
+        m.off[lane] = incl - len;
+      }
+      if (lane == 0) {
+        m.off[nrun] = total;
+        for (int c = 0; c < ncol; ++c) {
+          m.cx[c] = cxs[c];
+          m.cy[c] = cys[c];
+          m.zb[c] = zlo[c] - 1;
+        }
+      }
+      staged = total > 0u && total <= (uint32_t)TCAP && !BDM_TILE_NOSTAGE;
+      __syncwarp();
+      if (staged) {
+        if (lane == 0) {
+          m.t0 = t0;
+          m.staged = 1;
+          m.ncol = ncol;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&ts.full[slot], total * 16u);  // (the producer's arrival, with the byte count)
+        }
+        __syncwarp();
+        if (lane < nrun && len) bulk_g2s(&ts.buf[slot][incl - len], agf + ub, len * 16u, &ts.full[slot]);
+        return;
+      }
+    }
+  }
+  if (lane == 0) {
+    m.t0 = t0;
+    m.staged = 0;
+    m.ncol = 0;
+    mbar_arrive(&ts.full[slot]);
+  }
+}
+
+// Candidate loop over runs of buffer indices (a staged tile): half_scan reading shared memory.
+__device__ __forceinline__ void tile_scan(HalfASmem& sm, const float4* __restrict__ sbuf, const TileMeta& m,
+                                          uint32_t rr_base, uint32_t wmax, uint32_t w, uint32_t i,
+                                          unsigned long long mxy, unsigned long long mzr, int& cnt, uint32_t& extra,
+                                          uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
+  const int lane = threadIdx.x & 31;
+  uint2 cur = sm.rr[0][lane];
+  uint32_t q = cur.x, e = cur.y;
+  uint2 nx = sm.rr[1][lane];
+  uint32_t kaddr = rr_base + 2u * 256u;
+  for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
+    uint32_t qs[NSLOT];
+    bool ok[NSLOT];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+      ok[t] = s0 + t < w;
+      qs[t] = ok[t] ? q : 0u;
+      ++q;
+      const uint32_t sw = q == e;
+      q = sw ? nx.x : q;
+      e = sw ? nx.y : e;
+      asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, 0;\n\t@p ld.shared.v2.u32 {%0, %1}, [%3];\n\t}"
+                   : "+r"(nx.x), "+r"(nx.y) : "r"(sw), "r"(kaddr));
+      kaddr += sw * 256u;
+    }
+    float4 o[NSLOT];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) o[t] = sbuf[qs[t]];
+#pragma unroll
+    for (int t = 0; t < NSLOT; ++t) {
+      float2 dxy, dzs;
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dxy))
+          : "l"(mxy), "l"(pack2(o[t].x, o[t].y)));
+      asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(*reinterpret_cast<unsigned long long*>(&dzs))
+          : "l"(mzr), "l"(pack2(o[t].z, o[t].w)));
+      float2 sq, qz;
+      asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&sq))
+          : "l"(*reinterpret_cast<unsigned long long*>(&dxy)));
+      asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(*reinterpret_cast<unsigned long long*>(&qz))
+          : "l"(*reinterpret_cast<unsigned long long*>(&dzs)));
+      const float d2 = (sq.x + sq.y) + qz.x;
+      if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) {
+        if (cnt < HLA) {
+          sm.list[cnt++][lane] = qs[t];
+        } else {  // rare: the partner (global index) still gets its backward entry
+          uint32_t r = 0;
+          while (r + 1 < (uint32_t)(5 * m.ncol) && qs[t] >= m.off[r + 1]) ++r;
+          const uint32_t j = qs[t] - m.off[r] + m.ub[r];
+          const uint32_t sl = atomicAdd(&bcnt[j], 1u);
+          if (sl < (uint32_t)HBC) bwd[(size_t)j * HBC + sl] = i;
+          ++extra;
+        }
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
+    k_half_search_tile(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin,
+                       uint32_t s_end, GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt,
+                       uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt, Extents* ext, bool count_searched,
+                       const uint32_t* __restrict__ s_end_dev = nullptr) {
+  if (s_end_dev) s_end = __ldg(s_end_dev);
+  extern __shared__ __align__(128) unsigned char s_raw[];
+  TileSmem& ts = *reinterpret_cast<TileSmem*>(s_raw);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (count_searched && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ext->searched, s_end - s_begin);
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < 2; ++k) {
+      mbar_init_n(&ts.full[k], 1u);
+      mbar_init_n(&ts.empty[k], (uint32_t)TILE_W);
+    }
+  }
+  __syncthreads();
+  if (warp == TILE_W) {  // ---- producer
+    uint32_t tnext = 0;  // the next tile's ticket, taken one tile ahead (the atomic's round trip overlaps)
+    if (lane == 0) tnext = atomicAdd(&ext->work_a, 1u);
+    for (uint32_t k = 0;; ++k) {
+      const int slot = (int)(k & 1u);
+      uint32_t t = __shfl_sync(FULL, tnext, 0);
+      if (lane == 0) tnext = atomicAdd(&ext->work_a, 1u);
+      if (k >= 2) mbar_wait(&ts.empty[slot], ((k >> 1) - 1u) & 1u);  // the consumers released the slot
+      const uint64_t a = (uint64_t)s_begin + (uint64_t)TILE_AG * t;
+      const uint32_t t0 = a < s_end ? (uint32_t)a : s_end;
+      tile_produce(ts, slot, t0, s_end, ag, agf, g);
+      if (t0 >= s_end) break;
+    }
+    return;
+  }
+  // ---- consumers
+  HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw + sizeof(TileSmem))[warp];
+  const uint32_t rr_base = (uint32_t)__cvta_generic_to_shared(&sm.rr[0][lane]);
+  for (uint32_t k = 0;; ++k) {
+    const int slot = (int)(k & 1u);
+    mbar_wait(&ts.full[slot], (k >> 1) & 1u);
+    const TileMeta& m = ts.meta[slot];
+    const uint32_t t0 = m.t0;
+    if (t0 >= s_end) break;
+    const bool staged = m.staged != 0;
+    const uint32_t i = t0 + 32u * warp + lane;
+    const bool valid = i < s_end;
+    if (__any_sync(FULL, valid)) {
+      const float4 mf = valid ? __ldg(&agf[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      int bx, by, bz;
+      {
+        const float inv32 = (float)g.inv;
+        const float t[3] = {mf.x * inv32, mf.y * inv32, mf.z * inv32};
+        int b3[3];
+        bool amb = false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float fl = floorf(t[a]);
+          const float tol = fabsf(t[a]) * 0x1p-21f + 0x1p-30f;
+          amb |= t[a] - fl <= tol || fl + 1.0f - t[a] <= tol;
+          b3[a] = (int)fl;
+        }
+        if (valid && amb) {
+          const double4 me = ag[i];
+          b3[0] = (int)floor(me.x * g.inv);
+          b3[1] = (int)floor(me.y * g.inv);
+          b3[2] = (int)floor(me.z * g.inv);
+        }
+        bx = b3[0];
+        by = b3[1];
+        bz = b3[2];
+      }
+      const double ri = (double)__fmul_ru(-mf.w, 1.0f + 0x1p-20f);
+      uint32_t cull = 0u;
+      {
+        const float mm = (float)g.m32;
+        const float rp = (-mf.w + (float)g.thr_pad + mm) * (1.0f + 0x1p-19f);
+        const float Rc = rp + 3.0f * mm;
+        const float Rc2 = Rc * Rc * (1.0f + 0x1p-18f);
+        const float Lb = (float)(1.0 / g.inv);
+        const float fy = fmaxf(mf.y - (float)by * Lb, 0.f), gy = fmaxf((float)(by + 1) * Lb - mf.y, 0.f);
+        const float gx = fmaxf((float)(bx + 1) * Lb - mf.x, 0.f);
+        const float fz = fmaxf(mf.z - (float)bz * Lb, 0.f), gz = fmaxf((float)(bz + 1) * Lb - mf.z, 0.f);
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          const float ex = q >= 2 ? gx : 0.f;
+          const float ey = q == 1 || q == 4 ? gy : (q == 2 ? fy : 0.f);
+          const float exy2 = ex * ex + ey * ey;
+          cull |= (uint32_t)(exy2 <= Rc2) << q;
+          cull |= (uint32_t)(exy2 + fz * fz > Rc2) << (8 + q);
+          cull |= (uint32_t)(exy2 + gz * gz > Rc2) << (16 + q);
+        }
+      }
+      // this lane's forward z-runs in canonical (= ascending sorted) order; staged: buffer indices
+      int nr = 0;
+      uint32_t w = 0;
+      int c = 0;
+      if (staged)
+        while (c + 1 < m.ncol && !(m.cx[c] == bx && m.cy[c] == by)) ++c;
+      if (valid) {
+#pragma unroll
+        for (int q = 0; q < 5; ++q) {
+          if (!((cull >> q) & 1u)) continue;
+          const int z0 = q == 0 ? bz : bz - 1 + (int)((cull >> (8 + q)) & 1u);
+          const int z1 = bz + 1 - (int)((cull >> (16 + q)) & 1u);
+          uint32_t b = 0, e = 0;
+          if (staged) {
+            const int r = 5 * c + q;
+            b = ts.tab[slot][r][z0 - m.zb[c]];
+            e = ts.tab[slot][r][z1 - m.zb[c] + 1];
+            if (q == 0) b = i + 1;
+            if (b < e) {
+              const uint32_t d = m.ub[r] - m.off[r];
+              b -= d;
+              e -= d;
+            }
+          } else {
+            const int cx = bx + (q >= 2 ? 1 : 0), cy = by + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
+            zrun(g, cx, cy, z0, z1, b, e);
+            if (q == 0) b = i + 1;
+          }
+          if (b < e) {
+            sm.rr[nr][lane] = make_uint2(b, e);
+            w += e - b;
+            ++nr;
+          }
+        }
+      }
+      sm.rr[nr][lane] = make_uint2(0u, 0u);
+      __syncwarp();
+      const uint32_t wmax = __reduce_max_sync(FULL, w);
+      const float ri32 = __double2float_ru(ri + g.m32);
+      const unsigned long long mxy = pack2(mf.x, mf.y), mzr = pack2(mf.z, ri32);
+      int cnt = 0;
+      uint32_t extra = 0;
+      if (staged) {
+        tile_scan(sm, ts.buf[slot], m, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+        for (int x = 0; x < cnt; ++x) {  // buffer index -> global sorted index
+          const uint32_t vv = sm.list[x][lane];
+          uint32_t r = 0;
+          while (r + 1 < (uint32_t)(5 * m.ncol) && vv >= m.off[r + 1]) ++r;
+          sm.list[x][lane] = vv - m.off[r] + m.ub[r];
+        }
+      } else {
+        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+      }
+      if (valid) {
+        half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
+        const uint32_t nf = (uint32_t)cnt + extra;
+        fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&ts.empty[slot]);  // this warp is done with the slot
+  }
+}
+
 struct HalfBSmem {
   uint32_t list[HFC + HBC][32];  // all contact candidates of this lane, ascending sorted index
   double term[3][32];
