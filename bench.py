@@ -297,7 +297,7 @@ def run_bdm(args):
                "unit": "GB/s", "frac": rebuild_bytes / grid_s / 1e9 / float(peaks["hbm_gbs"]),
                "ms_per_step": grid_s * 1e3, "bytes_per_agent": rebuild_bpa}
     traffic = None
-    tf = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
+    tf = os.path.join(ROOT, "profiles", "r02_force_traffic.json")
     if args.config == 3 and os.path.exists(tf):  # measured DRAM bytes of the force kernel (committed capture)
         with open(tf) as f:
             t = json.load(f)
@@ -330,7 +330,7 @@ def run_bdm(args):
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / fp64_peak, "traffic": traffic,
                          "kernel": "force phase: k_half_search + k_half_sum" if tm["search_ms"] > 0 else "k_force",
-                         "traffic_source": "profiles/r01_force_traffic.json" if traffic else None,
+                         "traffic_source": "profiles/r02_force_traffic.json" if traffic else None,
                          "ms_per_launch": force_s * 1e3,
                          "passes_ms": {"search": tm["search_ms"] / max(tm["steps"], 1),
                                        "sum": tm["sum_ms"] / max(tm["steps"], 1)},
@@ -480,7 +480,7 @@ def run_dist(args):
         traffic = None
         tf = os.path.join(ROOT, "profiles", "r02_force_traffic.json")
         if not os.path.exists(tf):
-            tf = os.path.join(ROOT, "profiles", "r01_force_traffic.json")
+            tf = os.path.join(ROOT, "profiles", "r02_force_traffic.json")
         if args.config == 3 and os.path.exists(tf):
             with open(tf) as f:
                 tr = json.load(f)

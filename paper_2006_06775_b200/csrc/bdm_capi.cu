@@ -740,10 +740,13 @@ int force_step(bdm_ctx* h, bool want_dp) {
                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
                                                  h->skip_active ? h->hot : nullptr,
                                                  h->hist[0] ? h->hist[dst] : nullptr, nullptr);
-  k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
+  if (!h->last_half) {  // (the half-shell path launched its own diagnosis)
+    k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
+    h->launches += 1;
+  }
   CU(h, cudaGetLastError());
   DBG(h, "k_force");
-  h->launches += 3;
+  h->launches += h->last_half ? 1 : 2;  // k_ext_reset (+ k_force)
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
   // pointers (the kernel already captured its arguments) instead of copying.
   h->out_ids = h->id[src];

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Write profiles/r01_force_traffic.json (DRAM bytes of the force-phase kernels per step, read by
+"""Write profiles/r02_force_traffic.json (DRAM bytes of the force-phase kernels per step, read by
 bench.py as roofline.traffic) from an ncu --set full capture of k_half_search + k_half_sum.
 
   python tools/force_traffic.py gpurun_out/half.ncu-rep"""
@@ -28,10 +28,11 @@ for row in r[2:]:
 out = {"kernels": ks,
        "workload": "cfg3, steady-state step (tools/profile_step.py --steps 2, first step captured: no dp write, "
                    "as in bench.py's timed mech_step(K))",
-       "source": f"ncu --set full --clock-control none ({rep}); summary profiles/r01_half_kernels_cfg3.txt",
+       "source": f"ncu --set full --clock-control none ({rep}); summary profiles/r02_half_kernels_cfg3.txt",
        "kernel": "force phase: k_half_search + k_half_sum",
+       "n_agents": 20_000_000,
        "dram_bytes_read": sum(k["dram_bytes_read"] for k in ks),
        "dram_bytes_write": sum(k["dram_bytes_write"] for k in ks)}
-with open(os.path.join(ROOT, "profiles", "r01_force_traffic.json"), "w") as f:
+with open(os.path.join(ROOT, "profiles", "r02_force_traffic.json"), "w") as f:
     json.dump(out, f, indent=1)
 print(json.dumps(out, indent=1))
