@@ -2023,6 +2023,7 @@ int bdm_slab_step(bdm_handle h, const int32_t* glo3, const int32_t* ghi3, int32_
     g.hi[0] = h->nlo[0] + h->nnx - 1;
     g.hi[1] = h->nlo[1] + h->nny - 1;
     g.ny = h->nny;
+    g.n_cols = (uint32_t)((int64_t)h->nnx * h->nny);  // (the column count of this frame, before its pass)
     const int64_t m = n_tot - h->fused_n0;
     if (m > 0) {
       k_col_ext<<<blocks(m, 512), 256, 0, s>>>(h->ag[h->cur] + h->fused_n0, (uint32_t)m, g, h->czlo2, h->czhi2);

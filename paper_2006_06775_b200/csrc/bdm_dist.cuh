@@ -189,25 +189,28 @@ __global__ void k_dist_ingest(double4* __restrict__ ag, uint32_t* __restrict__ i
                               int fused) {
   const uint32_t live = dc[DC_LIVE];
   bool ovf = false;
-  auto clampc = [&](uint32_t v, uint32_t lim) {
-    if (v > lim) {
-      ovf = true;
-      return lim;
-    }
-    return v;
-  };
-  // own split (the emigrants are at the front of the send records, the stayers at the back)
-  const uint32_t mig_lo = clampc(cnt[0], cap), mig_hi = clampc(cnt[2], cap);
+  // own split (the emigrants are at the front of the send records, the stayers at the back).  A message
+  // whose records exceeded the capacity is not used at all (its front and back may overlap): the chunk
+  // is void and re-run, and dropping it keeps the state consistent (no torn or duplicated agents)
+  const bool own_lo_bad = (uint64_t)cnt[0] + cnt[1] > cap, own_hi_bad = (uint64_t)cnt[2] + cnt[3] > cap;
+  ovf |= own_lo_bad || own_hi_bad;
+  const uint32_t mig_lo = own_lo_bad ? 0u : cnt[0], mig_hi = own_hi_bad ? 0u : cnt[2];
   uint32_t imm_lo = 0, imm_hi = 0, gin_lo = 0, gin_hi = 0;
   if (has_lo) {
-    imm_lo = clampc(hdr_u32(recv_lo, 0), cap);
-    gin_lo = clampc(hdr_u32(recv_lo, 1), cap - imm_lo);
-    ovf |= recv_lo[2] != 0.0;
+    if (recv_lo[2] != 0.0 || (uint64_t)hdr_u32(recv_lo, 0) + hdr_u32(recv_lo, 1) > cap) {
+      ovf = true;
+    } else {
+      imm_lo = hdr_u32(recv_lo, 0);
+      gin_lo = hdr_u32(recv_lo, 1);
+    }
   }
   if (has_hi) {
-    imm_hi = clampc(hdr_u32(recv_hi, 0), cap);
-    gin_hi = clampc(hdr_u32(recv_hi, 1), cap - imm_hi);
-    ovf |= recv_hi[2] != 0.0;
+    if (recv_hi[2] != 0.0 || (uint64_t)hdr_u32(recv_hi, 0) + hdr_u32(recv_hi, 1) > cap) {
+      ovf = true;
+    } else {
+      imm_hi = hdr_u32(recv_hi, 0);
+      gin_hi = hdr_u32(recv_hi, 1);
+    }
   }
   // segments appended at `live`: [imm_lo][imm_hi][gin_lo][mig_lo][gin_hi][mig_hi]
   uint32_t seg[6] = {imm_lo, imm_hi, gin_lo, mig_lo, gin_hi, mig_hi};
@@ -229,6 +232,7 @@ __global__ void k_dist_ingest(double4* __restrict__ ag, uint32_t* __restrict__ i
       ++k;
     }
     const uint64_t rec = back[k] ? (uint64_t)cap - 1 - r : r;
+    BDM_ASSERT(k < 6 && rec < cap && live + t < room);
     const double* q = src[k] + (size_t)REC * rec;
     ag[live + t] = make_double4(q[0], q[1], q[2], q[3]);
     ids[live + t] = (uint32_t)q[4];

@@ -17,8 +17,22 @@
 //   K7 k_unpermute_*     sorted order -> id order for the getters
 //   K8 k_pairs_*         neighbour / contact pair export (tests)
 #pragma once
+#include <cassert>
 #include <cstdint>
 #include <cuda_runtime.h>
+
+// BDM_CHECK=1 (tools/build_variant.sh checked -DBDM_CHECK=1): device-side bounds assertions on the index
+// computations of the hot kernels (table keys, scatter / place destinations, column indices, z-runs,
+// row partners, distributed ingest) -- the substitute for compute-sanitizer, which is closed on this
+// pool.  Off in the product build.
+#ifndef BDM_CHECK
+#define BDM_CHECK 0
+#endif
+#if BDM_CHECK
+#define BDM_ASSERT(c) assert(c)
+#else
+#define BDM_ASSERT(c) ((void)0)
+#endif
 
 namespace bdm {
 
@@ -259,13 +273,16 @@ __device__ __forceinline__ uint32_t box_key(const GridDev& g, int bx, int by, in
 __device__ __forceinline__ bool zrun(const GridDev& g, int cx, int cy, int z0, int z1, uint32_t& b, uint32_t& e) {
   if (cx < g.lo[0] || cx > g.hi[0] || cy < g.lo[1] || cy > g.hi[1]) return false;
   const uint32_t c = col_of(g, cx, cy);
+  BDM_ASSERT(c < g.n_cols);
   const int4 ci = __ldg(&g.col[c]);
   const int zl = ci.x, zh = ci.y;
   const int a = z0 > zl ? z0 : zl, d = z1 < zh ? z1 : zh;
   if (a > d) return false;
   const uint32_t o = (uint32_t)ci.z;
+  BDM_ASSERT(o + (uint32_t)(d - zl) + 1u <= __ldg(&g.coff[g.n_cols]));
   b = __ldg(&g.table[o + (uint32_t)(a - zl)]);
   e = __ldg(&g.table[o + (uint32_t)(d - zl) + 1u]);
+  BDM_ASSERT(b <= e);
   return true;
 }
 
@@ -330,6 +347,7 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
       // distributed steps (rng): the frame is fixed for a chunk; an agent outside it is left to the
       // guarded key pass (which reports it) instead of indexing outside the column arrays
       if (!rng || (bx >= g.lo[0] && bx <= g.hi[0] && by >= g.lo[1] && by <= g.hi[1])) c = col_of(g, bx, by);
+      BDM_ASSERT(c == 0xffffffffu || c < g.n_cols);
     }
     // warp-aggregated: agents arrive mostly in box order, so a warp touches few columns; each group
     // of lanes with the same column reduces with redux.sync over its own member mask
@@ -413,7 +431,7 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
     peers[u] = __match_any_sync(FULL, kk[u]);
     base[u] = 0u;
     if (kk[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1)
-      base[u] = atomicAdd(&count[kk[u]], (uint32_t)__popc(peers[u]));
+      base[u] = (BDM_ASSERT(kk[u] < __ldg(&g.coff[g.n_cols])), atomicAdd(&count[kk[u]], (uint32_t)__popc(peers[u])));
   }
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
@@ -464,7 +482,10 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
   for (int u = 0; u < KHP; ++u) {
     peers[u] = __match_any_sync(FULL, k[u]);
     base[u] = 0u;
-    if (k[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1) base[u] = atomicAdd(&count[k[u]], (uint32_t)__popc(peers[u]));
+    if (k[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1) {
+      BDM_ASSERT(k[u] < __ldg(&g.coff[g.n_cols]));
+      base[u] = atomicAdd(&count[k[u]], (uint32_t)__popc(peers[u]));
+    }
   }
 #pragma unroll
   for (int u = 0; u < KHP; ++u) {
@@ -615,6 +636,7 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __re
   for (int u = 0; u < KSC; ++u) {
     if (k[u] == 0xffffffffu) continue;
     const uint32_t d = st[u] + sl[u];
+    BDM_ASSERT(d < n);
     tsrc[d] = i0 + u * blockDim.x;
     tid[d] = id[u];
     tkey[d] = k[u];
@@ -638,6 +660,7 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
 #pragma unroll 4
   for (uint32_t t = b; t < e; ++t) rank += tid[t] < id;
   const uint32_t dst = b + rank;
+  BDM_ASSERT(b <= q && q < e && dst < e);
   st_state(&ag_out[dst], p);
   ids_out[dst] = id;
   if (hist_out) hist_out[dst] = hist_in[src];
@@ -1317,7 +1340,10 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (x0 + u < cnt && slot[u] < (uint32_t)HBC) bwd[(size_t)j[u] * HBC + slot[u]] = i;
+      if (x0 + u < cnt && slot[u] < (uint32_t)HBC) {
+        BDM_ASSERT(j[u] > i);  // forward partners only (the half-shell order)
+        bwd[(size_t)j[u] * HBC + slot[u]] = i;
+      }
   }
 }
 
@@ -2325,6 +2351,13 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
           if (4 * v + k < nf) fc[32 * (4 * v + k)] = u[k];
       }
       cnt = (int)(nb + nf);
+#if BDM_CHECK
+      for (int t = 0; t < cnt; ++t) {  // canonical order: backward partners ascending below i, then forward above
+        const uint32_t j = col[32 * t];
+        BDM_ASSERT(t < (int)nb ? j < i : j > i);
+        BDM_ASSERT(t == 0 || col[32 * (t - 1)] < j);
+      }
+#endif
     }
     __syncwarp();
     double Fx = 0.0, Fy = 0.0, Fz = 0.0;
