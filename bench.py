@@ -388,7 +388,11 @@ def run_dist(args):
         torch.cuda.empty_cache()
     dist.broadcast(units, 0) if world > 1 else None
     uid = bdist.broadcast_uid(dist, bdm, dev) if world > 1 else bdm.bdm_nccl_unique_id()
-    ids, pos, diam = bdist.rank_inputs(bdm, torch, bdm_inputs, args.config, n, rank, world, dev, stream)
+    if args.slab_of > 1:  # one rank's x-slab of the config at slab_of ranks, alone on this GPU (memory / rate)
+        ids, pos, diam = slab_share(bdm, torch, args.config, n, args.slab_of, dev, stream)
+        n = int(ids.shape[0])
+    else:
+        ids, pos, diam = bdist.rank_inputs(bdm, torch, bdm_inputs, args.config, n, rank, world, dev, stream)
     t0 = time.perf_counter()
     h = bdm.bdm_init_dist(ids, pos, diam, bdm.bdm_params_default(), rank=rank, world=world, uid=uid, device=local,
                           stream=stream)
@@ -417,6 +421,12 @@ def run_dist(args):
         dist.barrier()
     tm = bdm.bdm_get_timing(h)
     s1 = bdm.bdm_get_stats(h)
+    free_b, total_b = torch.cuda.mem_get_info(dev)
+    import resource
+
+    mem = {"gpu_used_gib": round((total_b - free_b) / 2 ** 30, 2), "gpu_total_gib": round(total_b / 2 ** 30, 2),
+           "host_maxrss_gib": round(resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2 ** 20, 2),
+           "note": "rank 0 after the timed steps: device memory in use (libbdm's buffers + torch's cache), host peak RSS"}
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -497,7 +507,10 @@ def run_dist(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": dict(config_obj(args, n, world), cuts=[int(c) for c in cuts[1:-1]]),
+                "config": dict(config_obj(args, n, world), cuts=[int(c) for c in cuts[1:-1]],
+                               **({"slab_of": args.slab_of, "note": f"rank 0's x-slab of the {args.config} population at "
+                                   f"{args.slab_of} ranks, alone on one GPU (no neighbours: no exchange traffic)"}
+                                  if args.slab_of > 1 else {})),
                 "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
                              "frac": achieved / fp64_peak, "traffic": traffic,
                              "traffic_source": (os.path.relpath(tf, ROOT) + " scaled to rank 0's owned agents")
@@ -508,6 +521,7 @@ def run_dist(args):
                              "note": "rank 0's owned agents x the per-agent fp64-pipe ops of the recorded step "
                                      "(9 per candidate + 44 per contact + 40 per agent, DESIGN.md §6.2) over its "
                                      "force-phase event time; peak = 148 SM x 64 fp64 lanes x sm_max_mhz"},
+                "mem": mem,
                 "dist": {"host_syncs": int(agg[1].item()), "launches": int(agg[0].item()),
                          "exchange_bytes": int(agg[2].item()), "migrated": int(agg[3].item()),
                          "setup_s": setup_s, "rank0_agents": own,
@@ -520,6 +534,28 @@ def run_dist(args):
         dist.barrier()
     dist.destroy_process_group()
     return 0
+
+
+def slab_share(bdm, torch, cfg, n_full, slabs, dev, stream):
+    """The first of `slabs` equal x-slabs of a uniform counter-hash config (4, 5), generated on the device
+    in id chunks (kernel K0) and filtered: what rank 0 of `slabs` ranks owns."""
+    assert cfg in (4, 5), "--slab-of needs a uniform counter-hash config (4 or 5)"
+    lo, hi = bdm_inputs.box_of(cfg, n_full)
+    xcut = lo[0] + (hi[0] - lo[0]) / slabs
+    keep_i, keep_p, keep_d = [], [], []
+    step = 50_000_000
+    for a in range(0, n_full, step):
+        m = min(step, n_full - a)
+        p = torch.empty((m, 3), dtype=torch.float64, device=dev)
+        d = torch.empty(m, dtype=torch.float64, device=dev)
+        bdm.bdm_generate_uniform(cfg, a, m, lo, hi, 8.0, 12.0, p, d, stream)
+        torch.cuda.synchronize(dev)
+        sel = p[:, 0] < xcut
+        keep_i.append(torch.nonzero(sel).squeeze(1) + a)
+        keep_p.append(p[sel])
+        keep_d.append(d[sel])
+        del p, d, sel
+    return torch.cat(keep_i).to(torch.int64), torch.cat(keep_p).contiguous(), torch.cat(keep_d).contiguous()
 
 
 def free_port() -> int:
@@ -668,7 +704,9 @@ def main():
     ap.add_argument("--cpu-stride-1t", type=int, default=200, help="single-threaded oracle sample stride")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--slabs", action="store_true", help="use the x-slab driver even at one rank (testing)")
+    ap.add_argument("--slabs", action="store_true", help="use the distributed runtime even at one rank")
+    ap.add_argument("--slab-of", type=int, default=1,
+                    help="with --slabs at one rank: run only rank 0's x-slab of a uniform config at this many ranks")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "bdm":
         print("note: timing rules need >= 3 warm-up steps; raising warmup to 3", file=sys.stderr)
