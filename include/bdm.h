@@ -219,7 +219,7 @@ int bdm_get_skip_stats(bdm_handle h, int64_t* out3);
 int bdm_get_path_stats(bdm_handle h, int64_t* out2);
 
 /* Force-path selection for plain steps of this handle: BDM_PATH_AUTO (default)
- * runs the half-shell passes whenever their pair rows (133 B/agent) can be allocated and falls back
+ * runs the half-shell passes whenever their pair rows (72 B/agent) can be allocated and falls back
  * to the single-pass k_force otherwise (e.g. 10^9 agents on one GPU); BDM_PATH_SINGLE always runs
  * k_force.  Both compute O3-O7 in the canonical order: results are bit-identical.  EINVAL for any
  * other value. */

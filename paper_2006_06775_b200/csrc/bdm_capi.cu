@@ -353,7 +353,8 @@ void init_device_info(bdm_ctx* h) {
   h->half_b_blocks_per_sm = per_sm > 0 ? per_sm : 1;
 }
 
-// Pair rows of the half-shell path for cap agents (16 + 16 u32 + counters: 133 B/agent).  An
+// Pair rows of the half-shell path for cap agents (one merged row of 16 u32 + counter + slow-list
+// slot: 72 B/agent; 133 B/agent with separate rows, BDM_MROW=0).  An
 // allocation failure is not an error: the handle falls back to k_force (no rows needed).
 bool ensure_half(bdm_ctx* h) {
   if (h->half_off || h->force_path == BDM_PATH_SINGLE) return false;
@@ -363,9 +364,10 @@ bool ensure_half(bdm_ctx* h) {
   h->h_fwd = h->h_bwd = h->h_bcnt = h->h_slow = nullptr;
   h->h_fcnt = nullptr;
   const size_t N = (size_t)std::max<int64_t>(h->cap, 1);
+  const size_t Nsep = BDM_MROW ? 1 : N;  // (merged rows: no separate backward rows / forward counts)
   if (cudaMalloc(&h->h_fwd, N * HFC * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMalloc(&h->h_bwd, N * HBC * sizeof(uint32_t)) != cudaSuccess ||
-      cudaMalloc(&h->h_bcnt, N * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->h_fcnt, N) != cudaSuccess ||
+      cudaMalloc(&h->h_bwd, Nsep * HBC * sizeof(uint32_t)) != cudaSuccess ||
+      cudaMalloc(&h->h_bcnt, N * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->h_fcnt, Nsep) != cudaSuccess ||
       cudaMalloc(&h->h_slow, N * sizeof(uint32_t)) != cudaSuccess) {
     (void)cudaGetLastError();
     for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt, (void*)h->h_slow})

@@ -1308,12 +1308,38 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
 }
 constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 
-// End of a chunk: the forward row of i as whole 32-byte sectors (entries past cnt are don't-care;
-// full sectors avoid read-modify-write of partially written sectors in DRAM), and one backward-row
-// entry per pair through an atomic slot of the partner.
-__device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint32_t i, uint32_t* __restrict__ fwd,
-                                          uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
-#if BDM_V256
+#ifndef BDM_MROW
+#define BDM_MROW 1  // one merged pair row per agent (forward and backward entries under one counter)
+#endif
+#ifndef BDM_HRPF
+#define BDM_HRPF 0  // pass B: counts two chunks ahead, first row vector one chunk ahead (merged rows; spills: slower)
+#endif
+#ifndef BDM_HPPF
+#define BDM_HPPF 1  // pass B: partner states prefetched into L1 as soon as the row is read
+#endif
+// BDM_MROW: agent j's row fwd[j * HFC ..] holds all its pair candidates, forward (found by its own
+// search) and backward (found by partners' searches), packed from the front in arrival order through
+// one atomic counter bcnt[j]; the sum pass sorts the row.  A typical agent's entries then share one
+// 32-byte sector (instead of one sector in each of two rows): the sum pass reads half the row bytes.
+// Otherwise: a forward row written by the owner and a backward row (bwd, bcnt) filled by partners.
+__device__ __forceinline__ void bw_put(uint32_t* __restrict__ fwd, uint32_t* __restrict__ bwd,
+                                       uint32_t j, uint32_t slot, uint32_t i) {
+  if (slot < (uint32_t)HBC) (BDM_MROW ? fwd : bwd)[(size_t)j * HBC + slot] = i;
+}
+
+// End of a chunk (lane of agent i, cnt survivors in its list, extra beyond it): the forward entries
+// of i and one backward entry per pair through an atomic slot of the partner.  Separate rows: the
+// forward row as whole 32-byte sectors (entries past cnt are don't-care; full sectors avoid
+// read-modify-write of partially written sectors in DRAM).
+__device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint32_t extra, uint32_t i,
+                                          uint32_t* __restrict__ fwd, uint32_t* __restrict__ bwd,
+                                          uint32_t* __restrict__ bcnt) {
+#if BDM_MROW
+  // own entries: a base slot for all of them (the overflow beyond the list counts, so a row that
+  // cannot hold everything is recognised by its count); its round trip overlaps the partners' atomics
+  const uint32_t nf = (uint32_t)cnt + extra;
+  const uint32_t base = nf ? atomicAdd(&bcnt[i], nf) : 0u;
+#elif BDM_V256
   uint32_t* frow = fwd + (size_t)i * HFC;  // 64-byte rows: one 256-bit store per used sector
 #pragma unroll
   for (int v = 0; v < HFC / 8; ++v)
@@ -1340,11 +1366,16 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (x0 + u < cnt && slot[u] < (uint32_t)HBC) {
+      if (x0 + u < cnt) {
         BDM_ASSERT(j[u] > i);  // forward partners only (the half-shell order)
-        bwd[(size_t)j[u] * HBC + slot[u]] = i;
+        bw_put(fwd, bwd, j[u], slot[u], i);
       }
   }
+#if BDM_MROW
+  uint32_t* row = fwd + (size_t)i * HFC;
+  for (int k = 0; k < cnt; ++k)
+    if (base + (uint32_t)k < (uint32_t)HFC) row[base + k] = sm.list[k][lane];
+#endif
 }
 
 // Candidate loop of pass A over this lane's runs rr[] (flattened, branch-free run switch): fp32
@@ -1354,7 +1385,8 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
 template <bool STAGED>
 __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restrict__ agf, uint32_t rr_base,
                                           uint32_t wmax, uint32_t w, uint32_t i, unsigned long long mxy,
-                                          unsigned long long mzr, int& cnt, uint32_t& extra, uint32_t* __restrict__ bwd,
+                                          unsigned long long mzr, int& cnt, uint32_t& extra,
+                                          uint32_t* __restrict__ fwd_rows, uint32_t* __restrict__ bwd,
                                           uint32_t* __restrict__ bcnt) {
   const int lane = threadIdx.x & 31;
   uint2 cur = sm.rr[0][lane];
@@ -1413,8 +1445,7 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
             j = j - sm.off[c] + sm.ub[c];
           }
 #endif
-          const uint32_t sl = atomicAdd(&bcnt[j], 1u);
-          if (sl < (uint32_t)HBC) bwd[(size_t)j * HBC + sl] = i;
+          bw_put(fwd_rows, bwd, j, atomicAdd(&bcnt[j], 1u), i);
           ++extra;
         }
       }
@@ -1429,8 +1460,8 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
 __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __restrict__ agf, const uint32_t S[5],
                                               const uint32_t A[5], uint32_t wmax, uint32_t w, uint32_t i,
                                               unsigned long long mxy, unsigned long long mzr, int& cnt,
-                                              uint32_t& extra, uint32_t* __restrict__ bwd,
-                                              uint32_t* __restrict__ bcnt) {
+                                              uint32_t& extra, uint32_t* __restrict__ fwd_rows,
+                                              uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
   const int lane = threadIdx.x & 31;
   for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
     uint32_t qs[NSLOT];
@@ -1464,8 +1495,7 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
         if (cnt < HLA) {
           sm.list[cnt++][lane] = qs[t];
         } else {  // rare: the partner still gets its backward entry
-          const uint32_t sl = atomicAdd(&bcnt[qs[t]], 1u);
-          if (sl < (uint32_t)HBC) bwd[(size_t)qs[t] * HBC + sl] = i;
+          bw_put(fwd_rows, bwd, qs[t], atomicAdd(&bcnt[qs[t]], 1u), i);
           ++extra;
         }
       }
@@ -1726,7 +1756,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     if (staged) {
       mbar_wait(&sm.bar, phase);
       phase ^= 1u;
-      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
       // buffer index -> global sorted index (each union run is contiguous in both)
       for (int x = 0; x < cnt; ++x) {
         const uint32_t v = sm.list[x][lane];
@@ -1739,14 +1769,16 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     } else
 #endif
 #if BDM_HMAP
-      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
 #else
-      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
 #endif
     if (valid) {
-      half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
-      const uint32_t nf = (uint32_t)cnt + extra;
-      fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+      half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
+      if (!BDM_MROW) {
+        const uint32_t nf = (uint32_t)cnt + extra;
+        fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+      }
     }
     __syncwarp();
   }
@@ -1977,7 +2009,8 @@ __device__ void tile_produce(TileSmem& ts, int slot, uint32_t t0, uint32_t s_end
 __device__ __forceinline__ void tile_scan(HalfASmem& sm, const float4* __restrict__ sbuf, const TileMeta& m,
                                           uint32_t rr_base, uint32_t wmax, uint32_t w, uint32_t i,
                                           unsigned long long mxy, unsigned long long mzr, int& cnt, uint32_t& extra,
-                                          uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
+                                          uint32_t* __restrict__ fwd_rows, uint32_t* __restrict__ bwd,
+                                          uint32_t* __restrict__ bcnt) {
   const int lane = threadIdx.x & 31;
   uint2 cur = sm.rr[0][lane];
   uint32_t q = cur.x, e = cur.y;
@@ -2021,8 +2054,7 @@ __device__ __forceinline__ void tile_scan(HalfASmem& sm, const float4* __restric
           uint32_t r = 0;
           while (r + 1 < (uint32_t)(5 * m.ncol) && qs[t] >= m.off[r + 1]) ++r;
           const uint32_t j = qs[t] - m.off[r] + m.ub[r];
-          const uint32_t sl = atomicAdd(&bcnt[j], 1u);
-          if (sl < (uint32_t)HBC) bwd[(size_t)j * HBC + sl] = i;
+          bw_put(fwd_rows, bwd, j, atomicAdd(&bcnt[j], 1u), i);
           ++extra;
         }
       }
@@ -2163,7 +2195,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
       int cnt = 0;
       uint32_t extra = 0;
       if (staged) {
-        tile_scan(sm, ts.buf[slot], m, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+        tile_scan(sm, ts.buf[slot], m, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
         for (int x = 0; x < cnt; ++x) {  // buffer index -> global sorted index
           const uint32_t vv = sm.list[x][lane];
           uint32_t r = 0;
@@ -2171,12 +2203,14 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
           sm.list[x][lane] = vv - m.off[r] + m.ub[r];
         }
       } else {
-        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, bwd, bcnt);
+        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
       }
       if (valid) {
-        half_emit(sm, lane, cnt, i, fwd, bwd, bcnt);
-        const uint32_t nf = (uint32_t)cnt + extra;
-        fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+        half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
+        if (!BDM_MROW) {
+          const uint32_t nf = (uint32_t)cnt + extra;
+          fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
+        }
       }
     }
     __syncwarp();
@@ -2270,7 +2304,21 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   __syncwarp();
   uint32_t n_moved = 0;
   Tickets tk(a_end - a_begin);
-#if BDM_HBCNT
+#if BDM_HRPF
+  // merged rows: the pair counts are loaded two chunks ahead and the first vector of each row one
+  // chunk ahead (the count is there by then), so a chunk's dependent chain starts at its partners
+  uint32_t chunk = tk.take(&ext_next->work, lane);
+  uint32_t chunk_n = tk.take(&ext_next->work, lane);
+  uint32_t nb_n = 0u, nb_nn = 0u;
+  uint4 r4_n = make_uint4(0u, 0u, 0u, 0u);
+  {
+    const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
+    nb_n = i1 < a_end ? bcnt[i1] : 0u;
+    if (nb_n) r4_n = __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)i1 * HBC));
+    const uint64_t i2 = (uint64_t)a_begin + 32ull * chunk_n + lane;
+    nb_nn = i2 < a_end ? bcnt[i2] : 0u;
+  }
+#elif BDM_HBCNT
   // the next chunk's pair counts are loaded one chunk ahead (two registers): a chunk's dependent
   // chain then starts at its rows
   uint32_t chunk = tk.take(&ext_next->work, lane);
@@ -2278,13 +2326,13 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   {
     const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
     if (i1 < a_end) {
-      nf_n = fcnt[i1];
+      nf_n = BDM_MROW ? 0u : fcnt[i1];  // (merged rows: bcnt counts every entry of the one row)
       nb_n = bcnt[i1];
     }
   }
 #endif
   while (true) {
-#if !BDM_HBCNT
+#if !BDM_HBCNT && !BDM_HRPF
     const uint32_t chunk = tk.take(&ext_next->work, lane);
 #endif
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
@@ -2293,29 +2341,57 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const bool valid = i < a_end;
     // the agent and both counts, then the first 4 entries of each non-empty row (one vector load;
     // entries past a count are stale and ignored)
-    const uint4* brow = reinterpret_cast<const uint4*>(bwd + (size_t)i * HBC);
+    const uint4* brow = reinterpret_cast<const uint4*>((BDM_MROW ? fwd : bwd) + (size_t)i * HBC);
     const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
     const double4 me = valid ? ld_state(&ag[i]) : make_double4(0.0, 0.0, 0.0, 0.0);
-#if BDM_HBCNT
+#if BDM_HRPF
+    const uint32_t nf = 0u, nb = nb_n;
+    const uint4 r4 = r4_n;
+    {  // rotate: next chunk's first row vector (its count arrived during this chunk's predecessor),
+       // the count of the chunk after it
+      chunk = chunk_n;
+      chunk_n = tk.take(&ext_next->work, lane);
+      const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
+      nb_n = nb_nn;
+      r4_n = nb_n ? __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)i1 * HBC)) : make_uint4(0u, 0u, 0u, 0u);
+      const uint64_t i2 = (uint64_t)a_begin + 32ull * chunk_n + lane;
+      nb_nn = i2 < a_end ? bcnt[i2] : 0u;
+    }
+#elif BDM_HBCNT
     const uint32_t nf = nf_n, nb = nb_n;
     chunk = tk.take(&ext_next->work, lane);
     {
       const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
-      nf_n = i1 < a_end ? fcnt[i1] : 0u;
+      nf_n = i1 < a_end && !BDM_MROW ? fcnt[i1] : 0u;
       nb_n = i1 < a_end ? bcnt[i1] : 0u;
     }
 #else
-    const uint32_t nf = valid ? fcnt[i] : 0u;
+    const uint32_t nf = valid && !BDM_MROW ? fcnt[i] : 0u;
     const uint32_t nb = valid ? bcnt[i] : 0u;
 #endif
     // (rows are read only where the count says so: a speculative read of every row costs more DRAM
     // traffic than the round trip it saves)
+#if BDM_HRPF
+    const uint4 b4 = r4;
+    const uint4 f4 = make_uint4(0u, 0u, 0u, 0u);
+#else
     const uint4 b4 = nb ? __ldg(brow) : make_uint4(0u, 0u, 0u, 0u);
     const uint4 f4 = nf ? __ldg(frow) : make_uint4(0u, 0u, 0u, 0u);
+#endif
     const double ri = 0.5 * me.w;
     const bool slow = nf > (uint32_t)HFC || nb > (uint32_t)HBC;
     int cnt = 0;
     if (!slow) {
+#if BDM_HPPF
+      {  // the partners' states toward L1 while the row is sorted (the contact phase gathers them)
+        const uint32_t e4[4] = {b4.x, b4.y, b4.z, b4.w}, g4[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if ((uint32_t)k < nb) asm volatile("prefetch.global.L1 [%0];" ::"l"(ag + e4[k]));
+          if (!BDM_MROW && (uint32_t)k < nf) asm volatile("prefetch.global.L1 [%0];" ::"l"(ag + g4[k]));
+        }
+      }
+#endif
       // backward partners (all < i) sorted ascending, then forward partners (all > i, ascending)
       uint32_t* col = &sm.list[0][lane];
       col[0] = b4.x;
@@ -2354,7 +2430,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
 #if BDM_CHECK
       for (int t = 0; t < cnt; ++t) {  // canonical order: backward partners ascending below i, then forward above
         const uint32_t j = col[32 * t];
-        BDM_ASSERT(t < (int)nb ? j < i : j > i);
+        BDM_ASSERT(BDM_MROW ? j != i : (t < (int)nb ? j < i : j > i));
         BDM_ASSERT(t == 0 || col[32 * (t - 1)] < j);
       }
 #endif
