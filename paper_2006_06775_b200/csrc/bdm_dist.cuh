@@ -440,6 +440,8 @@ struct DistSlab {
   int64_t room = 0;           // capacity of the slab buffers
   int32_t flo[3] = {0, 0, 0}, fhi[3] = {0, 0, 0};  // grid frame of the current chunk
   double fm32 = 0.0;                                 // its fp32 prefilter margin
+  bool fvalid = false;        // the frame above is in use (kept across chunks while it holds the agents)
+  int32_t zbits = 0;          // packed new boxes (column << zbits | z - flo[2]) of the sum pass, 0 = off
 };
 
 struct DistGroup {
@@ -691,6 +693,7 @@ int dist_load_slab(bdm_ctx* H, DistGroup* G, int s, const double* rec, int64_t c
   ++G->syncs;
   D.live = cnt;
   D.stepped = false;
+  D.fvalid = false;
   D.xb = G->cuts[D.rank];
   D.xe = G->cuts[D.rank + 1];
   return BDM_OK;
@@ -781,8 +784,9 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   cudaStream_t st = G->stream;
   const uint32_t room = (uint32_t)D.room;
   // emigrants of the split are marked dead in place (the sort drops them)
+  const bool packed = h->cols_next && D.zbits > 0;  // the last sum pass wrote packed new boxes of [0, LIVE)
   k_slab_mark_dead<<<h->sm_count * 4, 256, 0, st>>>(h->ag[h->cur], room, h->cnt + 4, h->grid.inv, D.xb, D.xe,
-                                                    D.dc + DC_LIVE);
+                                                    D.dc + DC_LIVE, packed ? h->pbox : nullptr);
   DBG(h, "k_slab_mark_dead");
   const bool fused = h->cols_next;
   k_dist_ingest<<<h->sm_count * 2, 256, 0, st>>>(h->ag[h->cur], h->id[h->cur], D.dc, h->cnt, D.msg[0], D.msg[1],
@@ -834,7 +838,8 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     g.coff = h->coff;
     g.table = h->table;
     g.col = h->colrec;
-    k_col_ext<<<blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->czlo, h->czhi, D.dc + DC_CE0);
+    k_col_ext<<<fused ? h->sm_count * 2 : blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->czlo, h->czhi,
+                                                                          D.dc + DC_CE0);
     DBG(h, "k_col_ext(dist)");
     const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
     k_col_len<<<gs, 256, 0, st>>>(h->czlo, h->czhi, g.n_cols, h->coff);
@@ -843,8 +848,16 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     if (rc) return fail(H, rc, "%s", h->error.c_str());
     k_table_zero<<<h->sm_count * 8, 256, 0, st>>>(h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec);
     DBG(h, "k_table_zero(dist)");
-    k_key_hist<true><<<blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
-                                                        D.dc + DC_TOT);
+    if (packed) {  // the stepped agents' boxes from the sum pass (4 B), the appended records from their state
+      k_key_hist_packed<true><<<blocks(room, 256 * KHP), 256, 0, st>>>(h->pbox, room, g, D.flo[2], D.zbits, h->key,
+                                                                      h->slot, h->table, h->err, D.dc + DC_LIVE);
+      k_key_hist<true><<<h->sm_count * 4, 256, 0, st>>>(h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
+                                                        D.dc + DC_TOT, D.dc + DC_LIVE);
+      h->launches += 1;
+    } else {
+      k_key_hist<true><<<blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
+                                                          D.dc + DC_TOT);
+    }
     DBG(h, "k_key_hist(dist)");
     rc = scan(h, h->table, 0, h->coff + nc);
     if (rc) return fail(H, rc, "%s", h->error.c_str());
@@ -875,6 +888,11 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     cn.czhi = h->czhi2;
     const unsigned gs = (unsigned)std::min<uint64_t>((nc2 + 256) / 256, 148u * 16u);
     k_col_reset<<<gs, 256, 0, st>>>(h->czlo2, h->czhi2, (uint32_t)nc2);
+    if (D.zbits > 0) {  // packed new boxes for the next build's key pass (the frame is fixed for the chunk)
+      cn.pbox = h->pbox;
+      cn.z0 = D.flo[2];
+      cn.zbits = D.zbits;
+    }
   }
   k_ext_reset<<<1, 32, 0, st>>>(h->ext, 1);
   CU(H, cudaMemsetAsync(h->h_bcnt, 0, (size_t)room * sizeof(uint32_t), st));
@@ -949,6 +967,7 @@ int dist_chunk_begin(bdm_ctx* H, DistGroup* G, int K) {
       D.h = h = nh;
       D.room = nroom;
       D.stepped = false;
+      D.fvalid = false;
       h->cur = 0;
       h->cols_next = false;
       h->state = State::NoGrid;
@@ -983,13 +1002,30 @@ int dist_chunk_begin(bdm_ctx* H, DistGroup* G, int K) {
       CU(H, cudaMemcpyAsync(D.ck_id, h->id[h->cur], D.live * sizeof(uint32_t), cudaMemcpyDeviceToDevice, G->stream));
     }
     // the frame of this chunk: x = [xb - 1, xe] clipped to the global extents +- M; y, z global +- M
-    // (applied by the chunk's first build: the first split still reads the last step's grid)
-    D.flo[0] = (int32_t)std::max<int64_t>((int64_t)D.xb - 1, (int64_t)G->glo[0] - M);
-    D.fhi[0] = (int32_t)std::min<int64_t>((int64_t)D.xe, (int64_t)G->ghi[0] + M);
-    if (D.flo[0] > D.fhi[0]) D.fhi[0] = D.flo[0];  // (a rank without agents near its slab)
+    // (applied by the chunk's first build: the first split still reads the last step's grid).  The
+    // previous chunk's frame is kept while it holds every agent of this chunk (the global extents
+    // +- (K + 1) boxes): then the last sum pass's fused columns and packed boxes stay valid.
+    int32_t nlo[3], nhi[3];
+    nlo[0] = (int32_t)std::max<int64_t>((int64_t)D.xb - 1, (int64_t)G->glo[0] - M);
+    nhi[0] = (int32_t)std::min<int64_t>((int64_t)D.xe, (int64_t)G->ghi[0] + M);
+    if (nlo[0] > nhi[0]) nhi[0] = nlo[0];  // (a rank without agents near its slab)
     for (int a = 1; a < 3; ++a) {
-      D.flo[a] = G->glo[a] - M;
-      D.fhi[a] = G->ghi[a] + M;
+      nlo[a] = G->glo[a] - M;
+      nhi[a] = G->ghi[a] + M;
+    }
+    bool keep = D.fvalid;
+    for (int a = 0; a < 3; ++a) keep = keep && nlo[a] >= D.flo[a] && nhi[a] <= D.fhi[a];
+    const bool keep_cols = keep && h->cols_next;
+    if (!keep) {  // a new frame, with the full margin of a longest chunk (kept for longer)
+      const int32_t MM = DIST_CHUNK + 1;
+      D.flo[0] = (int32_t)std::max<int64_t>((int64_t)D.xb - 1, (int64_t)G->glo[0] - MM);
+      D.fhi[0] = (int32_t)std::min<int64_t>((int64_t)D.xe, (int64_t)G->ghi[0] + MM);
+      if (D.flo[0] > D.fhi[0]) D.fhi[0] = D.flo[0];
+      for (int a = 1; a < 3; ++a) {
+        D.flo[a] = G->glo[a] - MM;
+        D.fhi[a] = G->ghi[a] + MM;
+      }
+      D.fvalid = true;
     }
     for (int a = 0; a < 3; ++a)
       if (D.flo[a] < -(1 << 20) + 2 || D.fhi[a] > (1 << 20) - 2)
@@ -1003,7 +1039,19 @@ int dist_chunk_begin(bdm_ctx* H, DistGroup* G, int K) {
       P = std::max(P, std::max(std::fabs((double)D.flo[a]), std::fabs((double)D.fhi[a] + 1.0)) * G->L * (1.0 + 0x1p-20));
     const double ulp32 = P > 0.0 ? std::ldexp(1.0, std::ilogb(P) - 23) : 0x1p-149;
     D.fm32 = 2.0 * ulp32 + 0x1p-18 + G->L * 0x1p-20;
-    h->cols_next = false;  // the first build of a chunk runs its own column pass
+    h->cols_next = keep_cols;  // else the first build of the chunk runs its own column pass
+    {  // packed new boxes: (column << zbits | z - flo[2]) when that fits 32 bits
+      const uint64_t ncols = (uint64_t)(D.fhi[0] - D.flo[0] + 1) * (uint64_t)(D.fhi[1] - D.flo[1] + 1);
+      int zb = 1;
+      while ((1 << zb) < D.fhi[2] - D.flo[2] + 1) ++zb;
+      D.zbits = zb < 31 && ncols <= (0xffffffffull >> zb) ? zb : 0;
+      if (D.zbits && (int64_t)h->pbox_cap < D.room) {
+        if (h->pbox) cudaFree(h->pbox);
+        h->pbox = nullptr;
+        CU(H, cudaMalloc(&h->pbox, D.room * sizeof(uint32_t)));
+        h->pbox_cap = (size_t)D.room;
+      }
+    }
     CU(H, cudaMemsetAsync(D.dc + DC_OVF, 0, 4 * sizeof(uint32_t), G->stream));  // OVF, NEED, MIG, GHOSTS
   }
   return BDM_OK;  // (no host synchronisation: everything above is ordered on the stream)

@@ -320,7 +320,8 @@ __global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ cz
   }
 }
 
-// rng (distributed steps, device counts): the agents [rng[0], rng[1]) of ag instead of [0, n) (n = bound)
+// rng (distributed steps, device counts): the agents [rng[0], rng[1]) of ag instead of [0, n), block-
+// strided over a small grid (the range is often short: the records appended since the last step)
 __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g, int32_t* __restrict__ czlo,
                           int32_t* __restrict__ czhi, const uint32_t* __restrict__ rng = nullptr) {
   uint32_t b0 = 0u;
@@ -329,8 +330,8 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
     n = __ldg(&rng[1]) - b0;
     ag += b0;
   }
-  if (blockIdx.x * (2 * blockDim.x) >= n) return;  // (whole blocks only: the warps reduce below)
-  const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
+  for (uint32_t blk = blockIdx.x; blk * (2 * blockDim.x) < n; blk += rng ? gridDim.x : 0xffffffffu) {
+  const uint32_t i0 = blk * (2 * blockDim.x) + threadIdx.x;
   const uint32_t ia[2] = {i0, i0 + blockDim.x};
   double4 pa[2];
 #pragma unroll
@@ -358,6 +359,8 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
       if (zmin < __ldcg(&czlo[c])) atomicMin(&czlo[c], zmin);
       if (zmax > __ldcg(&czhi[c])) atomicMax(&czhi[c], zmax);
     }
+  }
+  if (!rng) break;
   }
 }
 
@@ -393,8 +396,15 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
 template <bool GUARD>
 __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g, uint32_t* __restrict__ key,
                            uint32_t* __restrict__ slot, uint32_t* __restrict__ count, ErrDev* err,
-                           const uint32_t* __restrict__ n_dev = nullptr) {
+                           const uint32_t* __restrict__ n_dev = nullptr, const uint32_t* __restrict__ b0_dev = nullptr) {
   if (n_dev) n = __ldg(n_dev);
+  if (b0_dev) {  // (the agents [*b0_dev, n) only: the records appended after the packed ones)
+    const uint32_t b0 = __ldg(b0_dev);
+    n = n > b0 ? n - b0 : 0u;
+    ag += b0;
+    key += b0;
+    slot += b0;
+  }
   if (blockIdx.x * (2 * blockDim.x) >= n) return;  // (whole blocks only: the warps aggregate below)
   const uint32_t i0 = blockIdx.x * (2 * blockDim.x) + threadIdx.x;
   const uint32_t ia[2] = {i0, i0 + blockDim.x};
@@ -452,7 +462,8 @@ constexpr int KHP = BDM_KHP;
 template <bool GUARD>
 __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n, GridDev g, int32_t z0, int32_t zbits,
                                   uint32_t* __restrict__ key, uint32_t* __restrict__ slot,
-                                  uint32_t* __restrict__ count, ErrDev* err) {
+                                  uint32_t* __restrict__ count, ErrDev* err, const uint32_t* __restrict__ n_dev = nullptr) {
+  if (n_dev) n = __ldg(n_dev);  // (distributed steps: dead emigrants carry pbox 0xffffffff and are dropped)
   const uint32_t i0 = blockIdx.x * (KHP * blockDim.x) + threadIdx.x;
   uint32_t pa[KHP];
 #pragma unroll
@@ -464,7 +475,7 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
   for (int u = 0; u < KHP; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
     k[u] = 0xffffffffu;
-    if (i < n) {
+    if (i < n && pa[u] != 0xffffffffu) {
       uint32_t c = pa[u] >> zbits;
       const int bz = z0 + (int)(pa[u] & ((1u << zbits) - 1u));
       const bool okc = !GUARD || c < g.n_cols;
@@ -2756,7 +2767,8 @@ __global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __r
 
 // bdm_slab_commit: emigrants of the split (same boundary ranges) are marked dead (D < 0) in place.
 __global__ void k_slab_mark_dead(double4* __restrict__ ag, uint32_t n, const uint32_t* __restrict__ r2, double inv,
-                                 int32_t x_begin, int32_t x_end, const uint32_t* __restrict__ n_dev = nullptr) {
+                                 int32_t x_begin, int32_t x_end, const uint32_t* __restrict__ n_dev = nullptr,
+                                 uint32_t* __restrict__ pbox = nullptr) {
   if (n_dev) n = __ldg(n_dev);
   const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
   const uint32_t hi0 = r2[1] > n_lo_part ? r2[1] : n_lo_part;
@@ -2764,7 +2776,10 @@ __global__ void k_slab_mark_dead(double4* __restrict__ ag, uint32_t n, const uin
   for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t i = t < n_lo_part ? (uint32_t)t : hi0 + (uint32_t)(t - n_lo_part);
     const int bx = (int)floor(ag[i].x * inv);
-    if (bx < x_begin || bx >= x_end) ag[i].w = -1.0;
+    if (bx < x_begin || bx >= x_end) {
+      ag[i].w = -1.0;
+      if (pbox) pbox[i] = 0xffffffffu;
+    }
   }
 }
 
