@@ -388,6 +388,22 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
 }
 
 // ------------------------------------------------------------------------------------------ K2
+// Warp aggregation of histogram atomics over runs of equal keys in consecutive lanes (the agents
+// arrive in the last step's sorted order, so a box's agents are mostly adjacent): one shuffle and
+// one ballot per element instead of __match_any_sync (which kept the key passes MIO-throttled).
+// Returns the run's first lane; *len the run length.  Equal keys in separate runs get separate
+// atomics (correct, just not merged).
+__device__ __forceinline__ int key_run(uint32_t k, int lane, uint32_t& len) {
+  const uint32_t prev = __shfl_up_sync(FULL, k, 1);
+  const unsigned heads = __ballot_sync(FULL, lane == 0 || prev != k);
+  const unsigned upto = lane == 31 ? FULL : ((2u << lane) - 1u);  // lanes 0..lane
+  const int start = 31 - __clz(heads & upto);
+  const unsigned above = heads & ~upto;
+  const int end = above ? __ffs(above) - 1 : 32;
+  len = (uint32_t)(end - start);
+  return start;
+}
+
 // Two agents per thread (block-strided, both loads coalesced and in flight together).
 // GUARD (deferred builds, whose extents were not checked on the host): an agent whose box lies
 // outside the grid (a non-finite or out-of-range position) is counted in box 0 and reported (code 7)
@@ -435,20 +451,21 @@ __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g
     }
     kk[u] = k;
   }
-  // warp-aggregated histogram (one atomic per distinct key in the warp), both atomics in flight
+  // warp-aggregated histogram (one atomic per run of equal keys), both atomics in flight
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    peers[u] = __match_any_sync(FULL, kk[u]);
+    uint32_t len;
+    peers[u] = (uint32_t)key_run(kk[u], lane, len);  // (the run's first lane)
     base[u] = 0u;
-    if (kk[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1)
-      base[u] = (BDM_ASSERT(kk[u] < __ldg(&g.coff[g.n_cols])), atomicAdd(&count[kk[u]], (uint32_t)__popc(peers[u])));
+    if (kk[u] != 0xffffffffu && lane == (int)peers[u])
+      base[u] = (BDM_ASSERT(kk[u] < __ldg(&g.coff[g.n_cols])), atomicAdd(&count[kk[u]], len));
   }
 #pragma unroll
   for (int u = 0; u < 2; ++u) {
-    const uint32_t b = __shfl_sync(FULL, base[u], __ffs(peers[u]) - 1);
+    const uint32_t b = __shfl_sync(FULL, base[u], (int)peers[u]);
     if (ia[u] < n) {
       key[ia[u]] = kk[u];
-      slot[ia[u]] = b + __popc(peers[u] & ((1u << lane) - 1u));
+      slot[ia[u]] = b + (uint32_t)(lane - (int)peers[u]);
     }
   }
 }
@@ -488,23 +505,25 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
       }
     }
   }
-  // the four warp-aggregated atomics in flight together, then their bases broadcast
+  // the four warp-aggregated atomics (one per run of equal keys) in flight together, then their bases
+  // broadcast
 #pragma unroll
   for (int u = 0; u < KHP; ++u) {
-    peers[u] = __match_any_sync(FULL, k[u]);
+    uint32_t len;
+    peers[u] = (uint32_t)key_run(k[u], lane, len);  // (the run's first lane)
     base[u] = 0u;
-    if (k[u] != 0xffffffffu && lane == __ffs(peers[u]) - 1) {
+    if (k[u] != 0xffffffffu && lane == (int)peers[u]) {
       BDM_ASSERT(k[u] < __ldg(&g.coff[g.n_cols]));
-      base[u] = atomicAdd(&count[k[u]], (uint32_t)__popc(peers[u]));
+      base[u] = atomicAdd(&count[k[u]], len);
     }
   }
 #pragma unroll
   for (int u = 0; u < KHP; ++u) {
     const uint32_t i = i0 + u * blockDim.x;
-    const uint32_t b = __shfl_sync(FULL, base[u], __ffs(peers[u]) - 1);
+    const uint32_t b = __shfl_sync(FULL, base[u], (int)peers[u]);
     if (i < n) {
       key[i] = k[u];
-      slot[i] = b + __popc(peers[u] & ((1u << lane) - 1u));
+      slot[i] = b + (uint32_t)(lane - (int)peers[u]);
     }
   }
 }
