@@ -34,6 +34,9 @@ const int g_defer = std::getenv("BDM_DEFER") ? std::atoi(std::getenv("BDM_DEFER"
 // BDM_HTILE=1: pass A with the TMA-staged neighbourhood (k_half_search_tile, warp-specialised producer);
 // measured slower than k_half_search on cfg3, so off by default
 const bool g_htile = std::getenv("BDM_HTILE") && std::getenv("BDM_HTILE")[0] == '1';
+// BDM_BANDS=b: the force phase in b bands of the sorted order, the sum pass of band k on a second
+// stream as soon as the searches of bands 0..k are done; 1 = one launch per pass
+const int g_bands = std::getenv("BDM_BANDS") ? std::max(1, std::min(32, std::atoi(std::getenv("BDM_BANDS")))) : 1;
 // BDM_PBOX=0: the key pass re-reads the state instead of the sum pass's packed boxes
 const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
 
@@ -164,6 +167,9 @@ struct bdm_ctx {
   uint32_t last_n_lo = 0;      // slab: lower ghosts of the last step (sorted first)
   int32_t split_xb = 0, split_xe = 0;
   int sm_count = 0, force_blocks_per_sm = 0, half_a_blocks_per_sm = 0, half_b_blocks_per_sm = 0, tile_blocks_per_sm = 0;
+  cudaStream_t s2 = nullptr;          // banded force phase: the sum passes' stream
+  cudaEvent_t bev[33] = {};           // ... and its events (search of band k done; all sums done)
+  uint32_t* bwork = nullptr;          // ... chunk-ticket counters of every band's two passes
   int64_t launches = 0;  // kernels of this library launched by mech_step / grid_build (since bdm_get_timing)
   int64_t launches_total = 0;  // launches before the last bdm_get_timing reset
   int64_t host_syncs = 0;      // host synchronisations with the device (bdm_get_stats)
@@ -433,6 +439,50 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     }
   }
   CU(h, cudaMemsetAsync(h->h_bcnt, 0, (size_t)std::max<uint32_t>(n_all, 1) * sizeof(uint32_t), s));
+  // banded force phase: bands of >= 2^20 agents each
+  const int nb = force_only ? 1 : (int)std::min<int64_t>(g_bands, std::max<int64_t>(1, ((int64_t)a_end - a_begin) >> 20));
+  if (nb > 1) {
+    if (!h->s2) {
+      CU(h, cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
+      for (int k = 0; k < 33; ++k) CU(h, cudaEventCreateWithFlags(&h->bev[k], cudaEventDisableTiming));
+      CU(h, cudaMalloc(&h->bwork, 64 * sizeof(uint32_t)));
+    }
+    CU(h, cudaMemsetAsync(h->bwork, 0, 64 * sizeof(uint32_t), s));
+    const uint32_t bs = (uint32_t)(((((uint64_t)a_end - a_begin) / nb) + 31) / 32 * 32);
+    auto cut = [&](int k) { return k == 0 ? a_begin : (k >= nb ? a_end : std::min<uint32_t>(a_end, a_begin + (uint32_t)k * bs)); };
+    for (int k = 0; k < nb; ++k) {
+      const uint32_t sb = k == 0 ? s_begin : cut(k), se = cut(k + 1);
+      const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
+                                                       std::max<uint64_t>(1, (se - sb + HA_THREADS - 1) / HA_THREADS));
+      k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, s>>>(h->ag[src], h->agf, sb, se, h->grid, h->h_fwd, h->h_fcnt,
+                                                           h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr && k == 0,
+                                                           nullptr, h->bwork + k);
+      CU(h, cudaEventRecord(h->bev[k], s));
+    }
+    if (h->timing && !h->timed.empty() && !h->timed.back().e3) {
+      CU(h, cudaEventCreate(&h->timed.back().e3));
+      CU(h, cudaEventRecord(h->timed.back().e3, s));
+    }
+    for (int k = 0; k < nb; ++k) {  // band k's rows are complete once the searches of bands 0..k are
+      CU(h, cudaStreamWaitEvent(h->s2, h->bev[k], 0));
+      const uint32_t ab = cut(k), ae = cut(k + 1);
+      const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
+                                                       std::max<uint64_t>(1, (ae - ab + FORCE_THREADS - 1) / FORCE_THREADS));
+      k_half_sum<false><<<gb, FORCE_THREADS, HB_SMEM_BYTES, h->s2>>>(
+          h->ag[src], h->id[src], ab, ae, h->grid, pd, ag_out, id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt,
+          h->h_bwd, h->h_bcnt, cn, hist_out, h->h_slow, nullptr, h->bwork + 32 + k, (int64_t)a_begin);
+    }
+    CU(h, cudaEventRecord(h->bev[nb], h->s2));
+    CU(h, cudaStreamWaitEvent(s, h->bev[nb], 0));
+    const unsigned gs = (unsigned)h->sm_count * 4;
+    k_half_slow<false><<<gs, 128, 0, s>>>(h->ag[src], h->id[src], a_begin, h->grid, pd, ag_out, id_out, dp, dp_ids,
+                                          h->ext, h->err, cn, hist_out, h->h_slow);
+    k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
+    CU(h, cudaGetLastError());
+    h->launches += 2 * nb + 2;
+    h->cols_next = fuse_cols;
+    return BDM_OK;
+  }
   if (g_htile) {  // staged neighbourhood
     const unsigned gt = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->tile_blocks_per_sm,
                                                      std::max<uint64_t>(1, (a_end - s_begin + TILE_AG - 1) / TILE_AG));
@@ -1066,6 +1116,13 @@ void bdm_destroy(bdm_handle h) {
   cudaGetDevice(&prev);
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->stream);
+  if (h->s2) {
+    cudaStreamSynchronize(h->s2);
+    cudaStreamDestroy(h->s2);
+    for (auto& e : h->bev)
+      if (e) cudaEventDestroy(e);
+    cudaFree(h->bwork);
+  }
   for (auto& t : h->timed) {
     cudaEventDestroy(t.e0);
     cudaEventDestroy(t.e1);

@@ -1542,8 +1542,9 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     k_half_search(const double4* __restrict__ ag, const float4* __restrict__ agf, uint32_t s_begin, uint32_t s_end,
                   GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
                   uint32_t* __restrict__ bcnt, Extents* ext, bool count_searched,
-                  const uint32_t* __restrict__ s_end_dev = nullptr) {
+                  const uint32_t* __restrict__ s_end_dev = nullptr, uint32_t* __restrict__ work = nullptr) {
   if (s_end_dev) s_end = __ldg(s_end_dev);
+  if (!work) work = &ext->work_a;  // (banded launches: the band's own counter)
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfASmem& sm = reinterpret_cast<HalfASmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -1560,7 +1561,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   Tickets tk(s_end - s_begin);
 #if BDM_HAPF
   // the next chunk's fp32 agents are loaded one chunk ahead (four registers)
-  uint32_t chunk = tk.take(&ext->work_a, lane);
+  uint32_t chunk = tk.take(work, lane);
   float4 mf_next = make_float4(0.f, 0.f, 0.f, 0.f);
   {
     const uint64_t i1 = (uint64_t)s_begin + 32ull * chunk + lane;
@@ -1569,7 +1570,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
 #endif
   while (true) {
 #if !BDM_HAPF
-    const uint32_t chunk = tk.take(&ext->work_a, lane);
+    const uint32_t chunk = tk.take(work, lane);
 #endif
     const uint64_t base = (uint64_t)s_begin + 32ull * chunk;
     if (base >= s_end) break;
@@ -1577,7 +1578,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     const bool valid = i < s_end;
 #if BDM_HAPF
     const float4 mf = mf_next;
-    chunk = tk.take(&ext->work_a, lane);
+    chunk = tk.take(work, lane);
     {
       const uint64_t i1 = (uint64_t)s_begin + 32ull * chunk + lane;
       mf_next = i1 < s_end ? __ldg(&agf[i1]) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -2325,11 +2326,16 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                double* __restrict__ dp_out, uint32_t* __restrict__ dp_id_out, Extents* ext_next, ErrDev* err,
                const uint32_t* __restrict__ fwd, const uint8_t* __restrict__ fcnt, const uint32_t* __restrict__ bwd,
                const uint32_t* __restrict__ bcnt, ColNext cn, unsigned long long* __restrict__ hist_out,
-               uint32_t* __restrict__ slow_list, const uint32_t* __restrict__ ab_dev = nullptr) {
+               uint32_t* __restrict__ slow_list, const uint32_t* __restrict__ ab_dev = nullptr,
+               uint32_t* __restrict__ work = nullptr, int64_t o_base = -1) {
   if (ab_dev) {  // distributed steps: the owned range [a_begin, a_end) read on the device
     a_begin = __ldg(&ab_dev[0]);
     a_end = __ldg(&ab_dev[1]);
   }
+  // banded launches: this launch sums [a_begin, a_end), outputs are indexed from the
+  // whole owned range's first agent o_base, chunk tickets come from the band's own counter
+  const uint32_t ob = o_base >= 0 ? (uint32_t)o_base : a_begin;
+  if (!work) work = &ext_next->work;
   extern __shared__ __align__(16) unsigned char s_raw[];
   HalfBSmem& sm = reinterpret_cast<HalfBSmem*>(s_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
@@ -2342,8 +2348,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
 #if BDM_HRPF
   // merged rows: the pair counts are loaded two chunks ahead and the first vector of each row one
   // chunk ahead (the count is there by then), so a chunk's dependent chain starts at its partners
-  uint32_t chunk = tk.take(&ext_next->work, lane);
-  uint32_t chunk_n = tk.take(&ext_next->work, lane);
+  uint32_t chunk = tk.take(work, lane);
+  uint32_t chunk_n = tk.take(work, lane);
   uint32_t nb_n = 0u, nb_nn = 0u;
   uint4 r4_n = make_uint4(0u, 0u, 0u, 0u);
   {
@@ -2356,7 +2362,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
 #elif BDM_HBCNT
   // the next chunk's pair counts are loaded one chunk ahead (two registers): a chunk's dependent
   // chain then starts at its rows
-  uint32_t chunk = tk.take(&ext_next->work, lane);
+  uint32_t chunk = tk.take(work, lane);
   uint32_t nf_n = 0u, nb_n = 0u;
   {
     const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
@@ -2368,7 +2374,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
 #endif
   while (true) {
 #if !BDM_HBCNT && !BDM_HRPF
-    const uint32_t chunk = tk.take(&ext_next->work, lane);
+    const uint32_t chunk = tk.take(work, lane);
 #endif
     const uint64_t base = (uint64_t)a_begin + 32ull * chunk;
     if (base >= a_end) break;
@@ -2385,7 +2391,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     {  // rotate: next chunk's first row vector (its count arrived during this chunk's predecessor),
        // the count of the chunk after it
       chunk = chunk_n;
-      chunk_n = tk.take(&ext_next->work, lane);
+      chunk_n = tk.take(work, lane);
       const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
       nb_n = nb_nn;
       r4_n = nb_n ? __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)i1 * HBC)) : make_uint4(0u, 0u, 0u, 0u);
@@ -2394,7 +2400,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     }
 #elif BDM_HBCNT
     const uint32_t nf = nf_n, nb = nb_n;
-    chunk = tk.take(&ext_next->work, lane);
+    chunk = tk.take(work, lane);
     {
       const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
       nf_n = i1 < a_end && !BDM_MROW ? fcnt[i1] : 0u;
@@ -2491,7 +2497,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     if (FONLY) {
       if (live) {
         if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz))) report(err, 6u /*ENONFINITE*/, ids[i], i);
-        const size_t o = 3 * (size_t)(i - a_begin);
+        const size_t o = 3 * (size_t)(i - ob);
         dp_out[o] = Fx;
         dp_out[o + 1] = Fy;
         dp_out[o + 2] = Fz;
@@ -2518,7 +2524,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     if (live) {
       if (!(isfinite(Fx) && isfinite(Fy) && isfinite(Fz) && isfinite(fn))) report(err, 6u /*ENONFINITE*/, ids[i], i);
       const double4 np = make_double4(me.x + dpx, me.y + dpy, me.z + dpz, me.w);
-      const uint32_t o = i - a_begin;
+      const uint32_t o = i - ob;
       st_state(&ag_out[o], np);
       if (hist_out) {
         const bool moved = dpx != 0.0 || dpy != 0.0 || dpz != 0.0;
@@ -2567,7 +2573,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
         if (cn.pbox) {  // the next build's column and z, so its key pass need not re-read the state
           const uint32_t uz = (uint32_t)(nb3[2] - cn.z0);
           out |= uz >> cn.zbits != 0u;
-          cn.pbox[i - a_begin] = (c << cn.zbits) | uz;
+          cn.pbox[i - ob] = (c << cn.zbits) | uz;
         }
       }
       const unsigned peers = __match_any_sync(FULL, c);  // (a run-based mask here measured slower: 0.77 ms)
