@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan(uint32_t* __restrict__ da
 // ------------------------------------------------------------------------------------------ K4
 // (KSC agents per thread, all loads of a level in flight together: the pass is latency-bound)
 #ifndef BDM_KSC
-#define BDM_KSC 4  // agents per thread in k_scatter
+#define BDM_KSC 2  // agents per thread in k_scatter
 #endif
 constexpr int KSC = BDM_KSC;
 __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __restrict__ slot,
@@ -1280,12 +1280,12 @@ constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
 #endif
 constexpr int HA_THREADS = 256;
 #ifndef BDM_HA_MIN_BLOCKS
-#define BDM_HA_MIN_BLOCKS 4
+#define BDM_HA_MIN_BLOCKS 5
 #endif
 #ifndef BDM_HB_MIN_BLOCKS
 #define BDM_HB_MIN_BLOCKS 4
 #endif
-constexpr int HA_MIN_BLOCKS = BDM_HA_MIN_BLOCKS;  // pass A: 4 x 8 resident warps per SM
+constexpr int HA_MIN_BLOCKS = BDM_HA_MIN_BLOCKS;  // pass A: 5 x 8 resident warps per SM (48 registers)
 constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 
 #ifndef BDM_HMAP
