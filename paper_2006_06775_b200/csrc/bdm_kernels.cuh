@@ -808,7 +808,7 @@ constexpr int FORCE_WARPS = FORCE_THREADS / 32;
 #endif
 constexpr int FORCE_MIN_BLOCKS = BDM_FORCE_MIN_BLOCKS;  // 3: 24 resident warps per SM
 #ifndef BDM_NSLOT
-#define BDM_NSLOT 4  // candidate slots per iteration of the k_force candidate loop
+#define BDM_NSLOT 3  // candidate slots per iteration of the candidate loops (k_force, pass A)
 #endif
 constexpr int NSLOT = BDM_NSLOT;
 #ifndef BDM_CURSOR
