@@ -116,14 +116,14 @@ int bdm_grid_build(bdm_handle h);
  * update all positions (O7, Jacobi).  Asynchronous; errors detected on the device are reported by
  * the next synchronising call.  Inside one call, the rebuilds of steps 0..n_steps-2 may skip their
  * host round trip (deferred builds; at most bdm_set_defer's count in a row, default
- * 0 = off): a range or frame error of such a step is then reported by the next
+ * 8): a range or frame error of such a step is then reported by the next
  * synchronised rebuild (at the latest the last step of the same call) as BDM_ERANGE, and the handle
  * is poisoned; the results of the steps in between are not to be used.  Displacements are stored
  * for the last step of the call only (bdm_get_displacements). */
 int bdm_mech_step(bdm_handle h, int32_t n_steps);
 
 /* At most max_deferred consecutive deferred builds inside one bdm_mech_step call (see above; 0 = a
- * host round trip every build, the default unless the environment sets BDM_DEFER).  EINVAL if
+ * host round trip every build; default 8, or the environment's BDM_DEFER).  EINVAL if
  * max_deferred < 0. */
 int bdm_set_defer(bdm_handle h, int max_deferred);
 
