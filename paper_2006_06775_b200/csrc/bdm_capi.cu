@@ -707,7 +707,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
     k_scatter<<<blocks(n, 256 * KSC), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
     DBG(h, "k_scatter");
     const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
-    k_place<<<blocks(n - n_dead, 256), 256, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n - n_dead, h->ag[dst],
+    k_place<<<blocks(n - n_dead, PLACE_T), PLACE_T, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n - n_dead, h->ag[dst],
                                            h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
                                            perm_hist ? h->hist[dst] : nullptr);
     DBG(h, "k_place");

@@ -460,6 +460,12 @@ struct DistGroup {
   // statistics
   int64_t steps = 0, chunks = 0, redo = 0, syncs = 0, bytes = 0, migrated = 0, ghosts = 0;
   double* red = nullptr;  // device scratch for reductions (64 doubles)
+  // CUDA graph of two steady steps (fused columns, no displacements kept), replayed inside chunks;
+  // valid while the signature of what its launches baked in is unchanged
+  cudaGraphExec_t gexec = nullptr;
+  std::vector<uintptr_t> gsig;
+  int64_t graph_launches = 0, graph_bytes = 0;  // per replay: kernels and exchange bytes of the pair
+  int64_t replays = 0;
 };
 
 // Host reductions across ranks.  Virtual mode: the local slabs are all the ranks (reduced here);
@@ -864,7 +870,7 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     k_scatter<<<blocks(room, 256 * KSC), 256, 0, st>>>(h->key, h->slot, h->id[src0], h->table, room, h->tsrc, h->tid,
                                                        h->tkey, D.dc + DC_TOT);
     DBG(h, "k_scatter(dist)");
-    k_place<<<blocks(room, 256), 256, 0, st>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src0], room, h->ag[1 - src0],
+    k_place<<<blocks(room, PLACE_T), PLACE_T, 0, st>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src0], room, h->ag[1 - src0],
                                               h->id[1 - src0], h->agf, nullptr, nullptr, D.dc + DC_SORTED);
     DBG(h, "k_place(dist)");
     CU(H, cudaGetLastError());
@@ -1151,18 +1157,101 @@ int dist_mech_step(bdm_ctx* H, int32_t n_steps) {
   return rc;
 }
 
+int dist_step(bdm_ctx* H, DistGroup* G, bool want_dp) {
+  int rc = dist_split_all(H, G);
+  if (rc) return rc;
+  for (auto& D : G->sl)
+    if ((rc = dist_ingest_build_force(H, G, D, want_dp))) return rc;
+  return BDM_OK;
+}
+
+// What the steady pair's launches bake in: buffers, frame, capacity, parity, column arrays.
+std::vector<uintptr_t> dist_signature(DistGroup* G) {
+  std::vector<uintptr_t> v{(uintptr_t)G->cap, (uintptr_t)G->stream};
+  for (auto& D : G->sl) {
+    bdm_ctx* h = D.h;
+    for (uintptr_t x : {(uintptr_t)h, (uintptr_t)h->cur, (uintptr_t)h->czlo, (uintptr_t)h->czlo2, (uintptr_t)h->table,
+                        (uintptr_t)h->coff, (uintptr_t)h->colrec, (uintptr_t)h->pbox, (uintptr_t)h->h_fwd,
+                        (uintptr_t)h->scan_state, (uintptr_t)D.room, (uintptr_t)D.zbits, (uintptr_t)D.msg[0],
+                        (uintptr_t)D.msg[2], (uintptr_t)(uint32_t)D.flo[0], (uintptr_t)(uint32_t)D.flo[1],
+                        (uintptr_t)(uint32_t)D.flo[2], (uintptr_t)(uint32_t)D.fhi[0], (uintptr_t)(uint32_t)D.fhi[1],
+                        (uintptr_t)(uint32_t)D.fhi[2], (uintptr_t)h->cols_next, (uintptr_t)D.stepped})
+      v.push_back(x);
+  }
+  return v;
+}
+
+// npairs x two steady steps through one CUDA graph (captured once per signature): the ~30 launches and
+// the NCCL group of a step cost a few microseconds each when issued one by one.  The host-side state a
+// step mutates (buffer parity, column array swaps) has period two, so it is back where it started.
+int dist_steady_pairs(bdm_ctx* H, DistGroup* G, int npairs) {
+  const std::vector<uintptr_t> sig = dist_signature(G);
+  if (!G->gexec || sig != G->gsig) {
+    if (G->gexec) cudaGraphExecDestroy(G->gexec);
+    G->gexec = nullptr;
+    int64_t l0 = 0, b0 = G->bytes;
+    for (auto& D : G->sl) l0 += D.h->launches;
+    CU(H, cudaStreamBeginCapture(G->stream, cudaStreamCaptureModeThreadLocal));
+    int rc = dist_step(H, G, false);
+    if (!rc) rc = dist_step(H, G, false);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(G->stream, &graph);
+    if (rc || ce != cudaSuccess || !graph) {
+      (void)cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      return rc ? rc : fail(H, BDM_ECUDA, "graph capture of the steady steps: %s", cudaGetErrorString(ce));
+    }
+    const cudaError_t ie = cudaGraphInstantiate(&G->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      (void)cudaGetLastError();
+      G->gexec = nullptr;
+      return fail(H, BDM_ECUDA, "graph instantiation: %s", cudaGetErrorString(ie));
+    }
+    int64_t l1 = 0;
+    for (auto& D : G->sl) l1 += D.h->launches;
+    G->graph_launches = l1 - l0;
+    G->graph_bytes = G->bytes - b0;  // (the capture counted one pair: that of the launch just below)
+    G->gsig = dist_signature(G);
+    if (G->gsig != sig) return fail(H, BDM_ECUDA, "steady steps are not of period two");
+    // the capture recorded one pair without running it: run it now
+    --npairs;
+    CU(H, cudaGraphLaunch(G->gexec, G->stream));
+    ++G->replays;
+  }
+  for (int p = 0; p < npairs; ++p) {
+    CU(H, cudaGraphLaunch(G->gexec, G->stream));
+    ++G->replays;
+    G->sl[0].h->launches += G->graph_launches;
+    G->bytes += G->graph_bytes;
+  }
+  return BDM_OK;
+}
+
 int dist_mech_step_(bdm_ctx* H, int32_t n_steps) {
   DistGroup* G = H->dist;
   int done = 0;
+  // graphs need a capturable stream (not the legacy default stream) and no per-step host work
+  bool use_graph = G->stream != nullptr && !g_debug && !std::getenv("BDM_DIST_NOGRAPH");
+  for (auto& D : G->sl) use_graph = use_graph && !D.h->timing;
   while (done < n_steps) {
     const int K = std::min(DIST_CHUNK, n_steps - done);
     int rc = dist_chunk_begin(H, G, K);
     if (rc) return rc;
-    for (int k = 0; k < K; ++k) {
+    int k = 0;
+    while (k < K) {
       const bool last = done + k == n_steps - 1;
-      if ((rc = dist_split_all(H, G))) return rc;
-      for (auto& D : G->sl)
-        if ((rc = dist_ingest_build_force(H, G, D, last))) return rc;
+      // steady pairs: after the chunk's first step (fused columns from then on), before the last step
+      // of the call (which keeps the displacements)
+      const int steady = (K - 1) - k - (done + K == n_steps ? 1 : 0);
+      if (use_graph && k >= 1 && steady >= 2) {
+        const int np = steady / 2;
+        if ((rc = dist_steady_pairs(H, G, np))) return rc;
+        k += 2 * np;
+        continue;
+      }
+      if ((rc = dist_step(H, G, last))) return rc;
+      ++k;
     }
     int redo = 0;
     if ((rc = dist_chunk_end(H, G, &redo))) return rc;
@@ -1220,6 +1309,7 @@ int dist_get_timing(bdm_ctx* H, double* out6) {
 
 void dist_destroy(DistGroup* G) {
   if (!G) return;
+  if (G->gexec) cudaGraphExecDestroy(G->gexec);
   for (auto& D : G->sl) {
     for (int k = 0; k < 4; ++k)
       if (D.msg[k]) cudaFree(D.msg[k]);

@@ -678,6 +678,10 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __re
   }
 }
 
+#ifndef BDM_PLACE_T
+#define BDM_PLACE_T 256
+#endif
+constexpr int PLACE_T = BDM_PLACE_T;  // threads per k_place block
 // Rank inside the box by id (boxes hold a handful of agents), then gather the payload.
 __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __restrict__ tid,
                         const uint32_t* __restrict__ tkey, const uint32_t* __restrict__ start,
