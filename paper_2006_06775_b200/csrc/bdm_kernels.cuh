@@ -1270,8 +1270,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
 //     the balanced contact phase of k_force, then O6/O7.  So Δp is bit-identical to k_force's.
 // Rows hold HFC / HBC entries; an agent whose row overflowed takes a slow path in pass B (a full
 // 27-box canonical search of its own), so the result does not depend on the capacities.
-constexpr int HFC = 16;  // forward row capacity (entries per agent)
-constexpr int HBC = 16;  // backward row capacity
+#ifndef BDM_HROW
+#define BDM_HROW 16
+#endif
+constexpr int HFC = BDM_HROW;  // forward row capacity (entries per agent; merged rows: all its entries)
+constexpr int HBC = BDM_HROW;  // backward row capacity
 constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
 #ifndef BDM_HBCNT
 #define BDM_HBCNT 1  // pass B loads the next chunk's pair counts one chunk ahead
@@ -1376,7 +1379,9 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
 #if BDM_MROW
   // own entries: a base slot for all of them (the overflow beyond the list counts, so a row that
   // cannot hold everything is recognised by its count); its round trip overlaps the partners' atomics
-  const uint32_t nf = (uint32_t)cnt + extra;
+  // (survivors beyond the list were not kept: push the count past the row so the sum pass takes the
+  // exact full search for i)
+  const uint32_t nf = (uint32_t)cnt + extra + (extra ? (uint32_t)HFC : 0u);
   const uint32_t base = nf ? atomicAdd(&bcnt[i], nf) : 0u;
 #elif BDM_V256
   uint32_t* frow = fwd + (size_t)i * HFC;  // 64-byte rows: one 256-bit store per used sector
@@ -2266,23 +2271,29 @@ struct HalfBSmem {
 };
 constexpr size_t HB_SMEM_BYTES = sizeof(HalfBSmem) * FORCE_WARPS;
 
-// Full canonical 27-box sum of agent i (O3-O5 as written): the overflow path of pass B.
-__device__ __noinline__ double3 full_force(const GridDev& g, const double4* __restrict__ ag,
-                                           const uint32_t* __restrict__ ids, const ParamsDev& p, uint32_t i,
-                                           double4 me) {
+// Full canonical 27-box sum of agent i (O3-O5 as written) by one warp -- the overflow path of pass B.
+// All lanes call it and all return the sum: the lanes evaluate 32 candidates of a z-run at a time,
+// then every lane adds the batch's contact terms in candidate order (shuffled from their lanes), the
+// same sequence of separately rounded additions as a sequential walk, without one thread walking a
+// dense neighbourhood alone (a lone overflow agent of a cfg3 step took ~40 us that way).
+__device__ __forceinline__ double3 full_force_warp(const GridDev& g, const double4* __restrict__ ag,
+                                                   const uint32_t* __restrict__ ids, const ParamsDev& p, uint32_t i,
+                                                   double4 me, int lane) {
   const double ri = 0.5 * me.w;
   const int bx = (int)floor(me.x * g.inv), by = (int)floor(me.y * g.inv), bz = (int)floor(me.z * g.inv);
   double Fx = 0.0, Fy = 0.0, Fz = 0.0;
   for (int c = 0; c < 9; ++c) {
     uint32_t b = 0, e = 0;
     if (!zrun(g, bx + c / 3 - 1, by + c % 3 - 1, bz - 1, bz + 1, b, e)) continue;
-    for (uint32_t j = b; j < e; ++j) {
-      if (j == i) continue;
-      double tx, ty, tz, fa;
-      if (pair_term(me.x, me.y, me.z, ri, i, ag[j], ids, j, p, tx, ty, tz, fa)) {
-        Fx = Fx + tx;
-        Fy = Fy + ty;
-        Fz = Fz + tz;
+    for (uint32_t j0 = b; j0 < e; j0 += 32) {
+      const uint32_t j = j0 + (uint32_t)lane;
+      double tx = 0.0, ty = 0.0, tz = 0.0, fa;
+      const bool hit = j < e && j != i && pair_term(me.x, me.y, me.z, ri, i, ag[j], ids, j, p, tx, ty, tz, fa);
+      for (unsigned m = __ballot_sync(FULL, hit); m; m &= m - 1u) {
+        const int src = __ffs(m) - 1;
+        Fx = Fx + __shfl_sync(FULL, tx, src);
+        Fy = Fy + __shfl_sync(FULL, ty, src);
+        Fz = Fz + __shfl_sync(FULL, tz, src);
       }
     }
   }
@@ -2618,10 +2629,13 @@ __global__ void __launch_bounds__(128) k_half_slow(const double4* __restrict__ a
                                                    const uint32_t* __restrict__ ab_dev = nullptr) {
   if (ab_dev) a_begin = __ldg(&ab_dev[0]);
   const uint32_t n_slow = __ldcg(&ext_next->slow);
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_slow; k += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+  for (uint32_t k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < n_slow; k += warps) {  // warp per agent
     const uint32_t i = slow_list[k];
     const double4 me = ag[i];
-    const double3 f = full_force(g, ag, ids, p, i, me);
+    const double3 f = full_force_warp(g, ag, ids, p, i, me, lane);
+    if (lane != 0) continue;  // (lane 0 writes the agent's results)
     const double Fx = f.x, Fy = f.y, Fz = f.z;
     const uint32_t o = i - a_begin;
     if (FONLY) {
