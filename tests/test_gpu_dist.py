@@ -184,3 +184,40 @@ def test_dist_graph_replayed_steps_equal_oracle(bdm, G):
     o_p, o_dp = oracle.run(pos, diam, 20)
     assert np.array_equal(p, o_p) and np.array_equal(d, o_dp)
     assert bdm.bdm_get_stats(h)["chunks"] == 2
+
+
+def test_dist_new_batch_reuses_handle(bdm):
+    """bdm_set_agents_dist: a second population through the same handle (communicator and buffers
+    reused, cuts recomputed) is stepped exactly like a fresh one."""
+    import torch
+
+    st = torch.cuda.Stream()
+    p1, d1 = bdm_inputs.make_config(2, n=25 ** 3)
+    p2, d2 = bdm_inputs.random_instance(21, 9000, 260.0, 8.0, 12.0)
+    uid = bdm.bdm_nccl_unique_id()
+    h = bdm.bdm_init_dist(np.arange(len(d1), dtype=np.int64), p1, d1, rank=0, world=1, uid=uid, device=0, stream=st)
+    bdm.bdm_mech_step(h, 3)
+    bdm.bdm_set_agents_dist(h, np.arange(len(d2), dtype=np.int64), p2, d2)
+    bdm.bdm_mech_step(h, 4)
+    p = gather(bdm, h, bdm.BDM_OWNED_POSITIONS, len(d2))
+    o_p, _ = oracle.run(p2, d2, 4)
+    assert np.array_equal(p, o_p)
+
+
+def test_dist_cuts_balance_work_not_count(bdm):
+    """Gaussian population (dense core): the work-balanced cuts give the core ranks narrower slabs
+    than count-balanced cuts would; every inner slab is at least 2 boxes wide."""
+    pos, diam = bdm_inputs.make_config(3, n=400_000)
+    n = len(diam)
+    G = 4
+    h = bdm.bdm_init_dist_local(G, [n // G] * (G - 1) + [n - (G - 1) * (n // G)], np.arange(n, dtype=np.int64),
+                                pos, diam)
+    cuts = bdm.bdm_get_cuts(h)
+    L = float(diam.max())
+    bx = np.floor(pos[:, 0] * (1.0 / (L * (1.0 + 2.0 ** -30)))).astype(np.int64)
+    owned = [int(((bx >= cuts[g]) & (bx < cuts[g + 1])).sum()) for g in range(G)]
+    assert all(b - a >= 2 for a, b in zip(cuts[1:-2], cuts[2:-1]))
+    # the two central ranks hold fewer agents than the outer ones (their agents have more candidates)
+    assert owned[1] < owned[0] and owned[2] < owned[3], owned
+    ids, _ = bdm.bdm_get_local(h, bdm.BDM_OWNED_POSITIONS)
+    assert len(ids) == n
