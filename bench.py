@@ -323,6 +323,17 @@ def run_bdm(args):
             what = f"the whole {n}-agent workload"
         cpu = cpu_baseline(ps, ds, what, args.cpu_stride_1t)
 
+    step_hbm = None
+    tr = os.path.join(ROOT, "profiles", "r02_rebuild_traffic.json")
+    if traffic and os.path.exists(tr):  # the whole step's measured DRAM bytes (ncu) over its event time
+        with open(tr) as f:
+            t = json.load(f)
+        sb = traffic + t["dram_bytes_read"] + t["dram_bytes_write"]
+        ach = sb / (total_s / args.steps) / 1e9
+        step_hbm = {"bytes_per_step": sb, "achieved_gbs": ach, "peak_gbs": float(peaks["hbm_gbs"]),
+                    "frac": ach / float(peaks["hbm_gbs"]),
+                    "source": "ncu DRAM bytes of the force phase (profiles/r02_force_traffic.json) + rebuild "
+                              "(profiles/r02_rebuild_traffic.json), cfg3 steady state, over the timed ms/step"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total_s / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -338,7 +349,7 @@ def run_bdm(args):
                                  "agent, DESIGN.md §6.2) over the force phase's event time (both passes); peak = "
                                  f"148 SM x 64 fp64 lanes x {sm_max:.0f} MHz ({peak_kind} sm_max_mhz)",
                          "units": {"candidates": n_cand, "contacts": n_ct, "agents": n}},
-            "roofline_rebuild": rebuild,
+            "roofline_rebuild": rebuild, "step_hbm": step_hbm,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": tm["launches"],
             "clocks": clk.summary(), "step_ms": [round(x, 4) for x in step_ms]}
     print(json.dumps(line), flush=True)
