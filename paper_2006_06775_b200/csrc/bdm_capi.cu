@@ -1225,6 +1225,7 @@ int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, 
 }
 
 int bdm_set_agents(bdm_handle h, const double* pos, const double* diam) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_set_agents: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_agents: NULL handle");
   if (h->n > 0 && (!pos || !diam)) return fail(h, BDM_EINVAL, "bdm_set_agents: NULL array with n > 0");
   CU(h, cudaSetDevice(h->device));
@@ -1253,6 +1254,7 @@ int bdm_sync(bdm_handle h) {
 }
 
 int bdm_grid_build(bdm_handle h) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_grid_build: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_grid_build: NULL handle");
   CU(h, cudaSetDevice(h->device));
   return grid_build(h);
@@ -1311,6 +1313,7 @@ int bdm_mech_step(bdm_handle h, int32_t n_steps) {
 }
 
 int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_set_growth: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_growth: NULL handle");
   if (h->slab || h->fields_on || h->n_el) return fail(h, BDM_EINVAL, "bdm_set_growth: not available with slabs, fields or neurites");
   if (!(growth >= 0.0) || !std::isfinite(growth) || !(div_diam > 0.0))
@@ -1323,6 +1326,7 @@ int bdm_set_growth(bdm_handle h, double growth, double div_diam, uint64_t seed) 
 }
 
 int bdm_set_fields(bdm_handle h, const bdm_field_params* fp, const int8_t* types) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_set_fields: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !fp) return fail(h, BDM_EINVAL, "bdm_set_fields: NULL argument");
   if (h->slab || h->growth_on) return fail(h, BDM_EINVAL, "bdm_set_fields: not available with slabs or growth");
   const double h_ = fp->h;
@@ -1376,6 +1380,7 @@ int bdm_set_fields(bdm_handle h, const bdm_field_params* fp, const int8_t* types
 }
 
 int bdm_get_field(bdm_handle h, int which, double* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_field: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !out || (which != 0 && which != 1)) return fail(h, BDM_EINVAL, "bdm_get_field: bad arguments");
   if (!h->fields_on) return fail(h, BDM_ESTATE, "bdm_get_field: no fields (bdm_set_fields)");
   CU(h, cudaSetDevice(h->device));
@@ -1387,6 +1392,7 @@ int bdm_get_field(bdm_handle h, int which, double* out) {
 
 int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const double* diam, const double* rest_len,
                      const double* anchor, const int64_t* mother, const int64_t* daughters, double k_spring) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_set_neurites: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_neurites: NULL handle");
   if (h->slab || h->growth_on || h->fields_on)
     return fail(h, BDM_EINVAL, "bdm_set_neurites: not available with slabs, growth or fields");
@@ -1457,6 +1463,7 @@ int bdm_set_neurites(bdm_handle h, int64_t n_el, const double* distal, const dou
 }
 
 int bdm_get_neurites(bdm_handle h, double* distal, double* ddistal) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_neurites: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_neurites: NULL handle");
   if (h->n_el == 0) return BDM_OK;
   CU(h, cudaSetDevice(h->device));
@@ -1479,6 +1486,7 @@ int bdm_get_neurites(bdm_handle h, double* distal, double* ddistal) {
 }
 
 int bdm_reserve(bdm_handle h, int64_t capacity) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_reserve: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_reserve: NULL handle");
   if (h->slab) return fail(h, BDM_EINVAL, "bdm_reserve: not available in slab mode");
   CU(h, cudaSetDevice(h->device));
@@ -1493,6 +1501,7 @@ int bdm_get_count(bdm_handle h, int64_t* out2) {
 }
 
 int bdm_set_force_path(bdm_handle h, int path) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_set_force_path: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_set_force_path: NULL handle");
   if (path != BDM_PATH_AUTO && path != BDM_PATH_SINGLE) return fail(h, BDM_EINVAL, "bdm_set_force_path: bad path %d", path);
   h->force_path = path;
@@ -1500,6 +1509,7 @@ int bdm_set_force_path(bdm_handle h, int path) {
 }
 
 int bdm_set_defer(bdm_handle h, int max_deferred) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_set_defer: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || max_deferred < 0) return fail(h, BDM_EINVAL, "bdm_set_defer: NULL handle or negative count");
   h->defer_max = max_deferred;
   return BDM_OK;
@@ -1555,6 +1565,7 @@ int bdm_get_timing(bdm_handle h, double* out4) {
 }
 
 int bdm_get_displacements(bdm_handle h, double* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_displacements: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_displacements: NULL handle");
   if (!h->have_dp) return fail(h, BDM_ESTATE, "bdm_get_displacements: no step has been run");
   if (h->n_dp == 0) return BDM_OK;
@@ -1576,6 +1587,7 @@ int bdm_get_displacements(bdm_handle h, double* out) {
 }
 
 int bdm_get_positions(bdm_handle h, double* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_positions: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_positions: NULL handle");
   if (h->n == 0) return BDM_OK;
   if (!out) return fail(h, BDM_EINVAL, "bdm_get_positions: NULL output");
@@ -1595,6 +1607,7 @@ int bdm_get_positions(bdm_handle h, double* out) {
 }
 
 int bdm_get_diameters(bdm_handle h, double* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_diameters: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_diameters: NULL handle");
   if (h->n == 0) return BDM_OK;
   if (!out) return fail(h, BDM_EINVAL, "bdm_get_diameters: NULL output");
@@ -1614,6 +1627,7 @@ int bdm_get_diameters(bdm_handle h, double* out) {
 }
 
 int bdm_get_box_coords(bdm_handle h, int32_t* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_box_coords: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h) return fail(nullptr, BDM_EINVAL, "bdm_get_box_coords: NULL handle");
   if (h->n == 0) return BDM_OK;
   if (!out) return fail(h, BDM_EINVAL, "bdm_get_box_coords: NULL output");
@@ -1637,6 +1651,7 @@ int bdm_get_box_coords(bdm_handle h, int32_t* out) {
 }
 
 int bdm_get_grid_info(bdm_handle h, bdm_grid_info* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_grid_info: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !out) return fail(h, BDM_EINVAL, "bdm_get_grid_info: NULL argument");
   if (!h->have_grid) return fail(h, BDM_ESTATE, "bdm_get_grid_info: no grid built yet");
   out->L = h->grid.L;
@@ -1654,6 +1669,7 @@ int bdm_get_grid_info(bdm_handle h, bdm_grid_info* out) {
 }
 
 int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_agent_stats: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !out) return fail(h, BDM_EINVAL, "bdm_get_agent_stats: NULL argument");
   if (!(h->prm.flags & BDM_RECORD) || !h->have_record)
     return fail(h, BDM_ESTATE, "bdm_get_agent_stats: needs BDM_RECORD at init and one step");
@@ -1687,6 +1703,7 @@ int bdm_get_agent_stats(bdm_handle h, const bdm_agent_stats* out) {
 }
 
 int bdm_get_pairs(bdm_handle h, int kind, int64_t* n_pairs, int64_t* out, int64_t cap) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_pairs: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !n_pairs) return fail(h, BDM_EINVAL, "bdm_get_pairs: NULL argument");
   if (kind != BDM_NEIGHBOR && kind != BDM_CONTACT) return fail(h, BDM_EINVAL, "bdm_get_pairs: bad kind %d", kind);
   if (cap < 0 || (cap > 0 && !out)) return fail(h, BDM_EINVAL, "bdm_get_pairs: bad output buffer");
@@ -2166,6 +2183,7 @@ int bdm_slab_get(bdm_handle h, int what, int64_t* n, uint32_t* ids, double* vals
 }
 
 int bdm_get_skip_stats(bdm_handle h, int64_t* out3) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_skip_stats: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !out3) return fail(h, BDM_EINVAL, "bdm_get_skip_stats: NULL argument");
   CU(h, cudaSetDevice(h->device));
   if (!h->ext_valid || h->state != State::Stepped) {
@@ -2182,6 +2200,7 @@ int bdm_get_skip_stats(bdm_handle h, int64_t* out3) {
 }
 
 int bdm_get_path_stats(bdm_handle h, int64_t* out2) {
+  if (h && h->dist) return fail(h, BDM_ESTATE, "bdm_get_path_stats: not for distributed handles (bdm_get_local, bdm_set_agents_dist)");
   if (!h || !out2) return fail(h, BDM_EINVAL, "bdm_get_path_stats: NULL argument");
   CU(h, cudaSetDevice(h->device));
   if (!h->ext_valid || h->state != State::Stepped) {

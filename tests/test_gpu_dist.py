@@ -221,3 +221,16 @@ def test_dist_cuts_balance_work_not_count(bdm):
     assert owned[1] < owned[0] and owned[2] < owned[3], owned
     ids, _ = bdm.bdm_get_local(h, bdm.BDM_OWNED_POSITIONS)
     assert len(ids) == n
+
+
+def test_dist_handle_rejects_single_handle_calls(bdm):
+    """Single-handle getters and setters on a distributed handle fail with ESTATE (no crash)."""
+    pos, diam = bdm_inputs.make_config(1)
+    h = bdm.bdm_init_dist_local(2, [2048, 2048], np.arange(4096, dtype=np.int64), pos, diam)
+    for call in (lambda: bdm.bdm_grid_build(h), lambda: bdm.bdm_get_positions(h),
+                 lambda: bdm.bdm_get_pairs(h, bdm.BDM_CONTACT), lambda: bdm.bdm_set_force_path(h, 1)):
+        with pytest.raises(bdm.BdmError) as e:
+            call()
+        assert e.value.code == bdm.BDM_ESTATE
+    bdm.bdm_mech_step(h, 1)
+    assert len(bdm.bdm_get_local(h, bdm.BDM_LAST_DISPLACEMENTS)[0]) == 4096
