@@ -55,6 +55,21 @@ for G in a.ranks:
     out[f"virtual_{G}_ms"] = ms
     out[f"virtual_{G}_fixed_us_per_rank"] = 1e3 * (ms - out["single_ms"]) / G
     out[f"virtual_{G}_syncs"] = s["host_syncs"]
+    cuts = bdm.bdm_get_cuts(hd)
     hd.close()
     torch.cuda.empty_cache()
+    if G > 1:  # the same slabs as independent single handles (no ghosts, no protocol): sum of their steps
+        L = float(diam.max())
+        bx = np.floor(pos[:, 0] * (1.0 / (L * (1.0 + 2.0 ** -30)))).astype(np.int64)
+        tot = 0.0
+        for g in range(G):
+            m = np.flatnonzero((bx >= cuts[g]) & (bx < cuts[g + 1]))
+            if len(m) == 0:
+                continue
+            hs = bdm.bdm_init(torch.from_numpy(pos[m].copy()).cuda(), torch.from_numpy(diam[m].copy()).cuda(),
+                              stream=st)
+            tot += timed(hs, a.steps)
+            hs.close()
+        out[f"singles_{G}_sum_ms"] = tot
+        out[f"virtual_{G}_protocol_us_per_rank"] = 1e3 * (out[f"virtual_{G}_ms"] - tot) / G
 print(json.dumps(out))
