@@ -778,11 +778,7 @@ int dist_split_all(bdm_ctx* H, DistGroup* G) {
       msgs.push_back(Msg{r, to, a ? a->msg[side] : nullptr, b ? b->msg[side == 0 ? 3 : 2] : nullptr, cnt});
     }
   }
-  static const int dsync = std::getenv("BDM_DIST_SYNC") ? std::atoi(std::getenv("BDM_DIST_SYNC")) : 0;
-  if (dsync & 2) CU(H, cudaStreamSynchronize(G->stream));
-  int rc = dist_p2p(H, G, msgs);
-  if (!rc && (dsync & 1)) CU(H, cudaStreamSynchronize(G->stream));
-  return rc;
+  return dist_p2p(H, G, msgs);
 }
 
 int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp) {
