@@ -38,6 +38,8 @@ const bool g_htile = std::getenv("BDM_HTILE") && std::getenv("BDM_HTILE")[0] == 
 const int g_bands = std::getenv("BDM_BANDS") ? std::max(1, std::min(32, std::atoi(std::getenv("BDM_BANDS")))) : 1;
 // BDM_PBOX=0: the key pass re-reads the state instead of the sum pass's packed boxes
 const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
+// BDM_PDL=0: the step's launch chain without programmatic dependent launch (lx below)
+const bool g_pdl = !(std::getenv("BDM_PDL") && std::getenv("BDM_PDL")[0] == '0');
 
 enum class State { NoGrid, Fresh, Stepped };
 
@@ -229,6 +231,24 @@ int dalloc(bdm_ctx* h, T** p, size_t count) {
 
 unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Launch of a kernel of the step's chain with programmatic stream serialisation (PDL): it may be
+// scheduled while its predecessor drains and waits in pdl_wait() (bdm_kernels.cuh) for that grid's
+// completion.  Only kernels that call pdl_wait() before any memory access go through here.
+template <typename... KArgs, typename... Args>
+cudaError_t lx(void (*k)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 bool params_ok(const bdm_params* p) {
   auto fin = [](double v) { return std::isfinite(v); };
   return p && p->eta > 0.0 && p->max_disp > 0.0 && fin(p->eta) && fin(p->max_disp) && p->k_rep >= 0.0 &&
@@ -393,23 +413,21 @@ bool ensure_half(bdm_ctx* h) {
 int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t a_end, uint32_t n_all,
                const ParamsDev& pd, double4* ag_out, uint32_t* id_out, double* dp, uint32_t* dp_ids,
                bool fuse_cols = false, const int32_t* frame4 = nullptr, unsigned long long* hist_out = nullptr,
-               double* force_only = nullptr) {
+               double* force_only = nullptr, int ext_mode = -1) {
   cudaStream_t s = h->stream;
   ColNext cn{0, 0, 0, 0, nullptr, nullptr, nullptr, 0, 0};
+  size_t nc2 = 0;
   h->cols_next = false;
   if (fuse_cols) {  // next build's frame: this step's tight extents +- 1 box (|dp| < L)
     cn.lo0 = frame4 ? frame4[0] : h->tlo[0] - 1;
     cn.lo1 = frame4 ? frame4[1] : h->tlo[1] - 1;
     cn.nx = frame4 ? frame4[2] : h->thi[0] - h->tlo[0] + 3;
     cn.ny = frame4 ? frame4[3] : h->thi[1] - h->tlo[1] + 3;
-    const size_t nc2 = (size_t)cn.nx * (size_t)cn.ny;
+    nc2 = (size_t)cn.nx * (size_t)cn.ny;
     int rc = ensure_columns(h, nc2 + 1, true);
     if (rc) return rc;
     cn.czlo = h->czlo2;
     cn.czhi = h->czhi2;
-    const unsigned gs = (unsigned)std::min<uint64_t>((nc2 + 256) / 256, 148u * 16u);
-    k_col_reset<<<gs, 256, 0, s>>>(h->czlo2, h->czhi2, (uint32_t)nc2);
-    h->launches += 1;
     h->nlo[0] = cn.lo0;
     h->nlo[1] = cn.lo1;
     h->nnx = cn.nx;
@@ -437,7 +455,13 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
       }
     }
   }
-  CU(h, cudaMemsetAsync(h->h_bcnt, 0, (size_t)std::max<uint32_t>(n_all, 1) * sizeof(uint32_t), s));
+  {  // one launch: the extents reset (ext_mode >= 0), the next build's column ranges, the pair counters
+    const uint64_t w = std::max<uint64_t>(nc2, (uint64_t)n_all / 4 + 1);
+    const unsigned gr = (unsigned)std::min<uint64_t>((w + 255) / 256, 148u * 16u);
+    CU(h, lx(k_force_reset, gr, 256, 0, s, h->ext, ext_mode, fuse_cols ? h->czlo2 : nullptr, h->czhi2, (uint32_t)nc2,
+             h->h_bcnt, std::max<uint32_t>(n_all, 1)));
+    h->launches += 1;
+  }
   // banded force phase: bands of >= 2^20 agents each
   const int nb = force_only ? 1 : (int)std::min<int64_t>(g_bands, std::max<int64_t>(1, ((int64_t)a_end - a_begin) >> 20));
   if (nb > 1) {
@@ -491,8 +515,8 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   } else {
     const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
                                                      std::max<uint64_t>(1, (a_end - s_begin + HA_THREADS - 1) / HA_THREADS));
-    k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, s>>>(h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
-                                                         h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr);
+    CU(h, lx(k_half_search, ga, HA_THREADS, HA_SMEM_BYTES, s, h->ag[src], h->agf, s_begin, a_end, h->grid, h->h_fwd,
+             h->h_fcnt, h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr, nullptr, nullptr));
   }
   DBG(h, "k_half_search");
   const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
@@ -510,16 +534,15 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     k_half_slow<true><<<gs, 128, 0, s>>>(h->ag[src], h->id[src], a_begin, h->grid, pd, nullptr, nullptr, force_only,
                                          nullptr, h->ext, h->err, cn, nullptr, h->h_slow);
   } else {
-    k_half_sum<false><<<gb, FORCE_THREADS, HB_SMEM_BYTES, s>>>(h->ag[src], h->id[src], a_begin, a_end, h->grid, pd,
-                                                                ag_out, id_out, dp, dp_ids, h->ext, h->err, h->h_fwd,
-                                                                h->h_fcnt, h->h_bwd, h->h_bcnt, cn, hist_out,
-                                                                h->h_slow);
-    k_half_slow<false><<<gs, 128, 0, s>>>(h->ag[src], h->id[src], a_begin, h->grid, pd, ag_out, id_out, dp, dp_ids,
-                                          h->ext, h->err, cn, hist_out, h->h_slow);
+    CU(h, lx(k_half_sum<false>, gb, FORCE_THREADS, HB_SMEM_BYTES, s, h->ag[src], h->id[src], a_begin, a_end, h->grid,
+             pd, ag_out, id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, hist_out,
+             h->h_slow, nullptr, nullptr, (int64_t)-1));
+    CU(h, lx(k_half_slow<false>, gs, 128, 0, s, h->ag[src], h->id[src], a_begin, h->grid, pd, ag_out, id_out, dp,
+             dp_ids, h->ext, h->err, cn, hist_out, h->h_slow, nullptr));
   }
   DBG(h, "k_half_slow");
   DBG(h, "k_half_sum");
-  k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
+  CU(h, lx(k_locate_nonfinite, 1, 32, 0, s, h->ag[src], h->id[src], h->grid, pd, h->err));
   CU(h, cudaGetLastError());
   h->launches += 4;
   h->cols_next = fuse_cols;
@@ -528,26 +551,37 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
 
 // In-place exclusive scan of data[0 .. items) -- items given on the host, or read on the device as
 // *n_dev + 1 (persistent decoupled look-back, grid = resident capacity).
-int scan(bdm_ctx* h, uint32_t* data, uint64_t items, const uint32_t* n_dev) {
+// Tile states for a host-sized scan of `items` (column offsets, division ranks may need more slots).
+int scan_reserve(bdm_ctx* h, uint64_t items) {
+  const size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
+  if (tiles > h->scan_tiles_cap) {
+    if (h->scan_state) CU(h, cudaFree(h->scan_state));
+    h->scan_state = nullptr;
+    const size_t cap = tiles + tiles / 4 + 256;
+    CU(h, cudaMalloc(&h->scan_state, cap * sizeof(unsigned long long)));
+    h->scan_tiles_cap = cap;
+  }
+  return BDM_OK;
+}
+
+// prezeroed: the tile states and the ticket were zeroed by the preceding kernel (k_col_len,
+// k_table_zero), so the launch chain has no memset node.
+int scan(bdm_ctx* h, uint32_t* data, uint64_t items, const uint32_t* n_dev, bool prezeroed = false) {
   init_device_info(h);
-  if (items) {  // host-sized scans (column offsets, division ranks) may need more tile slots
-    const size_t tiles = (items + SCAN_TILE - 1) / SCAN_TILE;
-    if (tiles > h->scan_tiles_cap) {
-      if (h->scan_state) CU(h, cudaFree(h->scan_state));
-      h->scan_state = nullptr;
-      const size_t cap = tiles + tiles / 4 + 256;
-      CU(h, cudaMalloc(&h->scan_state, cap * sizeof(unsigned long long)));
-      h->scan_tiles_cap = cap;
-    }
+  if (items) {
+    int rc = scan_reserve(h, items);
+    if (rc) return rc;
   }
   size_t tiles_bound = h->scan_tiles_cap;
   uint64_t want = items ? (items + SCAN_TILE - 1) / SCAN_TILE : tiles_bound;
-  CU(h, cudaMemsetAsync(h->scan_state, 0, std::min<uint64_t>(want, tiles_bound) * sizeof(unsigned long long),
-                        h->stream));
-  CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), h->stream));
+  if (!prezeroed) {
+    CU(h, cudaMemsetAsync(h->scan_state, 0, std::min<uint64_t>(want, tiles_bound) * sizeof(unsigned long long),
+                          h->stream));
+    CU(h, cudaMemsetAsync(h->scan_ticket, 0, sizeof(uint32_t), h->stream));
+  }
   const uint64_t cap = (uint64_t)h->sm_count * h->scan_blocks_per_sm;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min(want, cap));
-  k_scan<<<grid, SCAN_THREADS, 0, h->stream>>>(data, n_dev, items, h->scan_state, h->scan_ticket);
+  CU(h, lx(k_scan, grid, SCAN_THREADS, 0, h->stream, data, n_dev, items, h->scan_state, h->scan_ticket));
   DBG(h, "k_scan");
   CU(h, cudaGetLastError());
   return BDM_OK;
@@ -674,46 +708,46 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
     g.czlo = h->czlo;
     g.czhi = h->czhi;
     g.coff = h->coff;
-    h->launches -= 2;
   } else {
-    k_col_reset<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols);
+    CU(h, lx(k_col_reset, gs, 256, 0, s, h->czlo, h->czhi, g.n_cols));
     DBG(h, "k_col_reset");
-    if (n > 0) k_col_ext<<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->czlo, h->czhi);
+    if (n > 0) CU(h, lx(k_col_ext, blocks(n, 512), 256, 0, s, h->ag[src], n, g, h->czlo, h->czhi, nullptr));
     DBG(h, "k_col_ext");
+    h->launches += n > 0 ? 2 : 1;
   }
-  k_col_len<<<gs, 256, 0, s>>>(h->czlo, h->czhi, g.n_cols, h->coff);
-  DBG(h, "k_col_len");
-  rc = scan(h, h->coff, nc + 1, nullptr);  // exclusive: coff[c] = table offset, coff[nc] = T
+  // (k_col_len zeroes the offset scan's tile states, k_table_zero the table scan's)
+  rc = scan_reserve(h, nc + 1);
   if (rc) return rc;
-  k_table_zero<<<h->sm_count * 8, 256, 0, s>>>(h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec);
+  CU(h, lx(k_col_len, gs, 256, 0, s, h->czlo, h->czhi, g.n_cols, h->coff, h->scan_state,
+           (uint32_t)((nc + 1 + SCAN_TILE - 1) / SCAN_TILE), h->scan_ticket));
+  DBG(h, "k_col_len");
+  rc = scan(h, h->coff, nc + 1, nullptr, true);  // exclusive: coff[c] = table offset, coff[nc] = T
+  if (rc) return rc;
+  CU(h, lx(k_table_zero, h->sm_count * 8, 256, 0, s, h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec,
+           h->scan_state, (uint32_t)h->scan_tiles_cap, h->scan_ticket));
   DBG(h, "k_table_zero");
   if (n > 0 && packed) {  // boxes from the last sum pass (4 B/agent instead of the state)
-    if (h->deferred > 0)
-      k_key_hist_packed<true><<<blocks(n, 256 * KHP), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key, h->slot,
-                                                              h->table, h->err);
-    else
-      k_key_hist_packed<false><<<blocks(n, 256 * KHP), 256, 0, s>>>(h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key,
-                                                               h->slot, h->table, h->err);
+    CU(h, lx(h->deferred > 0 ? k_key_hist_packed<true> : k_key_hist_packed<false>, blocks(n, 256 * KHP), 256, 0, s,
+             h->pbox, n, g, h->pb_z0, h->pb_zbits, h->key, h->slot, h->table, h->err, nullptr));
   } else if (n > 0) {
-    if (h->deferred > 0)
-      k_key_hist<true><<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
-    else
-      k_key_hist<false><<<blocks(n, 512), 256, 0, s>>>(h->ag[src], n, g, h->key, h->slot, h->table, h->err);
+    CU(h, lx(h->deferred > 0 ? k_key_hist<true> : k_key_hist<false>, blocks(n, 512), 256, 0, s, h->ag[src], n, g,
+             h->key, h->slot, h->table, h->err, nullptr, nullptr));
   }
   DBG(h, "k_key_hist");
-  rc = scan(h, h->table, 0, h->coff + nc);  // T + 1 items: table[k] = first agent of box k, table[T] = n
+  rc = scan(h, h->table, 0, h->coff + nc, true);  // T + 1 items: table[k] = first agent of box k, table[T] = n
   if (rc) return rc;
   if (n > 0) {
-    k_scatter<<<blocks(n, 256 * KSC), 256, 0, s>>>(h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid, h->tkey);
+    CU(h, lx(k_scatter, blocks(n, 256 * KSC), 256, 0, s, h->key, h->slot, h->id[src], h->table, n, h->tsrc, h->tid,
+             h->tkey, nullptr));
     DBG(h, "k_scatter");
     const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
-    k_place<<<blocks(n - n_dead, PLACE_T), PLACE_T, 0, s>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src], n - n_dead, h->ag[dst],
-                                           h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
-                                           perm_hist ? h->hist[dst] : nullptr);
+    CU(h, lx(k_place, blocks(n - n_dead, PLACE_T), PLACE_T, 0, s, h->tsrc, h->tid, h->tkey, h->table, h->ag[src],
+             n - n_dead, h->ag[dst], h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
+             perm_hist ? h->hist[dst] : nullptr, nullptr));
     DBG(h, "k_place");
   }
   CU(h, cudaGetLastError());
-  h->launches += n > 0 ? 8 : 4;
+  h->launches += n > 0 ? 7 : 4;
   h->cur = dst;
   return BDM_OK;
 }
@@ -765,7 +799,7 @@ int force_step(bdm_ctx* h, bool want_dp) {
   const uint32_t n = (uint32_t)h->n;
   cudaStream_t s = h->stream;
   const int src = h->cur, dst = 1 - h->cur;
-  k_ext_reset<<<1, 32, 0, s>>>(h->ext, h->deferred > 0 ? 2 : 1);
+  const int ext_mode = h->deferred > 0 ? 2 : 1;
   RecordDev rec{h->r_cand, h->r_nb, h->r_ct, h->r_branch, h->r_nbh, h->r_cth};
   ParamsDev pd = params_dev(h->prm);
   double* dp = want_dp ? h->dp : nullptr;
@@ -780,24 +814,24 @@ int force_step(bdm_ctx* h, bool want_dp) {
     const bool fuse = !h->growth_on && !h->fields_on && h->n_el == 0 && !h->slab &&
                       h->prm.max_disp < h->grid.L * (1.0 - 0x1p-20);
     int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr, fuse, nullptr,
-                        h->hist[0] ? h->hist[dst] : nullptr);
+                        h->hist[0] ? h->hist[dst] : nullptr, nullptr, ext_mode);  // (k_force_reset resets ext)
     if (rc) return rc;
-  } else if (h->prm.flags & BDM_RECORD)
-    k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd, h->ag[dst],
-                                                nullptr, dp, nullptr, h->ext, h->err, rec, nullptr,
-                                                h->hist[0] ? h->hist[dst] : nullptr, nullptr);
-  else
-    k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
-                                                 h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
-                                                 h->skip_active ? h->hot : nullptr,
-                                                 h->hist[0] ? h->hist[dst] : nullptr, nullptr);
-  if (!h->last_half) {  // (the half-shell path launched its own diagnosis)
+  } else {
+    k_ext_reset<<<1, 32, 0, s>>>(h->ext, ext_mode);
+    if (h->prm.flags & BDM_RECORD)
+      k_force<true><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
+                                                                  h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
+                                                                  nullptr, h->hist[0] ? h->hist[dst] : nullptr, nullptr);
+    else
+      k_force<false><<<grid, FORCE_THREADS, FORCE_SMEM_BYTES, s>>>(h->ag[src], h->agf, h->id[src], 0u, n, h->grid, pd,
+                                                                   h->ag[dst], nullptr, dp, nullptr, h->ext, h->err, rec,
+                                                                   h->skip_active ? h->hot : nullptr,
+                                                                   h->hist[0] ? h->hist[dst] : nullptr, nullptr);
     k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
-    h->launches += 1;
+    h->launches += 3;  // (the half-shell path counts its own launches)
   }
   CU(h, cudaGetLastError());
   DBG(h, "k_force");
-  h->launches += h->last_half ? 1 : 2;  // k_ext_reset (+ k_force)
   // The stepped positions keep the sorted order, so they keep the sorted id buffer: swap the id
   // pointers (the kernel already captured its arguments) instead of copying.
   h->out_ids = h->id[src];

@@ -196,7 +196,24 @@ __device__ __forceinline__ void block_minmax_atomic(Extents* ext, const int b[3]
   }
 }
 
+// Programmatic dependent launch (the step's kernels are launched with programmatic stream
+// serialisation, so a kernel's launch and block scheduling overlap its predecessor's drain): every
+// kernel of the chain waits here, before touching anything its predecessor reads or writes, for the
+// predecessor grid to complete and its memory to be visible; then it lets its own successor launch
+// (whose blocks take the SMs this grid's tail frees and wait in turn -- the trigger fires only once
+// every block of this grid has started, so they never displace one of its blocks).  A no-op for
+// ordinary launches.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+#ifndef BDM_SCAN_ITEMS
+#define BDM_SCAN_ITEMS 16
+#endif
+constexpr uint32_t SCAN_TILE_C = 256u * BDM_SCAN_ITEMS;  // items per scan tile (= SCAN_TILE, below)
+
 // integer box coordinate of one component; flags |q| >= 2^20 (R9)
+
 __device__ __forceinline__ int box_coord(double p, double inv, bool& bad) {
   double q = p * inv;
   bad |= !(fabs(q) < 1048576.0);
@@ -241,6 +258,7 @@ __device__ __forceinline__ void st_state(double4* p, double4 v) {
 // mode 0: also clear the sticky flags; 1: the range flag of the last step becomes sticky first; 2: so
 // does its frame flag (the build just made was deferred: its frame had to hold every agent)
 __global__ void k_ext_reset(Extents* ext, int mode = 1) {
+  pdl_wait();
   if (threadIdx.x == 0)
     ext->sticky = mode == 0 ? 0u
                             : ext->sticky | (ext->range_err ? 1u : 0u) | (mode == 2 && ext->col_bad ? 2u : 0u);
@@ -328,8 +346,44 @@ __device__ __forceinline__ int key_run(uint32_t k, int lane, uint32_t& len) {
   return start;
 }
 
+// Start of a half-shell force phase, one launch: the extents / counters reset of k_ext_reset (block 0),
+// the next build's column ranges of the fused pass (czlo2 / czhi2, nc2 columns) and the pair counters
+// (nb agents).
+__global__ void k_force_reset(Extents* ext, int ext_mode, int32_t* __restrict__ czlo2, int32_t* __restrict__ czhi2,
+                              uint32_t nc2, uint32_t* __restrict__ bcnt, uint32_t nb) {
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x < 32 && ext_mode >= 0) {
+    if (threadIdx.x == 0)
+      ext->sticky = ext_mode == 0 ? 0u
+                                  : ext->sticky | (ext->range_err ? 1u : 0u) | (ext_mode == 2 && ext->col_bad ? 2u : 0u);
+    __syncwarp();
+    if (threadIdx.x < 3) {
+      ext->lo[threadIdx.x] = INT32_MAX;
+      ext->hi[threadIdx.x] = INT32_MIN;
+    }
+    if (threadIdx.x == 3) ext->range_err = 0;
+    if (threadIdx.x == 4) ext->work = 0u;
+    if (threadIdx.x == 5) ext->moved = 0u;
+    if (threadIdx.x == 6) ext->searched = 0u;
+    if (threadIdx.x == 7) ext->work_a = 0u;
+    if (threadIdx.x == 8) ext->slow = 0u;
+    if (threadIdx.x == 9) ext->col_bad = 0u;
+  }
+  const uint32_t t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  if (czlo2)
+    for (uint32_t c = t0; c < nc2; c += stride) {
+      czlo2[c] = INT32_MAX;
+      czhi2[c] = INT32_MIN;
+    }
+  const uint32_t n4 = nb / 4;
+  uint4* b4 = reinterpret_cast<uint4*>(bcnt);
+  for (uint32_t k = t0; k < n4; k += stride) b4[k] = make_uint4(0u, 0u, 0u, 0u);
+  for (uint32_t k = 4 * n4 + t0; k < nb; k += stride) bcnt[k] = 0u;
+}
+
 // ---- column pass: occupied z-range of every column, then lengths for the offset scan
 __global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ czhi, uint32_t nc) {
+  pdl_wait();
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x) {
     czlo[c] = INT32_MAX;
     czhi[c] = INT32_MIN;
@@ -340,6 +394,7 @@ __global__ void k_col_reset(int32_t* __restrict__ czlo, int32_t* __restrict__ cz
 // strided over a small grid (the range is often short: the records appended since the last step)
 __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g, int32_t* __restrict__ czlo,
                           int32_t* __restrict__ czhi, const uint32_t* __restrict__ rng = nullptr) {
+  pdl_wait();
   uint32_t b0 = 0u;
   if (rng) {
     b0 = __ldg(&rng[0]);
@@ -385,8 +440,15 @@ __global__ void k_col_ext(const double4* __restrict__ ag, uint32_t n, GridDev g,
   }
 }
 
+// (st / st_n / ticket: the next scan's tile states and ticket are zeroed here, so that no memset node
+// interrupts the launch chain)
 __global__ void k_col_len(const int32_t* __restrict__ czlo, const int32_t* __restrict__ czhi, uint32_t nc,
-                          uint32_t* __restrict__ len) {
+                          uint32_t* __restrict__ len, unsigned long long* __restrict__ st = nullptr, uint32_t st_n = 0,
+                          uint32_t* __restrict__ ticket = nullptr) {
+  pdl_wait();
+  if (st)
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < st_n; t += gridDim.x * blockDim.x) st[t] = 0ull;
+  if (ticket && blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c <= nc; c += gridDim.x * blockDim.x)
     len[c] = c < nc && czhi[c] >= czlo[c] ? (uint32_t)(czhi[c] - czlo[c] + 1) : 0u;
 }
@@ -395,7 +457,14 @@ __global__ void k_col_len(const int32_t* __restrict__ czlo, const int32_t* __res
 // column records (czlo, czhi, coff) for the lookups
 __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __restrict__ coff, uint32_t nc,
                              const int32_t* __restrict__ czlo, const int32_t* __restrict__ czhi,
-                             int4* __restrict__ col) {
+                             int4* __restrict__ col, unsigned long long* __restrict__ st = nullptr,
+                             uint32_t st_cap = 0, uint32_t* __restrict__ ticket = nullptr) {
+  pdl_wait();
+  if (st) {  // the table scan's tile states (T + 1 items) and ticket (see k_col_len)
+    const uint32_t tiles = min(st_cap, (__ldg(&coff[nc]) + 1u + (uint32_t)SCAN_TILE_C - 1u) / (uint32_t)SCAN_TILE_C);
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < tiles; t += gridDim.x * blockDim.x) st[t] = 0ull;
+    if (ticket && blockIdx.x == 0 && threadIdx.x == 0) *ticket = 0u;
+  }
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
     col[c] = make_int4(czlo[c], czhi[c], (int)coff[c], 0);
   const uint32_t T = coff[nc];
@@ -418,6 +487,7 @@ template <bool GUARD>
 __global__ void k_key_hist(const double4* __restrict__ ag, uint32_t n, GridDev g, uint32_t* __restrict__ key,
                            uint32_t* __restrict__ slot, uint32_t* __restrict__ count, ErrDev* err,
                            const uint32_t* __restrict__ n_dev = nullptr, const uint32_t* __restrict__ b0_dev = nullptr) {
+  pdl_wait();
   if (n_dev) n = __ldg(n_dev);
   if (b0_dev) {  // (the agents [*b0_dev, n) only: the records appended after the packed ones)
     const uint32_t b0 = __ldg(b0_dev);
@@ -485,6 +555,7 @@ template <bool GUARD>
 __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n, GridDev g, int32_t z0, int32_t zbits,
                                   uint32_t* __restrict__ key, uint32_t* __restrict__ slot,
                                   uint32_t* __restrict__ count, ErrDev* err, const uint32_t* __restrict__ n_dev = nullptr) {
+  pdl_wait();
   if (n_dev) n = __ldg(n_dev);  // (distributed steps: dead emigrants carry pbox 0xffffffff and are dropped)
   const uint32_t i0 = blockIdx.x * (KHP * blockDim.x) + threadIdx.x;
   uint32_t pa[KHP];
@@ -535,9 +606,6 @@ __global__ void k_key_hist_packed(const uint32_t* __restrict__ pbox, uint32_t n,
 
 // ------------------------------------------------------------------------------------------ K3
 constexpr int SCAN_THREADS = 256;
-#ifndef BDM_SCAN_ITEMS
-#define BDM_SCAN_ITEMS 16
-#endif
 constexpr int SCAN_ITEMS = BDM_SCAN_ITEMS;  // per thread
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
@@ -561,6 +629,7 @@ __device__ __forceinline__ uint32_t warp_sum(uint32_t v) { return __reduce_add_s
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan(uint32_t* __restrict__ data, const uint32_t* __restrict__ n_dev,
                                                        uint64_t n_items_host, unsigned long long* __restrict__ state,
                                                        uint32_t* __restrict__ ticket) {
+  pdl_wait();
   __shared__ uint32_t s_tile;
   __shared__ uint32_t s_warp[SCAN_THREADS / 32];
   __shared__ uint32_t s_prefix;
@@ -654,6 +723,7 @@ __global__ void k_scatter(const uint32_t* __restrict__ key, const uint32_t* __re
                           const uint32_t* __restrict__ ids, const uint32_t* __restrict__ start, uint32_t n,
                           uint32_t* __restrict__ tsrc, uint32_t* __restrict__ tid, uint32_t* __restrict__ tkey,
                           const uint32_t* __restrict__ n_dev = nullptr) {
+  pdl_wait();
   if (n_dev) n = __ldg(n_dev);
   if (blockIdx.x * (KSC * blockDim.x) >= n) return;
   const uint32_t i0 = blockIdx.x * (KSC * blockDim.x) + threadIdx.x;
@@ -689,6 +759,7 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
                         uint32_t* __restrict__ ids_out, float4* __restrict__ agf_out,
                         const unsigned long long* __restrict__ hist_in, unsigned long long* __restrict__ hist_out,
                         const uint32_t* __restrict__ n_dev = nullptr) {
+  pdl_wait();
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (n_dev) n = __ldg(n_dev);
   if (q >= n) return;
@@ -1552,6 +1623,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
                   GridDev g, uint32_t* __restrict__ fwd, uint8_t* __restrict__ fcnt, uint32_t* __restrict__ bwd,
                   uint32_t* __restrict__ bcnt, Extents* ext, bool count_searched,
                   const uint32_t* __restrict__ s_end_dev = nullptr, uint32_t* __restrict__ work = nullptr) {
+  pdl_wait();
   if (s_end_dev) s_end = __ldg(s_end_dev);
   if (!work) work = &ext->work_a;  // (banded launches: the band's own counter)
   extern __shared__ __align__(16) unsigned char s_raw[];
@@ -2306,6 +2378,7 @@ __device__ __forceinline__ double3 full_force_warp(const GridDev& g, const doubl
 // adding it, is not finite.  Returns at once when nothing was reported (one load).
 __global__ void k_locate_nonfinite(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, GridDev g,
                                    ParamsDev p, ErrDev* err) {
+  pdl_wait();
   if (threadIdx.x != 0 || __ldcg(&err->code) != 6u || __ldcg(&err->second) != 0xffffffffu) return;
   const uint32_t i = (uint32_t)(__ldcg(&err->bad) & 0xffffffffull);
   const double4 me = ag[i];
@@ -2343,6 +2416,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                const uint32_t* __restrict__ bcnt, ColNext cn, unsigned long long* __restrict__ hist_out,
                uint32_t* __restrict__ slow_list, const uint32_t* __restrict__ ab_dev = nullptr,
                uint32_t* __restrict__ work = nullptr, int64_t o_base = -1) {
+  pdl_wait();
   if (ab_dev) {  // distributed steps: the owned range [a_begin, a_end) read on the device
     a_begin = __ldg(&ab_dev[0]);
     a_end = __ldg(&ab_dev[1]);
@@ -2627,6 +2701,7 @@ __global__ void __launch_bounds__(128) k_half_slow(const double4* __restrict__ a
                                                    unsigned long long* __restrict__ hist_out,
                                                    const uint32_t* __restrict__ slow_list,
                                                    const uint32_t* __restrict__ ab_dev = nullptr) {
+  pdl_wait();
   if (ab_dev) a_begin = __ldg(&ab_dev[0]);
   const uint32_t n_slow = __ldcg(&ext_next->slow);
   const int lane = threadIdx.x & 31;
