@@ -1378,6 +1378,9 @@ constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 constexpr int HPCAP = BDM_HPCAP;  // staged candidates (float4) per warp
 
 #define HA_RR (!BDM_HMAP || BDM_HSTAGE)  // the shared-memory run list (cursor with refills)
+#ifndef BDM_HBATCH
+#define BDM_HBATCH 1  // pass A: the z-run lookups of the 5 forward columns batched in two load levels
+#endif
 #ifndef BDM_HCOOP
 #define BDM_HCOOP BDM_HSTAGE  // single-column chunks stage their box starts cooperatively (needed by BDM_HSTAGE;
                               // per-lane lookups are slightly faster otherwise)
@@ -1829,6 +1832,41 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
 #endif
 #if HA_RR
     uint32_t wr = 0;  // total length of the run list (staged path, or BDM_HMAP=0)
+#if BDM_HBATCH
+    if (valid && !coop) {
+      // the 5 column records first, then the 9 box starts (own column: its run starts at i + 1), each
+      // level's loads all in flight together: two dependent levels instead of five zrun chains
+      int4 ci[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int cx = bx + (q >= 2 ? 1 : 0), cy = by + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
+        const bool in = ((cull >> q) & 1u) && cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1];
+        BDM_ASSERT(!in || col_of(g, cx, cy) < g.n_cols);
+        ci[q] = in ? __ldg(&g.col[col_of(g, cx, cy)]) : make_int4(1, 0, 0, 0);  // (empty: zl > zh)
+      }
+      uint32_t rb[5], re[5];
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const int z0 = q == 0 ? bz : bz - 1 + (int)((cull >> (8 + q)) & 1u);
+        const int z1 = bz + 1 - (int)((cull >> (16 + q)) & 1u);
+        const int a = z0 > ci[q].x ? z0 : ci[q].x, d = z1 < ci[q].y ? z1 : ci[q].y;
+        rb[q] = q == 0 ? i + 1 : 0u;
+        re[q] = 0u;
+        if (a <= d) {
+          BDM_ASSERT((uint32_t)ci[q].z + (uint32_t)(d - ci[q].x) + 1u <= __ldg(&g.coff[g.n_cols]));
+          if (q != 0) rb[q] = __ldg(&g.table[(uint32_t)ci[q].z + (uint32_t)(a - ci[q].x)]);
+          re[q] = __ldg(&g.table[(uint32_t)ci[q].z + (uint32_t)(d - ci[q].x) + 1u]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 5; ++q)
+        if (rb[q] < re[q]) {
+          sm.rr[nr][lane] = make_uint2(rb[q], re[q]);
+          wr += re[q] - rb[q];
+          ++nr;
+        }
+    } else
+#endif
     if (valid) {
 #pragma unroll
       for (int q = 0; q < 5; ++q) {
