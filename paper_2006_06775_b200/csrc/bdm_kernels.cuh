@@ -1378,6 +1378,9 @@ constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 constexpr int HPCAP = BDM_HPCAP;  // staged candidates (float4) per warp
 
 #define HA_RR (!BDM_HMAP || BDM_HSTAGE)  // the shared-memory run list (cursor with refills)
+#ifndef BDM_HLST
+#define BDM_HLST 1  // pass A: survivor appends through a precomputed shared address
+#endif
 #ifndef BDM_HBATCH
 #define BDM_HBATCH 1  // pass A: the z-run lookups of the 5 forward columns batched in two load levels
 #endif
@@ -1511,6 +1514,15 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
   uint32_t q = cur.x, e = cur.y;
   uint2 nx = sm.rr[1][lane];
   uint32_t kaddr = rr_base + 2u * 256u;  // address of the run after nx
+#if BDM_HLST
+  // shared address of this lane's list column, from the run list's (the generic -> shared address of
+  // sm.list would otherwise be rematerialised at every append under the register cap)
+  // (through an opaque move: the compiler cannot rematerialise it and keeps it in a register)
+  uint32_t laddr;
+  asm volatile("mov.u32 %0, %1;"
+               : "=r"(laddr)
+               : "r"(rr_base + (uint32_t)(offsetof(HalfASmem, list) - offsetof(HalfASmem, rr)) - 4u * (uint32_t)lane));
+#endif
   for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
     uint32_t qs[NSLOT];
     bool ok[NSLOT];
@@ -1552,7 +1564,12 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
       const float d2 = (sq.x + sq.y) + qz.x;
       if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) {
         if (cnt < HLA) {
+#if BDM_HLST
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(laddr + 128u * (uint32_t)cnt), "r"(qs[t]) : "memory");
+          ++cnt;
+#else
           sm.list[cnt++][lane] = qs[t];
+#endif
         } else {  // rare: the partner still gets its backward entry
           uint32_t j = qs[t];
 #if BDM_HSTAGE
