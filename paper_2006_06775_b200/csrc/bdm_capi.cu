@@ -863,13 +863,23 @@ int regrow(bdm_ctx* h, T** p, size_t keep, size_t new_count) {
   return BDM_OK;
 }
 
+// The padding agent after the fp32 copy's capacity N: agf[N] = (+inf, +inf, +inf, 0), which fails
+// every prefilter test (pass A's slots past a lane's last candidate read it; GridDev::pad).
+int set_agf_pad(bdm_ctx* h, size_t N) {
+  const float inf = __builtin_huge_valf();
+  const float4 pad = make_float4(inf, inf, inf, 0.f);
+  CU(h, cudaMemcpy(h->agf + N, &pad, sizeof pad, cudaMemcpyHostToDevice));
+  h->grid.pad = (uint32_t)N;
+  return BDM_OK;
+}
+
 int grow_capacity(bdm_ctx* h, int64_t new_cap) {
   if (new_cap <= h->cap) return BDM_OK;
   if (new_cap >= (int64_t)0xffffffffll) return fail(h, BDM_ERANGE, "population would exceed 2^32 - 1 agents");
   const size_t N = (size_t)new_cap, n = (size_t)h->n, nd = (size_t)h->n_dp;
   const int oi = h->out_ids == h->id[0] ? 0 : (h->out_ids == h->id[1] ? 1 : -1);
   int rc;
-  if ((rc = regrow(h, &h->ag[0], n, N)) || (rc = regrow(h, &h->ag[1], n, N)) || (rc = regrow(h, &h->agf, 0, N)) ||
+  if ((rc = regrow(h, &h->ag[0], n, N)) || (rc = regrow(h, &h->ag[1], n, N)) || (rc = regrow(h, &h->agf, 0, N + 1)) ||
       (rc = regrow(h, &h->id[0], n, N)) || (rc = regrow(h, &h->id[1], n, N)) || (rc = regrow(h, &h->key, 0, N)) ||
       (rc = regrow(h, &h->slot, 0, N)) || (rc = regrow(h, &h->tsrc, 0, N)) || (rc = regrow(h, &h->tid, 0, N)) ||
       (rc = regrow(h, &h->tkey, 0, N)) || (rc = regrow(h, &h->dp, 3 * nd, 3 * N)) ||
@@ -879,6 +889,7 @@ int grow_capacity(bdm_ctx* h, int64_t new_cap) {
       (rc = regrow(h, &h->hist[1], 0, N)) || (rc = regrow(h, &h->gflag, n + 1, N + 1)))
     return rc;
   if (oi >= 0) h->out_ids = h->id[oi];
+  if ((rc = set_agf_pad(h, N))) return rc;
   if (h->stage) {
     CU(h, cudaFree(h->stage));
     h->stage = nullptr;
@@ -1214,7 +1225,8 @@ int bdm_init(bdm_handle* out, int64_t n, const double* pos, const double* diam, 
   const size_t N = (size_t)n;
   TRY(dalloc(h, &h->ag[0], N));
   TRY(dalloc(h, &h->ag[1], N));
-  TRY(dalloc(h, &h->agf, N));
+  TRY(dalloc(h, &h->agf, N + 1));
+  TRY(set_agf_pad(h, N));
   TRY(dalloc(h, &h->id[0], N));
   TRY(dalloc(h, &h->id[1], N));
   TRY(dalloc(h, &h->key, N));
@@ -1846,7 +1858,8 @@ int bdm_slab_init(bdm_handle* out, int64_t n_local, int64_t capacity, const uint
   const size_t N = (size_t)capacity;
   TRY(dalloc(h, &h->ag[0], N));
   TRY(dalloc(h, &h->ag[1], N));
-  TRY(dalloc(h, &h->agf, N));
+  TRY(dalloc(h, &h->agf, N + 1));
+  TRY(set_agf_pad(h, N));
   TRY(dalloc(h, &h->id[0], N));
   TRY(dalloc(h, &h->id[1], N));
   TRY(dalloc(h, &h->key, N));

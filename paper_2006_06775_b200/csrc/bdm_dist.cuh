@@ -965,6 +965,7 @@ int dist_chunk_begin(bdm_ctx* H, DistGroup* G, int K) {
       nh->timing = h->timing;
       nh->launches = h->launches;
       nh->grid = h->grid;
+      nh->grid.pad = (uint32_t)nroom;  // (its own padding agent)
       bdm_destroy(h);
       D.h = h = nh;
       D.room = nroom;

@@ -59,6 +59,8 @@ struct GridDev {
   const uint32_t* coff;  // n_cols + 1
   const uint32_t* table;
   const int4* col;       // per column (czlo, czhi, coff, 0): one 16-byte load per column lookup
+  uint32_t pad;          // index of the padding agent agf[pad] = (+inf, +inf, +inf, 0) (capacity; pass A's
+                         // slots past the end of a lane's candidates read it and fail the filter)
 };
 
 struct ParamsDev {
@@ -1508,7 +1510,7 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
                                           uint32_t wmax, uint32_t w, uint32_t i, unsigned long long mxy,
                                           unsigned long long mzr, int& cnt, uint32_t& extra,
                                           uint32_t* __restrict__ fwd_rows, uint32_t* __restrict__ bwd,
-                                          uint32_t* __restrict__ bcnt) {
+                                          uint32_t* __restrict__ bcnt, uint32_t pad) {
   const int lane = threadIdx.x & 31;
   uint2 cur = sm.rr[0][lane];
   uint32_t q = cur.x, e = cur.y;
@@ -1528,8 +1530,10 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
     bool ok[NSLOT];
 #pragma unroll
     for (int t = 0; t < NSLOT; ++t) {
-      ok[t] = s0 + t < w;
-      qs[t] = ok[t] ? q : 0u;
+      // unstaged: past its last run a lane walks the sentinel run (pad, ~0): every slot reads the
+      // padding agent, which fails the filter, so no per-slot bound test
+      ok[t] = STAGED ? s0 + t < w : true;
+      qs[t] = STAGED ? (ok[t] ? q : 0u) : min(q, pad);
       ++q;
       const uint32_t sw = q == e;
       q = sw ? nx.x : q;
@@ -1913,7 +1917,8 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
         }
       }
     }
-    sm.rr[nr][lane] = make_uint2(0u, 0u);  // sentinel: after the last run q never meets e again
+    // sentinel: after the last run q never meets e again (unstaged: the padding run, see half_scan)
+    sm.rr[nr][lane] = staged ? make_uint2(0u, 0u) : make_uint2(g.pad, 0xffffffffu);
 #if !BDM_HMAP
     w = wr;
 #endif
@@ -1928,7 +1933,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     if (staged) {
       mbar_wait(&sm.bar, phase);
       phase ^= 1u;
-      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
+      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
       // buffer index -> global sorted index (each union run is contiguous in both)
       for (int x = 0; x < cnt; ++x) {
         const uint32_t v = sm.list[x][lane];
@@ -1943,7 +1948,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
 #if BDM_HMAP
       half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
 #else
-      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
+      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
 #endif
     if (valid) {
       half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
@@ -2359,7 +2364,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
           }
         }
       }
-      sm.rr[nr][lane] = make_uint2(0u, 0u);
+      sm.rr[nr][lane] = staged ? make_uint2(0u, 0u) : make_uint2(g.pad, 0xffffffffu);
       __syncwarp();
       const uint32_t wmax = __reduce_max_sync(FULL, w);
       const float ri32 = __double2float_ru(ri + g.m32);
@@ -2375,7 +2380,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
           sm.list[x][lane] = vv - m.off[r] + m.ub[r];
         }
       } else {
-        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
+        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
       }
       if (valid) {
         half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
