@@ -1435,6 +1435,9 @@ constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 #ifndef BDM_HRPF
 #define BDM_HRPF 0  // pass B: counts two chunks ahead, first row vector one chunk ahead (merged rows; spills: slower)
 #endif
+#ifndef BDM_HNET
+#define BDM_HNET 1  // pass B: rows of <= 4 entries sorted by a register sorting network (else insertion sort)
+#endif
 #ifndef BDM_HPPF
 #define BDM_HPPF 1  // pass B: partner states prefetched into L1 as soon as the row is read
 #endif
@@ -2584,6 +2587,21 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
 #endif
       // backward partners (all < i) sorted ascending, then forward partners (all > i, ascending)
       uint32_t* col = &sm.list[0][lane];
+#if BDM_HNET
+      if (nb <= 4u) {  // (the common case) a 4-input sorting network in registers, missing entries as ~0
+        uint32_t a0 = b4.x, a1 = nb > 1u ? b4.y : ~0u, a2 = nb > 2u ? b4.z : ~0u, a3 = nb > 3u ? b4.w : ~0u, t;
+        t = min(a0, a1); a1 = max(a0, a1); a0 = t;
+        t = min(a2, a3); a3 = max(a2, a3); a2 = t;
+        t = min(a0, a2); a2 = max(a0, a2); a0 = t;
+        t = min(a1, a3); a3 = max(a1, a3); a1 = t;
+        t = min(a1, a2); a2 = max(a1, a2); a1 = t;
+        col[0] = a0;
+        col[32] = a1;
+        col[64] = a2;
+        col[96] = a3;
+      } else
+#endif
+      {
       col[0] = b4.x;
       col[32] = b4.y;
       col[64] = b4.z;
@@ -2603,6 +2621,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
           --x;
         }
         col[32 * x] = v;
+      }
       }
       uint32_t* fc = col + 32 * nb;
       if (nf > 0) fc[0] = f4.x;
