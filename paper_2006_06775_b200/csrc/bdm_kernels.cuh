@@ -1380,6 +1380,9 @@ constexpr int HB_MIN_BLOCKS = BDM_HB_MIN_BLOCKS;  // pass B
 constexpr int HPCAP = BDM_HPCAP;  // staged candidates (float4) per warp
 
 #define HA_RR (!BDM_HMAP || BDM_HSTAGE)  // the shared-memory run list (cursor with refills)
+#ifndef BDM_HDEF
+#define BDM_HDEF 1  // pass A: a chunk's row stores deferred to the next chunk (the atomics' latency hidden)
+#endif
 #ifndef BDM_HLST
 #define BDM_HLST 1  // pass A: survivor appends through a precomputed shared address
 #endif
@@ -1503,6 +1506,46 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
     if (base + (uint32_t)k < (uint32_t)HFC) row[base + k] = sm.list[k][lane];
 #endif
 }
+
+#if BDM_MROW
+// BDM_HDEF: half_emit in two halves.  At a chunk's end the atomics are issued (the owner's base slot,
+// a slot in each of the first four partners' rows; a fifth survivor onwards is emitted at once, rare);
+// the stores that need their results are done at the next chunk, after its set-up, so the atomics'
+// round trip hides behind that chunk's dependent loads.  sm.list still holds the survivors then.
+struct HalfPending {
+  uint32_t i, base, cnt;  // cnt = 0: nothing pending
+  uint32_t slot[4];
+};
+__device__ __forceinline__ void half_emit_issue(HalfASmem& sm, int lane, int cnt, uint32_t extra, uint32_t i,
+                                                uint32_t* __restrict__ fwd, uint32_t* __restrict__ bcnt,
+                                                HalfPending& pd) {
+  const uint32_t nf = (uint32_t)cnt + extra + (extra ? (uint32_t)HFC : 0u);
+  pd.base = nf ? atomicAdd(&bcnt[i], nf) : 0u;
+  pd.i = i;
+  pd.cnt = (uint32_t)cnt;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if (u < cnt) pd.slot[u] = atomicAdd(&bcnt[sm.list[u][lane]], 1u);
+  for (int x = 4; x < cnt; ++x) {  // (rare)
+    const uint32_t j = sm.list[x][lane];
+    bw_put(fwd, fwd, j, atomicAdd(&bcnt[j], 1u), i);
+  }
+}
+__device__ __forceinline__ void half_emit_finish(HalfASmem& sm, int lane, uint32_t* __restrict__ fwd,
+                                                 HalfPending& pd) {
+  if (pd.cnt == 0u) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+    if ((uint32_t)u < pd.cnt) {
+      BDM_ASSERT(sm.list[u][lane] > pd.i);
+      bw_put(fwd, fwd, sm.list[u][lane], pd.slot[u], pd.i);
+    }
+  uint32_t* row = fwd + (size_t)pd.i * HFC;
+  for (uint32_t k = 0; k < pd.cnt; ++k)
+    if (pd.base + k < (uint32_t)HFC) row[pd.base + k] = sm.list[k][lane];
+  pd.cnt = 0u;
+}
+#endif
 
 // Candidate loop of pass A over this lane's runs rr[] (flattened, branch-free run switch): fp32
 // conservative filter of k_force; survivors to the lane's list (STAGED: runs and survivors are
@@ -1667,6 +1710,10 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   __syncwarp();
 #endif
   Tickets tk(s_end - s_begin);
+#if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
+  HalfPending pd;
+  pd.cnt = 0u;
+#endif
 #if BDM_HAPF
   // the next chunk's fp32 agents are loaded one chunk ahead (four registers)
   uint32_t chunk = tk.take(work, lane);
@@ -1951,10 +1998,19 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
 #if BDM_HMAP
       half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
 #else
+    {
+#if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
+      half_emit_finish(sm, lane, fwd, pd);  // the last chunk's stores (before the list is overwritten)
+#endif
       half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
+    }
 #endif
     if (valid) {
+#if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
+      half_emit_issue(sm, lane, cnt, extra, i, fwd, bcnt, pd);
+#else
       half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
+#endif
       if (!BDM_MROW) {
         const uint32_t nf = (uint32_t)cnt + extra;
         fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
@@ -1962,6 +2018,9 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     }
     __syncwarp();
   }
+#if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
+  half_emit_finish(sm, lane, fwd, pd);
+#endif
 }
 
 // ---- Pass A with the neighbourhood staged in shared memory (north_star: "a force kernel that stages
