@@ -120,8 +120,11 @@ __device__ __forceinline__ uint32_t hdr_u32(const double* m, int k) { return (ui
 // Owned count after a step and the ranges the split scans: after a step only the first two and
 // last two box-x layers of the step's sorted order can hold emigrants or boundary stayers
 // (k_layer_bounds); mode 0 (first step of a chunk after setup or a restore): the whole array.
+// (cnt4: the split's four counters, zeroed here so that no memset interrupts the launch chain)
 __global__ void k_dist_prep(GridDev g, int mode, int32_t x_begin, int32_t x_end, uint32_t* __restrict__ dc,
-                            uint32_t* __restrict__ r2) {
+                            uint32_t* __restrict__ r2, uint32_t* __restrict__ cnt4 = nullptr) {
+  pdl_wait();
+  if (cnt4 && threadIdx.x < 4) cnt4[threadIdx.x] = 0u;
   if (threadIdx.x != 0) return;
   uint32_t live = dc[DC_LIVE];
   if (mode == 1) {
@@ -159,6 +162,7 @@ __global__ void k_dist_prep(GridDev g, int mode, int32_t x_begin, int32_t x_end,
 // [3] stayers hi); a side whose records exceed the capacity is flagged (the chunk is re-run).
 __global__ void k_dist_header(const uint32_t* __restrict__ cnt, uint64_t cap, double* __restrict__ msg_lo,
                               double* __restrict__ msg_hi, uint32_t* __restrict__ dc) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   const uint64_t nlo = (uint64_t)cnt[0] + cnt[1], nhi = (uint64_t)cnt[2] + cnt[3];
   const bool olo = nlo > cap, ohi = nhi > cap;
@@ -187,6 +191,7 @@ __global__ void k_dist_ingest(double4* __restrict__ ag, uint32_t* __restrict__ i
                               const double* __restrict__ send_hi, const double* __restrict__ recv_lo,
                               const double* __restrict__ recv_hi, uint32_t cap, int has_lo, int has_hi, uint32_t room,
                               int fused) {
+  pdl_wait();
   const uint32_t live = dc[DC_LIVE];
   bool ovf = false;
   // own split (the emigrants are at the front of the send records, the stayers at the back).  A message
@@ -748,14 +753,12 @@ int dist_split_all(bdm_ctx* H, DistGroup* G) {
   cudaStream_t st = G->stream;
   for (auto& D : G->sl) {
     bdm_ctx* h = D.h;
-    k_dist_prep<<<1, 32, 0, st>>>(h->grid, D.stepped ? 1 : 0, D.xb, D.xe, D.dc, h->cnt + 4);
+    CU(H, lx(k_dist_prep, 1, 32, 0, st, h->grid, D.stepped ? 1 : 0, D.xb, D.xe, D.dc, h->cnt + 4, h->cnt));
     DBG(h, "k_dist_prep");
-    CU(H, cudaMemsetAsync(h->cnt, 0, 4 * sizeof(uint32_t), st));
-    k_slab_split<<<h->sm_count * 4, 256, 0, st>>>(h->ag[h->cur], h->id[h->cur], (uint32_t)D.room, h->cnt + 4,
-                                                   h->grid.inv, D.xb, D.xe, D.msg[0] + HDR, D.msg[1] + HDR,
-                                                   (uint64_t)G->cap, h->cnt, D.dc + DC_LIVE);
+    CU(H, lx(k_slab_split, h->sm_count * 4, 256, 0, st, h->ag[h->cur], h->id[h->cur], (uint32_t)D.room, h->cnt + 4,
+             h->grid.inv, D.xb, D.xe, D.msg[0] + HDR, D.msg[1] + HDR, (uint64_t)G->cap, h->cnt, D.dc + DC_LIVE));
     DBG(h, "k_slab_split");
-    k_dist_header<<<1, 32, 0, st>>>(h->cnt, (uint64_t)G->cap, D.msg[0], D.msg[1], D.dc);
+    CU(H, lx(k_dist_header, 1, 32, 0, st, h->cnt, (uint64_t)G->cap, D.msg[0], D.msg[1], D.dc));
     DBG(h, "k_dist_header");
     CU(H, cudaGetLastError());
     h->launches += 3;
@@ -787,13 +790,13 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   const uint32_t room = (uint32_t)D.room;
   // emigrants of the split are marked dead in place (the sort drops them)
   const bool packed = h->cols_next && D.zbits > 0;  // the last sum pass wrote packed new boxes of [0, LIVE)
-  k_slab_mark_dead<<<h->sm_count * 4, 256, 0, st>>>(h->ag[h->cur], room, h->cnt + 4, h->grid.inv, D.xb, D.xe,
-                                                    D.dc + DC_LIVE, packed ? h->pbox : nullptr);
+  CU(H, lx(k_slab_mark_dead, h->sm_count * 4, 256, 0, st, h->ag[h->cur], room, h->cnt + 4, h->grid.inv, D.xb, D.xe,
+           D.dc + DC_LIVE, packed ? h->pbox : nullptr));
   DBG(h, "k_slab_mark_dead");
   const bool fused = h->cols_next;
-  k_dist_ingest<<<h->sm_count * 2, 256, 0, st>>>(h->ag[h->cur], h->id[h->cur], D.dc, h->cnt, D.msg[0], D.msg[1],
-                                                 D.msg[2], D.msg[3], (uint32_t)G->cap, D.rank > 0,
-                                                 D.rank + 1 < G->world, room, fused ? 1 : 0);
+  CU(H, lx(k_dist_ingest, h->sm_count * 2, 256, 0, st, h->ag[h->cur], h->id[h->cur], D.dc, h->cnt, D.msg[0], D.msg[1],
+           D.msg[2], D.msg[3], (uint32_t)G->cap, D.rank > 0 ? 1 : 0, D.rank + 1 < G->world ? 1 : 0, room,
+           fused ? 1 : 0));
   DBG(h, "k_dist_ingest");
   CU(H, cudaGetLastError());
   h->launches += 2;
@@ -832,7 +835,7 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
       if (rc) return fail(H, rc, "%s", h->error.c_str());
     } else {
       const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
-      k_col_reset<<<gs, 256, 0, st>>>(h->czlo, h->czhi, g.n_cols);
+      CU(H, lx(k_col_reset, gs, 256, 0, st, h->czlo, h->czhi, g.n_cols));
       h->launches += 1;
     }
     g.czlo = h->czlo;
@@ -840,34 +843,38 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     g.coff = h->coff;
     g.table = h->table;
     g.col = h->colrec;
-    k_col_ext<<<fused ? h->sm_count * 2 : blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->czlo, h->czhi,
-                                                                          D.dc + DC_CE0);
+    CU(H, lx(k_col_ext, fused ? h->sm_count * 2 : blocks(room, 512), 256, 0, st, h->ag[src0], room, g, h->czlo,
+             h->czhi, D.dc + DC_CE0));
     DBG(h, "k_col_ext(dist)");
     const unsigned gs = (unsigned)std::min<uint64_t>((nc + 256) / 256, 148u * 16u);
-    k_col_len<<<gs, 256, 0, st>>>(h->czlo, h->czhi, g.n_cols, h->coff);
-    DBG(h, "k_col_len(dist)");
-    rc = scan(h, h->coff, nc + 1, nullptr);
+    rc = scan_reserve(h, nc + 1);  // (k_col_len zeroes the offset scan's tile states, k_table_zero the table scan's)
     if (rc) return fail(H, rc, "%s", h->error.c_str());
-    k_table_zero<<<h->sm_count * 8, 256, 0, st>>>(h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec);
+    CU(H, lx(k_col_len, gs, 256, 0, st, h->czlo, h->czhi, g.n_cols, h->coff, h->scan_state,
+             (uint32_t)((nc + 1 + SCAN_TILE - 1) / SCAN_TILE), h->scan_ticket));
+    DBG(h, "k_col_len(dist)");
+    rc = scan(h, h->coff, nc + 1, nullptr, true);
+    if (rc) return fail(H, rc, "%s", h->error.c_str());
+    CU(H, lx(k_table_zero, h->sm_count * 8, 256, 0, st, h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec,
+             h->scan_state, (uint32_t)h->scan_tiles_cap, h->scan_ticket));
     DBG(h, "k_table_zero(dist)");
     if (packed) {  // the stepped agents' boxes from the sum pass (4 B), the appended records from their state
-      k_key_hist_packed<true><<<blocks(room, 256 * KHP), 256, 0, st>>>(h->pbox, room, g, D.flo[2], D.zbits, h->key,
-                                                                      h->slot, h->table, h->err, D.dc + DC_LIVE);
-      k_key_hist<true><<<h->sm_count * 4, 256, 0, st>>>(h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
-                                                        D.dc + DC_TOT, D.dc + DC_LIVE);
+      CU(H, lx(k_key_hist_packed<true>, blocks(room, 256 * KHP), 256, 0, st, h->pbox, room, g, D.flo[2], D.zbits,
+               h->key, h->slot, h->table, h->err, D.dc + DC_LIVE));
+      CU(H, lx(k_key_hist<true>, h->sm_count * 4, 256, 0, st, h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
+               D.dc + DC_TOT, D.dc + DC_LIVE));
       h->launches += 1;
     } else {
-      k_key_hist<true><<<blocks(room, 512), 256, 0, st>>>(h->ag[src0], room, g, h->key, h->slot, h->table, h->err,
-                                                          D.dc + DC_TOT);
+      CU(H, lx(k_key_hist<true>, blocks(room, 512), 256, 0, st, h->ag[src0], room, g, h->key, h->slot, h->table,
+               h->err, D.dc + DC_TOT, nullptr));
     }
     DBG(h, "k_key_hist(dist)");
-    rc = scan(h, h->table, 0, h->coff + nc);
+    rc = scan(h, h->table, 0, h->coff + nc, true);
     if (rc) return fail(H, rc, "%s", h->error.c_str());
-    k_scatter<<<blocks(room, 256 * KSC), 256, 0, st>>>(h->key, h->slot, h->id[src0], h->table, room, h->tsrc, h->tid,
-                                                       h->tkey, D.dc + DC_TOT);
+    CU(H, lx(k_scatter, blocks(room, 256 * KSC), 256, 0, st, h->key, h->slot, h->id[src0], h->table, room, h->tsrc,
+             h->tid, h->tkey, D.dc + DC_TOT));
     DBG(h, "k_scatter(dist)");
-    k_place<<<blocks(room, PLACE_T), PLACE_T, 0, st>>>(h->tsrc, h->tid, h->tkey, h->table, h->ag[src0], room, h->ag[1 - src0],
-                                              h->id[1 - src0], h->agf, nullptr, nullptr, D.dc + DC_SORTED);
+    CU(H, lx(k_place, blocks(room, PLACE_T), PLACE_T, 0, st, h->tsrc, h->tid, h->tkey, h->table, h->ag[src0], room,
+             h->ag[1 - src0], h->id[1 - src0], h->agf, nullptr, nullptr, D.dc + DC_SORTED));
     DBG(h, "k_place(dist)");
     CU(H, cudaGetLastError());
     h->launches += 7;
@@ -888,24 +895,25 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     if (rc) return fail(H, rc, "%s", h->error.c_str());
     cn.czlo = h->czlo2;
     cn.czhi = h->czhi2;
-    const unsigned gs = (unsigned)std::min<uint64_t>((nc2 + 256) / 256, 148u * 16u);
-    k_col_reset<<<gs, 256, 0, st>>>(h->czlo2, h->czhi2, (uint32_t)nc2);
     if (D.zbits > 0) {  // packed new boxes for the next build's key pass (the frame is fixed for the chunk)
       cn.pbox = h->pbox;
       cn.z0 = D.flo[2];
       cn.zbits = D.zbits;
     }
+    // one launch: extents reset, the next build's column ranges, the pair counters
+    const uint64_t w = std::max<uint64_t>(nc2, (uint64_t)room / 4 + 1);
+    const unsigned gr = (unsigned)std::min<uint64_t>((w + 255) / 256, 148u * 16u);
+    CU(H, lx(k_force_reset, gr, 256, 0, st, h->ext, 1, h->czlo2, h->czhi2, (uint32_t)nc2, h->h_bcnt,
+             std::max<uint32_t>(room, 1u)));
   }
-  k_ext_reset<<<1, 32, 0, st>>>(h->ext, 1);
-  CU(H, cudaMemsetAsync(h->h_bcnt, 0, (size_t)room * sizeof(uint32_t), st));
   if (g_htile) {
     const unsigned gt = (unsigned)h->sm_count * h->tile_blocks_per_sm;
     k_half_search_tile<<<gt, TILE_THREADS, TILE_SMEM_BYTES, st>>>(h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt,
                                                               h->h_bwd, h->h_bcnt, h->ext, false, D.dc + DC_AEND);
   } else {
     const unsigned ga = (unsigned)h->sm_count * h->half_a_blocks_per_sm;
-    k_half_search<<<ga, HA_THREADS, HA_SMEM_BYTES, st>>>(h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt,
-                                                         h->h_bwd, h->h_bcnt, h->ext, false, D.dc + DC_AEND);
+    CU(H, lx(k_half_search, ga, HA_THREADS, HA_SMEM_BYTES, st, h->ag[src], h->agf, 0u, room, g, h->h_fwd, h->h_fcnt,
+             h->h_bwd, h->h_bcnt, h->ext, false, D.dc + DC_AEND, nullptr));
   }
   DBG(h, "k_half_search(dist)");
   if (h->timing && !h->timed.empty() && !h->timed.back().e3) {
@@ -915,18 +923,16 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   const unsigned gb = (unsigned)h->sm_count * h->half_b_blocks_per_sm;
   double* dp = want_dp ? h->dp : nullptr;
   uint32_t* dpi = want_dp ? h->dp_ids : nullptr;
-  k_half_sum<false><<<gb, FORCE_THREADS, HB_SMEM_BYTES, st>>>(h->ag[src], h->id[src], 0u, room, g, pd, h->ag[dst],
-                                                              h->id[dst], dp, dpi, h->ext, h->err, h->h_fwd, h->h_fcnt,
-                                                              h->h_bwd, h->h_bcnt, cn, nullptr, h->h_slow,
-                                                              D.dc + DC_ABEGIN);
+  CU(H, lx(k_half_sum<false>, gb, FORCE_THREADS, HB_SMEM_BYTES, st, h->ag[src], h->id[src], 0u, room, g, pd,
+           h->ag[dst], h->id[dst], dp, dpi, h->ext, h->err, h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, nullptr,
+           h->h_slow, D.dc + DC_ABEGIN, nullptr, (int64_t)-1));
   DBG(h, "k_half_sum(dist)");
-  k_half_slow<false><<<(unsigned)h->sm_count * 4, 128, 0, st>>>(h->ag[src], h->id[src], 0u, g, pd, h->ag[dst],
-                                                               h->id[dst], dp, dpi, h->ext, h->err, cn, nullptr,
-                                                               h->h_slow, D.dc + DC_ABEGIN);
+  CU(H, lx(k_half_slow<false>, (unsigned)h->sm_count * 4, 128, 0, st, h->ag[src], h->id[src], 0u, g, pd, h->ag[dst],
+           h->id[dst], dp, dpi, h->ext, h->err, cn, nullptr, h->h_slow, D.dc + DC_ABEGIN));
   DBG(h, "k_half_slow(dist)");
-  k_locate_nonfinite<<<1, 32, 0, st>>>(h->ag[src], h->id[src], g, pd, h->err);
+  CU(H, lx(k_locate_nonfinite, 1, 32, 0, st, h->ag[src], h->id[src], g, pd, h->err));
   CU(H, cudaGetLastError());
-  h->launches += 7;
+  h->launches += 5;  // k_force_reset, search, sum, slow, locate
   if (h->timing) CU(H, cudaEventRecord(ts.e2, st));
   h->cur = dst;
   h->cols_next = true;

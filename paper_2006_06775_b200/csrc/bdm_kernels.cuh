@@ -1438,6 +1438,9 @@ constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 #ifndef BDM_HRPF
 #define BDM_HRPF 0  // pass B: counts two chunks ahead, first row vector one chunk ahead (merged rows; spills: slower)
 #endif
+#ifndef BDM_HDIRECT
+#define BDM_HDIRECT 0  // pass B: each lane evaluates its own contacts (instead of the balanced contact phase)
+#endif
 #ifndef BDM_HNET
 #define BDM_HNET 1  // pass B: rows of <= 4 entries sorted by a register sorting network (else insertion sort)
 #endif
@@ -2707,9 +2710,26 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     double Fx = 0.0, Fy = 0.0, Fz = 0.0;
     int32_t n_ct = 0;
     unsigned long long ct_hash = 0;
+#if BDM_HDIRECT
+    {  // each lane its own candidates, in canonical order (a divergent loop: lanes of one chunk have
+       // similar counts)
+      const uint32_t* col = &sm.list[0][lane];
+      for (int t = 0; t < cnt; ++t) {
+        const uint32_t j = col[32 * t];
+        double tx, ty, tz, fa;
+        if (pair_term(me.x, me.y, me.z, ri, i, ld_state(&ag[j]), ids, j, p, tx, ty, tz, fa)) {
+          Fx = Fx + tx;
+          Fy = Fy + ty;
+          Fz = Fz + tz;
+        }
+      }
+      cnt = 0;
+    }
+#else
     if (__any_sync(FULL, cnt > 0))
       flush_contacts<false, HalfBSmem>(sm, lane, cnt, me.x, me.y, me.z, ri, i, ag, ids, p, Fx, Fy, Fz, n_ct,
                                        ct_hash);
+#endif
     {  // overflowing agents go to the slow list: k_half_slow sums and steps them (keeping the full
        // search out of this kernel keeps its registers and stack small)
       const unsigned sm_ = __ballot_sync(FULL, slow);
@@ -2980,6 +3000,7 @@ __global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __r
                              const uint32_t* __restrict__ r2, double inv, int32_t x_begin, int32_t x_end,
                              double* __restrict__ send_lo, double* __restrict__ send_hi, uint64_t cap,
                              uint32_t* __restrict__ cnt, const uint32_t* __restrict__ n_dev = nullptr) {
+  pdl_wait();
   __shared__ uint32_t s_cnt[4], s_base[4];
   if (n_dev) n = __ldg(n_dev);
   const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
@@ -3030,6 +3051,7 @@ __global__ void k_slab_split(const double4* __restrict__ ag, const uint32_t* __r
 __global__ void k_slab_mark_dead(double4* __restrict__ ag, uint32_t n, const uint32_t* __restrict__ r2, double inv,
                                  int32_t x_begin, int32_t x_end, const uint32_t* __restrict__ n_dev = nullptr,
                                  uint32_t* __restrict__ pbox = nullptr) {
+  pdl_wait();
   if (n_dev) n = __ldg(n_dev);
   const uint32_t n_lo_part = r2[0] < n ? r2[0] : n;
   const uint32_t hi0 = r2[1] > n_lo_part ? r2[1] : n_lo_part;

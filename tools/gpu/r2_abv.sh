@@ -3,7 +3,7 @@
 # VARIANTS="a b" REPS=2 TESTS="tests/test_gpu_parity.py ..." bash tools/gpu/r2_abv.sh
 mkdir -p gpurun_out
 make -s all 2>&1 | tail -2
-timeout 900 python -m pytest ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_half.py} -x -q > gpurun_out/pytest_ab.log 2>&1; echo pytest rc=$?
+BDM_LIBRARY=${TESTLIB:-} timeout 900 python -m pytest ${TESTS:-tests/test_gpu_parity.py tests/test_gpu_half.py} -x -q > gpurun_out/pytest_ab.log 2>&1; echo pytest rc=$?
 tail -2 gpurun_out/pytest_ab.log
 for rep in $(seq ${REPS:-2}); do
 for v in ${VARIANTS}; do
