@@ -1402,9 +1402,7 @@ struct HalfASmem {
   uint32_t pad_;
 #endif
   uint32_t list[HLA][32];  // survivors (sorted index j, or staged buffer index) of this lane, ascending
-#if HA_RR
-  uint2 rr[7][32];         // this lane's non-empty forward z-runs [b, e), then the sentinel (0, 0)
-#endif
+  uint2 rr[7][32];         // this lane's non-empty forward z-runs [b, e), then the sentinel
   uint32_t tab[5][BDM_HCOOP ? TSPAN : 1];  // box starts of the 5 forward columns (cooperative lookups only:
                                            // otherwise the shared memory goes to L1)
 };
@@ -1553,7 +1551,6 @@ __device__ __forceinline__ void half_emit_finish(HalfASmem& sm, int lane, uint32
 // Candidate loop of pass A over this lane's runs rr[] (flattened, branch-free run switch): fp32
 // conservative filter of k_force; survivors to the lane's list (STAGED: runs and survivors are
 // buffer indices of sm.buf).  A survivor beyond the list (rare) gets its backward entry at once.
-#if HA_RR
 template <bool STAGED>
 __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restrict__ agf, uint32_t rr_base,
                                           uint32_t wmax, uint32_t w, uint32_t i, unsigned long long mxy,
@@ -1641,15 +1638,14 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
   }
 }
 
-#endif
-
 // BDM_HMAP: the candidate loop with the closed-form cursor -- no shared-memory run refills and no
 // serial dependency between the slots of an iteration.
 __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __restrict__ agf, const uint32_t S[5],
                                               const uint32_t A[5], uint32_t wmax, uint32_t w, uint32_t i,
                                               unsigned long long mxy, unsigned long long mzr, int& cnt,
                                               uint32_t& extra, uint32_t* __restrict__ fwd_rows,
-                                              uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt) {
+                                              uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt, uint32_t pad,
+                                              uint32_t laddr) {
   const int lane = threadIdx.x & 31;
   for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
     uint32_t qs[NSLOT];
@@ -1660,8 +1656,8 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
       uint32_t a = A[0];
 #pragma unroll
       for (int q = 1; q < 5; ++q) a = k >= S[q] ? A[q] : a;
-      ok[t] = k < w;
-      qs[t] = ok[t] ? k + a : 0u;
+      ok[t] = true;  // (slots past w read the padding agent, which fails the filter)
+      qs[t] = k < w ? k + a : pad;
     }
     float4 o[NSLOT];
 #pragma unroll
@@ -1681,12 +1677,42 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
       const float d2 = (sq.x + sq.y) + qz.x;
       if (ok[t] && d2 <= __fmaf_rn(qz.y, 0x1p-20f, qz.y)) {
         if (cnt < HLA) {
-          sm.list[cnt++][lane] = qs[t];
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(laddr + 128u * (uint32_t)cnt), "r"(qs[t]) : "memory");
+          ++cnt;
         } else {  // rare: the partner still gets its backward entry
           bw_put(fwd_rows, bwd, qs[t], atomicAdd(&bcnt[qs[t]], 1u), i);
           ++extra;
         }
       }
+    }
+  }
+}
+
+// The forward z-runs [rb[q], re[q]) of the 5 forward columns q of agent i in box (bx, by, bz) with
+// culling bits `cull` (empty: rb >= re): the 5 column records first, then the 9 box starts (own
+// column: its run starts at i + 1), each level's loads all in flight together -- two dependent
+// levels instead of five zrun chains.
+__device__ __forceinline__ void forward_runs(const GridDev& g, int bx, int by, int bz, uint32_t i, uint32_t cull,
+                                             uint32_t rb[5], uint32_t re[5]) {
+  int4 ci[5];
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int cx = bx + (q >= 2 ? 1 : 0), cy = by + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
+    const bool in = ((cull >> q) & 1u) && cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1];
+    BDM_ASSERT(!in || col_of(g, cx, cy) < g.n_cols);
+    ci[q] = in ? __ldg(&g.col[col_of(g, cx, cy)]) : make_int4(1, 0, 0, 0);  // (empty: zl > zh)
+  }
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int z0 = q == 0 ? bz : bz - 1 + (int)((cull >> (8 + q)) & 1u);
+    const int z1 = bz + 1 - (int)((cull >> (16 + q)) & 1u);
+    const int a = z0 > ci[q].x ? z0 : ci[q].x, d = z1 < ci[q].y ? z1 : ci[q].y;
+    rb[q] = q == 0 ? i + 1 : 0u;
+    re[q] = 0u;
+    if (a <= d) {
+      BDM_ASSERT((uint32_t)ci[q].z + (uint32_t)(d - ci[q].x) + 1u <= __ldg(&g.coff[g.n_cols]));
+      if (q != 0) rb[q] = __ldg(&g.table[(uint32_t)ci[q].z + (uint32_t)(a - ci[q].x)]);
+      re[q] = __ldg(&g.table[(uint32_t)ci[q].z + (uint32_t)(d - ci[q].x) + 1u]);
     }
   }
 }
@@ -1704,6 +1730,10 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
   const int lane = threadIdx.x & 31;
 #if HA_RR
   const uint32_t rr_base = (uint32_t)__cvta_generic_to_shared(&sm.rr[0][lane]);
+#endif
+#if BDM_HMAP
+  uint32_t la_base;  // shared address of this lane's list column (opaque: kept in a register)
+  asm volatile("mov.u32 %0, %1;" : "=r"(la_base) : "r"((uint32_t)__cvta_generic_to_shared(&sm.list[0][lane])));
 #endif
   // statistics of the stationary-region skip mode (bdm_get_skip_stats): this path searches everyone
   if (count_searched && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&ext->searched, s_end - s_begin);
@@ -1883,6 +1913,19 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     // closed-form cursor (BDM_HMAP): run q occupies flattened positions [S[q], S[q+1]); position k
     // maps to k + A[q] (empty runs are skipped by the compare chain)
     uint32_t S[5], A[5];
+#if BDM_HBATCH
+    if (valid && !coop) {
+      uint32_t rb[5], re[5];
+      forward_runs(g, bx, by, bz, i, cull, rb, re);
+#pragma unroll
+      for (int q = 0; q < 5; ++q) {
+        const uint32_t b = rb[q] < re[q] ? rb[q] : 0u, e = rb[q] < re[q] ? re[q] : 0u;
+        S[q] = w;
+        A[q] = b - w;
+        w += e - b;
+      }
+    } else
+#endif
 #pragma unroll
     for (int q = 0; q < 5; ++q) {
       uint32_t b = 0, e = 0;
@@ -1908,30 +1951,8 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     uint32_t wr = 0;  // total length of the run list (staged path, or BDM_HMAP=0)
 #if BDM_HBATCH
     if (valid && !coop) {
-      // the 5 column records first, then the 9 box starts (own column: its run starts at i + 1), each
-      // level's loads all in flight together: two dependent levels instead of five zrun chains
-      int4 ci[5];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        const int cx = bx + (q >= 2 ? 1 : 0), cy = by + (q == 1 || q == 4 ? 1 : (q == 2 ? -1 : 0));
-        const bool in = ((cull >> q) & 1u) && cx >= g.lo[0] && cx <= g.hi[0] && cy >= g.lo[1] && cy <= g.hi[1];
-        BDM_ASSERT(!in || col_of(g, cx, cy) < g.n_cols);
-        ci[q] = in ? __ldg(&g.col[col_of(g, cx, cy)]) : make_int4(1, 0, 0, 0);  // (empty: zl > zh)
-      }
       uint32_t rb[5], re[5];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        const int z0 = q == 0 ? bz : bz - 1 + (int)((cull >> (8 + q)) & 1u);
-        const int z1 = bz + 1 - (int)((cull >> (16 + q)) & 1u);
-        const int a = z0 > ci[q].x ? z0 : ci[q].x, d = z1 < ci[q].y ? z1 : ci[q].y;
-        rb[q] = q == 0 ? i + 1 : 0u;
-        re[q] = 0u;
-        if (a <= d) {
-          BDM_ASSERT((uint32_t)ci[q].z + (uint32_t)(d - ci[q].x) + 1u <= __ldg(&g.coff[g.n_cols]));
-          if (q != 0) rb[q] = __ldg(&g.table[(uint32_t)ci[q].z + (uint32_t)(a - ci[q].x)]);
-          re[q] = __ldg(&g.table[(uint32_t)ci[q].z + (uint32_t)(d - ci[q].x) + 1u]);
-        }
-      }
+      forward_runs(g, bx, by, bz, i, cull, rb, re);
 #pragma unroll
       for (int q = 0; q < 5; ++q)
         if (rb[q] < re[q]) {
@@ -1999,7 +2020,12 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     } else
 #endif
 #if BDM_HMAP
-      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
+    {
+#if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
+      half_emit_finish(sm, lane, fwd, pd);  // the last chunk's stores (before the list is overwritten)
+#endif
+      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad, la_base);
+    }
 #else
     {
 #if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
