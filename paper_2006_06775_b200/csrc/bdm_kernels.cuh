@@ -975,14 +975,16 @@ __device__ __forceinline__ void flush_contacts(Smem& sm, int lane, int& cnt, dou
         flag = RECORD ? ids[j] : 0u;  // id for the contact digest; any value != ~0 marks a contact
       }
     }
-    sm.cidx[lane] = flag;
+    // which batch entries are contacts: a ballot (the id for the RECORD digest goes through cidx)
+    const unsigned cmask = __ballot_sync(FULL, flag != 0xffffffffu);
+    if (RECORD) sm.cidx[lane] = flag;
     __syncwarp();
     const int lo = excl > b0 ? excl : b0;
     const int hi = incl < b0 + 32 ? incl : b0 + 32;
     for (int x = lo; x < hi; ++x) {
       const int t = x - b0;
-      const uint32_t fl = sm.cidx[t];
-      if (fl != 0xffffffffu) {
+      const uint32_t fl = RECORD ? sm.cidx[t] : 0u;
+      if ((cmask >> t) & 1u) {
         Fx = Fx + sm.term[0][t];
         Fy = Fy + sm.term[1][t];
         Fz = Fz + sm.term[2][t];
