@@ -38,6 +38,8 @@ const bool g_htile = std::getenv("BDM_HTILE") && std::getenv("BDM_HTILE")[0] == 
 const int g_bands = std::getenv("BDM_BANDS") ? std::max(1, std::min(32, std::atoi(std::getenv("BDM_BANDS")))) : 1;
 // BDM_PBOX=0: the key pass re-reads the state instead of the sum pass's packed boxes
 const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
+// BDM_FUSE=0: no fused column pass in the sum pass (the build runs its own column pass)
+const bool g_fuse = !(std::getenv("BDM_FUSE") && std::getenv("BDM_FUSE")[0] == '0');
 // BDM_PDL=0: the step's launch chain without programmatic dependent launch (lx below)
 const bool g_pdl = !(std::getenv("BDM_PDL") && std::getenv("BDM_PDL")[0] == '0');
 
@@ -811,7 +813,7 @@ int force_step(bdm_ctx* h, bool want_dp) {
   if (h->last_half) {
     // fuse the next build's column pass when nothing moves agents between this step and that build
     // and one step moves an agent by less than a box (|dp| <= max_disp (1 + 4u) < L)
-    const bool fuse = !h->growth_on && !h->fields_on && h->n_el == 0 && !h->slab &&
+    const bool fuse = g_fuse && !h->growth_on && !h->fields_on && h->n_el == 0 && !h->slab &&
                       h->prm.max_disp < h->grid.L * (1.0 - 0x1p-20);
     int rc = half_force(h, src, 0u, 0u, n, n, pd, h->ag[dst], nullptr, dp, nullptr, fuse, nullptr,
                         h->hist[0] ? h->hist[dst] : nullptr, nullptr, ext_mode);  // (k_force_reset resets ext)
