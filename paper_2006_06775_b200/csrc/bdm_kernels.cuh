@@ -893,6 +893,9 @@ constexpr int NSLOT = BDM_NSLOT;
 #endif
 constexpr int LCAP = 16;             // per-lane survivor list capacity (flushed before overflow)
 
+#ifndef BDM_PTSPEC
+#define BDM_PTSPEC 1
+#endif
 // One contact candidate of agent i (O4), returns false if delta <= 0.
 // i, j are sorted indices; ids[] is read only for coincident centres (the R8 tie-break, rare).
 __device__ __forceinline__ bool pair_term(double xi, double yi, double zi, double ri, uint32_t i, const double4& o,
@@ -904,10 +907,19 @@ __device__ __forceinline__ bool pair_term(double xi, double yi, double zi, doubl
   double d2 = (dx * dx + dy * dy) + dz * dz;
   double rj = 0.5 * o.w;
   double s = ri + rj;
+#if BDM_PTSPEC
+  // (the reduced radius first: its division then overlaps the square root instead of following the
+  // contact test -- nearly every candidate that reaches here is a contact)
+  double r = (ri * rj) / s;
+  double d = sqrt(d2);
+  double delta = s - d;
+  if (!(delta > 0.0)) return false;
+#else
   double d = sqrt(d2);
   double delta = s - d;
   if (!(delta > 0.0)) return false;
   double r = (ri * rj) / s;
+#endif
   double f = p.k_rep * delta - p.gamma_att * sqrt(r * delta);
   fabs_out = fabs(f);
   if (d2 == 0.0) {  // coincident centres (R8)
