@@ -40,6 +40,8 @@ const int g_bands = std::getenv("BDM_BANDS") ? std::max(1, std::min(32, std::ato
 const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '0');
 // BDM_FUSE=0: no fused column pass in the sum pass (the build runs its own column pass)
 const bool g_fuse = !(std::getenv("BDM_FUSE") && std::getenv("BDM_FUSE")[0] == '0');
+// BDM_TZERO=0: the build zeroes its histogram itself (default: the last sum pass zeroed it, table2)
+const bool g_tzero = !(std::getenv("BDM_TZERO") && std::getenv("BDM_TZERO")[0] == '0');
 // BDM_PDL=0: the step's launch chain without programmatic dependent launch (lx below)
 const bool g_pdl = !(std::getenv("BDM_PDL") && std::getenv("BDM_PDL")[0] == '0');
 
@@ -68,6 +70,10 @@ struct bdm_ctx {
   uint32_t *key = nullptr, *slot = nullptr, *tsrc = nullptr, *tid = nullptr, *tkey = nullptr;
   uint32_t* table = nullptr;
   size_t table_cap = 0;  // entries
+  // the next build's histogram buffer (same capacity), zeroed by the last sum pass up to ext->zeroed
+  // entries while the current table was still in use (table_pre: that happened; the build swaps them)
+  uint32_t* table2 = nullptr;
+  bool table_pre = false;
   unsigned long long* scan_state = nullptr;
   uint32_t* scan_ticket = nullptr;
   size_t scan_tiles_cap = 0;
@@ -296,6 +302,9 @@ int ensure_table(bdm_ctx* h, size_t entries, size_t min_scan_items) {
   if (entries > h->table_cap) {
     if (h->table) CU(h, cudaFree(h->table));
     h->table = nullptr;
+    if (h->table2) CU(h, cudaFree(h->table2));  // (reallocated on demand with the new capacity)
+    h->table2 = nullptr;
+    h->table_pre = false;
     size_t cap = entries + entries / 4 + (1u << 20);  // generous: no reallocation as extents drift
     CU(h, cudaMalloc(&h->table, cap * sizeof(uint32_t)));
     h->table_cap = cap;
@@ -457,6 +466,25 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
       }
     }
   }
+  // the next build's histogram buffer, zeroed on a side stream during this force phase (the current
+  // table is in use until its end): k_table_zero_tma, joined before half_force returns
+  bool tz = false;
+  if (fuse_cols && !frame4 && !h->slab && g_tzero && !force_only && h->table_cap >= 8) {
+    if (!h->table2) CU(h, cudaMalloc(&h->table2, h->table_cap * sizeof(uint32_t)));
+    if (!h->s2) {
+      CU(h, cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
+      for (int k = 0; k < 33; ++k) CU(h, cudaEventCreateWithFlags(&h->bev[k], cudaEventDisableTiming));
+      CU(h, cudaMalloc(&h->bwork, 64 * sizeof(uint32_t)));
+    }
+    CU(h, cudaEventRecord(h->bev[31], s));
+    CU(h, cudaStreamWaitEvent(h->s2, h->bev[31], 0));
+    k_table_zero_tma<<<h->sm_count, 32, 0, h->s2>>>(h->table2, h->coff, h->grid.n_cols,
+                                                    (uint32_t)std::min<size_t>((h->table_cap - 4) & ~(size_t)3, 0xfffffff0u),
+                                                    &h->ext->zeroed);
+    CU(h, cudaEventRecord(h->bev[32], h->s2));
+    h->launches += 1;
+    tz = true;
+  }
   {  // one launch: the extents reset (ext_mode >= 0), the next build's column ranges, the pair counters
     const uint64_t w = std::max<uint64_t>(nc2, (uint64_t)n_all / 4 + 1);
     const unsigned gr = (unsigned)std::min<uint64_t>((w + 255) / 256, 148u * 16u);
@@ -467,6 +495,8 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   // banded force phase: bands of >= 2^20 agents each
   const int nb = force_only ? 1 : (int)std::min<int64_t>(g_bands, std::max<int64_t>(1, ((int64_t)a_end - a_begin) >> 20));
   if (nb > 1) {
+    if (tz) CU(h, cudaStreamWaitEvent(s, h->bev[32], 0));  // (the bands reuse the side stream's events)
+    tz = false;
     if (!h->s2) {
       CU(h, cudaStreamCreateWithFlags(&h->s2, cudaStreamNonBlocking));
       for (int k = 0; k < 33; ++k) CU(h, cudaEventCreateWithFlags(&h->bev[k], cudaEventDisableTiming));
@@ -545,6 +575,10 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
   DBG(h, "k_half_slow");
   DBG(h, "k_half_sum");
   CU(h, lx(k_locate_nonfinite, 1, 32, 0, s, h->ag[src], h->id[src], h->grid, pd, h->err));
+  if (tz) {  // join the side stream's zeroing
+    CU(h, cudaStreamWaitEvent(s, h->bev[32], 0));
+    h->table_pre = true;
+  }
   CU(h, cudaGetLastError());
   h->launches += 4;
   h->cols_next = fuse_cols;
@@ -717,6 +751,14 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
     DBG(h, "k_col_ext");
     h->launches += n > 0 ? 2 : 1;
   }
+  // the histogram buffer the last sum pass zeroed (ensure_table above cleared the flag if it had to
+  // reallocate); k_table_zero then zeroes only what lies beyond ext->zeroed
+  const bool pre = h->table_pre && h->table2;
+  if (pre) {
+    std::swap(h->table, h->table2);
+    g.table = h->table;
+    h->table_pre = false;
+  }
   // (k_col_len zeroes the offset scan's tile states, k_table_zero the table scan's)
   rc = scan_reserve(h, nc + 1);
   if (rc) return rc;
@@ -726,7 +768,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
   rc = scan(h, h->coff, nc + 1, nullptr, true);  // exclusive: coff[c] = table offset, coff[nc] = T
   if (rc) return rc;
   CU(h, lx(k_table_zero, h->sm_count * 8, 256, 0, s, h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec,
-           h->scan_state, (uint32_t)h->scan_tiles_cap, h->scan_ticket));
+           h->scan_state, (uint32_t)h->scan_tiles_cap, h->scan_ticket, pre ? &h->ext->zeroed : nullptr));
   DBG(h, "k_table_zero");
   if (n > 0 && packed) {  // boxes from the last sum pass (4 B/agent instead of the state)
     CU(h, lx(h->deferred > 0 ? k_key_hist_packed<true> : k_key_hist_packed<false>, blocks(n, 256 * KHP), 256, 0, s,
@@ -1175,7 +1217,7 @@ void bdm_destroy(bdm_handle h) {
     cudaEventDestroy(t.e2);
     if (t.e3) cudaEventDestroy(t.e3);
   }
-  void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table,
+  void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table, h->table2,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->pbox, h->colrec, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
                   h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->h_slow, h->czlo2, h->czhi2};
   for (void* p : ptrs)

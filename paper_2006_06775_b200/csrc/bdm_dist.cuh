@@ -855,7 +855,7 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
     rc = scan(h, h->coff, nc + 1, nullptr, true);
     if (rc) return fail(H, rc, "%s", h->error.c_str());
     CU(H, lx(k_table_zero, h->sm_count * 8, 256, 0, st, h->table, h->coff, g.n_cols, h->czlo, h->czhi, h->colrec,
-             h->scan_state, (uint32_t)h->scan_tiles_cap, h->scan_ticket));
+             h->scan_state, (uint32_t)h->scan_tiles_cap, h->scan_ticket, nullptr));
     DBG(h, "k_table_zero(dist)");
     if (packed) {  // the stepped agents' boxes from the sum pass (4 B), the appended records from their state
       CU(H, lx(k_key_hist_packed<true>, blocks(room, 256 * KHP), 256, 0, st, h->pbox, room, g, D.flo[2], D.zbits,

@@ -78,6 +78,7 @@ struct Extents {
   uint32_t slow;      // agents of the half-shell sum pass whose pair rows overflowed (full search)
   uint32_t col_bad;   // fused column pass: some agent's new box left its frame (columns invalid)
   uint32_t sticky;    // range_err (bit 0) / col_bad (bit 1) of earlier steps (deferred builds)
+  uint32_t zeroed;    // entries of the next build's histogram buffer the last sum pass zeroed (ColNext::zbuf)
 };
 
 // Fused column pass (k_half_sum): occupied z-range of every column (bx, by) of the NEXT build's
@@ -460,7 +461,8 @@ __global__ void k_col_len(const int32_t* __restrict__ czlo, const int32_t* __res
 __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __restrict__ coff, uint32_t nc,
                              const int32_t* __restrict__ czlo, const int32_t* __restrict__ czhi,
                              int4* __restrict__ col, unsigned long long* __restrict__ st = nullptr,
-                             uint32_t st_cap = 0, uint32_t* __restrict__ ticket = nullptr) {
+                             uint32_t st_cap = 0, uint32_t* __restrict__ ticket = nullptr,
+                             const uint32_t* __restrict__ zeroed = nullptr) {
   pdl_wait();
   if (st) {  // the table scan's tile states (T + 1 items) and ticket (see k_col_len)
     const uint32_t tiles = min(st_cap, (__ldg(&coff[nc]) + 1u + (uint32_t)SCAN_TILE_C - 1u) / (uint32_t)SCAN_TILE_C);
@@ -470,13 +472,43 @@ __global__ void k_table_zero(uint32_t* __restrict__ table, const uint32_t* __res
   for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nc; c += gridDim.x * blockDim.x)
     col[c] = make_int4(czlo[c], czhi[c], (int)coff[c], 0);
   const uint32_t T = coff[nc];
-  // 16-byte stores (the table is 256-byte aligned), then the last T+1 mod 4 entries
+  // 16-byte stores (the table is 256-byte aligned), then the last T+1 mod 4 entries; entries the last
+  // sum pass already zeroed (a multiple of 4) are skipped
   const uint32_t n4 = (T + 1) / 4;
+  const uint32_t z4 = zeroed ? min(*zeroed / 4u, n4) : 0u;
   uint4* t4 = reinterpret_cast<uint4*>(table);
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += gridDim.x * blockDim.x)
+  for (uint32_t k = z4 + blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += gridDim.x * blockDim.x)
     t4[k] = make_uint4(0u, 0u, 0u, 0u);
   const uint32_t k = 4 * n4 + blockIdx.x * blockDim.x + threadIdx.x;
   if (k <= T) table[k] = 0u;
+}
+
+// The next build's histogram buffer zeroed while the force phase runs (a side stream; the search is
+// bound by the L1 data pipe and leaves HBM idle): TMA bulk stores from a zeroed shared-memory block
+// (async proxy: no LSU wavefronts), one CTA per SM with a contiguous slice each.  Zeroes the first
+// min(cap4, T + T/8 + 4096) entries (T: the current grid's table size, a multiple of 4) and records
+// the count in *zdone for k_table_zero.
+constexpr int ZT_BYTES = 4096;
+__global__ void __launch_bounds__(32) k_table_zero_tma(uint32_t* __restrict__ table2, const uint32_t* __restrict__ coff,
+                                                       uint32_t nc, uint32_t cap4, uint32_t* __restrict__ zdone) {
+  __shared__ __align__(128) uint4 zbuf[ZT_BYTES / 16];
+  for (int k = threadIdx.x; k < ZT_BYTES / 16; k += blockDim.x) zbuf[k] = make_uint4(0u, 0u, 0u, 0u);
+  const uint32_t T = __ldg(&coff[nc]);
+  const uint32_t zn = min(cap4, (T + T / 8u + 4096u) & ~3u);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *zdone = zn;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  if (threadIdx.x != 0) return;
+  const uint64_t bytes = (uint64_t)zn * 4u, per = ((bytes / gridDim.x) + 15u) & ~15ull;
+  const uint64_t b0 = per * blockIdx.x, b1 = min(bytes, b0 + per);
+  const uint32_t src = (uint32_t)__cvta_generic_to_shared(zbuf);
+  for (uint64_t o = b0; o < b1; o += ZT_BYTES) {
+    const uint32_t len = (uint32_t)(b1 - o < (uint64_t)ZT_BYTES ? b1 - o : (uint64_t)ZT_BYTES);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                     reinterpret_cast<char*>(table2) + o), "r"(src), "r"(len) : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // ------------------------------------------------------------------------------------------ K2
