@@ -43,6 +43,9 @@ def kernel(path):
                 "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                 "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
                 "smsp__thread_inst_executed_per_inst_executed.ratio", "l1tex__t_sector_hit_rate.pct",
+                "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed",
+                "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+                "l1tex__t_output_wavefronts_pipe_lsu_mem_global_op_ld.sum",
                 "lts__t_sector_hit_rate.pct", "launch__registers_per_thread", "launch__grid_size", "launch__block_size"]
         units = dict(zip(r[0], r[1]))
         for k in keys:
