@@ -794,7 +794,7 @@ int sort_into(bdm_ctx* h, uint32_t n, uint32_t n_dead = 0) {
     const bool perm_hist = h->hist[0] && h->skip_valid && !h->slab;
     CU(h, lx(k_place, blocks(n - n_dead, PLACE_T), PLACE_T, 0, s, h->tsrc, h->tid, h->tkey, h->table, h->ag[src],
              n - n_dead, h->ag[dst], h->id[dst], h->agf, perm_hist ? h->hist[src] : nullptr,
-             perm_hist ? h->hist[dst] : nullptr, nullptr));
+             perm_hist ? h->hist[dst] : nullptr, nullptr, nullptr, nullptr));
     DBG(h, "k_place");
   }
   CU(h, cudaGetLastError());

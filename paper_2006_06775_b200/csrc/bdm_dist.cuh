@@ -874,7 +874,8 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
              h->tid, h->tkey, D.dc + DC_TOT));
     DBG(h, "k_scatter(dist)");
     CU(H, lx(k_place, blocks(room, PLACE_T), PLACE_T, 0, st, h->tsrc, h->tid, h->tkey, h->table, h->ag[src0], room,
-             h->ag[1 - src0], h->id[1 - src0], h->agf, nullptr, nullptr, D.dc + DC_SORTED));
+             h->ag[1 - src0], h->id[1 - src0], h->agf, nullptr, nullptr, D.dc + DC_SORTED, h->id[src0],
+             D.dc + DC_ABEGIN));
     DBG(h, "k_place(dist)");
     CU(H, cudaGetLastError());
     h->launches += 7;
@@ -924,7 +925,8 @@ int dist_ingest_build_force(bdm_ctx* H, DistGroup* G, DistSlab& D, bool want_dp)
   double* dp = want_dp ? h->dp : nullptr;
   uint32_t* dpi = want_dp ? h->dp_ids : nullptr;
   CU(H, lx(k_half_sum<false>, gb, FORCE_THREADS, HB_SMEM_BYTES, st, h->ag[src], h->id[src], 0u, room, g, pd,
-           h->ag[dst], h->id[dst], dp, dpi, h->ext, h->err, h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, nullptr,
+           h->ag[dst], nullptr /* (ids: k_place wrote the owned range) */, dp, dpi, h->ext, h->err, h->h_fwd, h->h_fcnt,
+           h->h_bwd, h->h_bcnt, cn, nullptr,
            h->h_slow, D.dc + DC_ABEGIN, nullptr, (int64_t)-1));
   DBG(h, "k_half_sum(dist)");
   CU(H, lx(k_half_slow<false>, (unsigned)h->sm_count * 4, 128, 0, st, h->ag[src], h->id[src], 0u, g, pd, h->ag[dst],

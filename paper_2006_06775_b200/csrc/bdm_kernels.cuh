@@ -792,7 +792,8 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
                         const double4* __restrict__ ag_in, uint32_t n, double4* __restrict__ ag_out,
                         uint32_t* __restrict__ ids_out, float4* __restrict__ agf_out,
                         const unsigned long long* __restrict__ hist_in, unsigned long long* __restrict__ hist_out,
-                        const uint32_t* __restrict__ n_dev = nullptr) {
+                        const uint32_t* __restrict__ n_dev = nullptr, uint32_t* __restrict__ ids_owned = nullptr,
+                        const uint32_t* __restrict__ ab_dev = nullptr) {
   pdl_wait();
   uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (n_dev) n = __ldg(n_dev);
@@ -807,6 +808,12 @@ __global__ void k_place(const uint32_t* __restrict__ tsrc, const uint32_t* __res
   BDM_ASSERT(b <= q && q < e && dst < e);
   st_state(&ag_out[dst], p);
   ids_out[dst] = id;
+  // distributed steps: the owned range [A_BEGIN, A_END) of this order is what the force phase steps;
+  // its ids go straight to the stepped state's id buffer (compacted), so the sum pass need not copy them
+  if (ids_owned) {
+    const uint32_t ab = __ldg(&ab_dev[0]), ae = __ldg(&ab_dev[1]);
+    if (dst >= ab && dst < ae) ids_owned[dst - ab] = id;
+  }
   if (hist_out) hist_out[dst] = hist_in[src];
   // fp32 copy of the position for the force kernel's conservative candidate filter
   agf_out[dst] = make_float4(__double2float_rn(p.x), __double2float_rn(p.y), __double2float_rn(p.z),
