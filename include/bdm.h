@@ -211,16 +211,17 @@ int bdm_get_count(bdm_handle h, int64_t* out2);
 int bdm_get_skip_stats(bdm_handle h, int64_t* out3);
 
 /* Force path of the last step: out2[0] = 1 if it ran the half-shell pair path
- * (k_half_search + k_half_sum: each candidate pair tested once, Newton's third law), 0 if the
- * single-pass k_force (BDM_RECORD, BDM_SKIP_STATIONARY, bdm_set_force_path(BDM_PATH_SINGLE), or the
- * pair rows could not be allocated); out2[1] = agents of that step whose pair rows overflowed and
- * took the exact full-search path (results are identical either way).  -1 entries before the first
- * step. */
+ * (k_half_search + k_half_sum: each candidate pair tested once, Newton's third law), 2 if it ran it
+ * band by band over a ring of pair rows (populations whose rows do not fit beside the state, e.g.
+ * 10^9 agents on one GPU), 0 if the single-pass k_force (BDM_RECORD, BDM_SKIP_STATIONARY,
+ * bdm_set_force_path(BDM_PATH_SINGLE), or no pair rows / a grid whose two-layer span exceeds the
+ * ring); out2[1] = agents of that step whose pair rows overflowed and took the exact full-search path
+ * (results are identical either way).  -1 entries before the first step. */
 int bdm_get_path_stats(bdm_handle h, int64_t* out2);
 
 /* Force-path selection for plain steps of this handle: BDM_PATH_AUTO (default)
- * runs the half-shell passes whenever their pair rows (72 B/agent) can be allocated and falls back
- * to the single-pass k_force otherwise (e.g. 10^9 agents on one GPU); BDM_PATH_SINGLE always runs
+ * runs the half-shell passes (band by band over a ring of pair rows when rows for every agent, 72 B
+ * each, do not fit) and falls back to the single-pass k_force otherwise; BDM_PATH_SINGLE always runs
  * k_force.  Both compute O3-O7 in the canonical order: results are bit-identical.  EINVAL for any
  * other value. */
 #define BDM_PATH_AUTO 0

@@ -42,6 +42,8 @@ const bool g_pbox = !(std::getenv("BDM_PBOX") && std::getenv("BDM_PBOX")[0] == '
 const bool g_fuse = !(std::getenv("BDM_FUSE") && std::getenv("BDM_FUSE")[0] == '0');
 // BDM_TZERO=0: the build zeroes its histogram itself (default: the last sum pass zeroed it, table2)
 const bool g_tzero = !(std::getenv("BDM_TZERO") && std::getenv("BDM_TZERO")[0] == '0');
+// BDM_RING=k: the banded force phase with a ring of 2^k pair rows even when the rows would fit (tests)
+const int g_ring_log = std::getenv("BDM_RING") ? std::atoi(std::getenv("BDM_RING")) : 0;
 // BDM_PDL=0: the step's launch chain without programmatic dependent launch (lx below)
 const bool g_pdl = !(std::getenv("BDM_PDL") && std::getenv("BDM_PDL")[0] == '0');
 
@@ -74,6 +76,15 @@ struct bdm_ctx {
   // entries while the current table was still in use (table_pre: that happened; the build swaps them)
   uint32_t* table2 = nullptr;
   bool table_pre = false;
+  // banded force phase (populations whose pair rows do not fit, or BDM_RING): rows for a ring of two
+  // bands of ring/2 agents (GridDev::rmask = ring - 1); per-band chunk counters; layer starts
+  uint32_t ring = 0;
+  uint32_t* rwork = nullptr;
+  size_t rwork_cap = 0;
+  uint32_t* lstart = nullptr;
+  uint32_t* lstart_host = nullptr;
+  size_t lstart_cap = 0;
+  uint32_t ring_band = 0;  // band size of the current step (0: the ring does not hold this grid's reach)
   unsigned long long* scan_state = nullptr;
   uint32_t* scan_ticket = nullptr;
   size_t scan_tiles_cap = 0;
@@ -399,8 +410,33 @@ bool ensure_half(bdm_ctx* h) {
     if (q) cudaFree(q);
   h->h_fwd = h->h_bwd = h->h_bcnt = h->h_slow = nullptr;
   h->h_fcnt = nullptr;
+  h->ring = 0;
   const size_t N = (size_t)std::max<int64_t>(h->cap, 1);
   const size_t Nsep = BDM_MROW ? 1 : N;  // (merged rows: no separate backward rows / forward counts)
+  // the banded phase (single handle, merged rows): rows for a ring of R agents when all N rows do not
+  // fit beside the state (or BDM_RING asks for it); the overflow list keeps one entry per agent
+  size_t free_b = 0, total_b = 0;
+  (void)cudaMemGetInfo(&free_b, &total_b);
+  const bool want_ring = BDM_MROW && !h->slab && !g_htile &&
+                         (g_ring_log > 0 || N * (HFC * 4 + 8) + (size_t)(4ull << 30) > free_b);
+  if (want_ring) {
+    const size_t R = (size_t)1 << (g_ring_log > 0 ? std::min(g_ring_log, 30) : 25);
+    if (cudaMalloc(&h->h_fwd, R * HFC * sizeof(uint32_t)) == cudaSuccess &&
+        cudaMalloc(&h->h_bwd, sizeof(uint32_t) * HBC) == cudaSuccess &&
+        cudaMalloc(&h->h_bcnt, R * sizeof(uint32_t)) == cudaSuccess && cudaMalloc(&h->h_fcnt, 1) == cudaSuccess &&
+        cudaMalloc(&h->h_slow, N * sizeof(uint32_t)) == cudaSuccess) {
+      h->ring = (uint32_t)R;
+      h->h_cap = h->cap;
+      return true;
+    }
+    (void)cudaGetLastError();
+    for (void* q : {(void*)h->h_fwd, (void*)h->h_bwd, (void*)h->h_bcnt, (void*)h->h_fcnt, (void*)h->h_slow})
+      if (q) cudaFree(q);
+    h->h_fwd = h->h_bwd = h->h_bcnt = h->h_slow = nullptr;
+    h->h_fcnt = nullptr;
+    h->half_off = true;
+    return false;
+  }
   if (cudaMalloc(&h->h_fwd, N * HFC * sizeof(uint32_t)) != cudaSuccess ||
       cudaMalloc(&h->h_bwd, Nsep * HBC * sizeof(uint32_t)) != cudaSuccess ||
       cudaMalloc(&h->h_bcnt, N * sizeof(uint32_t)) != cudaSuccess || cudaMalloc(&h->h_fcnt, Nsep) != cudaSuccess ||
@@ -415,6 +451,36 @@ bool ensure_half(bdm_ctx* h) {
   }
   h->h_cap = h->cap;
   return true;
+}
+
+// Banded phase: the band size for this grid -- half the ring, if that is no smaller than the largest
+// sorted span of two consecutive box-x layers (an agent's forward partners lie before the end of the
+// next layer, so the rows written while a band is searched belong to it or to the next band).
+// One small device-to-host read per step.  0: the ring cannot hold this grid (the step takes k_force).
+int ring_band(bdm_ctx* h, uint32_t n, uint32_t* band) {
+  *band = 0;
+  const GridDev& g = h->grid;
+  const uint32_t nx = (uint32_t)(g.hi[0] - g.lo[0] + 1);
+  if ((size_t)nx + 1 > h->lstart_cap) {
+    if (h->lstart) CU(h, cudaFree(h->lstart));
+    if (h->lstart_host) CU(h, cudaFreeHost(h->lstart_host));
+    h->lstart = nullptr;
+    h->lstart_host = nullptr;
+    h->lstart_cap = (size_t)nx + 1 + 1024;
+    CU(h, cudaMalloc(&h->lstart, h->lstart_cap * sizeof(uint32_t)));
+    CU(h, cudaMallocHost(&h->lstart_host, h->lstart_cap * sizeof(uint32_t)));
+  }
+  k_layer_starts<<<std::max(1u, std::min(148u * 4u, (nx + 256u) / 256u)), 256, 0, h->stream>>>(g, nx, n, h->lstart);
+  CU(h, cudaMemcpyAsync(h->lstart_host, h->lstart, ((size_t)nx + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                        h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  ++h->host_syncs;
+  uint32_t span = 0;
+  for (uint32_t x = 0; x < nx; ++x) span = std::max(span, h->lstart_host[std::min(x + 2, nx)] - h->lstart_host[x]);
+  // the largest band the ring holds (fewer launches and persistent-grid tails), if it covers the span
+  const uint32_t b = h->ring / 2;
+  if (b >= span && b >= 32u) *band = b;
+  return BDM_OK;
 }
 
 // Half-shell force step over the owned sorted range [a_begin, a_end) of ag[src]; pass A searches
@@ -496,11 +562,11 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     const uint64_t w = std::max<uint64_t>(nc2, (uint64_t)n_all / 4 + 1);
     const unsigned gr = (unsigned)std::min<uint64_t>((w + 255) / 256, 148u * 16u);
     CU(h, lx(k_force_reset, gr, 256, 0, s, h->ext, ext_mode, fuse_cols ? h->czlo2 : nullptr, h->czhi2, (uint32_t)nc2,
-             h->h_bcnt, std::max<uint32_t>(n_all, 1)));
+             h->h_bcnt, h->ring ? h->ring : std::max<uint32_t>(n_all, 1)));
     h->launches += 1;
   }
   // banded force phase: bands of >= 2^20 agents each
-  const int nb = force_only ? 1 : (int)std::min<int64_t>(g_bands, std::max<int64_t>(1, ((int64_t)a_end - a_begin) >> 20));
+  const int nb = force_only || h->ring ? 1 : (int)std::min<int64_t>(g_bands, std::max<int64_t>(1, ((int64_t)a_end - a_begin) >> 20));
   if (nb > 1) {
     if (tz) CU(h, cudaStreamWaitEvent(s, h->bev[32], 0));  // (the bands reuse the side stream's events)
     tz = false;
@@ -542,6 +608,50 @@ int half_force(bdm_ctx* h, int src, uint32_t s_begin, uint32_t a_begin, uint32_t
     k_locate_nonfinite<<<1, 32, 0, s>>>(h->ag[src], h->id[src], h->grid, pd, h->err);
     CU(h, cudaGetLastError());
     h->launches += 2 * nb + 2;
+    h->cols_next = fuse_cols;
+    return BDM_OK;
+  }
+  if (h->ring) {  // banded phase over a ring of pair rows (populations whose rows do not fit)
+    const uint32_t B = h->ring_band;
+    if (!B || force_only || frame4 || h->slab || s_begin != a_begin) return fail(h, BDM_ESTATE, "ring phase misuse");
+    const uint32_t nbands = (a_end - a_begin + B - 1) / B;
+    if (2 * (size_t)nbands > h->rwork_cap) {
+      if (h->rwork) CU(h, cudaFree(h->rwork));
+      h->rwork = nullptr;
+      h->rwork_cap = 2 * (size_t)nbands + 64;
+      CU(h, cudaMalloc(&h->rwork, h->rwork_cap * sizeof(uint32_t)));
+    }
+    CU(h, cudaMemsetAsync(h->rwork, 0, 2 * (size_t)nbands * sizeof(uint32_t), s));
+    GridDev gr = h->grid;
+    gr.rmask = 2u * B - 1u;
+    for (uint32_t k = 0; k < nbands; ++k) {
+      const uint32_t lo = a_begin + k * B, hi = std::min<uint32_t>(a_end, lo + B);
+      const unsigned ga = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_a_blocks_per_sm,
+                                                       std::max<uint64_t>(1, (hi - lo + HA_THREADS - 1) / HA_THREADS));
+      CU(h, lx(k_half_search, ga, HA_THREADS, HA_SMEM_BYTES, s, h->ag[src], h->agf, lo, hi, gr, h->h_fwd, h->h_fcnt,
+               h->h_bwd, h->h_bcnt, h->ext, hist_out != nullptr, nullptr, h->rwork + 2 * k));
+      const unsigned gb = (unsigned)std::min<uint64_t>((uint64_t)h->sm_count * h->half_b_blocks_per_sm,
+                                                       std::max<uint64_t>(1, (hi - lo + FORCE_THREADS - 1) / FORCE_THREADS));
+      CU(h, lx(k_half_sum<false, true>, gb, FORCE_THREADS, HB_SMEM_BYTES, s, h->ag[src], h->id[src], lo, hi, gr, pd,
+               ag_out, id_out, dp, dp_ids, h->ext, h->err, h->h_fwd, h->h_fcnt, h->h_bwd, h->h_bcnt, cn, hist_out,
+               h->h_slow, nullptr, h->rwork + 2 * k + 1, (int64_t)a_begin));
+      if (k + 2 < nbands) {  // band k's ring slot is band k+2's: its counts zeroed before search k+1 writes there
+        const unsigned gz = (unsigned)std::min<uint64_t>((B / 4 + 255) / 256, 148u * 16u);
+        CU(h, lx(k_force_reset, gz, 256, 0, s, h->ext, -1, (int32_t*)nullptr, (int32_t*)nullptr, 0u,
+                 h->h_bcnt + (size_t)(k & 1u) * B, B));
+      }
+    }
+    h->launches += 3 * nbands;
+    const unsigned gs = (unsigned)h->sm_count * 4;
+    CU(h, lx(k_half_slow<false>, gs, 128, 0, s, h->ag[src], h->id[src], a_begin, h->grid, pd, ag_out, id_out, dp,
+             dp_ids, h->ext, h->err, cn, hist_out, h->h_slow, nullptr));
+    CU(h, lx(k_locate_nonfinite, 1, 32, 0, s, h->ag[src], h->id[src], h->grid, pd, h->err));
+    if (tz) {
+      CU(h, cudaStreamWaitEvent(s, h->bev[32], 0));
+      h->table_pre = true;
+    }
+    CU(h, cudaGetLastError());
+    h->launches += 2;
     h->cols_next = fuse_cols;
     return BDM_OK;
   }
@@ -858,6 +968,12 @@ int force_step(bdm_ctx* h, bool want_dp) {
   // the single-pass k_force serves the stationary-region skip (it skips the whole search of quiet
   // agents); otherwise the half-shell path, which also keeps the skip statistics (hist) current
   h->last_half = !(h->prm.flags & BDM_RECORD) && !h->skip_active && n > 0 && ensure_half(h);
+  h->ring_band = 0;
+  if (h->last_half && h->ring) {  // banded phase: the bands must hold two layers' span
+    int rc = ring_band(h, n, &h->ring_band);
+    if (rc) return rc;
+    if (!h->ring_band) h->last_half = false;
+  }
   h->cols_next = false;
   if (h->last_half) {
     // fuse the next build's column pass when nothing moves agents between this step and that build
@@ -2308,7 +2424,7 @@ int bdm_get_path_stats(bdm_handle h, int64_t* out2) {
   CU(h, cudaMemcpyAsync(h->ext_host, h->ext, sizeof(Extents), cudaMemcpyDeviceToHost, h->stream));
   int rc = check_async(h);
   if (rc) return rc;
-  out2[0] = h->last_half ? 1 : 0;
+  out2[0] = h->last_half ? (h->ring_band ? 2 : 1) : 0;
   out2[1] = h->last_half ? (int64_t)h->ext_host->slow : 0;
   return BDM_OK;
 }

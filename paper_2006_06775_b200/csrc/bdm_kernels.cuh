@@ -61,6 +61,8 @@ struct GridDev {
   const int4* col;       // per column (czlo, czhi, coff, 0): one 16-byte load per column lookup
   uint32_t pad;          // index of the padding agent agf[pad] = (+inf, +inf, +inf, 0) (capacity; pass A's
                          // slots past the end of a lane's candidates read it and fail the filter)
+  uint32_t rmask = 0xffffffffu;  // pair rows / counts of agent j at index j & rmask (a ring of two bands
+                                 // in the banded force phase of very large populations; else all ones)
 };
 
 struct ParamsDev {
@@ -509,6 +511,14 @@ __global__ void __launch_bounds__(32) k_table_zero_tma(uint32_t* __restrict__ ta
   }
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Sorted-order start of every box-x layer of the grid (out[x] for x in [0, nx), out[nx] = n): the
+// banded force phase of very large populations sizes its bands from the largest two-layer span.
+__global__ void k_layer_starts(GridDev g, uint32_t nx, uint32_t n, uint32_t* __restrict__ out) {
+  pdl_wait();
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x <= nx; x += gridDim.x * blockDim.x)
+    out[x] = x < nx ? __ldg(&g.table[__ldg(&g.coff[x * (uint32_t)g.ny])]) : n;
 }
 
 // ------------------------------------------------------------------------------------------ K2
@@ -1504,8 +1514,8 @@ constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 // 32-byte sector (instead of one sector in each of two rows): the sum pass reads half the row bytes.
 // Otherwise: a forward row written by the owner and a backward row (bwd, bcnt) filled by partners.
 __device__ __forceinline__ void bw_put(uint32_t* __restrict__ fwd, uint32_t* __restrict__ bwd,
-                                       uint32_t j, uint32_t slot, uint32_t i) {
-  if (slot < (uint32_t)HBC) (BDM_MROW ? fwd : bwd)[(size_t)j * HBC + slot] = i;
+                                       uint32_t j, uint32_t slot, uint32_t i, uint32_t rm) {
+  if (slot < (uint32_t)HBC) (BDM_MROW ? fwd : bwd)[(size_t)(j & rm) * HBC + slot] = i;
 }
 
 // End of a chunk (lane of agent i, cnt survivors in its list, extra beyond it): the forward entries
@@ -1514,16 +1524,16 @@ __device__ __forceinline__ void bw_put(uint32_t* __restrict__ fwd, uint32_t* __r
 // read-modify-write of partially written sectors in DRAM).
 __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint32_t extra, uint32_t i,
                                           uint32_t* __restrict__ fwd, uint32_t* __restrict__ bwd,
-                                          uint32_t* __restrict__ bcnt) {
+                                          uint32_t* __restrict__ bcnt, uint32_t rm) {
 #if BDM_MROW
   // own entries: a base slot for all of them (the overflow beyond the list counts, so a row that
   // cannot hold everything is recognised by its count); its round trip overlaps the partners' atomics
   // (survivors beyond the list were not kept: push the count past the row so the sum pass takes the
   // exact full search for i)
   const uint32_t nf = (uint32_t)cnt + extra + (extra ? (uint32_t)HFC : 0u);
-  const uint32_t base = nf ? atomicAdd(&bcnt[i], nf) : 0u;
+  const uint32_t base = nf ? atomicAdd(&bcnt[i & rm], nf) : 0u;
 #elif BDM_V256
-  uint32_t* frow = fwd + (size_t)i * HFC;  // 64-byte rows: one 256-bit store per used sector
+  uint32_t* frow = fwd + (size_t)(i & rm) * HFC;  // 64-byte rows: one 256-bit store per used sector
 #pragma unroll
   for (int v = 0; v < HFC / 8; ++v)
     if (cnt > 8 * v) {
@@ -1533,7 +1543,7 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
                    : "memory");
     }
 #else
-  uint4* frow = reinterpret_cast<uint4*>(fwd + (size_t)i * HFC);
+  uint4* frow = reinterpret_cast<uint4*>(fwd + (size_t)(i & rm) * HFC);
 #pragma unroll
   for (int v = 0; v < HFC / 4; ++v)
     if (cnt > 8 * (v / 2))
@@ -1545,17 +1555,17 @@ __device__ __forceinline__ void half_emit(HalfASmem& sm, int lane, int cnt, uint
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       j[u] = x0 + u < cnt ? sm.list[x0 + u][lane] : 0u;
-      if (x0 + u < cnt) slot[u] = atomicAdd(&bcnt[j[u]], 1u);  // four atomics in flight
+      if (x0 + u < cnt) slot[u] = atomicAdd(&bcnt[j[u] & rm], 1u);  // four atomics in flight
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (x0 + u < cnt) {
         BDM_ASSERT(j[u] > i);  // forward partners only (the half-shell order)
-        bw_put(fwd, bwd, j[u], slot[u], i);
+        bw_put(fwd, bwd, j[u], slot[u], i, rm);
       }
   }
 #if BDM_MROW
-  uint32_t* row = fwd + (size_t)i * HFC;
+  uint32_t* row = fwd + (size_t)(i & rm) * HFC;
   for (int k = 0; k < cnt; ++k)
     if (base + (uint32_t)k < (uint32_t)HFC) row[base + k] = sm.list[k][lane];
 #endif
@@ -1572,29 +1582,29 @@ struct HalfPending {
 };
 __device__ __forceinline__ void half_emit_issue(HalfASmem& sm, int lane, int cnt, uint32_t extra, uint32_t i,
                                                 uint32_t* __restrict__ fwd, uint32_t* __restrict__ bcnt,
-                                                HalfPending& pd) {
+                                                HalfPending& pd, uint32_t rm) {
   const uint32_t nf = (uint32_t)cnt + extra + (extra ? (uint32_t)HFC : 0u);
-  pd.base = nf ? atomicAdd(&bcnt[i], nf) : 0u;
+  pd.base = nf ? atomicAdd(&bcnt[i & rm], nf) : 0u;
   pd.i = i;
   pd.cnt = (uint32_t)cnt;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
-    if (u < cnt) pd.slot[u] = atomicAdd(&bcnt[sm.list[u][lane]], 1u);
+    if (u < cnt) pd.slot[u] = atomicAdd(&bcnt[sm.list[u][lane] & rm], 1u);
   for (int x = 4; x < cnt; ++x) {  // (rare)
     const uint32_t j = sm.list[x][lane];
-    bw_put(fwd, fwd, j, atomicAdd(&bcnt[j], 1u), i);
+    bw_put(fwd, fwd, j, atomicAdd(&bcnt[j & rm], 1u), i, rm);
   }
 }
 __device__ __forceinline__ void half_emit_finish(HalfASmem& sm, int lane, uint32_t* __restrict__ fwd,
-                                                 HalfPending& pd) {
+                                                 HalfPending& pd, uint32_t rm) {
   if (pd.cnt == 0u) return;
 #pragma unroll
   for (int u = 0; u < 4; ++u)
     if ((uint32_t)u < pd.cnt) {
       BDM_ASSERT(sm.list[u][lane] > pd.i);
-      bw_put(fwd, fwd, sm.list[u][lane], pd.slot[u], pd.i);
+      bw_put(fwd, fwd, sm.list[u][lane], pd.slot[u], pd.i, rm);
     }
-  uint32_t* row = fwd + (size_t)pd.i * HFC;
+  uint32_t* row = fwd + (size_t)(pd.i & rm) * HFC;
   for (uint32_t k = 0; k < pd.cnt; ++k)
     if (pd.base + k < (uint32_t)HFC) row[pd.base + k] = sm.list[k][lane];
   pd.cnt = 0u;
@@ -1609,7 +1619,7 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
                                           uint32_t wmax, uint32_t w, uint32_t i, unsigned long long mxy,
                                           unsigned long long mzr, int& cnt, uint32_t& extra,
                                           uint32_t* __restrict__ fwd_rows, uint32_t* __restrict__ bwd,
-                                          uint32_t* __restrict__ bcnt, uint32_t pad) {
+                                          uint32_t* __restrict__ bcnt, uint32_t pad, uint32_t rm) {
   const int lane = threadIdx.x & 31;
   uint2 cur = sm.rr[0][lane];
   uint32_t q = cur.x, e = cur.y;
@@ -1683,7 +1693,7 @@ __device__ __forceinline__ void half_scan(HalfASmem& sm, const float4* __restric
             j = j - sm.off[c] + sm.ub[c];
           }
 #endif
-          bw_put(fwd_rows, bwd, j, atomicAdd(&bcnt[j], 1u), i);
+          bw_put(fwd_rows, bwd, j, atomicAdd(&bcnt[j & rm], 1u), i, rm);
           ++extra;
         }
       }
@@ -1698,7 +1708,7 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
                                               unsigned long long mxy, unsigned long long mzr, int& cnt,
                                               uint32_t& extra, uint32_t* __restrict__ fwd_rows,
                                               uint32_t* __restrict__ bwd, uint32_t* __restrict__ bcnt, uint32_t pad,
-                                              uint32_t laddr) {
+                                              uint32_t laddr, uint32_t rm) {
   const int lane = threadIdx.x & 31;
   for (uint32_t s0 = 0; s0 < wmax; s0 += NSLOT) {
     uint32_t qs[NSLOT];
@@ -1733,7 +1743,7 @@ __device__ __forceinline__ void half_scan_map(HalfASmem& sm, const float4* __res
           asm volatile("st.shared.u32 [%0], %1;" ::"r"(laddr + 128u * (uint32_t)cnt), "r"(qs[t]) : "memory");
           ++cnt;
         } else {  // rare: the partner still gets its backward entry
-          bw_put(fwd_rows, bwd, qs[t], atomicAdd(&bcnt[qs[t]], 1u), i);
+          bw_put(fwd_rows, bwd, qs[t], atomicAdd(&bcnt[qs[t] & rm], 1u), i, rm);
           ++extra;
         }
       }
@@ -2060,7 +2070,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     if (staged) {
       mbar_wait(&sm.bar, phase);
       phase ^= 1u;
-      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
+      half_scan<true>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad, g.rmask);
       // buffer index -> global sorted index (each union run is contiguous in both)
       for (int x = 0; x < cnt; ++x) {
         const uint32_t v = sm.list[x][lane];
@@ -2075,23 +2085,23 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
 #if BDM_HMAP
     {
 #if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
-      half_emit_finish(sm, lane, fwd, pd);  // the last chunk's stores (before the list is overwritten)
+      half_emit_finish(sm, lane, fwd, pd, g.rmask);  // the last chunk's stores (before the list is overwritten)
 #endif
-      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad, la_base);
+      half_scan_map(sm, agf, S, A, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad, la_base, g.rmask);
     }
 #else
     {
 #if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
-      half_emit_finish(sm, lane, fwd, pd);  // the last chunk's stores (before the list is overwritten)
+      half_emit_finish(sm, lane, fwd, pd, g.rmask);  // the last chunk's stores (before the list is overwritten)
 #endif
-      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
+      half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad, g.rmask);
     }
 #endif
     if (valid) {
 #if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
-      half_emit_issue(sm, lane, cnt, extra, i, fwd, bcnt, pd);
+      half_emit_issue(sm, lane, cnt, extra, i, fwd, bcnt, pd, g.rmask);
 #else
-      half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
+      half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt, g.rmask);
 #endif
       if (!BDM_MROW) {
         const uint32_t nf = (uint32_t)cnt + extra;
@@ -2101,7 +2111,7 @@ __global__ void __launch_bounds__(HA_THREADS, HA_MIN_BLOCKS)
     __syncwarp();
   }
 #if BDM_HDEF && BDM_MROW && !BDM_HSTAGE
-  half_emit_finish(sm, lane, fwd, pd);
+  half_emit_finish(sm, lane, fwd, pd, g.rmask);
 #endif
 }
 
@@ -2331,7 +2341,7 @@ __device__ __forceinline__ void tile_scan(HalfASmem& sm, const float4* __restric
                                           uint32_t rr_base, uint32_t wmax, uint32_t w, uint32_t i,
                                           unsigned long long mxy, unsigned long long mzr, int& cnt, uint32_t& extra,
                                           uint32_t* __restrict__ fwd_rows, uint32_t* __restrict__ bwd,
-                                          uint32_t* __restrict__ bcnt) {
+                                          uint32_t* __restrict__ bcnt, uint32_t rm) {
   const int lane = threadIdx.x & 31;
   uint2 cur = sm.rr[0][lane];
   uint32_t q = cur.x, e = cur.y;
@@ -2375,7 +2385,7 @@ __device__ __forceinline__ void tile_scan(HalfASmem& sm, const float4* __restric
           uint32_t r = 0;
           while (r + 1 < (uint32_t)(5 * m.ncol) && qs[t] >= m.off[r + 1]) ++r;
           const uint32_t j = qs[t] - m.off[r] + m.ub[r];
-          bw_put(fwd_rows, bwd, j, atomicAdd(&bcnt[j], 1u), i);
+          bw_put(fwd_rows, bwd, j, atomicAdd(&bcnt[j & rm], 1u), i, rm);
           ++extra;
         }
       }
@@ -2516,7 +2526,7 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
       int cnt = 0;
       uint32_t extra = 0;
       if (staged) {
-        tile_scan(sm, ts.buf[slot], m, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt);
+        tile_scan(sm, ts.buf[slot], m, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.rmask);
         for (int x = 0; x < cnt; ++x) {  // buffer index -> global sorted index
           const uint32_t vv = sm.list[x][lane];
           uint32_t r = 0;
@@ -2524,10 +2534,10 @@ __global__ void __launch_bounds__(TILE_THREADS, TILE_MIN_BLOCKS)
           sm.list[x][lane] = vv - m.off[r] + m.ub[r];
         }
       } else {
-        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad);
+        half_scan<false>(sm, agf, rr_base, wmax, w, i, mxy, mzr, cnt, extra, fwd, bwd, bcnt, g.pad, g.rmask);
       }
       if (valid) {
-        half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt);
+        half_emit(sm, lane, cnt, extra, i, fwd, bwd, bcnt, g.rmask);
         if (!BDM_MROW) {
           const uint32_t nf = (uint32_t)cnt + extra;
           fcnt[i] = (uint8_t)(nf > 255u ? 255u : nf);
@@ -2611,7 +2621,7 @@ __global__ void k_locate_nonfinite(const double4* __restrict__ ag, const uint32_
 
 // FONLY (neurite steps): the sphere-sphere sums F go to dp_out (3 per agent, the force-only output
 // fss of k_force), the displacement rule and everything after it are left to k_sc_rows.
-template <bool FONLY>
+template <bool FONLY, bool RING = false>
 __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     k_half_sum(const double4* __restrict__ ag, const uint32_t* __restrict__ ids, uint32_t a_begin, uint32_t a_end,
                GridDev g, ParamsDev p, double4* __restrict__ ag_out, uint32_t* __restrict__ id_out,
@@ -2621,6 +2631,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
                uint32_t* __restrict__ slow_list, const uint32_t* __restrict__ ab_dev = nullptr,
                uint32_t* __restrict__ work = nullptr, int64_t o_base = -1) {
   pdl_wait();
+  const uint32_t rmk = RING ? g.rmask : 0xffffffffu;  // (the ring of rows of the banded phase: RING only)
   if (ab_dev) {  // distributed steps: the owned range [a_begin, a_end) read on the device
     a_begin = __ldg(&ab_dev[0]);
     a_end = __ldg(&ab_dev[1]);
@@ -2647,10 +2658,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
   uint4 r4_n = make_uint4(0u, 0u, 0u, 0u);
   {
     const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
-    nb_n = i1 < a_end ? bcnt[i1] : 0u;
-    if (nb_n) r4_n = __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)i1 * HBC));
+    nb_n = i1 < a_end ? bcnt[i1 & rmk] : 0u;
+    if (nb_n) r4_n = __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)(i1 & rmk) * HBC));
     const uint64_t i2 = (uint64_t)a_begin + 32ull * chunk_n + lane;
-    nb_nn = i2 < a_end ? bcnt[i2] : 0u;
+    nb_nn = i2 < a_end ? bcnt[i2 & rmk] : 0u;
   }
 #elif BDM_HBCNT
   // the next chunk's pair counts are loaded one chunk ahead (two registers): a chunk's dependent
@@ -2661,7 +2672,7 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
     if (i1 < a_end) {
       nf_n = BDM_MROW ? 0u : fcnt[i1];  // (merged rows: bcnt counts every entry of the one row)
-      nb_n = bcnt[i1];
+      nb_n = bcnt[i1 & rmk];
     }
   }
 #endif
@@ -2675,8 +2686,8 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     const bool valid = i < a_end;
     // the agent and both counts, then the first 4 entries of each non-empty row (one vector load;
     // entries past a count are stale and ignored)
-    const uint4* brow = reinterpret_cast<const uint4*>((BDM_MROW ? fwd : bwd) + (size_t)i * HBC);
-    const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)i * HFC);
+    const uint4* brow = reinterpret_cast<const uint4*>((BDM_MROW ? fwd : bwd) + (size_t)(i & rmk) * HBC);
+    const uint4* frow = reinterpret_cast<const uint4*>(fwd + (size_t)(i & rmk) * HFC);
     const double4 me = valid ? ld_state(&ag[i]) : make_double4(0.0, 0.0, 0.0, 0.0);
 #if BDM_HRPF
     const uint32_t nf = 0u, nb = nb_n;
@@ -2687,9 +2698,9 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       chunk_n = tk.take(work, lane);
       const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
       nb_n = nb_nn;
-      r4_n = nb_n ? __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)i1 * HBC)) : make_uint4(0u, 0u, 0u, 0u);
+      r4_n = nb_n ? __ldg(reinterpret_cast<const uint4*>(fwd + (size_t)(i1 & rmk) * HBC)) : make_uint4(0u, 0u, 0u, 0u);
       const uint64_t i2 = (uint64_t)a_begin + 32ull * chunk_n + lane;
-      nb_nn = i2 < a_end ? bcnt[i2] : 0u;
+      nb_nn = i2 < a_end ? bcnt[i2 & rmk] : 0u;
     }
 #elif BDM_HBCNT
     const uint32_t nf = nf_n, nb = nb_n;
@@ -2697,11 +2708,11 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
     {
       const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
       nf_n = i1 < a_end && !BDM_MROW ? fcnt[i1] : 0u;
-      nb_n = i1 < a_end ? bcnt[i1] : 0u;
+      nb_n = i1 < a_end ? bcnt[i1 & rmk] : 0u;
     }
 #else
     const uint32_t nf = valid && !BDM_MROW ? fcnt[i] : 0u;
-    const uint32_t nb = valid ? bcnt[i] : 0u;
+    const uint32_t nb = valid ? bcnt[i & rmk] : 0u;
 #endif
     // (rows are read only where the count says so: a speculative read of every row costs more DRAM
     // traffic than the round trip it saves)

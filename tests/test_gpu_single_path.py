@@ -1,6 +1,7 @@
-"""The single-pass force kernel k_force as a product path: it runs whenever the
-half-shell pair rows do not fit (the 10^9-agent single-GPU run) and when selected per handle with
-bdm_set_force_path(BDM_PATH_SINGLE).  Checked against the CPU oracle element by element, like the
+"""The single-pass force kernel k_force as a product path: it runs when selected per
+handle with bdm_set_force_path(BDM_PATH_SINGLE), in RECORD / skip steps, and when neither the pair
+rows nor a ring of them fit (the 10^9-agent single-GPU run now takes the banded ring phase, also
+checked here at full size).  Checked against the CPU oracle element by element, like the
 default path (BASELINE.json north_star parity contract), plus the ENONFINITE
 diagnosis (a non-finite force aborts with the offending pair)."""
 import numpy as np
@@ -120,12 +121,9 @@ def test_nonfinite_force_names_the_pair(bdm):
         assert "(3, 7)" in str(e.value), str(e.value)
 
 
-@pytest.mark.slow
-def test_cfg5_full_size_window_single_pass(bdm):
-    """configs[4] at full size: 10^9 agents generated on the device (K0) on ONE GPU, where the
-    half-shell pair rows do not fit and the step takes k_force automatically (the launch
-    configuration DESIGN.md §6.5 measures).  Every agent of a window is checked against the oracle
-    run on the window plus a margin of 2.2 box edges, with the global box edge."""
+def cfg5_window_step(bdm, path):
+    """configs[4] at full size: 10^9 agents generated on the device (K0) on ONE GPU, one step on the
+    given force path; returns the path taken and (window agents' displacements, oracle's)."""
     import torch
 
     n = bdm_inputs.CFG_N[5]
@@ -152,8 +150,9 @@ def test_cfg5_full_size_window_single_pass(bdm):
     h = bdm.bdm_init(pos, diam, bdm.bdm_params_default())
     del pos, diam, p, sel
     torch.cuda.empty_cache()
+    bdm.bdm_set_force_path(h, path)
     bdm.bdm_mech_step(h, 1)
-    assert bdm.bdm_get_path_stats(h)["half"] == 0  # the rows did not fit: k_force
+    taken = bdm.bdm_get_path_stats(h)["half"]
     dp = torch.empty((n, 3), dtype=torch.float64, device="cuda")
     bdm.bdm_get_displacements(h, dp)
     dps = dp[idx].cpu().numpy()
@@ -163,4 +162,24 @@ def test_cfg5_full_size_window_single_pass(bdm):
     inner = np.all(np.abs(ps - c) < w, axis=1)
     assert inner.sum() > 100
     o = oracle.step(ps, ds, oracle.params(box_edge_min=L), sample=np.flatnonzero(inner), record=False)
-    assert np.array_equal(dps[inner], o["dp"])
+    return taken, dps[inner], o["dp"]
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_window_single_pass(bdm):
+    """configs[4] at full size on one GPU with the single-pass k_force (BDM_PATH_SINGLE): every agent of
+    a window is checked against the oracle run on the window plus a margin of 2.2 box edges, with the
+    global box edge."""
+    taken, dp, odp = cfg5_window_step(bdm, bdm.BDM_PATH_SINGLE)
+    assert taken == 0
+    assert np.array_equal(dp, odp)
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_window_ring(bdm):
+    """configs[4] at full size on one GPU with the default path: the pair rows of 10^9 agents do not fit
+    beside the state, so the half-shell phase runs band by band over a ring of rows (path 2, the launch
+    configuration DESIGN.md §6.5 measures); the window check as above."""
+    taken, dp, odp = cfg5_window_step(bdm, bdm.BDM_PATH_AUTO)
+    assert taken == 2
+    assert np.array_equal(dp, odp)
