@@ -1175,7 +1175,7 @@ int neurite_step(bdm_ctx* h, bool want_dp) {
   RecordDev rec{};
   ParamsDev pd = params_dev(h->prm);
   if (n > 0) {  // sphere-sphere sums (half-shell passes when the pair rows fit, else k_force)
-    if (!(h->prm.flags & BDM_RECORD) && ensure_half(h)) {
+    if (!(h->prm.flags & BDM_RECORD) && ensure_half(h) && !h->ring) {  // (no force-only ring phase: k_force)
       rc = half_force(h, src, 0u, 0u, n, n, pd, nullptr, nullptr, nullptr, nullptr, false, nullptr, nullptr, h->fss);
       if (rc) return rc;
     } else {
