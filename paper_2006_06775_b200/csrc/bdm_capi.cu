@@ -1342,10 +1342,11 @@ void bdm_destroy(bdm_handle h) {
   }
   void* ptrs[] = {h->ag[0], h->ag[1], h->agf, h->id[0], h->id[1], h->key, h->slot, h->tsrc, h->tid, h->tkey, h->table, h->table2,
                   h->scan_state, h->scan_ticket, h->dp, h->stage, h->dp_ids, h->cnt, h->czlo, h->czhi, h->coff, h->hist[0], h->hist[1], h->hot, h->gflag, h->field[0][0], h->field[0][1], h->field[1][0], h->field[1][1], h->fcnt, h->type_by_id, h->eq[0], h->eq[1], h->ea, h->et, h->edq, h->cpos, h->cdiam, h->fss, h->scnt, h->srow, h->geo, h->pbox, h->colrec, h->ext, h->err, h->maxd_bits, h->r_cand, h->r_nb, h->r_ct,
-                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->h_slow, h->czlo2, h->czhi2};
+                  h->r_branch, h->r_nbh, h->r_cth, h->h_fwd, h->h_bwd, h->h_bcnt, h->h_fcnt, h->h_slow, h->czlo2, h->czhi2, h->rwork, h->lstart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (h->ext_host) cudaFreeHost(h->ext_host);
+  if (h->lstart_host) cudaFreeHost(h->lstart_host);
   if (h->err_host) cudaFreeHost(h->err_host);
   if (h->cnt_host) cudaFreeHost(h->cnt_host);
   cudaSetDevice(prev);
