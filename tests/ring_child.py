@@ -1,5 +1,6 @@
-"""Child process of tests/test_gpu_ring.py: steps a population through libbdm with the banded force
-phase forced by BDM_RING (read when the library loads) and checks it against the oracle."""
+"""Child process of tests/test_gpu_ring.py and tests/test_gpu_switches.py: steps a population through
+libbdm under the environment switches its parent set (read when the library loads, e.g. BDM_RING) and
+checks the trajectory against the oracle's."""
 import json
 import sys
 
