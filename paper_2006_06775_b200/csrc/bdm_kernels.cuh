@@ -1502,6 +1502,9 @@ constexpr size_t HA_SMEM_BYTES = sizeof(HalfASmem) * (HA_THREADS / 32);
 #ifndef BDM_HDIRECT
 #define BDM_HDIRECT 0  // pass B: each lane evaluates its own contacts (instead of the balanced contact phase)
 #endif
+#ifndef BDM_HNPF
+#define BDM_HNPF 2  // pass B: prefetch the next chunk's row (1: measured slower) and / or state (2) into L1
+#endif
 #ifndef BDM_HNET
 #define BDM_HNET 1  // pass B: rows of <= 4 entries sorted by a register sorting network (else insertion sort)
 #endif
@@ -2709,6 +2712,12 @@ __global__ void __launch_bounds__(FORCE_THREADS, HB_MIN_BLOCKS)
       const uint64_t i1 = (uint64_t)a_begin + 32ull * chunk + lane;
       nf_n = i1 < a_end && !BDM_MROW ? fcnt[i1] : 0u;
       nb_n = i1 < a_end ? bcnt[i1 & rmk] : 0u;
+#if BDM_HNPF
+      if (i1 < a_end) {  // the next chunk's row (and state) toward L1 while this chunk runs
+        if (BDM_HNPF & 1) asm volatile("prefetch.global.L1 [%0];" ::"l"(fwd + (size_t)(i1 & rmk) * HBC));
+        if (BDM_HNPF & 2) asm volatile("prefetch.global.L1 [%0];" ::"l"(ag + i1));
+      }
+#endif
     }
 #else
     const uint32_t nf = valid && !BDM_MROW ? fcnt[i] : 0u;

@@ -8,5 +8,5 @@ tail -2 gpurun_out/pytest_ab.log
 for rep in $(seq ${REPS:-2}); do
 for v in ${VARIANTS}; do
   BDM_LIBRARY=build/variants/libbdm_$v.so timeout 300 python bench.py --no-cpu-baseline --steps 20 ${BENCH_ARGS} > gpurun_out/ab_$v.log 2>&1
-  echo "$v rc=$?"; python -c "import json;d=json.loads(open('gpurun_out/ab_$v.log').read().strip().splitlines()[-1]);print(d['ms_per_step'],d['roofline']['passes_ms'],d['roofline_rebuild']['ms_per_step'])" 2>&1 | tail -1
+  rc=$?; python -c "import json;d=json.loads(open('gpurun_out/ab_$v.log').read().strip().splitlines()[-1]);print('$v', $rc, d['ms_per_step'],d['roofline']['passes_ms'],d['roofline_rebuild']['ms_per_step'])" 2>&1 | tail -1
 done; done
