@@ -1411,7 +1411,10 @@ __global__ void __launch_bounds__(FORCE_THREADS, FORCE_MIN_BLOCKS)
 #endif
 constexpr int HFC = BDM_HROW;  // forward row capacity (entries per agent; merged rows: all its entries)
 constexpr int HBC = BDM_HROW;  // backward row capacity
-constexpr int HLA = 16;  // pass A survivor buffer per lane (shared memory)
+#ifndef BDM_HLA
+#define BDM_HLA 16
+#endif
+constexpr int HLA = BDM_HLA;  // pass A survivor buffer per lane (shared memory)
 #ifndef BDM_HBCNT
 #define BDM_HBCNT 1  // pass B loads the next chunk's pair counts one chunk ahead
 #endif
