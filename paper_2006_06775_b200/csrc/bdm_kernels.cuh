@@ -1,19 +1,29 @@
-// bdm_kernels.cuh -- sm_100a kernels of the mechanical-interaction step (DESIGN.md §4).
+// bdm_kernels.cuh -- sm_100a kernels of the mechanical-interaction step (DESIGN.md §6).
 //
 // Compiled with -fmad=false: every fp64 +,-,* on the method's path is a separately rounded IEEE
 // operation, so per-pair arithmetic is bit-identical to the reading in DESIGN.md §3 (O3-O6);
 // sqrt() and '/' on doubles are correctly rounded.  No tensor cores: nothing here is a dense
-// contraction (north_star).
+// contraction (north_star).  Kernels of the step chain start with pdl_wait() (programmatic
+// dependent launch).
 //
 //   K0 k_gen_uniform     counter-hash synthetic agents (bench / cfg4-5 utility)
 //   K1 k_pack            n x 3 positions + diameters -> double4 agents, validation, max D
 //      k_extents         min/max integer box coordinate per axis (first build only; later fused in K6)
-//   K2 k_key_hist        box key (x slowest) + per-box histogram with warp-aggregated atomics
+//   build:
+//      k_col_len / k_table_zero   ragged table layout from the column z-ranges (+ scan tile states)
+//   K2 k_key_hist(_packed)       box key (x slowest) + per-box histogram with warp-aggregated atomics
 //   K3 k_scan            single-pass decoupled look-back exclusive scan -> box start table
 //   K4 k_scatter         counting-sort scatter into box segments
 //      k_place           ascending-id order inside each box + payload gather (deterministic sort)
-//   K6 k_force           27-box search -> contact force -> sum -> adherence/clamp -> p' = p + dp,
-//                        fused with the next step's box extents
+//      k_table_zero_tma  the next build's histogram zeroed by TMA bulk stores (side stream)
+//   force phase (the default step):
+//      k_force_reset     extents / counters / next-frame columns / pair counters, one launch
+//      k_half_search     pass A: forward half of the 27 boxes, fp32 prefilter -> pair rows
+//      k_half_sum        pass B: canonical-order contact sums -> adherence/clamp -> p' = p + dp,
+//                        fused with the next build's extents, column ranges and packed boxes
+//      k_half_slow       agents whose rows overflowed: full canonical search, warp per agent
+//      k_layer_starts    band sizes of the ring phase (populations whose rows do not fit)
+//   K6 k_force           single pass: 27-box search -> force -> ... (RECORD, skip, neurites)
 //   K7 k_unpermute_*     sorted order -> id order for the getters
 //   K8 k_pairs_*         neighbour / contact pair export (tests)
 #pragma once
