@@ -118,16 +118,27 @@ def make_inputs(cfg: int, n: int | None):
 
 
 # ------------------------------------------------------------------------------------ oracle arm
+def host_cores() -> int:
+    """The host cores this process may run on (torchrun sets OMP_NUM_THREADS=1 for its workers, so the
+    oracle's "all cores" runs pass this count explicitly instead of relying on the OpenMP default)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except (AttributeError, OSError):
+        return os.cpu_count() or 1
+
+
 def oracle_sample_run(pos, diam, stride: int, nthreads: int = 0):
     """The CPU oracle as it stands on a bounded sample: the whole population is the environment
-    (the oracle rebuilds its grid over all N agents) and every stride-th agent id is updated."""
+    (the oracle rebuilds its grid over all N agents) and every stride-th agent id is updated.
+    nthreads 0: all host cores."""
     import oracle
 
+    threads = nthreads or host_cores()
     sample = np.arange(0, len(diam), stride, dtype=np.int64)
     t0 = time.perf_counter()
-    oracle.step(pos, diam, sample=sample, record=False, nthreads=nthreads)
+    oracle.step(pos, diam, sample=sample, record=False, nthreads=threads)
     dt = time.perf_counter() - t0
-    return len(sample), dt, (nthreads or oracle.threads())
+    return len(sample), dt, threads
 
 
 def host_info():
@@ -160,10 +171,10 @@ def cpu_baseline(pos, diam, what, stride_1t):
     figure includes the whole index build)."""
     import oracle
 
+    threads = host_cores()
     t0 = time.perf_counter()
-    oracle.step(pos, diam, record=False)
+    oracle.step(pos, diam, record=False, nthreads=threads)
     t_all = time.perf_counter() - t0
-    threads = oracle.threads()
     m, t_1, _ = oracle_sample_run(pos, diam, stride_1t, nthreads=1)
     n = len(diam)
     return {"value": n / t_all, "unit": UNIT, "cores": threads, "kind": "oracle",
