@@ -386,6 +386,8 @@ def run_dist(args):
     if not dist.is_initialized():
         if world > 1:
             dist.init_process_group("nccl", device_id=dev)
+        elif "MASTER_ADDR" in os.environ and "WORLD_SIZE" in os.environ:  # (1 rank under torchrun: its store)
+            dist.init_process_group("gloo")
         else:  # (--slabs at N = 1: a 1-rank group for the barriers)
             dist.init_process_group("gloo", rank=0, world_size=1, init_method="tcp://127.0.0.1:%d" % free_port())
     stream = torch.cuda.Stream(device=dev)
