@@ -289,7 +289,8 @@ def run_bdm(args):
         if prof:
             torch.cuda.profiler.stop()
     bdm.bdm_sync(h)
-    half_path = bdm.bdm_get_path_stats(h)["half"] == 1  # (packed new boxes exist only on the half-shell path)
+    path_kind = bdm.bdm_get_path_stats(h)["half"]  # 1 half-shell passes, 2 the same band by band (ring), 0 k_force
+    half_path = path_kind in (1, 2)  # (packed new boxes exist only on the half-shell path, ring or not)
     step_ms = [a.elapsed_time(b) for a, b in evs]
     tm = bdm.bdm_get_timing(h)
     total_s = sum(step_ms) / 1e3
@@ -351,7 +352,9 @@ def run_bdm(args):
             "config": config_obj(args, n, 1),
             "roofline": {"bound": "alu", "achieved": achieved / 1e12, "peak": fp64_peak / 1e12, "unit": "TFLOP/s",
                          "frac": achieved / fp64_peak, "traffic": traffic,
-                         "kernel": "force phase: k_half_search + k_half_sum" if tm["search_ms"] > 0 else "k_force",
+                         "kernel": {1: "force phase: k_half_search + k_half_sum",
+                                    2: "force phase: k_half_search + k_half_sum, band by band over a ring of pair rows"
+                                    }.get(path_kind, "k_force"),
                          "traffic_source": "profiles/r02_force_traffic.json" if traffic else None,
                          "ms_per_launch": force_s * 1e3,
                          "passes_ms": {"search": tm["search_ms"] / max(tm["steps"], 1),
