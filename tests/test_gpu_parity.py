@@ -321,6 +321,21 @@ def test_cfg3_full_size_sampled(bdm):
 
 
 @pytest.mark.slow
+def test_cfg3_full_size_every_agent(bdm):
+    """configs[2] at full size (2e7 agents), the bench's headline workload on the default product path:
+    the displacements and new positions of EVERY agent equal one full oracle step bit for bit."""
+    pos, diam = bdm_inputs.make_config(3)
+    h = bdm.bdm_init(pos, diam, bdm.bdm_params_default())
+    bdm.bdm_mech_step(h, 1)
+    assert bdm.bdm_get_path_stats(h)["half"] == 1
+    dp, p1 = bdm.bdm_get_displacements(h), bdm.bdm_get_positions(h)
+    h.close()
+    o = oracle.step(pos, diam, record=False)
+    assert np.array_equal(dp, o["dp"])
+    assert np.array_equal(p1, o["pos_new"])
+
+
+@pytest.mark.slow
 def test_cfg4_full_size_window(bdm):
     """configs[3] at full size (2e8 agents, generated on the device by K0) in the launch
     configuration bench.py times: the displacements of every agent inside a window are checked
