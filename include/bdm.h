@@ -247,7 +247,8 @@ int bdm_set_timing(bdm_handle h, int enabled);
 int bdm_get_timing(bdm_handle h, double* out4);
 /* As bdm_get_timing, plus the force phase split of the half-shell path:
  * out6[4] ms of the search pass (row-counter and fused-column resets + k_half_search), out6[5] ms of
- * the sum pass (k_half_sum); both 0 for steps that ran k_force.  Resets the sums. */
+ * the sum pass (k_half_sum); both 0 for steps that ran k_force or the banded ring phase (whose
+ * passes interleave).  Resets the sums. */
 int bdm_get_timing_ex(bdm_handle h, double* out6);
 
 /* Counter-based uniform population on the device (kernel K0; bdm_inputs/__init__.py holds the
@@ -399,7 +400,8 @@ typedef struct {
   int64_t launches;       /* kernels of this library launched */
   int64_t host_syncs;     /* host synchronisations with the device (distributed: set-up, one per chunk
                              of up to 16 steps, getters) */
-  int64_t half_path;      /* 1: the last step ran the half-shell passes, 0: k_force, -1: no step */
+  int64_t half_path;      /* 1: the last step ran the half-shell passes, 2: the same band by band over a
+                             ring of pair rows, 0: k_force, -1: no step */
   int64_t migrated;       /* distributed: agents that changed owner during steps */
   int64_t ghosts;         /* distributed: ghost agents of the last step (all local ranks) */
   int64_t exchange_bytes; /* distributed: bytes sent by this process's ranks */

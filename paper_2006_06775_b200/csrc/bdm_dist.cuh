@@ -1765,7 +1765,7 @@ int bdm_get_stats(bdm_handle h, bdm_stats* out) {
   out->steps = (int64_t)h->steps_total;
   out->launches = h->launches_total + h->launches;
   out->host_syncs = h->host_syncs;
-  out->half_path = h->steps_total ? (h->last_half ? 1 : 0) : -1;
+  out->half_path = h->steps_total ? (h->last_half ? (h->ring_band ? 2 : 1) : 0) : -1;
   out->world = 1;
   out->local_ranks = 1;
   return BDM_OK;
