@@ -372,6 +372,7 @@ void init_device_info(bdm_ctx* h) {
   cudaFuncSetAttribute(k_half_search, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HA_SMEM_BYTES);
   cudaFuncSetAttribute(k_half_sum<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
   cudaFuncSetAttribute(k_half_sum<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
+  cudaFuncSetAttribute(k_half_sum<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HB_SMEM_BYTES);
 #ifndef BDM_NO_CARVEOUT
   {  // shared memory only as large as the resident blocks need: the rest stays L1 for the gathers
     int smem_sm = 0;
@@ -383,6 +384,8 @@ void init_device_info(bdm_ctx* h) {
     cudaFuncSetAttribute(k_half_search, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HA_SMEM_BYTES, HA_MIN_BLOCKS));
     cudaFuncSetAttribute(k_half_sum<false>, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
     cudaFuncSetAttribute(k_half_sum<true>, cudaFuncAttributePreferredSharedMemoryCarveout, pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
+    cudaFuncSetAttribute(k_half_sum<false, true>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         pct(HB_SMEM_BYTES, HB_MIN_BLOCKS));
     (void)cudaGetLastError();
   }
 #endif
