@@ -1434,7 +1434,10 @@ constexpr int HLA = BDM_HLA;  // pass A survivor buffer per lane (shared memory)
 #ifndef BDM_HA32
 #define BDM_HA32 1  // pass A takes boxes and radii from the fp32 copy (fp64 position only near box faces)
 #endif
-constexpr int HA_THREADS = 256;
+#ifndef BDM_HA_THREADS
+#define BDM_HA_THREADS 256
+#endif
+constexpr int HA_THREADS = BDM_HA_THREADS;
 #ifndef BDM_HA_MIN_BLOCKS
 #define BDM_HA_MIN_BLOCKS 5
 #endif
